@@ -1,0 +1,218 @@
+/*
+ * espo.h — C ABI (v1) of libespo: the ESPO policy-loss pass of arXiv 2512.07710
+ * ("Each Prompt Matters", §2.4.1 Multi-Stage Zero-Variance Elimination and §2.4.2 ESPO),
+ * forward and backward, on NVIDIA B200 (sm_100a).
+ *
+ * What the library computes (citations: PAPER.md line + section/equation):
+ *   - prompt groups, zero-variance (ZV) mask and GRPO advantages
+ *       PAPER.md:77-79 (§2.4.1 "all rollouts receive identical rewards ... zero advantage");
+ *       PAPER.md:105-107 (§2.4.2 normalised advantage Â, GRPO group normalisation)
+ *   - per-token log-prob of the sampled token and token entropy from vocab-wide logits
+ *       PAPER.md:111 (Eq. 1 numerator π_θ(y_t|x,y_<t)); PAPER.md:119-121 (Eq. 3 e_t, log|V|)
+ *   - per-sequence entropy buckets τ, the length-normalised bucket ratio s_τ (Eq. 2,
+ *     PAPER.md:115) and the entropy-adaptive clip ε_τ (Eq. 3)
+ *   - the clipped surrogate J_ESPO with the stop-gradient token ratio
+ *     (Eq. 1), loss = −J, and d loss / d logits.
+ * Readings of silent/garbled passages are listed in DESIGN.md ("Readings", Q1-Q21);
+ * the config fields below name the reading they select.
+ *
+ * Call order per training step (one context per GPU / rank):
+ *   espo_prepare  →  espo_loss_fwd on chunks covering every token row exactly once
+ *   (any order; a chunk may split a sequence)  →  espo_loss_finalize  →
+ *   espo_loss_bwd on chunks (any order, any number of times).
+ * Every call is asynchronous on the given CUDA stream; the only host↔device
+ * synchronisation is espo_get_error. With world > 1, espo_loss_finalize issues the one
+ * NCCL all-reduce of the pass (global active-rollout / token counts and loss terms).
+ *
+ * Layout: token rows are packed (cu_seqlens): rollout i owns rows
+ * [seq_offsets[i], seq_offsets[i+1]). Logits row t is the distribution that produced
+ * tokens[t] (the caller applies the usual one-position shift). A padded [R, L] batch is
+ * seq_offsets[i] = i·L with mask = 0 on padding. Logits/dlogits are row-major with a
+ * leading dimension `ld`/`ldg` (elements) ≥ vocab.
+ *
+ * Ownership: all pointer arguments are caller-owned; "device" pointers must be CUDA
+ * device memory of the context's device, "host" pointers host memory. Inputs of a chunk
+ * call are read before the call's work completes on the stream; the context keeps what
+ * it needs (per-token workspace ≈ 30 B/token, per-rollout arrays) until the next prepare.
+ *
+ * Errors: host-detectable problems (NULL, sizes, alignment, call order, chunk overlap)
+ * return a status immediately and enqueue nothing. Data problems found on the device
+ * (NaN/+inf logit in a row that is read, non-finite reward, token ∉ [0, vocab), a target
+ * logit of −inf, non-contiguous group ids, inconsistent seq_offsets) set a sticky device
+ * error word: espo_loss_finalize then writes a NaN loss, and espo_get_error returns the
+ * code. Rows of eliminated (ZV) groups and masked rows are never read (garbage is legal).
+ * No C++ exception crosses this ABI and nothing aborts. A context is not thread-safe;
+ * distinct contexts are independent.
+ */
+#ifndef ESPO_H_
+#define ESPO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ESPO_ABI_VERSION 1
+#define ESPO_MAX_BUCKETS 4
+#define ESPO_UNIQUE_ID_BYTES 128
+
+typedef struct espo_ctx_s* espo_ctx_t;
+/* Same type as cudaStream_t; NULL = the legacy default stream. */
+typedef struct CUstream_st* espo_stream_t;
+
+typedef enum {
+  ESPO_OK = 0,
+  ESPO_ERR_INVALID_ARGUMENT = 1,     /* NULL pointer, bad size/enum, chunk outside [0,T) */
+  ESPO_ERR_ALIGNMENT = 2,            /* logits/dlogits base or row pitch not 16-byte aligned */
+  ESPO_ERR_GROUPS_NOT_CONTIGUOUS = 3,/* group_ids decrease somewhere (device-detected) */
+  ESPO_ERR_BAD_STATE = 4,            /* call order violated, rows uncovered or covered twice */
+  ESPO_ERR_NONFINITE_INPUT = 5,      /* NaN/+inf logit, −inf target logit, non-finite reward */
+  ESPO_ERR_TOKEN_OUT_OF_RANGE = 6,   /* tokens[t] ∉ [0, vocab) */
+  ESPO_ERR_OUT_OF_MEMORY = 7,
+  ESPO_ERR_CUDA = 8,
+  ESPO_ERR_NCCL = 9,
+  ESPO_ERR_UNSUPPORTED = 10
+} espo_status;
+
+typedef enum { ESPO_F32 = 0, ESPO_BF16 = 1 } espo_dtype;
+
+/* Eq. 1 denominator reading (Q1). R2 (default): sg[π_θ] as in GSPO-token, so the
+ * token ratio's value is s_τ and a singleton bucket is token-level PPO. R1: the printed
+ * sg[π_θold] literally, value s_τ·π_θ/π_old. */
+typedef enum { ESPO_RATIO_GSPO_TOKEN = 0, ESPO_RATIO_LITERAL_OLD = 1 } espo_ratio_mode;
+
+/* Token grouping (Q3). QUANTILE: per sequence, K buckets split at the K−1 entropy order
+ * statistics (K=2: rank ⌊split_num·n/split_den⌋, the 80/20 rule of PAPER.md:95; ties to
+ * the lower bucket). WHOLE: one bucket (GSPO-token). SINGLETON: one bucket per token. */
+typedef enum { ESPO_PART_QUANTILE = 0, ESPO_PART_WHOLE = 1, ESPO_PART_SINGLETON = 2 } espo_partition;
+
+/* Normaliser (Q2, Q10). SEQ: J = (1/N_active_rollouts) Σ_i (1/nb_i) Σ_τ (1/|y_τ|) Σ_t ℓ_t
+ * (PAPER.md:105). TOKEN: J = (1/T_active) Σ_t ℓ_t. */
+typedef enum { ESPO_NORM_SEQ = 0, ESPO_NORM_TOKEN = 1 } espo_norm;
+
+typedef struct {
+  int32_t vocab;               /* V: row width; log|V| of Eq. 3 (Q6) */
+  float alpha;                 /* Eq. 3 α (Q5), default 0.4 */
+  float eps_min;               /* floor on ε_τ (Q5), default 0.01; 0 = paper-literal */
+  int32_t n_buckets;           /* K ∈ [1, 4], default 2 */
+  int32_t split_num, split_den;/* K=2 split fraction, default 4/5 */
+  int32_t partition;           /* espo_partition */
+  int32_t ratio_mode;          /* espo_ratio_mode */
+  int32_t norm;                /* espo_norm */
+  int32_t std_unbiased;        /* 0 (default): population std (Q7) */
+  double adv_eps;              /* Â = (r−μ)/(σ + adv_eps), default 1e-6 (Q7) */
+  double zv_var_eps;           /* 0 (default): ZV iff all rewards compare equal (Q8);
+                                  > 0: ZV iff fp64 two-pass variance ≤ zv_var_eps */
+  float logit_scale;           /* λ = 1/temperature applied to logits (Q15), default 1 */
+  float log_ratio_clamp;       /* clamp of the Eq. 2 mean log-ratio (Q14), default 20; 0=off */
+  int32_t logits_dtype;        /* espo_dtype of logits */
+  int32_t grad_dtype;          /* espo_dtype of dlogits (bf16 logits may emit f32 grads) */
+  int32_t zero_fill_inactive_rows; /* 1 (default): bwd writes 0 to rows of masked tokens,
+                                      ZV groups and clipped tokens; 0: leaves them as-is */
+  int32_t reserved[7];
+} espo_config;
+
+/* Device-written statistics (all fp64). Per-bucket arrays are indexed by the pre-drop
+ * bucket id k (0 = lowest entropy); WHOLE and SINGLETON report everything in k = 0. */
+typedef struct {
+  double loss;
+  double n_active_rollouts;    /* N: rollouts of non-ZV groups with ≥ 1 valid token */
+  double n_active_tokens;      /* T_active */
+  double n_zv_groups;          /* eliminated prompt groups (ZV ratio) */
+  double n_groups;
+  double n_clipped_tokens;     /* tokens whose clipped branch zeroes the gradient */
+  double mean_abs_logratio;    /* mean |log π_θ − log π_old| (mismatch) */
+  double mean_entropy;         /* mean e_t over active tokens (nats) */
+  double clip_frac[ESPO_MAX_BUCKETS];
+  double mean_ratio[ESPO_MAX_BUCKETS];   /* token-weighted mean of the ratio value */
+  double mean_eps[ESPO_MAX_BUCKETS];     /* token-weighted mean of ε_τ */
+  double tokens_per_bucket[ESPO_MAX_BUCKETS];
+} espo_stats;
+
+/* Fills *cfg with the defaults listed above for the given vocab (bf16 logits and grads). */
+void espo_config_default(espo_config* cfg, int32_t vocab);
+
+/* Writes a fresh NCCL unique id (ESPO_UNIQUE_ID_BYTES bytes, host memory) for rank 0 to
+ * broadcast to the other ranks before espo_create. Loads libnccl.so.2 on first use. */
+espo_status espo_get_unique_id(void* out_id);
+
+/* Creates a context on CUDA device `cuda_device`. world == 1: nccl_unique_id must be
+ * NULL and NCCL is never touched. world > 1: collective over all ranks (ncclCommInitRank
+ * with the broadcast id, host memory). cfg is copied. */
+espo_status espo_create(const espo_config* cfg, const void* nccl_unique_id, int32_t rank,
+                        int32_t world, int32_t cuda_device, espo_ctx_t* out);
+espo_status espo_destroy(espo_ctx_t ctx);
+
+/* Step begin (K1 kernels). Device inputs: rewards f32[R], group_ids i32[R] (each prompt
+ * group is one run of equal ids; ids must be non-decreasing), seq_offsets i64[R+1] with
+ * seq_offsets[0] = 0, non-decreasing, seq_offsets[R] = n_tokens. Outputs (device,
+ * nullable): adv_out f32[R] (0 for ZV groups), zv_out u8[R] (1 = eliminated group).
+ * Resets the sticky error word and the chunk coverage; may grow the workspace
+ * (the only call that allocates). */
+espo_status espo_prepare(espo_ctx_t ctx, const float* rewards, const int32_t* group_ids,
+                         const int64_t* seq_offsets, int32_t n_rollouts, int64_t n_tokens,
+                         float* adv_out, uint8_t* zv_out, espo_stream_t stream);
+
+/* Forward sweep over token rows [row_begin, row_begin + n_rows) (K2). Device inputs,
+ * each pointing at row row_begin: logits (dtype cfg.logits_dtype, 16-byte aligned,
+ * ld·sizeof(dtype) % 16 == 0, ld ≥ vocab), tokens i32, old_logp f32 (rollout-engine
+ * log π_old, nats), mask u8 (nullable = all valid). flags must be 0. */
+espo_status espo_loss_fwd(espo_ctx_t ctx, const void* logits, int64_t ld,
+                          const int32_t* tokens, const float* old_logp, const uint8_t* mask,
+                          int64_t row_begin, int64_t n_rows, uint32_t flags,
+                          espo_stream_t stream);
+
+/* After all rows are covered (K3 per-sequence reduction, K4 reduction + NCCL all-reduce
+ * when world > 1). Device outputs, nullable: loss_dev f32[1] (= −J; 0 when no rollout is
+ * active; NaN after a device-detected data error), stats_dev espo_stats. */
+espo_status espo_loss_finalize(espo_ctx_t ctx, float* loss_dev, espo_stats* stats_dev,
+                               espo_stream_t stream);
+
+/* Backward sweep (K5): dlogits = d(grad_loss · loss)/d logits for rows
+ * [row_begin, row_begin+n_rows). logits as in espo_loss_fwd (the same values);
+ * dlogits (device, cfg.grad_dtype, 16-byte aligned, ldg ≥ vocab) may alias logits when
+ * ldg == ld and the dtypes match. grad_loss_dev: device f32[1], nullable = 1.0. */
+espo_status espo_loss_bwd(espo_ctx_t ctx, const void* logits, int64_t ld, void* dlogits,
+                          int64_t ldg, const float* grad_loss_dev, int64_t row_begin,
+                          int64_t n_rows, espo_stream_t stream);
+
+/* Synchronises `stream`, then returns the sticky device error (ESPO_OK if none) or
+ * ESPO_ERR_CUDA if a CUDA error is pending. */
+espo_status espo_get_error(espo_ctx_t ctx, espo_stream_t stream);
+
+const char* espo_status_string(espo_status s);
+
+/* ---- introspection (tests / tooling; not needed on the training path) ---- */
+
+/* Copies per-token workspace values of rows [row_begin, row_begin+n_rows) to device
+ * arrays (each nullable): lse/lp/H/q f32 (after fwd), coef f32 = ∂J_i/∂lp_t before the
+ * global 1/D (after finalize), bucket u8 (stats bucket), clip u8 (1 = gradient clipped),
+ * valid u8 (1 = row was read: active rollout and mask = 1). */
+espo_status espo_export_token_stats(espo_ctx_t ctx, int64_t row_begin, int64_t n_rows,
+                                    float* lse, float* lp, float* H, float* q, float* coef,
+                                    uint8_t* bucket, uint8_t* clip, uint8_t* valid,
+                                    espo_stream_t stream);
+
+/* Copies per-rollout results to device arrays (each nullable): adv f64, zv u8, active u8,
+ * J_i f64 (Σ_t w_t ℓ_t), nb i32 (non-empty buckets), theta f32[R·(K−1)] thresholds. */
+espo_status espo_export_rollout_stats(espo_ctx_t ctx, double* adv, uint8_t* zv,
+                                      uint8_t* active, double* J_i, int32_t* nb,
+                                      float* theta, espo_stream_t stream);
+
+/* Number of kernels this context has launched so far. */
+uint64_t espo_launch_count(espo_ctx_t ctx);
+
+/* Kernel-variant switches for A/B measurement. */
+typedef enum {
+  ESPO_OPT_FWD_IMPL = 0,       /* 0 = TMA bulk-copy smem ring (default), 1 = LDG.128 */
+  ESPO_OPT_BWD_IMPL = 1,       /* 0 = TMA bulk-copy smem ring (default), 1 = LDG.128 */
+  ESPO_OPT_BLOCKS_PER_SM = 2   /* persistent grid = blocks_per_sm × SM count (0 = auto) */
+} espo_option;
+espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESPO_H_ */

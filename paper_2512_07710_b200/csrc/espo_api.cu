@@ -1,0 +1,568 @@
+// espo_api.cu — libespo host side: the C ABI of include/espo.h (context, validation,
+// workspace, launches, NCCL). Kernels live in the k_*.cuh headers of this directory.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <new>
+
+#include "common.cuh"
+#include "k_dlogits.cuh"
+#include "k_rowstats.cuh"
+#include "k_rowlist.cuh"
+#include "k_seq.cuh"
+#include "workspace.cuh"
+
+using namespace espo;
+
+// ------------------------------------------------------------------------------ NCCL
+// Resolved at run time from libnccl.so.2 (the copy torch already loaded, when present),
+// so a world == 1 context never needs NCCL and there is no link-time dependency.
+namespace {
+typedef struct { char internal[ESPO_UNIQUE_ID_BYTES]; } nccl_uid;
+typedef void* nccl_comm;
+typedef int (*fn_get_uid)(nccl_uid*);
+typedef int (*fn_init_rank)(nccl_comm*, int, nccl_uid, int);
+typedef int (*fn_allreduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t);
+typedef int (*fn_destroy)(nccl_comm);
+constexpr int kNcclFloat64 = 8;  // ncclFloat64
+constexpr int kNcclSum = 0;      // ncclSum
+
+struct NcclApi {
+  void* lib = nullptr;
+  fn_get_uid get_uid = nullptr;
+  fn_init_rank init_rank = nullptr;
+  fn_allreduce allreduce = nullptr;
+  fn_destroy destroy = nullptr;
+  bool load() {
+    if (lib) return true;
+    lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return false;
+    get_uid = reinterpret_cast<fn_get_uid>(dlsym(lib, "ncclGetUniqueId"));
+    init_rank = reinterpret_cast<fn_init_rank>(dlsym(lib, "ncclCommInitRank"));
+    allreduce = reinterpret_cast<fn_allreduce>(dlsym(lib, "ncclAllReduce"));
+    destroy = reinterpret_cast<fn_destroy>(dlsym(lib, "ncclCommDestroy"));
+    return get_uid && init_rank && allreduce && destroy;
+  }
+};
+NcclApi g_nccl;
+
+enum class State { Created, Prepared, Finalized };
+}  // namespace
+
+struct espo_ctx_s {
+  espo_config cfg{};
+  int device = 0, rank = 0, world = 1;
+  nccl_comm comm = nullptr;
+  int num_sms = 148;
+  Workspace ws;
+  int64_t cap_T = 0;
+  int cap_R = -1;
+  int R = 0;
+  int64_t T = 0;
+  State state = State::Created;
+  std::map<int64_t, int64_t> covered;  // fwd chunks: begin → end
+  int64_t n_covered = 0;
+  uint64_t launches = 0;
+  int fwd_impl = 0, bwd_impl = 0;
+  int blocks_per_sm = 0;
+  void* blocks_tok = nullptr;  // one allocation for all per-token arrays
+  void* blocks_roll = nullptr; // one allocation for all per-rollout arrays
+  void* blocks_scalar = nullptr;
+};
+
+namespace {
+inline cudaStream_t S(espo_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+espo_status cuda_status(cudaError_t e) {
+  return e == cudaSuccess ? ESPO_OK
+                          : (e == cudaErrorMemoryAllocation ? ESPO_ERR_OUT_OF_MEMORY : ESPO_ERR_CUDA);
+}
+
+#define ESPO_CUDA(x)                                  \
+  do {                                                \
+    cudaError_t e_ = (x);                             \
+    if (e_ != cudaSuccess) return cuda_status(e_);    \
+  } while (0)
+
+#define ESPO_LAUNCHED(ctx)                                   \
+  do {                                                       \
+    (ctx)->launches++;                                       \
+    cudaError_t e_ = cudaGetLastError();                     \
+    if (e_ != cudaSuccess) return cuda_status(e_);           \
+  } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+size_t dsize(int dt) { return dt == ESPO_BF16 ? 2 : 4; }
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+espo_status validate_config(const espo_config& c) {
+  if (c.vocab < 2) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c.n_buckets < 1 || c.n_buckets > ESPO_MAX_BUCKETS) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c.split_den <= 0 || c.split_num < 0 || c.split_num > c.split_den) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c.partition < 0 || c.partition > 2 || c.ratio_mode < 0 || c.ratio_mode > 1 || c.norm < 0 ||
+      c.norm > 1)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (!(c.alpha >= 0.f) || !(c.eps_min >= 0.f) || !(c.adv_eps >= 0.0) || !(c.zv_var_eps >= 0.0) ||
+      !(c.logit_scale > 0.f) || !std::isfinite(c.logit_scale) || !(c.log_ratio_clamp >= 0.f))
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if ((c.logits_dtype != ESPO_F32 && c.logits_dtype != ESPO_BF16) ||
+      (c.grad_dtype != ESPO_F32 && c.grad_dtype != ESPO_BF16))
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (c.logits_dtype == ESPO_F32 && c.grad_dtype == ESPO_BF16) return ESPO_ERR_UNSUPPORTED;
+  return ESPO_OK;
+}
+
+espo_status ensure_workspace(espo_ctx_t c, int R, int64_t T) {
+  if (T > c->cap_T) {
+    if (c->blocks_tok) cudaFree(c->blocks_tok);
+    c->blocks_tok = nullptr;
+    const int64_t cap = std::max<int64_t>(T, 1);
+    // 6 f32 + 2 i32 + 3 u8 arrays, each 256-byte aligned
+    const size_t a4 = round_up(size_t(cap) * 4, 256), a1 = round_up(size_t(cap), 256);
+    const size_t a32 = round_up(size_t(cap) * 32, 256);
+    ESPO_CUDA(cudaMalloc(&c->blocks_tok, 9 * a4 + 3 * a1 + a32));
+    char* p = static_cast<char*>(c->blocks_tok);
+    auto take = [&](size_t n) { char* r = p; p += n; return r; };
+    c->ws.lse = reinterpret_cast<float*>(take(a4));
+    c->ws.lp = reinterpret_cast<float*>(take(a4));
+    c->ws.H = reinterpret_cast<float*>(take(a4));
+    c->ws.q = reinterpret_cast<float*>(take(a4));
+    c->ws.old = reinterpret_cast<float*>(take(a4));
+    c->ws.coef = reinterpret_cast<float*>(take(a4));
+    c->ws.y = reinterpret_cast<int32_t*>(take(a4));
+    c->ws.row_seq = reinterpret_cast<int32_t*>(take(a4));
+    c->ws.flag = reinterpret_cast<uint8_t*>(take(a1));
+    c->ws.bucket = reinterpret_cast<uint8_t*>(take(a1));
+    c->ws.clip = reinterpret_cast<uint8_t*>(take(a1));
+    c->ws.list = take(a32);
+    c->ws.zlist = reinterpret_cast<int32_t*>(take(a4));
+    c->cap_T = cap;
+  }
+  if (R > c->cap_R) {
+    if (c->blocks_roll) cudaFree(c->blocks_roll);
+    c->blocks_roll = nullptr;
+    const int cap = std::max(R, 1);
+    const size_t a8 = round_up(size_t(cap + 1) * 8, 256), a1 = round_up(size_t(cap), 256);
+    const size_t a4 = round_up(size_t(cap) * 4, 256);
+    const size_t ath = round_up(size_t(cap) * (kMaxK - 1) * 4, 256);
+    const size_t ared = round_up(size_t(cap) * kRedLen * 8, 256);
+    ESPO_CUDA(cudaMalloc(&c->blocks_roll, 3 * a8 + 3 * a1 + a4 + ath + ared));
+    char* p = static_cast<char*>(c->blocks_roll);
+    auto take = [&](size_t n) { char* r = p; p += n; return r; };
+    c->ws.seq_off = reinterpret_cast<int64_t*>(take(a8));
+    c->ws.adv = reinterpret_cast<double*>(take(a8));
+    c->ws.J = reinterpret_cast<double*>(take(a8));
+    c->ws.cand = reinterpret_cast<uint8_t*>(take(a1));
+    c->ws.ghead = reinterpret_cast<uint8_t*>(take(a1));
+    c->ws.active = reinterpret_cast<uint8_t*>(take(a1));
+    c->ws.nb = reinterpret_cast<int32_t*>(take(a4));
+    c->ws.theta = reinterpret_cast<float*>(take(ath));
+    c->ws.red_r = reinterpret_cast<double*>(take(ared));
+    c->cap_R = cap;
+  }
+  return ESPO_OK;
+}
+
+int grid_for(espo_ctx_t c, const void* kernel, int threads) {
+  int per_sm = c->blocks_per_sm;
+  if (per_sm <= 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess ||
+        occ <= 0)
+      occ = 1;
+    per_sm = occ;
+  }
+  return per_sm * c->num_sms;
+}
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+extern "C" {
+
+void espo_config_default(espo_config* cfg, int32_t vocab) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->vocab = vocab;
+  cfg->alpha = 0.4f;
+  cfg->eps_min = 0.01f;
+  cfg->n_buckets = 2;
+  cfg->split_num = 4;
+  cfg->split_den = 5;
+  cfg->partition = ESPO_PART_QUANTILE;
+  cfg->ratio_mode = ESPO_RATIO_GSPO_TOKEN;
+  cfg->norm = ESPO_NORM_SEQ;
+  cfg->std_unbiased = 0;
+  cfg->adv_eps = 1e-6;
+  cfg->zv_var_eps = 0.0;
+  cfg->logit_scale = 1.0f;
+  cfg->log_ratio_clamp = 20.0f;
+  cfg->logits_dtype = ESPO_BF16;
+  cfg->grad_dtype = ESPO_BF16;
+  cfg->zero_fill_inactive_rows = 1;
+}
+
+const char* espo_status_string(espo_status s) {
+  switch (s) {
+    case ESPO_OK: return "ESPO_OK";
+    case ESPO_ERR_INVALID_ARGUMENT: return "ESPO_ERR_INVALID_ARGUMENT";
+    case ESPO_ERR_ALIGNMENT: return "ESPO_ERR_ALIGNMENT";
+    case ESPO_ERR_GROUPS_NOT_CONTIGUOUS: return "ESPO_ERR_GROUPS_NOT_CONTIGUOUS";
+    case ESPO_ERR_BAD_STATE: return "ESPO_ERR_BAD_STATE";
+    case ESPO_ERR_NONFINITE_INPUT: return "ESPO_ERR_NONFINITE_INPUT";
+    case ESPO_ERR_TOKEN_OUT_OF_RANGE: return "ESPO_ERR_TOKEN_OUT_OF_RANGE";
+    case ESPO_ERR_OUT_OF_MEMORY: return "ESPO_ERR_OUT_OF_MEMORY";
+    case ESPO_ERR_CUDA: return "ESPO_ERR_CUDA";
+    case ESPO_ERR_NCCL: return "ESPO_ERR_NCCL";
+    case ESPO_ERR_UNSUPPORTED: return "ESPO_ERR_UNSUPPORTED";
+  }
+  return "ESPO_ERR_UNKNOWN";
+}
+
+espo_status espo_get_unique_id(void* out_id) {
+  if (!out_id) return ESPO_ERR_INVALID_ARGUMENT;
+  if (!g_nccl.load()) return ESPO_ERR_NCCL;
+  nccl_uid id;
+  if (g_nccl.get_uid(&id) != 0) return ESPO_ERR_NCCL;
+  std::memcpy(out_id, &id, sizeof(id));
+  return ESPO_OK;
+}
+
+espo_status espo_create(const espo_config* cfg, const void* nccl_unique_id, int32_t rank,
+                        int32_t world, int32_t cuda_device, espo_ctx_t* out) {
+  if (!cfg || !out) return ESPO_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return ESPO_ERR_INVALID_ARGUMENT;
+  if ((world == 1) != (nccl_unique_id == nullptr)) return ESPO_ERR_INVALID_ARGUMENT;
+  espo_status st = validate_config(*cfg);
+  if (st != ESPO_OK) return st;
+  int ndev = 0;
+  ESPO_CUDA(cudaGetDeviceCount(&ndev));
+  if (cuda_device < 0 || cuda_device >= ndev) return ESPO_ERR_INVALID_ARGUMENT;
+  DevGuard g(cuda_device);
+  espo_ctx_t c = new (std::nothrow) espo_ctx_s();
+  if (!c) return ESPO_ERR_OUT_OF_MEMORY;
+  c->cfg = *cfg;
+  c->device = cuda_device;
+  c->rank = rank;
+  c->world = world;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  cudaError_t e = cudaMalloc(&c->blocks_scalar, 1024);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_status(e);
+  }
+  char* p = static_cast<char*>(c->blocks_scalar);
+  c->ws.red = reinterpret_cast<double*>(p);
+  c->ws.bwd_scale = reinterpret_cast<float*>(p + 512);
+  c->ws.err = reinterpret_cast<int*>(p + 768);
+  c->ws.count = reinterpret_cast<int*>(p + 896);
+  cudaMemset(c->blocks_scalar, 0, 1024);
+  if (world > 1) {
+    if (!g_nccl.load()) {
+      espo_destroy(c);
+      return ESPO_ERR_NCCL;
+    }
+    nccl_uid id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    if (g_nccl.init_rank(&c->comm, world, id, rank) != 0) {
+      c->comm = nullptr;
+      espo_destroy(c);
+      return ESPO_ERR_NCCL;
+    }
+  }
+  *out = c;
+  return ESPO_OK;
+}
+
+espo_status espo_destroy(espo_ctx_t c) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  {
+    DevGuard g(c->device);
+    cudaDeviceSynchronize();
+    if (c->comm) g_nccl.destroy(c->comm);
+    if (c->blocks_tok) cudaFree(c->blocks_tok);
+    if (c->blocks_roll) cudaFree(c->blocks_roll);
+    if (c->blocks_scalar) cudaFree(c->blocks_scalar);
+  }
+  delete c;
+  return ESPO_OK;
+}
+
+espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  switch (option) {
+    case ESPO_OPT_FWD_IMPL:
+      if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
+      c->fwd_impl = static_cast<int>(value);
+      return ESPO_OK;
+    case ESPO_OPT_BWD_IMPL:
+      if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
+      c->bwd_impl = static_cast<int>(value);
+      return ESPO_OK;
+    case ESPO_OPT_BLOCKS_PER_SM:
+      if (value < 0 || value > 32) return ESPO_ERR_INVALID_ARGUMENT;
+      c->blocks_per_sm = static_cast<int>(value);
+      return ESPO_OK;
+  }
+  return ESPO_ERR_INVALID_ARGUMENT;
+}
+
+uint64_t espo_launch_count(espo_ctx_t c) { return c ? c->launches : 0; }
+
+espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* group_ids,
+                         const int64_t* seq_offsets, int32_t n_rollouts, int64_t n_tokens,
+                         float* adv_out, uint8_t* zv_out, espo_stream_t stream) {
+  if (!c || !rewards || !group_ids || !seq_offsets) return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rollouts < 0 || n_tokens < 0 || n_tokens > (int64_t(1) << 40))
+    return ESPO_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  espo_status st = ensure_workspace(c, n_rollouts, n_tokens);
+  if (st != ESPO_OK) return st;
+  cudaStream_t s = S(stream);
+  ESPO_CUDA(cudaMemsetAsync(c->ws.err, 0, sizeof(int), s));
+  c->R = n_rollouts;
+  c->T = n_tokens;
+  c->covered.clear();
+  c->n_covered = 0;
+  PrepParams p;
+  p.rewards = rewards;
+  p.group_ids = group_ids;
+  p.seq_offsets = seq_offsets;
+  p.R = n_rollouts;
+  p.T = n_tokens;
+  p.std_unbiased = c->cfg.std_unbiased;
+  p.adv_eps = c->cfg.adv_eps;
+  p.zv_var_eps = c->cfg.zv_var_eps;
+  p.adv_out = adv_out;
+  p.zv_out = zv_out;
+  p.ws = c->ws;
+  k_prepare_groups<<<(n_rollouts + 1 + 255) / 256, 256, 0, s>>>(p);
+  ESPO_LAUNCHED(c);
+  if (n_rollouts > 0) {
+    k_row_seq<<<n_rollouts, 256, 0, s>>>(c->ws, n_rollouts);
+    ESPO_LAUNCHED(c);
+  }
+  c->state = State::Prepared;
+  return ESPO_OK;
+}
+
+espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
+                          const float* old_logp, const uint8_t* mask, int64_t row_begin,
+                          int64_t n_rows, uint32_t flags, espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
+  if (flags != 0 || n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rows == 0) return ESPO_OK;
+  if (!logits || !tokens || !old_logp) return ESPO_ERR_INVALID_ARGUMENT;
+  const size_t es = dsize(c->cfg.logits_dtype);
+  if (ld < c->cfg.vocab) return ESPO_ERR_INVALID_ARGUMENT;
+  if (!aligned16(logits) || (size_t(ld) * es) % 16 != 0) return ESPO_ERR_ALIGNMENT;
+  // chunk coverage: reject overlaps with earlier chunks
+  const int64_t b = row_begin, e = row_begin + n_rows;
+  auto it = c->covered.upper_bound(b);
+  if (it != c->covered.begin()) {
+    auto pv = std::prev(it);
+    if (pv->second > b) return ESPO_ERR_BAD_STATE;
+  }
+  if (it != c->covered.end() && it->first < e) return ESPO_ERR_BAD_STATE;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  FwdParams p;
+  p.logits = logits;
+  p.ld = ld;
+  p.tokens = tokens;
+  p.old_logp = old_logp;
+  p.mask = mask;
+  p.row_begin = row_begin;
+  p.n_rows = n_rows;
+  p.V = c->cfg.vocab;
+  p.lam_log2e = c->cfg.logit_scale * kLog2e;
+  p.ws = c->ws;
+  const bool bf = c->cfg.logits_dtype == ESPO_BF16;
+  FwdRec* list = static_cast<FwdRec*>(c->ws.list);
+  ESPO_CUDA(cudaMemsetAsync(c->ws.count, 0, 2 * sizeof(int), s));
+  const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  if (bf)
+    k_fwd_rows<__nv_bfloat16><<<pre_grid, 256, 0, s>>>(logits, ld, tokens, old_logp, mask, row_begin,
+                                                       n_rows, p.V, p.lam_log2e, c->ws, list, c->ws.count);
+  else
+    k_fwd_rows<float><<<pre_grid, 256, 0, s>>>(logits, ld, tokens, old_logp, mask, row_begin, n_rows,
+                                               p.V, p.lam_log2e, c->ws, list, c->ws.count);
+  ESPO_LAUNCHED(c);
+  if (c->fwd_impl == 1) {
+    if (bf) {
+      auto k = k_rowstats_ldg<__nv_bfloat16, 8>;
+      k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, c->ws.count);
+    } else {
+      auto k = k_rowstats_ldg<float, 4>;
+      k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, c->ws.count);
+    }
+  } else {
+    cudaError_t le = bf ? launch_rowstats_tma<__nv_bfloat16>(p, list, c->ws.count, c->num_sms, c->blocks_per_sm, s)
+                        : launch_rowstats_tma<float>(p, list, c->ws.count, c->num_sms, c->blocks_per_sm, s);
+    if (le != cudaSuccess) return cuda_status(le);
+  }
+  ESPO_LAUNCHED(c);
+  c->covered[b] = e;
+  c->n_covered += n_rows;
+  return ESPO_OK;
+}
+
+espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_dev,
+                               espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Prepared || c->n_covered != c->T) return ESPO_ERR_BAD_STATE;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  const espo_config& cf = c->cfg;
+  if (c->R > 0) {
+    SeqParams sp;
+    sp.R = c->R;
+    sp.V = cf.vocab;
+    sp.alpha = cf.alpha;
+    sp.eps_min = cf.eps_min;
+    sp.K = cf.n_buckets;
+    sp.split_num = cf.split_num;
+    sp.split_den = cf.split_den;
+    sp.partition = cf.partition;
+    sp.ratio_mode = cf.ratio_mode;
+    sp.norm = cf.norm;
+    sp.log_ratio_clamp = cf.log_ratio_clamp;
+    sp.inv_logV = 1.0 / std::log(static_cast<double>(cf.vocab));
+    sp.ws = c->ws;
+    k_seq_reduce<<<c->R, kSeqThreads, 0, s>>>(sp);
+    ESPO_LAUNCHED(c);
+    k_reduce_rollouts<<<kRedLen, 256, 0, s>>>(c->ws, c->R);
+    ESPO_LAUNCHED(c);
+  } else {
+    ESPO_CUDA(cudaMemsetAsync(c->ws.red, 0, kRedLen * sizeof(double), s));
+  }
+  if (c->world > 1) {
+    if (g_nccl.allreduce(c->ws.red, c->ws.red, kRedLen, kNcclFloat64, kNcclSum, c->comm, s) != 0)
+      return ESPO_ERR_NCCL;
+  }
+  k_finalize_scalar<<<1, 1, 0, s>>>(c->ws, cf.norm, cf.logit_scale, loss_dev, stats_dev);
+  ESPO_LAUNCHED(c);
+  c->state = State::Finalized;
+  return ESPO_OK;
+}
+
+espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogits, int64_t ldg,
+                          const float* grad_loss_dev, int64_t row_begin, int64_t n_rows,
+                          espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Finalized) return ESPO_ERR_BAD_STATE;
+  if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rows == 0) return ESPO_OK;
+  if (!logits || !dlogits) return ESPO_ERR_INVALID_ARGUMENT;
+  const espo_config& cf = c->cfg;
+  const size_t ei = dsize(cf.logits_dtype), eo = dsize(cf.grad_dtype);
+  if (ld < cf.vocab || ldg < cf.vocab) return ESPO_ERR_INVALID_ARGUMENT;
+  if (!aligned16(logits) || !aligned16(dlogits) || (size_t(ld) * ei) % 16 || (size_t(ldg) * eo) % 16)
+    return ESPO_ERR_ALIGNMENT;
+  const bool aliased = logits == dlogits;
+  if (aliased && (ld != ldg || ei != eo)) return ESPO_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  BwdParams p;
+  p.logits = logits;
+  p.ld = ld;
+  p.dlogits = dlogits;
+  p.ldg = ldg;
+  p.grad_loss = grad_loss_dev;
+  p.row_begin = row_begin;
+  p.n_rows = n_rows;
+  p.V = cf.vocab;
+  p.lam_log2e = cf.logit_scale * kLog2e;
+  p.zero_fill = cf.zero_fill_inactive_rows;
+  p.aliased = aliased ? 1 : 0;
+  p.ws = c->ws;
+  const bool bi = cf.logits_dtype == ESPO_BF16, bo = cf.grad_dtype == ESPO_BF16;
+  BwdRec* list = static_cast<BwdRec*>(c->ws.list);
+  int32_t* zl = c->ws.zlist;
+  int* cnt = c->ws.count;
+  ESPO_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), s));
+  const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  k_bwd_rows<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, p.zero_fill, c->ws, list, zl, cnt);
+  ESPO_LAUNCHED(c);
+  if (c->bwd_impl == 1) {
+    if (bi && bo) {
+      auto k = k_dlogits_ldg<__nv_bfloat16, __nv_bfloat16, 8>;
+      k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, zl, cnt);
+    } else if (bi) {
+      auto k = k_dlogits_ldg<__nv_bfloat16, float, 8>;
+      k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, zl, cnt);
+    } else {
+      auto k = k_dlogits_ldg<float, float, 4>;
+      k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, zl, cnt);
+    }
+  } else {
+    cudaError_t le;
+    if (bi && bo) le = launch_dlogits_tma<__nv_bfloat16, __nv_bfloat16>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, s);
+    else if (bi) le = launch_dlogits_tma<__nv_bfloat16, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, s);
+    else le = launch_dlogits_tma<float, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, s);
+    if (le != cudaSuccess) return cuda_status(le);
+  }
+  ESPO_LAUNCHED(c);
+  return ESPO_OK;
+}
+
+espo_status espo_get_error(espo_ctx_t c, espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return ESPO_ERR_CUDA;
+  int err = 0;
+  e = cudaMemcpy(&err, c->ws.err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return ESPO_ERR_CUDA;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return ESPO_ERR_CUDA;
+  return static_cast<espo_status>(err);
+}
+
+espo_status espo_export_token_stats(espo_ctx_t c, int64_t row_begin, int64_t n_rows, float* lse,
+                                    float* lp, float* H, float* q, float* coef, uint8_t* bucket,
+                                    uint8_t* clip, uint8_t* valid, espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state == State::Created) return ESPO_ERR_BAD_STATE;
+  if (n_rows < 0 || row_begin < 0 || row_begin + n_rows > c->T) return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rows == 0) return ESPO_OK;
+  DevGuard g(c->device);
+  const int grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, 4096));
+  k_export_tokens<<<grid, 256, 0, S(stream)>>>(c->ws, row_begin, n_rows, lse, lp, H, q, coef,
+                                                bucket, clip, valid);
+  ESPO_LAUNCHED(c);
+  return ESPO_OK;
+}
+
+espo_status espo_export_rollout_stats(espo_ctx_t c, double* adv, uint8_t* zv, uint8_t* active,
+                                      double* J_i, int32_t* nb, float* theta, espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state == State::Created) return ESPO_ERR_BAD_STATE;
+  if (c->R == 0) return ESPO_OK;
+  DevGuard g(c->device);
+  k_export_rollouts<<<(c->R + 255) / 256, 256, 0, S(stream)>>>(c->ws, c->R, adv, zv, active, J_i,
+                                                                 nb, theta);
+  ESPO_LAUNCHED(c);
+  return ESPO_OK;
+}
+
+}  // extern "C"

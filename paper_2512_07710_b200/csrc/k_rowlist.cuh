@@ -1,0 +1,123 @@
+// k_rowlist.cuh — per-chunk row scheduling for the two vocab sweeps.
+//
+// Before each sweep a light kernel classifies the chunk's rows and appends the rows that
+// need the sweep to a compact list of fixed-size records (warp-aggregated atomics; the
+// order of the list does not matter because every row's result depends only on its own
+// data). The hot kernels then read one record per row instead of a chain of dependent
+// metadata loads, never touch rows that need no work, and balance over the rows that do.
+#pragma once
+#include "common.cuh"
+#include "workspace.cuh"
+
+namespace espo {
+
+struct __align__(16) FwdRec {
+  int32_t r;   // chunk-relative row
+  int32_t y;   // sampled token
+  float uy;    // λ·log2(e)·z_y (the sweep's initial reference)
+  int32_t pad;
+};
+
+struct __align__(16) BwdRec {
+  int32_t r;   // chunk-relative row
+  int32_t y;   // token, or −1: zero-fill the row
+  float ng;    // −λ·g_t : dz_v = ng·p_v
+  float nlseL; // −lse_t·log2(e)
+  float gq;    // λ·g_t·q_t : dz_y
+  float pad[3];
+};
+
+__device__ __forceinline__ int warp_append(bool take, int* count) {
+  const unsigned m = __ballot_sync(0xffffffffu, take);
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == 0 && m) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+// Forward: copies tokens/old_logp into the workspace, sets flag[t], lists valid rows of
+// active rollouts. Errors: token ∉ [0,V) and a non-finite target logit.
+template <typename Tin>
+__global__ void __launch_bounds__(256) k_fwd_rows(const void* logits, int64_t ld,
+                                                  const int32_t* tokens, const float* old_logp,
+                                                  const uint8_t* mask, int64_t row_begin,
+                                                  int64_t n_rows, int V, float lamL, Workspace ws,
+                                                  FwdRec* list, int* count) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t n_round = (n_rows + 31) / 32 * 32;  // whole warps stay converged
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_round; r += stride) {
+    bool valid = false;
+    int y = 0;
+    float uy = 0.f;
+    if (r < n_rows) {
+      const int64_t t = row_begin + r;
+      y = tokens[r];
+      const bool m = mask ? (mask[r] != 0) : true;
+      ws.old[t] = old_logp[r];
+      ws.y[t] = y;
+      valid = m && ws.cand[ws.row_seq[t]];
+      if (valid && (y < 0 || y >= V)) {
+        set_error(ws.err, ESPO_ERR_TOKEN_OUT_OF_RANGE);
+        valid = false;
+      }
+      if (valid) {
+        const char* row = static_cast<const char*>(logits) + r * ld * int64_t(sizeof(Tin));
+        uy = Vec<Tin>::load1(row, y) * lamL;
+        if (!(fabsf(uy) <= 3.0e38f)) {
+          set_error(ws.err, ESPO_ERR_NONFINITE_INPUT);
+          valid = false;
+        }
+      }
+      ws.flag[t] = valid ? 1 : 0;
+    }
+    const int pos = warp_append(valid, count);
+    if (valid) {
+      FwdRec rec;
+      rec.r = static_cast<int32_t>(r);
+      rec.y = y;
+      rec.uy = uy;
+      rec.pad = 0;
+      list[pos] = rec;
+    }
+  }
+}
+
+// Backward: rows with a nonzero coefficient get a sweep record; rows without gradient
+// (masked, eliminated group, inactive rollout, clipped token) go to the zero-fill list when
+// zero_fill is set and are left untouched otherwise. count[0] = sweeps, count[1] = zeros.
+__global__ void __launch_bounds__(256) k_bwd_rows(int64_t row_begin, int64_t n_rows,
+                                                  const float* grad_loss, int zero_fill,
+                                                  Workspace ws, BwdRec* list, int32_t* zlist,
+                                                  int* count) {
+  const float gl = grad_loss ? *grad_loss : 1.f;
+  const float gscale = -gl * *ws.bwd_scale;  // λ·g_t = gscale·c_t
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t n_round = (n_rows + 31) / 32 * 32;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_round; r += stride) {
+    bool sweep = false, zero = false;
+    BwdRec rec;
+    if (r < n_rows) {
+      const int64_t t = row_begin + r;
+      const float c = ws.flag[t] ? ws.coef[t] : 0.f;
+      const float g = gscale * c;
+      if (g != 0.f) {
+        sweep = true;
+        rec.r = static_cast<int32_t>(r);
+        rec.y = ws.y[t];
+        rec.ng = -g;
+        rec.nlseL = -ws.lse[t] * kLog2e;
+        rec.gq = g * ws.q[t];
+        rec.pad[0] = rec.pad[1] = rec.pad[2] = 0.f;
+      } else {
+        zero = zero_fill != 0;
+      }
+    }
+    const int ps = warp_append(sweep, count);
+    if (sweep) list[ps] = rec;
+    const int pz = warp_append(zero, count + 1);
+    if (zero) zlist[pz] = static_cast<int32_t>(r);
+  }
+}
+
+}  // namespace espo

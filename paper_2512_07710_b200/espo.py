@@ -1,0 +1,300 @@
+"""Thin Python binding of libespo (include/espo.h) — argument marshalling only.
+
+Every step of the ESPO loss pass runs in the CUDA kernels of ``libespo.so`` (sm_100a);
+this module only converts torch tensors to pointers/streams and status codes to
+exceptions. PyTorch provides device memory, streams and process groups. There is no CPU
+fallback: if ``libespo.so`` is missing or fails to load, every entry point raises.
+
+C call → method:  espo_create → Espo(...), espo_prepare → Espo.prepare,
+espo_loss_fwd → Espo.loss_fwd, espo_loss_finalize → Espo.loss_finalize,
+espo_loss_bwd → Espo.loss_bwd, espo_get_error → Espo.get_error.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libespo.so")
+
+ESPO_MAX_BUCKETS = 4
+F32, BF16 = 0, 1
+PART_QUANTILE, PART_WHOLE, PART_SINGLETON = 0, 1, 2
+RATIO_GSPO_TOKEN, RATIO_LITERAL_OLD = 0, 1
+NORM_SEQ, NORM_TOKEN = 0, 1
+OPT_FWD_IMPL, OPT_BWD_IMPL, OPT_BLOCKS_PER_SM = 0, 1, 2
+
+STATUS = {
+    0: "ESPO_OK", 1: "ESPO_ERR_INVALID_ARGUMENT", 2: "ESPO_ERR_ALIGNMENT",
+    3: "ESPO_ERR_GROUPS_NOT_CONTIGUOUS", 4: "ESPO_ERR_BAD_STATE",
+    5: "ESPO_ERR_NONFINITE_INPUT", 6: "ESPO_ERR_TOKEN_OUT_OF_RANGE",
+    7: "ESPO_ERR_OUT_OF_MEMORY", 8: "ESPO_ERR_CUDA", 9: "ESPO_ERR_NCCL",
+    10: "ESPO_ERR_UNSUPPORTED",
+}
+EXPORTED_SYMBOLS = [
+    "espo_config_default", "espo_get_unique_id", "espo_create", "espo_destroy", "espo_prepare",
+    "espo_loss_fwd", "espo_loss_finalize", "espo_loss_bwd", "espo_get_error",
+    "espo_status_string", "espo_export_token_stats", "espo_export_rollout_stats",
+    "espo_launch_count", "espo_set_option",
+]
+
+
+class EspoError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        self.code = STATUS.get(status, f"ESPO_ERR_{status}")
+        super().__init__(f"{where}: {self.code}")
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("vocab", ctypes.c_int32), ("alpha", ctypes.c_float), ("eps_min", ctypes.c_float),
+        ("n_buckets", ctypes.c_int32), ("split_num", ctypes.c_int32),
+        ("split_den", ctypes.c_int32), ("partition", ctypes.c_int32),
+        ("ratio_mode", ctypes.c_int32), ("norm", ctypes.c_int32),
+        ("std_unbiased", ctypes.c_int32), ("adv_eps", ctypes.c_double),
+        ("zv_var_eps", ctypes.c_double), ("logit_scale", ctypes.c_float),
+        ("log_ratio_clamp", ctypes.c_float), ("logits_dtype", ctypes.c_int32),
+        ("grad_dtype", ctypes.c_int32), ("zero_fill_inactive_rows", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 7),
+    ]
+
+
+STATS_FIELDS = ["loss", "n_active_rollouts", "n_active_tokens", "n_zv_groups", "n_groups",
+                "n_clipped_tokens", "mean_abs_logratio", "mean_entropy"]
+STATS_ARRAYS = ["clip_frac", "mean_ratio", "mean_eps", "tokens_per_bucket"]
+STATS_LEN = len(STATS_FIELDS) + ESPO_MAX_BUCKETS * len(STATS_ARRAYS)  # doubles
+
+
+def stats_to_dict(t: torch.Tensor) -> dict:
+    v = t.detach().to("cpu", torch.float64).tolist()
+    d = {k: v[i] for i, k in enumerate(STATS_FIELDS)}
+    o = len(STATS_FIELDS)
+    for j, k in enumerate(STATS_ARRAYS):
+        d[k] = v[o + j * ESPO_MAX_BUCKETS: o + (j + 1) * ESPO_MAX_BUCKETS]
+    return d
+
+
+_lib = None
+
+
+def load_library():
+    """Loads libespo.so (after torch, so a world>1 context reuses torch's libnccl.so.2)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                           "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, U32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+    sig = {
+        "espo_config_default": (None, [ctypes.POINTER(Config), I32]),
+        "espo_get_unique_id": (I32, [P]),
+        "espo_create": (I32, [ctypes.POINTER(Config), P, I32, I32, I32, ctypes.POINTER(P)]),
+        "espo_destroy": (I32, [P]),
+        "espo_prepare": (I32, [P, P, P, P, I32, I64, P, P, P]),
+        "espo_loss_fwd": (I32, [P, P, I64, P, P, P, I64, I64, U32, P]),
+        "espo_loss_finalize": (I32, [P, P, P, P]),
+        "espo_loss_bwd": (I32, [P, P, I64, P, I64, P, I64, I64, P]),
+        "espo_get_error": (I32, [P, P]),
+        "espo_status_string": (ctypes.c_char_p, [I32]),
+        "espo_export_token_stats": (I32, [P, I64, I64, P, P, P, P, P, P, P, P, P]),
+        "espo_export_rollout_stats": (I32, [P, P, P, P, P, P, P, P]),
+        "espo_launch_count": (ctypes.c_uint64, [P]),
+        "espo_set_option": (I32, [P, I32, I64]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _check(status, where):
+    if status != 0:
+        raise EspoError(status, where)
+
+
+_DT = {torch.float32: F32, torch.bfloat16: BF16}
+
+
+class Espo:
+    """One ESPO loss context on one CUDA device (one rank). See include/espo.h."""
+
+    def __init__(self, vocab: int, *, alpha=0.4, eps_min=0.01, n_buckets=2, split=(4, 5),
+                 partition=PART_QUANTILE, ratio_mode=RATIO_GSPO_TOKEN, norm=NORM_SEQ,
+                 std_unbiased=False, adv_eps=1e-6, zv_var_eps=0.0, logit_scale=1.0,
+                 log_ratio_clamp=20.0, logits_dtype=torch.bfloat16, grad_dtype=None,
+                 zero_fill_inactive_rows=True, device=None, rank=0, world=1,
+                 process_group=None):
+        lib = load_library()
+        self._lib = lib
+        cfg = Config()
+        lib.espo_config_default(ctypes.byref(cfg), int(vocab))
+        cfg.alpha, cfg.eps_min = float(alpha), float(eps_min)
+        cfg.n_buckets = int(n_buckets)
+        cfg.split_num, cfg.split_den = int(split[0]), int(split[1])
+        cfg.partition, cfg.ratio_mode, cfg.norm = int(partition), int(ratio_mode), int(norm)
+        cfg.std_unbiased = int(bool(std_unbiased))
+        cfg.adv_eps, cfg.zv_var_eps = float(adv_eps), float(zv_var_eps)
+        cfg.logit_scale, cfg.log_ratio_clamp = float(logit_scale), float(log_ratio_clamp)
+        self.logits_dtype = logits_dtype
+        self.grad_dtype = grad_dtype if grad_dtype is not None else logits_dtype
+        cfg.logits_dtype, cfg.grad_dtype = _DT[self.logits_dtype], _DT[self.grad_dtype]
+        cfg.zero_fill_inactive_rows = int(bool(zero_fill_inactive_rows))
+        self.cfg = cfg
+        self.vocab = int(vocab)
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self.rank, self.world = int(rank), int(world)
+        uid = None
+        if self.world > 1:
+            import torch.distributed as dist
+            buf = [None]
+            if self.rank == 0:
+                raw = ctypes.create_string_buffer(128)
+                _check(lib.espo_get_unique_id(raw), "espo_get_unique_id")
+                buf[0] = raw.raw
+            dist.broadcast_object_list(buf, src=0, group=process_group)
+            uid = ctypes.create_string_buffer(buf[0], 128)
+        h = ctypes.c_void_p()
+        _check(lib.espo_create(ctypes.byref(cfg), uid, self.rank, self.world,
+                               self.device.index, ctypes.byref(h)), "espo_create")
+        self._h = h
+        self.n_tokens = 0
+        self.n_rollouts = 0
+
+    # -- lifecycle ------------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.espo_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def set_option(self, option: int, value: int):
+        _check(self._lib.espo_set_option(self._h, int(option), int(value)), "espo_set_option")
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._lib.espo_launch_count(self._h))
+
+    # -- the pass ---------------------------------------------------------------------------
+    def prepare(self, rewards, group_ids, seq_offsets, n_tokens=None, adv_out=None, zv_out=None):
+        """espo_prepare: rewards f32[R], group_ids i32[R], seq_offsets i64[R+1] (device)."""
+        R = int(rewards.shape[0])
+        if n_tokens is None:
+            n_tokens = int(seq_offsets[-1].item())
+        self.n_tokens, self.n_rollouts = int(n_tokens), R
+        _check(self._lib.espo_prepare(self._h, _ptr(rewards), _ptr(group_ids), _ptr(seq_offsets),
+                                      R, int(n_tokens), _ptr(adv_out), _ptr(zv_out),
+                                      self._stream()), "espo_prepare")
+
+    def loss_fwd(self, logits, tokens, old_logp, mask=None, row_begin=0):
+        """espo_loss_fwd over rows [row_begin, row_begin + logits.shape[0])."""
+        if logits.dtype != self.logits_dtype:
+            raise TypeError(f"logits dtype {logits.dtype} != context {self.logits_dtype}")
+        n = int(logits.shape[0])
+        _check(self._lib.espo_loss_fwd(self._h, _ptr(logits), int(logits.stride(0)),
+                                       _ptr(tokens), _ptr(old_logp), _ptr(mask), int(row_begin),
+                                       n, 0, self._stream()), "espo_loss_fwd")
+
+    def loss_finalize(self, loss_out=None, stats_out=None):
+        """espo_loss_finalize → (loss f32[1], stats f64[STATS_LEN]) device tensors."""
+        if loss_out is None:
+            loss_out = torch.empty(1, dtype=torch.float32, device=self.device)
+        if stats_out is None:
+            stats_out = torch.empty(STATS_LEN, dtype=torch.float64, device=self.device)
+        _check(self._lib.espo_loss_finalize(self._h, _ptr(loss_out), _ptr(stats_out),
+                                            self._stream()), "espo_loss_finalize")
+        return loss_out, stats_out
+
+    def loss_bwd(self, logits, dlogits=None, row_begin=0, grad_loss=None):
+        """espo_loss_bwd: d(grad_loss·loss)/d logits for rows of this chunk."""
+        if dlogits is None:
+            dlogits = torch.empty(logits.shape, dtype=self.grad_dtype, device=logits.device)
+        _check(self._lib.espo_loss_bwd(self._h, _ptr(logits), int(logits.stride(0)),
+                                       _ptr(dlogits), int(dlogits.stride(0)), _ptr(grad_loss),
+                                       int(row_begin), int(logits.shape[0]), self._stream()),
+               "espo_loss_bwd")
+        return dlogits
+
+    def get_error(self):
+        """espo_get_error: synchronises the current stream; raises on a device error."""
+        _check(self._lib.espo_get_error(self._h, self._stream()), "espo_get_error")
+
+    # -- introspection ------------------------------------------------------------------------
+    def export_token_stats(self, row_begin=0, n_rows=None):
+        if n_rows is None:
+            n_rows = self.n_tokens - row_begin
+        f = lambda: torch.empty(n_rows, dtype=torch.float32, device=self.device)
+        u = lambda: torch.empty(n_rows, dtype=torch.uint8, device=self.device)
+        out = dict(lse=f(), lp=f(), H=f(), q=f(), coef=f(), bucket=u(), clip=u(), valid=u())
+        _check(self._lib.espo_export_token_stats(
+            self._h, int(row_begin), int(n_rows), *[_ptr(out[k]) for k in
+                                                    ("lse", "lp", "H", "q", "coef", "bucket",
+                                                     "clip", "valid")],
+            self._stream()), "espo_export_token_stats")
+        return out
+
+    def export_rollout_stats(self):
+        R = self.n_rollouts
+        d = self.device
+        out = dict(adv=torch.empty(R, dtype=torch.float64, device=d),
+                   zv=torch.empty(R, dtype=torch.uint8, device=d),
+                   active=torch.empty(R, dtype=torch.uint8, device=d),
+                   J=torch.empty(R, dtype=torch.float64, device=d),
+                   nb=torch.empty(R, dtype=torch.int32, device=d),
+                   theta=torch.empty(R * (ESPO_MAX_BUCKETS - 1), dtype=torch.float32, device=d))
+        _check(self._lib.espo_export_rollout_stats(
+            self._h, *[_ptr(out[k]) for k in ("adv", "zv", "active", "J", "nb", "theta")],
+            self._stream()), "espo_export_rollout_stats")
+        out["theta"] = out["theta"].view(R, ESPO_MAX_BUCKETS - 1)
+        return out
+
+
+def espo_loss(ctx: Espo, logits, tokens, old_logp, rewards, group_ids, seq_offsets, mask=None,
+              grad_loss=None, dlogits=None, with_grad=True):
+    """Single-chunk convenience: prepare → fwd → finalize → bwd. Returns
+    (loss f32[1], stats f64[...], dlogits or None), all on the device."""
+    ctx.prepare(rewards, group_ids, seq_offsets, n_tokens=int(logits.shape[0]))
+    ctx.loss_fwd(logits, tokens, old_logp, mask)
+    loss, stats = ctx.loss_finalize()
+    dz = ctx.loss_bwd(logits, dlogits, grad_loss=grad_loss) if with_grad else None
+    return loss, stats, dz
+
+
+class EspoLossFunction(torch.autograd.Function):
+    """autograd wrapper (single chunk): loss = ESPO(logits); backward = espo_loss_bwd."""
+
+    @staticmethod
+    def forward(fctx, logits, ctx, tokens, old_logp, rewards, group_ids, seq_offsets, mask=None):
+        ctx.prepare(rewards, group_ids, seq_offsets, n_tokens=int(logits.shape[0]))
+        ctx.loss_fwd(logits, tokens, old_logp, mask)
+        loss, _ = ctx.loss_finalize()
+        fctx.espo = ctx
+        fctx.save_for_backward(logits)
+        return loss.reshape(())
+
+    @staticmethod
+    def backward(fctx, grad_out):
+        (logits,) = fctx.saved_tensors
+        g = grad_out.reshape(1).to(torch.float32).contiguous()
+        dz = fctx.espo.loss_bwd(logits, grad_loss=g)
+        return (dz.to(logits.dtype),) + (None,) * 7

@@ -1,0 +1,145 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded
+inputs — C0 in full, config variants, bf16 logits, chunking, both kernel variants.
+Tolerances (north_star): bit-exact masks / membership / counts / advantages; 1e-5 relative
+(fp32 logits) and 2e-3 (bf16 logits) on loss and gradients, P11 decision-aware protocol."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import espo_oracle as O
+from tests._instances import tiny_instance, workload_instance
+from tests.gpu_common import (check_dlogits_bf16, check_dlogits_f32, check_exact_fields,
+                              check_loss, check_token_stats, decision_aware_reference,
+                              oracle_cfg, oracle_dlogits, require_cuda, run_gpu)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return require_cuda()
+
+
+@pytest.fixture(scope="module")
+def c0():
+    return workload_instance("C0")
+
+
+def full_check(g, inst, cfg, rtol=1e-5, grad="f32", grad_loss=1.0, rows=None):
+    ref = inst.run(cfg)
+    check_exact_fields(g, ref)
+    check_token_stats(g, ref)
+    ref2, flips = decision_aware_reference(g, inst, ref, cfg)
+    check_loss(g, ref2, rtol)
+    rows = np.arange(inst.T) if rows is None else rows
+    want = oracle_dlogits(ref2, inst, cfg, rows, grad_loss)
+    if grad == "f32":
+        check_dlogits_f32(g["dlogits"][rows], want, rtol)
+    else:
+        check_dlogits_bf16(g["dlogits"][rows], want)
+    return ref2, flips
+
+
+@pytest.mark.parametrize("fwd_impl,bwd_impl", [(0, 0), (1, 1)], ids=["tma", "ldg"])
+def test_c0_full_parity(dev, c0, fwd_impl, bwd_impl):
+    g = run_gpu(c0, dev, fwd_impl=fwd_impl, bwd_impl=bwd_impl)
+    ref, _ = full_check(g, c0, oracle_cfg(c0.V))
+    s = g["stats"]
+    assert s["n_zv_groups"] == 1
+    for k in ("mean_entropy", "mean_abs_logratio"):
+        assert s[k] == pytest.approx(ref.stats[k], rel=1e-5)
+    assert s["n_clipped_tokens"] == ref.stats["n_clipped_tokens"]
+    for k in range(4):
+        assert s["clip_frac"][k] == pytest.approx(ref.stats["clip_frac"][k], abs=1e-12)
+        assert s["mean_ratio"][k] == pytest.approx(ref.stats["mean_ratio"][k], rel=1e-5)
+        assert s["mean_eps"][k] == pytest.approx(ref.stats["mean_eps"][k], rel=1e-5)
+    # advantages exported as f32 and zero for the eliminated group
+    assert np.array_equal(g["adv_out"], ref.adv.astype(np.float32))
+
+
+VARIANTS = [
+    dict(ratio_mode=O.RATIO_LITERAL_OLD),
+    dict(norm=O.NORM_TOKEN),
+    dict(partition=O.PARTITION_SINGLETON),
+    dict(partition=O.PARTITION_WHOLE),
+    dict(n_buckets=3),
+    dict(n_buckets=4, logit_scale=0.8),
+    dict(std_unbiased=1, eps_min=0.0, alpha=0.9),
+    dict(log_ratio_clamp=0.0, adv_eps=1e-3),
+]
+
+
+@pytest.mark.parametrize("kw", VARIANTS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()))
+def test_config_variants(dev, kw):
+    inst = tiny_instance(5, V=1024, group_sizes=(4, 4, 3, 2, 1), L=40, mask_tail=8,
+                         sigma_seq=0.08, logit_scale=kw.get("logit_scale", 1.0))
+    g = run_gpu(inst, dev, cfgkw=kw)
+    full_check(g, inst, oracle_cfg(inst.V, **kw))
+
+
+def test_grad_loss_scale(dev, c0):
+    g = run_gpu(c0, dev, grad_loss=-2.5)
+    full_check(g, c0, oracle_cfg(c0.V), grad_loss=-2.5)
+
+
+@pytest.mark.parametrize("impl", [0, 1], ids=["tma", "ldg"])
+def test_bf16_logits_f32_grads_exact_grade(dev, impl):
+    """The bf16-input kernels must be exact-grade (1e-5) when they emit fp32 gradients."""
+    inst = workload_instance("C0", seed=77)
+    inst.logits = __import__("espo_synth").round_to_bf16(inst.logits)
+    inst.dtype = "bf16"
+    g = run_gpu(inst, dev, logits_dtype=torch.bfloat16, grad_dtype=torch.float32,
+                fwd_impl=impl, bwd_impl=impl)
+    full_check(g, inst, oracle_cfg(inst.V))
+
+
+@pytest.mark.parametrize("impl", [0, 1], ids=["tma", "ldg"])
+def test_bf16_logits_bf16_grads(dev, impl):
+    inst = tiny_instance(8, V=4096, group_sizes=(8, 8), L=48, dtype="bf16", mask_tail=5)
+    g = run_gpu(inst, dev, logits_dtype=torch.bfloat16, fwd_impl=impl, bwd_impl=impl)
+    full_check(g, inst, oracle_cfg(inst.V), rtol=2e-3, grad="bf16")
+
+
+def test_chunks_any_order_bitwise(dev, c0):
+    a = run_gpu(c0, dev)
+    T = c0.T
+    cuts = [(700, T), (0, 130), (130, 700)]   # splits sequences, out of order
+    b = run_gpu(c0, dev, chunks=cuts)
+    assert a["loss"] == b["loss"]
+    assert np.array_equal(a["dlogits"], b["dlogits"])
+    assert a["stats"] == b["stats"]
+
+
+def test_variants_agree_bitwise(dev, c0):
+    """TMA and LDG variants run the same arithmetic per row: identical outputs."""
+    a = run_gpu(c0, dev, fwd_impl=0, bwd_impl=0)
+    b = run_gpu(c0, dev, fwd_impl=1, bwd_impl=1)
+    assert a["loss"] == b["loss"]
+    assert np.array_equal(a["dlogits"], b["dlogits"])
+
+
+def test_determinism(dev, c0):
+    a = run_gpu(c0, dev)
+    b = run_gpu(c0, dev)
+    assert a["loss"] == b["loss"] and a["stats"] == b["stats"]
+    assert np.array_equal(a["dlogits"], b["dlogits"])
+    for k in a["tok"]:
+        assert np.array_equal(a["tok"][k], b["tok"][k], equal_nan=True), k
+
+
+def test_in_place_and_padded_ld(dev):
+    inst = tiny_instance(3, V=1002, group_sizes=(4, 4), L=33, mask_tail=4)   # ragged V
+    a = run_gpu(inst, dev, ld_pad=6)
+    full_check(a, inst, oracle_cfg(inst.V))
+    b = run_gpu(inst, dev, ld_pad=6, in_place=True)
+    assert np.array_equal(a["dlogits"], b["dlogits"])
+    c = run_gpu(inst, dev, ld_pad=6, fwd_impl=1, bwd_impl=1, in_place=True)
+    assert np.array_equal(a["dlogits"], c["dlogits"])
+
+
+@pytest.mark.parametrize("impl", [0, 1], ids=["tma", "ldg"])
+def test_bf16_ragged_vocab(dev, impl):
+    inst = tiny_instance(4, V=2051, group_sizes=(4, 4), L=20, dtype="bf16")
+    g = run_gpu(inst, dev, logits_dtype=torch.bfloat16, grad_dtype=torch.float32, ld_pad=5,
+                fwd_impl=impl, bwd_impl=impl)
+    full_check(g, inst, oracle_cfg(inst.V))
