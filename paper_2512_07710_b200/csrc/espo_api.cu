@@ -410,7 +410,7 @@ espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const in
       auto k = k_rowstats_ldg<__nv_bfloat16, 8>;
       k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, c->ws.count);
     } else {
-      auto k = k_rowstats_ldg<float, 4>;
+      auto k = k_rowstats_ldg<float, 8>;
       k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, c->ws.count);
     }
   } else {
