@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C1")
     p.add_argument("--buffer-rows", type=int, default=32768)
-    p.add_argument("--fwd-impl", type=int, default=0, help="0 = TMA ring, 1 = LDG")
+    p.add_argument("--fwd-impl", type=int, default=0, help="0/2/3/4 = TMA ring variants, 1 = LDG")
     p.add_argument("--bwd-impl", type=int, default=0, help="0 = TMA ring, 1 = LDG")
     p.add_argument("--blocks-per-sm", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=1)
@@ -245,20 +245,22 @@ def run_e2e(ctx, d, dlog, args, dev):
 
 
 def cpu_baseline(d, w, n_tok_per_rollout, log):
-    """The oracle, as it stands, on a bounded sample of the same workload: prompt group 0
-    (G rollouts) truncated to the first n tokens of each rollout, fwd (O1-O6) + dlogits
+    """The oracle, as it stands, on a bounded sample of the same workload: the first prompt
+    group that is not eliminated (G rollouts), truncated to the first n tokens of each rollout, fwd (O1-O6) + dlogits
     (O7) for every sampled row, on this host."""
     import torch
     from oracle import espo_oracle as O
     G, V = w.G, w.V
     L = n_tok_per_rollout
     so = d["np"]["seq_offsets"]
-    rows = np.concatenate([np.arange(so[i], so[i] + L) for i in range(G)])
+    rw_all = d["np"]["rewards"].reshape(-1, G)
+    g0 = next(g for g in range(rw_all.shape[0]) if rw_all[g].min() != rw_all[g].max())
+    rows = np.concatenate([np.arange(so[i], so[i] + L) for i in range(g0 * G, (g0 + 1) * G)])
     bufrows = rows % d["Rc"]
     z = d["buf"][torch.from_numpy(bufrows).to(d["buf"].device)].float().cpu().numpy()
     tok = d["tokens"][torch.from_numpy(rows).to(d["buf"].device)].cpu().numpy()
     old = d["old"][torch.from_numpy(rows).to(d["buf"].device)].cpu().numpy()
-    rw = d["np"]["rewards"][:G]
+    rw = rw_all[g0]
     gid = np.zeros(G, np.int32)
     so_s = np.arange(G + 1, dtype=np.int64) * L
     cfg = O.OracleConfig(vocab=V, alpha=float(np.float32(0.4)), eps_min=float(np.float32(0.01)))
@@ -270,7 +272,8 @@ def cpu_baseline(d, w, n_tok_per_rollout, log):
     n = len(rows)
     log(f"cpu oracle: {n} tokens in {dt:.1f}s")
     return {"value": n / dt, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"prompt group 0 of {w.name}: {G} rollouts x first {L} tokens = {n} "
+            "sample": f"prompt group {g0} of {w.name} (first non-zero-variance group): {G} "
+                      f"rollouts x first {L} tokens = {n} "
                       f"tokens, V={V}, fwd (O1-O6) + dlogits (O7) of every row, numpy fp64, "
                       f"single thread; host has {len(os.sched_getaffinity(0))} cores",
             "seconds": dt}
@@ -378,7 +381,8 @@ def main_ours(args):
             "global_batch_tokens": T * world, "seq_len": w.L, "parallelism": f"dp{world} (prompt-group sharded)",
             "chunk_rows": d["Rc"], "l2": "inputs larger than L2 (chunk buffer "
                                          f"{d['Rc'] * V * 2 / 1e9:.2f} GB > 126 MB)",
-            "fwd_impl": ["tma", "ldg"][args.fwd_impl], "bwd_impl": ["tma", "ldg"][args.bwd_impl],
+            "fwd_impl": ["tma16x3x4k_s4", "ldg", "tma16x3x4k", "tma8x3x8k", "tma20x2x4k", "tma24x2x4k_s4", "tma24x2x2k_s4", "tma32x2x2k_s4"][args.fwd_impl],
+            "bwd_impl": ["tma8x4x4k", "ldg", "tma16x3x4k", "tma16x2x4k", "tma12x4x4k", "tma8x6x4k"][args.bwd_impl],
             "achieved_hbm_gbs_step": step_gbs, "frac_of_8TBs_step": step_gbs / NOMINAL_HBM_GBS,
             "frac_of_measured_step": step_gbs / peak,
             "fwd_sweep_gbs": fwd_gbs, "fwd_sweep_ms_per_chunk": fwd_ms,

@@ -307,11 +307,11 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   switch (option) {
     case ESPO_OPT_FWD_IMPL:
-      if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 7) return ESPO_ERR_INVALID_ARGUMENT;
       c->fwd_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_BWD_IMPL:
-      if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 5) return ESPO_ERR_INVALID_ARGUMENT;
       c->bwd_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_BLOCKS_PER_SM:
@@ -414,8 +414,8 @@ espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const in
       k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, c->ws.count);
     }
   } else {
-    cudaError_t le = bf ? launch_rowstats_tma<__nv_bfloat16>(p, list, c->ws.count, c->num_sms, c->blocks_per_sm, s)
-                        : launch_rowstats_tma<float>(p, list, c->ws.count, c->num_sms, c->blocks_per_sm, s);
+    cudaError_t le = bf ? launch_rowstats_tma<__nv_bfloat16>(p, list, c->ws.count, c->num_sms, c->blocks_per_sm, c->fwd_impl, s)
+                        : launch_rowstats_tma<float>(p, list, c->ws.count, c->num_sms, c->blocks_per_sm, c->fwd_impl, s);
     if (le != cudaSuccess) return cuda_status(le);
   }
   ESPO_LAUNCHED(c);
@@ -515,9 +515,10 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
     }
   } else {
     cudaError_t le;
-    if (bi && bo) le = launch_dlogits_tma<__nv_bfloat16, __nv_bfloat16>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, s);
-    else if (bi) le = launch_dlogits_tma<__nv_bfloat16, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, s);
-    else le = launch_dlogits_tma<float, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, s);
+    const int v = c->bwd_impl;
+    if (bi && bo) le = launch_dlogits_tma<__nv_bfloat16, __nv_bfloat16>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
+    else if (bi) le = launch_dlogits_tma<__nv_bfloat16, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
+    else le = launch_dlogits_tma<float, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
     if (le != cudaSuccess) return cuda_status(le);
   }
   ESPO_LAUNCHED(c);

@@ -37,6 +37,7 @@ __device__ __forceinline__ void store_out(char* orow, int j, const float* d, int
     for (int h = 0; h < EPI / EPO; ++h)
       st_stream(orow + (int64_t(j) * EPI + h * EPO) * sizeof(Tout), Out<Tout>::pack(d + h * EPO));
   } else {
+#pragma unroll
     for (int e = 0; e < EPI; ++e) {
       const int c = j * EPI + e;
       if (c < V) {
@@ -68,7 +69,11 @@ __device__ __forceinline__ void dz_vec(const uint4& v, int j, int vy, int yoff, 
   Vec<Tin>::unpack(v, x);
 #pragma unroll
   for (int e = 0; e < EPV; ++e) d[e] = rec.ng * ex2(fmaf(x[e], lamL, rec.nlseL));
-  if (j == vy) d[yoff] = rec.gq;
+  if (j == vy) {
+#pragma unroll
+    for (int e = 0; e < EPV; ++e)
+      if (e == yoff) d[e] = rec.gq;
+  }
 }
 
 // zero-fill records: processed by the same warps after their sweep rows
@@ -206,26 +211,38 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dlogits_tma(const BwdParams p, c
   zero_rows<Tout>(p, zlist, nz, gw, nw, lane);
 }
 
-struct DlogitsTmaCfg {
-  static constexpr int NW = 8, STAGES = 4, CHUNK = 4096;
-  static constexpr size_t smem() { return size_t(NW) * STAGES * CHUNK + size_t(NW) * STAGES * 8; }
-};
-
-template <typename Tin, typename Tout>
-inline cudaError_t launch_dlogits_tma(const BwdParams& p, const BwdRec* list, const int32_t* zlist,
-                                      const int* count, int num_sms, int blocks_per_sm,
-                                      cudaStream_t s) {
-  using C = DlogitsTmaCfg;
-  auto k = k_dlogits_tma<Tin, Tout, C::NW, C::STAGES, C::CHUNK>;
+template <typename Tin, typename Tout, int NW, int STAGES, int CHUNK>
+inline cudaError_t launch_dlogits_tma_cfg(const BwdParams& p, const BwdRec* list,
+                                          const int32_t* zlist, const int* count, int num_sms,
+                                          int blocks_per_sm, cudaStream_t s) {
+  constexpr size_t smem = size_t(NW) * STAGES * CHUNK + size_t(NW) * STAGES * 8;
+  auto k = k_dlogits_tma<Tin, Tout, NW, STAGES, CHUNK>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::smem()));
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int bps = blocks_per_sm > 0 ? blocks_per_sm : 1;
-  k<<<num_sms * bps, C::NW * 32, C::smem(), s>>>(p, list, zlist, count);
+  k<<<num_sms * bps, NW * 32, smem, s>>>(p, list, zlist, count);
   return cudaGetLastError();
+}
+
+// variant → (warps, stages, chunk bytes)
+template <typename Tin, typename Tout>
+inline cudaError_t launch_dlogits_tma(const BwdParams& p, const BwdRec* list, const int32_t* zlist,
+                                      const int* count, int num_sms, int blocks_per_sm, int variant,
+                                      cudaStream_t s) {
+#define ESPO_BWD_CFG(NW, ST, CH) \
+  launch_dlogits_tma_cfg<Tin, Tout, NW, ST, CH>(p, list, zlist, count, num_sms, blocks_per_sm, s)
+  switch (variant) {
+    case 2: return ESPO_BWD_CFG(16, 3, 4096);
+    case 3: return ESPO_BWD_CFG(16, 2, 4096);
+    case 4: return ESPO_BWD_CFG(12, 4, 4096);
+    case 5: return ESPO_BWD_CFG(8, 6, 4096);
+    default: return ESPO_BWD_CFG(8, 4, 4096);
+  }
+#undef ESPO_BWD_CFG
 }
 
 }  // namespace espo

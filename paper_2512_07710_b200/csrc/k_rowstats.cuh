@@ -35,14 +35,20 @@ __device__ __forceinline__ float max_nan(float a, float b) {
 }
 
 // Accumulates EPV elements (already unpacked) into (s, w) relative to reference nref = −r.
-template <int EPV>
+// Fast form: a −inf logit gives e·t = 0·(−inf) = NaN, which routes the batch to the slow
+// path (SAFE form: t clamped at −127 with NaN propagation, so −inf contributes exactly 0).
+template <int EPV, bool SAFE = false>
 __device__ __forceinline__ void acc_vec(const float* x, float lamL, float nref, float& s,
                                         float& w) {
   float s0 = 0.f, s1 = 0.f, w0 = 0.f, w1 = 0.f;
 #pragma unroll
   for (int e = 0; e < EPV; e += 2) {
-    const float t0 = max_nan(fmaf(x[e], lamL, nref), -127.f);
-    const float t1 = max_nan(fmaf(x[e + 1], lamL, nref), -127.f);
+    float t0 = fmaf(x[e], lamL, nref);
+    float t1 = fmaf(x[e + 1], lamL, nref);
+    if (SAFE) {
+      t0 = max_nan(t0, -127.f);
+      t1 = max_nan(t1, -127.f);
+    }
     const float e0 = ex2(t0), e1 = ex2(t1);
     s0 += e0;
     s1 += e1;
@@ -56,10 +62,10 @@ __device__ __forceinline__ void acc_vec(const float* x, float lamL, float nref, 
 // Sets the target element and the elements past V of a vector to −inf (they contribute 0).
 template <int EPV>
 __device__ __forceinline__ void fix_special(float* x, int j, int vy, int yoff, int V) {
-  if (j == vy) x[yoff] = -INFINITY;
+  // compile-time element indices only (a runtime index would put x in local memory)
 #pragma unroll
   for (int e = 0; e < EPV; ++e)
-    if (j * EPV + e >= V) x[e] = -INFINITY;
+    if ((j == vy && e == yoff) || j * EPV + e >= V) x[e] = -INFINITY;
 }
 
 // Row epilogue: combine lanes (each lane may hold its own reference r), write lse/lp/H/q.
@@ -95,29 +101,26 @@ __device__ __forceinline__ void row_finish(float r, float S, float W, float uy, 
   }
 }
 
-// Slow path for one batch: NaN/+inf detection and a max-based reference.
-template <int EPV, int U>
-__device__ __noinline__ void batch_slow(const uint4* v, int j0, int nvec, int vy, int yoff, int V,
-                                        float lamL, float& r, float& S, float& W, float& bS,
-                                        float& bW, int* err, bool is_bf16) {
+// Slow path for one batch: NaN/+inf detection and a max-based reference. Re-unpacks the
+// packed vectors (kept in registers) instead of holding U·EPV floats.
+template <typename Tin, int U>
+__device__ __forceinline__ void batch_slow(const uint4* v, int j0, int nvec, int vy, int yoff,
+                                           int jrag, int V, float lamL, float& r, float& S,
+                                           float& W, float& bS, float& bW, int* err) {
+  constexpr int EPV = Vec<Tin>::EPV;
   float bm = -INFINITY;
   bool bad = false;
-  float xs[U][EPV];
 #pragma unroll
   for (int k = 0; k < U; ++k) {
     const int j = j0 + 32 * k;
-    if (is_bf16) Vec<__nv_bfloat16>::unpack(v[k], xs[k]);
-    else Vec<float>::unpack(v[k], xs[k]);
-    if (j >= nvec) {
-#pragma unroll
-      for (int e = 0; e < EPV; ++e) xs[k][e] = -INFINITY;
-    } else {
-      fix_special<EPV>(xs[k], j, vy, yoff, V);
-    }
+    if (j >= nvec) continue;
+    float x[EPV];
+    Vec<Tin>::unpack(v[k], x);
+    fix_special<EPV>(x, j, vy, yoff, V);
 #pragma unroll
     for (int e = 0; e < EPV; ++e) {
-      const float u = xs[k][e] * lamL;
-      if (isnan(u) || u == INFINITY) bad = true;
+      const float u = x[e] * lamL;
+      bad |= isnan(u) || u == INFINITY;
       bm = fmaxf(bm, u);
     }
   }
@@ -127,7 +130,7 @@ __device__ __noinline__ void batch_slow(const uint4* v, int j0, int nvec, int vy
     bW = bS;
     return;
   }
-  if (bm > r) {
+  if (bm > r + 60.f) {  // keep r = u_y (exact e_y = 1) unless the batch could overflow
     const float d = r - bm;
     const float sc = ex2(d);
     W = sc * fmaf(d, S, W);
@@ -137,23 +140,37 @@ __device__ __noinline__ void batch_slow(const uint4* v, int j0, int nvec, int vy
   bS = 0.f;
   bW = 0.f;
 #pragma unroll
-  for (int k = 0; k < U; ++k) acc_vec<EPV>(xs[k], lamL, -r, bS, bW);
+  for (int k = 0; k < U; ++k) {
+    const int j = j0 + 32 * k;
+    if (j >= nvec) continue;
+    float x[EPV];
+    Vec<Tin>::unpack(v[k], x);
+    fix_special<EPV>(x, j, vy, yoff, V);
+    acc_vec<EPV, true>(x, lamL, -r, bS, bW);
+  }
 }
 
-
-// Processes U vectors (global vector index j0 + 32k) into the batch sums (bS, bW).
+// Fast path: U vectors into the batch sums with no per-vector checks. The batch that
+// holds the target element or the ragged end of the row (at most two per lane and row)
+// is routed to batch_slow instead (see `special`).
 template <typename Tin, int U>
-__device__ __forceinline__ void acc_batch(const uint4* v, int j0, int vy, int yoff, int jrag, int V,
-                                          float lamL, float nref, float& bS, float& bW) {
+__device__ __forceinline__ void acc_batch(const uint4* v, float lamL, float nref, float& bS,
+                                          float& bW) {
   constexpr int EPV = Vec<Tin>::EPV;
 #pragma unroll
   for (int k = 0; k < U; ++k) {
     float x[EPV];
     Vec<Tin>::unpack(v[k], x);
-    const int j = j0 + 32 * k;
-    if (j == vy || j == jrag) fix_special<EPV>(x, j, vy, yoff, V);
     acc_vec<EPV>(x, lamL, nref, bS, bW);
   }
+}
+
+// True if the batch j0 + 32k (k < U) contains vector vy or the ragged last vector jrag.
+template <int U>
+__device__ __forceinline__ bool special_batch(int j0, int vy, int jrag) {
+  const unsigned dy = static_cast<unsigned>(vy - j0);
+  const unsigned dr = static_cast<unsigned>(jrag - j0);
+  return (dy < 32u * U && (dy & 31u) == 0) || (jrag >= 0 && dr < 32u * U && (dr & 31u) == 0);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -185,10 +202,9 @@ __global__ void __launch_bounds__(256) k_rowstats_ldg(const FwdParams p, const F
         v[u] = (j < nvec) ? ld_stream(row + int64_t(j) * 16) : ninf;
       }
       float bS = 0.f, bW = 0.f;
-      acc_batch<Tin, U>(v, j0, vy, yoff, jrag, p.V, lamL, -ref, bS, bW);
-      if (!(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f))
-        batch_slow<EPV, U>(v, j0, nvec, vy, yoff, p.V, lamL, ref, S, W, bS, bW, p.ws.err,
-                           sizeof(Tin) == 2);
+      acc_batch<Tin, U>(v, lamL, -ref, bS, bW);
+      if (special_batch<U>(j0, vy, jrag) || !(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f))
+        batch_slow<Tin, U>(v, j0, nvec, vy, yoff, jrag, p.V, lamL, ref, S, W, bS, bW, p.ws.err);
       S += bS;
       W += bW;
     }
@@ -198,16 +214,19 @@ __global__ void __launch_bounds__(256) k_rowstats_ldg(const FwdParams p, const F
 
 // ---------------------------------------------------------------------------------------
 // Variant TMA: warp per row; each warp owns a STAGES-deep ring of CHUNK-byte shared-memory
-// slots filled by cp.async.bulk (the TMA engine, completion on one mbarrier per slot).
-// Lane 0 keeps STAGES chunks in flight across row boundaries; all lanes consume a slot
-// with conflict-free 128-bit LDS, then release it (__syncwarp) for the next copy.
+// slots filled by cp.async.bulk (the TMA engine; completion on one mbarrier per slot).
+// Steady state per chunk: wait on the slot, read it with conflict-free 128-bit LDS in
+// sub-batches of 8 vectors per lane (computing as it goes), release the slot and have lane 0
+// issue the chunk STAGES ahead (same row or the next one) into it. The first STAGES chunks
+// of a warp are issued up front; the ring then runs across row boundaries.
 // ---------------------------------------------------------------------------------------
-template <typename Tin, int NW, int STAGES, int CHUNK>
+template <typename Tin, int NW, int STAGES, int CHUNK, int SUB>
 __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
                                                              const FwdRec* list, const int* count) {
   constexpr int EPV = Vec<Tin>::EPV;
-  constexpr int VPC = CHUNK / 16;  // vectors per chunk
-  constexpr int VPL = VPC / 32;    // vectors per lane per chunk
+  constexpr int VPC = CHUNK / 16;  // vectors per chunk; SUB = vectors per lane per sub-batch
+  constexpr int NSUB = VPC / (32 * SUB);
+  static_assert(VPC % (32 * SUB) == 0, "chunk must hold whole sub-batches");
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = smem + size_t(warp) * STAGES * CHUNK;
@@ -220,6 +239,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
   const int n = *count;
   const int nw = gridDim.x * NW;
   const int gw = blockIdx.x * NW + warp;
+  if (gw >= n) return;
   const int nvec = (p.V + EPV - 1) / EPV;
   const uint32_t rowbytes = uint32_t(nvec) * 16u;
   const int nch = static_cast<int>((rowbytes + CHUNK - 1) / CHUNK);
@@ -231,83 +251,95 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
   const uint4 ninf = make_uint4(Vec<Tin>::kNegInfWord, Vec<Tin>::kNegInfWord, Vec<Tin>::kNegInfWord,
                                 Vec<Tin>::kNegInfWord);
 
-  // producer cursor (row records prefetched one row ahead)
+  // producer cursor: (row pk with row index pr, chunk pc); pr_next prefetched one row ahead
   int pk = gw, pc = 0;
-  int pr = (pk < n) ? list[pk].r : 0;
+  int pr = list[pk].r;
   int pr_next = (pk + nw < n) ? list[pk + nw].r : 0;
-  uint32_t issued = 0, consumed = 0;
-  auto refill = [&]() {
-    while (issued - consumed < STAGES && pk < n) {
-      const int slot = issued % STAGES;
-      const uint32_t off = uint32_t(pc) * CHUNK;
-      const uint32_t bytes = min(uint32_t(CHUNK), rowbytes - off);
-      if (lane == 0) {
-        mbar_arrive_tx(&bars[slot], bytes);
-        bulk_g2s(ring + slot * CHUNK, base + int64_t(pr) * pitch + off, bytes, &bars[slot], pol);
-      }
-      ++issued;
-      if (++pc == nch) {
-        pc = 0;
-        pk += nw;
-        pr = pr_next;
-        pr_next = (pk + nw < n) ? list[pk + nw].r : 0;
-      }
+  auto issue_one = [&](int slot) {  // issues the cursor's chunk into `slot`, advances cursor
+    const uint32_t off = uint32_t(pc) * CHUNK;
+    const uint32_t bytes = min(uint32_t(CHUNK), rowbytes - off);
+    if (lane == 0) {
+      mbar_arrive_tx(&bars[slot], bytes);
+      bulk_g2s(ring + slot * CHUNK, base + int64_t(pr) * pitch + off, bytes, &bars[slot], pol);
+    }
+    if (++pc == nch) {
+      pc = 0;
+      pk += nw;
+      pr = pr_next;
+      pr_next = (pk + nw < n) ? list[pk + nw].r : 0;
     }
   };
-  refill();
-  FwdRec rec_next = (gw < n) ? list[gw] : FwdRec{};
+  for (int s = 0; s < STAGES && pk < n; ++s) issue_one(s);
+
+  uint32_t q = 0;  // chunks consumed by this warp
+  FwdRec rec_next = list[gw];
   for (int k = gw; k < n; k += nw) {
     const FwdRec rec = rec_next;
     if (k + nw < n) rec_next = list[k + nw];
     const int vy = rec.y / EPV, yoff = rec.y % EPV;
     float ref = rec.uy, S = 0.f, W = 0.f;
-    for (int c = 0; c < nch; ++c) {
-      const int slot = consumed % STAGES;
-      mbar_wait(&bars[slot], (consumed / STAGES) & 1u);
+    for (int c = 0; c < nch; ++c, ++q) {
+      const int slot = q % STAGES;
+      mbar_wait(&bars[slot], (q / STAGES) & 1u);
       const uint8_t* buf = ring + slot * CHUNK;
       const int vlim = min(VPC, nvec - c * VPC);
-      uint4 v[VPL];
 #pragma unroll
-      for (int u = 0; u < VPL; ++u) {
-        const int jl = lane + 32 * u;
-        v[u] = (jl < vlim) ? lds128(buf + jl * 16) : ninf;
+      for (int h = 0; h < NSUB; ++h) {
+        uint4 v[SUB];
+#pragma unroll
+        for (int u = 0; u < SUB; ++u) {
+          const int jl = h * 32 * SUB + lane + 32 * u;
+          v[u] = (jl < vlim) ? lds128(buf + jl * 16) : ninf;
+        }
+        if (h == NSUB - 1) {
+          __syncwarp();                        // every lane has read the slot
+          if (pk < n) issue_one(slot);         // refill it STAGES chunks ahead
+        }
+        const int j0 = c * VPC + h * 32 * SUB + lane;
+        float bS = 0.f, bW = 0.f;
+        acc_batch<Tin, SUB>(v, lamL, -ref, bS, bW);
+        if (special_batch<SUB>(j0, vy, jrag) || !(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f))
+          batch_slow<Tin, SUB>(v, j0, nvec, vy, yoff, jrag, p.V, lamL, ref, S, W, bS, bW, p.ws.err);
+        S += bS;
+        W += bW;
       }
-      __syncwarp();
-      ++consumed;
-      refill();  // the slot's data is in registers: reuse it right away
-      const int j0 = c * VPC + lane;
-      float bS = 0.f, bW = 0.f;
-      acc_batch<Tin, VPL>(v, j0, vy, yoff, jrag, p.V, lamL, -ref, bS, bW);
-      if (!(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f))
-        batch_slow<EPV, VPL>(v, j0, nvec, vy, yoff, p.V, lamL, ref, S, W, bS, bW, p.ws.err,
-                             sizeof(Tin) == 2);
-      S += bS;
-      W += bW;
     }
     row_finish(ref, S, W, rec.uy, p.ws, p.row_begin + rec.r, lane);
   }
 }
 
-template <typename Tin>
-struct RowstatsTmaCfg {
-  static constexpr int NW = 8, STAGES = 4, CHUNK = 4096;
-  static constexpr size_t smem() { return size_t(NW) * STAGES * CHUNK + size_t(NW) * STAGES * 8; }
-};
-
-template <typename Tin>
-inline cudaError_t launch_rowstats_tma(const FwdParams& p, const FwdRec* list, const int* count,
-                                       int num_sms, int blocks_per_sm, cudaStream_t s) {
-  using C = RowstatsTmaCfg<Tin>;
-  auto k = k_rowstats_tma<Tin, C::NW, C::STAGES, C::CHUNK>;
+template <typename Tin, int NW, int STAGES, int CHUNK, int SUB>
+inline cudaError_t launch_rowstats_tma_cfg(const FwdParams& p, const FwdRec* list, const int* count,
+                                           int num_sms, int blocks_per_sm, cudaStream_t s) {
+  constexpr size_t smem = size_t(NW) * STAGES * CHUNK + size_t(NW) * STAGES * 8;
+  auto k = k_rowstats_tma<Tin, NW, STAGES, CHUNK, SUB>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::smem()));
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int bps = blocks_per_sm > 0 ? blocks_per_sm : 1;
-  k<<<num_sms * bps, C::NW * 32, C::smem(), s>>>(p, list, count);
+  k<<<num_sms * bps, NW * 32, smem, s>>>(p, list, count);
   return cudaGetLastError();
+}
+
+// variant → (warps, stages, chunk bytes, vectors per lane per sub-batch)
+template <typename Tin>
+inline cudaError_t launch_rowstats_tma(const FwdParams& p, const FwdRec* list, const int* count,
+                                       int num_sms, int blocks_per_sm, int variant, cudaStream_t s) {
+#define ESPO_FWD_CFG(NW, ST, CH, SB) \
+  launch_rowstats_tma_cfg<Tin, NW, ST, CH, SB>(p, list, count, num_sms, blocks_per_sm, s)
+  switch (variant) {
+    case 2: return ESPO_FWD_CFG(16, 3, 4096, 8);
+    case 3: return ESPO_FWD_CFG(8, 3, 8192, 8);
+    case 4: return ESPO_FWD_CFG(20, 2, 4096, 8);
+    case 5: return ESPO_FWD_CFG(24, 2, 4096, 4);
+    case 6: return ESPO_FWD_CFG(24, 2, 2048, 4);
+    case 7: return ESPO_FWD_CFG(32, 2, 2048, 4);
+    default: return ESPO_FWD_CFG(16, 3, 4096, 4);  // measured best on C1 (K2)
+  }
+#undef ESPO_FWD_CFG
 }
 
 }  // namespace espo
