@@ -46,7 +46,24 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+// 2^t on the FMA pipe (FA4-style software exp2): Cody-Waite split t = n + f, f ∈ [-½, ½]
+// (magic-number rounding), degree-5 near-minimax polynomial for 2^f (max rel. err 2.3e-7 in
+// fp32 evaluation, same class as MUFU ex2.approx), exponent added as integer n << 23.
+// t ≤ −127 (incl. −inf) gives 0; NaN propagates. Used for a fraction of the elements so the
+// forward sweep is not bound by the MUFU (XU) pipe.
+__device__ __forceinline__ float ex2_poly(float t) {
+  asm("max.NaN.f32 %0, %0, 0fC2FE0000;" : "+f"(t));  // max(t, -127)
+  const float r = t + 12582912.0f;                    // 1.5·2^23: round(t) in the low bits
+  const float f = t - (r - 12582912.0f);
+  float p = fmaf(0x1.5c08e4p-10f, f, 0x1.3d0c52p-7f);
+  p = fmaf(p, f, 0x1.c6b6e4p-5f);
+  p = fmaf(p, f, 0x1.ebf918p-3f);
+  p = fmaf(p, f, 0x1.62e428p-1f);
+  p = fmaf(p, f, 0x1.000002p+0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
+}
+// low half via PRMT (ALU pipe) rather than IMAD.SHL (FMA pipe, already the busier one)
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(__byte_perm(w, 0u, 0x1044)); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;

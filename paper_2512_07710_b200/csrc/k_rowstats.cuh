@@ -40,23 +40,14 @@ __device__ __forceinline__ float max_nan(float a, float b) {
 template <int EPV, bool SAFE = false>
 __device__ __forceinline__ void acc_vec(const float* x, float lamL, float nref, float& s,
                                         float& w) {
-  float s0 = 0.f, s1 = 0.f, w0 = 0.f, w1 = 0.f;
 #pragma unroll
-  for (int e = 0; e < EPV; e += 2) {
-    float t0 = fmaf(x[e], lamL, nref);
-    float t1 = fmaf(x[e + 1], lamL, nref);
-    if (SAFE) {
-      t0 = max_nan(t0, -127.f);
-      t1 = max_nan(t1, -127.f);
-    }
-    const float e0 = ex2(t0), e1 = ex2(t1);
-    s0 += e0;
-    s1 += e1;
-    w0 = fmaf(e0, t0, w0);
-    w1 = fmaf(e1, t1, w1);
+  for (int e = 0; e < EPV; ++e) {
+    float t = fmaf(x[e], lamL, nref);
+    if (SAFE) t = max_nan(t, -127.f);
+    const float ex = ex2(t);
+    s += ex;
+    w = fmaf(ex, t, w);
   }
-  s += s0 + s1;
-  w += w0 + w1;
 }
 
 // Sets the target element and the elements past V of a vector to −inf (they contribute 0).
@@ -66,6 +57,15 @@ __device__ __forceinline__ void fix_special(float* x, int j, int vy, int yoff, i
 #pragma unroll
   for (int e = 0; e < EPV; ++e)
     if ((j == vy && e == yoff) || j * EPV + e >= V) x[e] = -INFINITY;
+}
+
+// Compensated (Kahan) accumulation of the per-batch sums into the per-lane row sums:
+// a lane adds ~150 batch sums per row, so a plain running sum would lose ~1e-5 relative.
+__device__ __forceinline__ void kahan_add(float& s, float& c, float x) {
+  const float y = x - c;
+  const float t = s + y;
+  c = (t - s) - y;
+  s = t;
 }
 
 // Row epilogue: combine lanes (each lane may hold its own reference r), write lse/lp/H/q.
@@ -153,16 +153,46 @@ __device__ __forceinline__ void batch_slow(const uint4* v, int j0, int nvec, int
 // Fast path: U vectors into the batch sums with no per-vector checks. The batch that
 // holds the target element or the ragged end of the row (at most two per lane and row)
 // is routed to batch_slow instead (see `special`).
-template <typename Tin, int U>
+// NPOLY elements of every 8 (the odd slots 7, then 3) take 2^t from ex2_poly on the FMA
+// pipe instead of MUFU.EX2, balancing the two pipes (K2).
+template <int NPOLY>
+__device__ __forceinline__ float ex2_mix(float t, int e) {
+  const bool poly = (NPOLY >= 1 && (e & 7) == 7) || (NPOLY >= 2 && (e & 7) == 3);
+  return poly ? ex2_poly(t) : ex2(t);
+}
+
+template <typename Tin, int U, int NPOLY = 0>
 __device__ __forceinline__ void acc_batch(const uint4* v, float lamL, float nref, float& bS,
                                           float& bW) {
   constexpr int EPV = Vec<Tin>::EPV;
+  // two (s, w) chains, seeded by the first vector (no 0 + x instructions)
+  float s0, s1, w0, w1;
+  {
+    float x[EPV];
+    Vec<Tin>::unpack(v[0], x);
+    const float t0 = fmaf(x[0], lamL, nref), t1 = fmaf(x[1], lamL, nref);
+    const float e0 = ex2_mix<NPOLY>(t0, 0), e1 = ex2_mix<NPOLY>(t1, 1);
+    s0 = e0; s1 = e1; w0 = e0 * t0; w1 = e1 * t1;
 #pragma unroll
-  for (int k = 0; k < U; ++k) {
+    for (int e = 2; e < EPV; e += 2) {
+      const float ta = fmaf(x[e], lamL, nref), tb = fmaf(x[e + 1], lamL, nref);
+      const float ea = ex2_mix<NPOLY>(ta, e), eb = ex2_mix<NPOLY>(tb, e + 1);
+      s0 += ea; s1 += eb; w0 = fmaf(ea, ta, w0); w1 = fmaf(eb, tb, w1);
+    }
+  }
+#pragma unroll
+  for (int k = 1; k < U; ++k) {
     float x[EPV];
     Vec<Tin>::unpack(v[k], x);
-    acc_vec<EPV>(x, lamL, nref, bS, bW);
+#pragma unroll
+    for (int e = 0; e < EPV; e += 2) {
+      const float ta = fmaf(x[e], lamL, nref), tb = fmaf(x[e + 1], lamL, nref);
+      const float ea = ex2_mix<NPOLY>(ta, e), eb = ex2_mix<NPOLY>(tb, e + 1);
+      s0 += ea; s1 += eb; w0 = fmaf(ea, ta, w0); w1 = fmaf(eb, tb, w1);
+    }
   }
+  bS = s0 + s1;
+  bW = w0 + w1;
 }
 
 // True if the batch j0 + 32k (k < U) contains vector vy or the ragged last vector jrag.
@@ -193,7 +223,7 @@ __global__ void __launch_bounds__(256) k_rowstats_ldg(const FwdParams p, const F
     const FwdRec rec = list[k];
     const char* row = static_cast<const char*>(p.logits) + int64_t(rec.r) * p.ld * int64_t(sizeof(Tin));
     const int vy = rec.y / EPV, yoff = rec.y % EPV;
-    float ref = rec.uy, S = 0.f, W = 0.f;
+    float ref = rec.uy, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f;
     for (int j0 = lane; j0 < nvec; j0 += 32 * U) {
       uint4 v[U];
 #pragma unroll
@@ -201,14 +231,18 @@ __global__ void __launch_bounds__(256) k_rowstats_ldg(const FwdParams p, const F
         const int j = j0 + 32 * u;
         v[u] = (j < nvec) ? ld_stream(row + int64_t(j) * 16) : ninf;
       }
-      float bS = 0.f, bW = 0.f;
+      float bS, bW;
       acc_batch<Tin, U>(v, lamL, -ref, bS, bW);
-      if (special_batch<U>(j0, vy, jrag) || !(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f))
+      if (special_batch<U>(j0, vy, jrag) || !(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {
+        S -= cS;
+        W -= cW;
+        cS = cW = 0.f;
         batch_slow<Tin, U>(v, j0, nvec, vy, yoff, jrag, p.V, lamL, ref, S, W, bS, bW, p.ws.err);
-      S += bS;
-      W += bW;
+      }
+      kahan_add(S, cS, bS);
+      kahan_add(W, cW, bW);
     }
-    row_finish(ref, S, W, rec.uy, p.ws, p.row_begin + rec.r, lane);
+    row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane);
   }
 }
 
@@ -220,7 +254,7 @@ __global__ void __launch_bounds__(256) k_rowstats_ldg(const FwdParams p, const F
 // issue the chunk STAGES ahead (same row or the next one) into it. The first STAGES chunks
 // of a warp are issued up front; the ring then runs across row boundaries.
 // ---------------------------------------------------------------------------------------
-template <typename Tin, int NW, int STAGES, int CHUNK, int SUB>
+template <typename Tin, int NW, int STAGES, int CHUNK, int SUB, int NPOLY>
 __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
                                                              const FwdRec* list, const int* count) {
   constexpr int EPV = Vec<Tin>::EPV;
@@ -277,11 +311,45 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
     const FwdRec rec = rec_next;
     if (k + nw < n) rec_next = list[k + nw];
     const int vy = rec.y / EPV, yoff = rec.y % EPV;
-    float ref = rec.uy, S = 0.f, W = 0.f;
+    float ref = rec.uy, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f;
+    const int cy = vy / VPC;  // chunk holding the target; the ragged vector is in the last
     for (int c = 0; c < nch; ++c, ++q) {
       const int slot = q % STAGES;
       mbar_wait(&bars[slot], (q / STAGES) & 1u);
       const uint8_t* buf = ring + slot * CHUNK;
+      if (c != cy && c != nch - 1) {
+        // ---- fast chunk: full, no target, no ragged end (all but ≤ 2 chunks of a row)
+        const uint8_t* lbuf = buf + lane * 16;
+        float cSum = 0.f, cWsum = 0.f;
+#pragma unroll
+        for (int h = 0; h < NSUB; ++h) {
+          uint4 v[SUB];
+#pragma unroll
+          for (int u = 0; u < SUB; ++u) v[u] = lds128(lbuf + (h * 32 * SUB + 32 * u) * 16);
+          if (h == NSUB - 1) {
+            __syncwarp();                        // every lane has read the slot
+            if (pk < n) issue_one(slot);         // refill it STAGES chunks ahead
+          }
+          float bS, bW;
+          acc_batch<Tin, SUB, NPOLY>(v, lamL, -ref, bS, bW);
+          if (!(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {
+            kahan_add(S, cS, cSum);
+            kahan_add(W, cW, cWsum);
+            cSum = cWsum = 0.f;
+            S -= cS;
+            W -= cW;
+            cS = cW = 0.f;
+            batch_slow<Tin, SUB>(v, c * VPC + h * 32 * SUB + lane, nvec, vy, yoff, jrag, p.V,
+                                 lamL, ref, S, W, bS, bW, p.ws.err);
+          }
+          cSum += bS;
+          cWsum += bW;
+        }
+        kahan_add(S, cS, cSum);
+        kahan_add(W, cW, cWsum);
+        continue;
+      }
+      // ---- general chunk: partial end of row, target vector, ragged vocabulary end
       const int vlim = min(VPC, nvec - c * VPC);
 #pragma unroll
       for (int h = 0; h < NSUB; ++h) {
@@ -292,27 +360,31 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
           v[u] = (jl < vlim) ? lds128(buf + jl * 16) : ninf;
         }
         if (h == NSUB - 1) {
-          __syncwarp();                        // every lane has read the slot
-          if (pk < n) issue_one(slot);         // refill it STAGES chunks ahead
+          __syncwarp();
+          if (pk < n) issue_one(slot);
         }
         const int j0 = c * VPC + h * 32 * SUB + lane;
-        float bS = 0.f, bW = 0.f;
+        float bS, bW;
         acc_batch<Tin, SUB>(v, lamL, -ref, bS, bW);
-        if (special_batch<SUB>(j0, vy, jrag) || !(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f))
+        if (special_batch<SUB>(j0, vy, jrag) || !(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {
+          S -= cS;
+          W -= cW;
+          cS = cW = 0.f;
           batch_slow<Tin, SUB>(v, j0, nvec, vy, yoff, jrag, p.V, lamL, ref, S, W, bS, bW, p.ws.err);
-        S += bS;
-        W += bW;
+        }
+        kahan_add(S, cS, bS);
+        kahan_add(W, cW, bW);
       }
     }
-    row_finish(ref, S, W, rec.uy, p.ws, p.row_begin + rec.r, lane);
+    row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane);
   }
 }
 
-template <typename Tin, int NW, int STAGES, int CHUNK, int SUB>
+template <typename Tin, int NW, int STAGES, int CHUNK, int SUB, int NPOLY>
 inline cudaError_t launch_rowstats_tma_cfg(const FwdParams& p, const FwdRec* list, const int* count,
                                            int num_sms, int blocks_per_sm, cudaStream_t s) {
   constexpr size_t smem = size_t(NW) * STAGES * CHUNK + size_t(NW) * STAGES * 8;
-  auto k = k_rowstats_tma<Tin, NW, STAGES, CHUNK, SUB>;
+  auto k = k_rowstats_tma<Tin, NW, STAGES, CHUNK, SUB, NPOLY>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -328,16 +400,16 @@ inline cudaError_t launch_rowstats_tma_cfg(const FwdParams& p, const FwdRec* lis
 template <typename Tin>
 inline cudaError_t launch_rowstats_tma(const FwdParams& p, const FwdRec* list, const int* count,
                                        int num_sms, int blocks_per_sm, int variant, cudaStream_t s) {
-#define ESPO_FWD_CFG(NW, ST, CH, SB) \
-  launch_rowstats_tma_cfg<Tin, NW, ST, CH, SB>(p, list, count, num_sms, blocks_per_sm, s)
+#define ESPO_FWD_CFG(NW, ST, CH, SB, NP) \
+  launch_rowstats_tma_cfg<Tin, NW, ST, CH, SB, NP>(p, list, count, num_sms, blocks_per_sm, s)
   switch (variant) {
-    case 2: return ESPO_FWD_CFG(16, 3, 4096, 8);
-    case 3: return ESPO_FWD_CFG(8, 3, 8192, 8);
-    case 4: return ESPO_FWD_CFG(20, 2, 4096, 8);
-    case 5: return ESPO_FWD_CFG(24, 2, 4096, 4);
-    case 6: return ESPO_FWD_CFG(24, 2, 2048, 4);
-    case 7: return ESPO_FWD_CFG(32, 2, 2048, 4);
-    default: return ESPO_FWD_CFG(16, 3, 4096, 4);  // measured best on C1 (K2)
+    case 2: return ESPO_FWD_CFG(16, 3, 4096, 4, 0);
+    case 3: return ESPO_FWD_CFG(16, 3, 4096, 4, 2);
+    case 4: return ESPO_FWD_CFG(20, 2, 4096, 8, 1);
+    case 5: return ESPO_FWD_CFG(24, 2, 4096, 4, 1);
+    case 6: return ESPO_FWD_CFG(16, 3, 4096, 8, 1);
+    case 7: return ESPO_FWD_CFG(8, 3, 8192, 8, 1);
+    default: return ESPO_FWD_CFG(16, 3, 4096, 4, 1);  // measured best on C1 (K2)
   }
 #undef ESPO_FWD_CFG
 }

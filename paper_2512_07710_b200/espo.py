@@ -126,6 +126,19 @@ def _check(status, where):
 _DT = {torch.float32: F32, torch.bfloat16: BF16}
 
 
+def bootstrap_unique_id(rank: int, process_group=None) -> bytes:
+    """Rank 0 draws the NCCL unique id through libespo (espo_get_unique_id) and broadcasts
+    its 128 bytes over the caller's torch.distributed process group (gloo or nccl)."""
+    import torch.distributed as dist
+    buf = [None]
+    if rank == 0:
+        raw = ctypes.create_string_buffer(128)
+        _check(load_library().espo_get_unique_id(raw), "espo_get_unique_id")
+        buf[0] = raw.raw
+    dist.broadcast_object_list(buf, src=0, group=process_group)
+    return buf[0]
+
+
 class Espo:
     """One ESPO loss context on one CUDA device (one rank). See include/espo.h."""
 
@@ -158,14 +171,8 @@ class Espo:
         self.rank, self.world = int(rank), int(world)
         uid = None
         if self.world > 1:
-            import torch.distributed as dist
-            buf = [None]
-            if self.rank == 0:
-                raw = ctypes.create_string_buffer(128)
-                _check(lib.espo_get_unique_id(raw), "espo_get_unique_id")
-                buf[0] = raw.raw
-            dist.broadcast_object_list(buf, src=0, group=process_group)
-            uid = ctypes.create_string_buffer(buf[0], 128)
+            uid = ctypes.create_string_buffer(
+                bootstrap_unique_id(self.rank, process_group), 128)
         h = ctypes.c_void_p()
         _check(lib.espo_create(ctypes.byref(cfg), uid, self.rank, self.world,
                                self.device.index, ctypes.byref(h)), "espo_create")

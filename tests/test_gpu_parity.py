@@ -110,12 +110,17 @@ def test_chunks_any_order_bitwise(dev, c0):
     assert a["stats"] == b["stats"]
 
 
-def test_variants_agree_bitwise(dev, c0):
-    """TMA and LDG variants run the same arithmetic per row: identical outputs."""
+def test_variants_agree(dev, c0):
+    """TMA-ring and LDG variants: same per-element arithmetic, different batching of the
+    fp32 partial sums — equal within fp32 summation error; the bwd sweep is elementwise and
+    bitwise identical given identical row statistics."""
     a = run_gpu(c0, dev, fwd_impl=0, bwd_impl=0)
     b = run_gpu(c0, dev, fwd_impl=1, bwd_impl=1)
-    assert a["loss"] == b["loss"]
-    assert np.array_equal(a["dlogits"], b["dlogits"])
+    assert b["loss"] == pytest.approx(a["loss"], rel=1e-6)
+    np.testing.assert_allclose(b["dlogits"], a["dlogits"], rtol=2e-6,
+                               atol=1e-6 * np.abs(a["dlogits"]).max())
+    c = run_gpu(c0, dev, fwd_impl=0, bwd_impl=1)
+    assert np.array_equal(a["dlogits"], c["dlogits"])
 
 
 def test_determinism(dev, c0):
@@ -134,7 +139,8 @@ def test_in_place_and_padded_ld(dev):
     b = run_gpu(inst, dev, ld_pad=6, in_place=True)
     assert np.array_equal(a["dlogits"], b["dlogits"])
     c = run_gpu(inst, dev, ld_pad=6, fwd_impl=1, bwd_impl=1, in_place=True)
-    assert np.array_equal(a["dlogits"], c["dlogits"])
+    d = run_gpu(inst, dev, ld_pad=6, fwd_impl=1, bwd_impl=1)
+    assert np.array_equal(c["dlogits"], d["dlogits"])
 
 
 @pytest.mark.parametrize("impl", [0, 1], ids=["tma", "ldg"])
