@@ -1,0 +1,112 @@
+"""Turn the raw ncu outputs of a round (gpurun_out/) into the committed summaries under
+profiles/<tag>/:  launches.md (per-kernel share of a step from the gpu__time_duration launch
+list), ncu_<name>.md (key metrics of each `--set full` capture), traffic.md + the
+profiles/ncu_traffic.json that bench.py reads for roofline.traffic (DRAM bytes per sweep
+launch averaged over one step's launches)."""
+import csv
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import launch_summary  # noqa: E402
+import ncu_summary  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def raw_rows(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    return rows[0], rows[1], rows[2:]
+
+
+def full_capture_md(rep, title):
+    hdr, units, rows = raw_rows(rep)
+    lines = [f"# {title}", "", f"source: `{os.path.basename(rep)}` (ncu --set full "
+             "--clock-control none --import-source on; cold-cache replays)", ""]
+    for n, vals in enumerate(rows):
+        lines.append(f"## launch {n}")
+        lines.append("")
+        lines.append("| metric | value | unit |")
+        lines.append("|---|---|---|")
+        for w in ncu_summary.WANT:
+            for i, h in enumerate(hdr):
+                if h == w:
+                    lines.append(f"| `{w}` | {vals[i]} | {units[i]} |")
+        lines.append("")
+    return "\n".join(lines)
+
+
+def traffic(csv_path):
+    """Mean DRAM bytes per espo_loss_fwd / espo_loss_bwd call from a metrics launch list."""
+    with open(csv_path) as f:
+        lines = [l for l in f if l.startswith('"')]
+    per = {}
+    for r in csv.DictReader(lines):
+        k = launch_summary.short(r["Kernel Name"])
+        if not k.startswith("k_"):
+            continue
+        v = float(r["Metric Value"].replace(",", ""))
+        u = r["Metric Unit"].lower()
+        scale = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "ns": 1, "usecond": 1e3,
+                 "msecond": 1e6}.get(u, 1)
+        per.setdefault((r["ID"], k), {})[r["Metric Name"]] = v * scale
+    fwd, bwd = [], []
+    for (i, k), m in per.items():
+        b = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+        if k.startswith(("k_rowstats", "k_fwd_rows")):
+            fwd.append((int(i), k, b, m.get("gpu__time_duration.sum", 0)))
+        if k.startswith(("k_dlogits", "k_bwd_rows")):
+            bwd.append((int(i), k, b, m.get("gpu__time_duration.sum", 0)))
+    nf = len([x for x in fwd if x[1].startswith("k_rowstats")])
+    nb = len([x for x in bwd if x[1].startswith("k_dlogits")])
+    return {"fwd_bytes_per_launch": sum(x[2] for x in fwd) / max(nf, 1),
+            "bwd_bytes_per_launch": sum(x[2] for x in bwd) / max(nb, 1),
+            "fwd_launches": nf, "bwd_launches": nb,
+            "fwd_ms_total": sum(x[3] for x in fwd) / 1e6, "bwd_ms_total": sum(x[3] for x in bwd) / 1e6}
+
+
+def main(tag, out_dir="gpurun_out"):
+    dst = os.path.join(ROOT, "profiles", tag)
+    os.makedirs(dst, exist_ok=True)
+    src = os.path.join(ROOT, out_dir)
+    ll = os.path.join(src, "launches.csv")
+    if os.path.exists(ll):
+        shutil.copy(ll, os.path.join(dst, "launches.csv"))
+        import io
+        import contextlib
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            launch_summary.main(ll)
+        open(os.path.join(dst, "launches.md"), "w").write(
+            "# ncu launch list (gpu__time_duration.sum, --clock-control none)\n\n"
+            "Command: `python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline` "
+            "(cold-cache serialised per-launch times: compare shares, not absolutes).\n\n"
+            + buf.getvalue())
+    for name in ("fwd", "bwd"):
+        rep = os.path.join(src, f"prof_{name}.ncu-rep")
+        if os.path.exists(rep):
+            open(os.path.join(dst, f"ncu_{name}.md"), "w").write(
+                full_capture_md(rep, f"K{'2' if name == 'fwd' else '5'} {name} sweep"))
+    tr = os.path.join(src, "traffic.csv")
+    if os.path.exists(tr):
+        t = traffic(tr)
+        t["source"] = f"profiles/{tag}/traffic.csv (ncu dram__bytes_read/write over one step)"
+        shutil.copy(tr, os.path.join(dst, "traffic.csv"))
+        json.dump(t, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+        open(os.path.join(dst, "traffic.md"), "w").write(
+            "# DRAM traffic per sweep launch (one step, ncu)\n\n```\n" + json.dumps(t, indent=1)
+            + "\n```\n")
+    for f in ("bench_full.json", "bench_full.err"):
+        p = os.path.join(src, f)
+        if os.path.exists(p):
+            shutil.copy(p, os.path.join(dst, f))
+    print("wrote", dst)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], *(sys.argv[2:3]))
