@@ -42,7 +42,7 @@ def parse():
     p.add_argument("--config", default="C1")
     p.add_argument("--buffer-rows", type=int, default=32768)
     p.add_argument("--fwd-impl", type=int, default=0, help="0/2/3/4 = TMA ring variants, 1 = LDG")
-    p.add_argument("--bwd-impl", type=int, default=0, help="0 = TMA ring, 1 = LDG")
+    p.add_argument("--bwd-impl", type=int, default=0, help="0/7 = tiled grid, 1 = LDG, 2-6 = TMA rings")
     p.add_argument("--blocks-per-sm", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=1)
     p.add_argument("--e2e-host-rows", type=int, default=2048)
@@ -381,8 +381,8 @@ def main_ours(args):
             "global_batch_tokens": T * world, "seq_len": w.L, "parallelism": f"dp{world} (prompt-group sharded)",
             "chunk_rows": d["Rc"], "l2": "inputs larger than L2 (chunk buffer "
                                          f"{d['Rc'] * V * 2 / 1e9:.2f} GB > 126 MB)",
-            "fwd_impl": ["tma16x3x4k_s4_p1", "ldg", "tma16x3x4k_s4_p0", "tma16x3x4k_s4_p2", "tma20x2x4k_s8_p1", "tma24x2x4k_s4_p1", "tma16x3x4k_s8_p1", "tma8x3x8k_s8_p1"][args.fwd_impl],
-            "bwd_impl": ["tma8x4x4k", "ldg", "tma16x3x4k", "tma16x2x4k", "tma12x4x4k", "tma8x6x4k"][args.bwd_impl],
+            "fwd_impl": ["tma16x3x4k_s4_p0", "ldg", "tma16x3x4k_s4_p1", "tma16x3x4k_s4_p2", "tma20x2x4k_s8_p1", "tma24x2x4k_s4_p1", "tma16x3x4k_s8_p1", "tma8x3x8k_s8_p1"][args.fwd_impl],
+            "bwd_impl": ["tile32k", "ldg", "tma16x3x4k", "tma16x2x4k", "tma12x4x4k", "tma8x6x4k", "tma8x4x4k", "tile16k"][args.bwd_impl],
             "achieved_hbm_gbs_step": step_gbs, "frac_of_8TBs_step": step_gbs / NOMINAL_HBM_GBS,
             "frac_of_measured_step": step_gbs / peak,
             "fwd_sweep_gbs": fwd_gbs, "fwd_sweep_ms_per_chunk": fwd_ms,

@@ -206,8 +206,10 @@ uint64_t espo_launch_count(espo_ctx_t ctx);
 
 /* Kernel-variant switches for A/B measurement. */
 typedef enum {
-  ESPO_OPT_FWD_IMPL = 0,       /* 0 = TMA bulk-copy smem ring (default), 1 = LDG.128 */
-  ESPO_OPT_BWD_IMPL = 1,       /* 0 = TMA bulk-copy smem ring (default), 1 = LDG.128 */
+  ESPO_OPT_FWD_IMPL = 0,       /* 0 = TMA bulk-copy smem ring (default), 1 = LDG.128 warp per
+                                  row, 2..7 = other ring geometries (K2) */
+  ESPO_OPT_BWD_IMPL = 1,       /* 0 = tiled (row, 32 KB tile) grid (default), 1 = LDG.128 warp
+                                  per row, 2..6 = TMA ring geometries, 7 = 16 KB tiles */
   ESPO_OPT_BLOCKS_PER_SM = 2   /* persistent grid = blocks_per_sm × SM count (0 = auto) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);

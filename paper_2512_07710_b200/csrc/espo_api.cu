@@ -311,7 +311,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->fwd_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_BWD_IMPL:
-      if (value < 0 || value > 5) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 7) return ESPO_ERR_INVALID_ARGUMENT;
       c->bwd_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_BLOCKS_PER_SM:
@@ -498,8 +498,30 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
   BwdRec* list = static_cast<BwdRec*>(c->ws.list);
   int32_t* zl = c->ws.zlist;
   int* cnt = c->ws.count;
-  ESPO_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), s));
   const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  if (c->bwd_impl == 0 || c->bwd_impl == 7) {
+    // tiled (default): per-row records indexed by row, non-persistent (row, tile) grid
+    k_bwd_recs<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, p.zero_fill, c->ws, list);
+    ESPO_LAUNCHED(c);
+    const int epv = bi ? 8 : 4;
+    const int nvec = (cf.vocab + epv - 1) / epv;
+    const int vpt = (c->bwd_impl == 7) ? 4 : 8;  // default 0: 32 KB tiles (measured best)
+    const int ntiles = (nvec + 256 * vpt - 1) / (256 * vpt);
+    const int64_t grid = n_rows * int64_t(ntiles);
+    if (grid > INT32_MAX) return ESPO_ERR_INVALID_ARGUMENT;
+    if (vpt == 4) {
+      if (bi && bo) k_dlogits_tile<__nv_bfloat16, __nv_bfloat16, 4><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+      else if (bi) k_dlogits_tile<__nv_bfloat16, float, 4><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+      else k_dlogits_tile<float, float, 4><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+    } else {
+      if (bi && bo) k_dlogits_tile<__nv_bfloat16, __nv_bfloat16, 8><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+      else if (bi) k_dlogits_tile<__nv_bfloat16, float, 8><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+      else k_dlogits_tile<float, float, 8><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+    }
+    ESPO_LAUNCHED(c);
+    return ESPO_OK;
+  }
+  ESPO_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), s));
   k_bwd_rows<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, p.zero_fill, c->ws, list, zl, cnt);
   ESPO_LAUNCHED(c);
   if (c->bwd_impl == 1) {
@@ -515,7 +537,7 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
     }
   } else {
     cudaError_t le;
-    const int v = c->bwd_impl;
+    const int v = c->bwd_impl;  // 2..5 geometry variants, 6 = 8 warps × 4 × 4 KB
     if (bi && bo) le = launch_dlogits_tma<__nv_bfloat16, __nv_bfloat16>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
     else if (bi) le = launch_dlogits_tma<__nv_bfloat16, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
     else le = launch_dlogits_tma<float, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);

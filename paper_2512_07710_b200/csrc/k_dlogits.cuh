@@ -211,6 +211,54 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dlogits_tma(const BwdParams p, c
   zero_rows<Tout>(p, zlist, nz, gw, nw, lane);
 }
 
+// Tiled variant: a non-persistent grid of (row, tile) blocks in row-major order, 256 threads,
+// VPT 16-byte input vectors per thread (16 KB bf16 tile): every block reads its tile with all
+// loads in flight, computes and writes it back — the access pattern of the fastest copy
+// measured on this part (tools/bwprobe.cu: 6.9 TB/s vs 6.3 for per-warp rings), and a
+// zero-fill tile is a pure write.
+template <typename Tin, typename Tout, int VPT>
+__global__ void __launch_bounds__(256) k_dlogits_tile(const BwdParams p, const BwdRec* rec,
+                                                      int ntiles) {
+  constexpr int EPV = Vec<Tin>::EPV;
+  const int r = blockIdx.x / ntiles;
+  const int tile = blockIdx.x - r * ntiles;
+  const BwdRec rc = rec[r];
+  if (rc.y == -2) return;
+  const int nvec = (p.V + EPV - 1) / EPV;
+  const int j0 = tile * (256 * VPT) + threadIdx.x;
+  char* orow = static_cast<char*>(p.dlogits) + int64_t(rc.r) * p.ldg * int64_t(sizeof(Tout));
+  if (rc.y < 0) {
+    float z[EPV];
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) z[e] = 0.f;
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int j = j0 + 256 * u;
+      if (j < nvec) store_out<Tin, Tout>(orow, j, z, p.V);
+    }
+    return;
+  }
+  const char* row = static_cast<const char*>(p.logits) + int64_t(rc.r) * p.ld * int64_t(sizeof(Tin));
+  const float lamL = p.lam_log2e;
+  const int vy = rc.y / EPV, yoff = rc.y % EPV;
+  uint4 v[VPT];
+#pragma unroll
+  for (int u = 0; u < VPT; ++u) {
+    const int j = j0 + 256 * u;
+    if (j < nvec)
+      v[u] = p.aliased ? ld_stream_coherent(row + int64_t(j) * 16) : ld_stream(row + int64_t(j) * 16);
+  }
+#pragma unroll
+  for (int u = 0; u < VPT; ++u) {
+    const int j = j0 + 256 * u;
+    if (j < nvec) {
+      float dd[EPV];
+      dz_vec<Tin>(v[u], j, vy, yoff, lamL, rc, dd);
+      store_out<Tin, Tout>(orow, j, dd, p.V);
+    }
+  }
+}
+
 template <typename Tin, typename Tout, int NW, int STAGES, int CHUNK>
 inline cudaError_t launch_dlogits_tma_cfg(const BwdParams& p, const BwdRec* list,
                                           const int32_t* zlist, const int* count, int num_sms,

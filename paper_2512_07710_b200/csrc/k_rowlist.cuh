@@ -120,4 +120,32 @@ __global__ void __launch_bounds__(256) k_bwd_rows(int64_t row_begin, int64_t n_r
   }
 }
 
+// Backward, tiled variant: one record per chunk row, indexed by the row (no compaction):
+// y ≥ 0 sweep, y = −1 zero-fill, y = −2 leave untouched (no gradient and zero_fill == 0).
+__global__ void __launch_bounds__(256) k_bwd_recs(int64_t row_begin, int64_t n_rows,
+                                                  const float* grad_loss, int zero_fill,
+                                                  Workspace ws, BwdRec* rec) {
+  const float gl = grad_loss ? *grad_loss : 1.f;
+  const float gscale = -gl * *ws.bwd_scale;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = row_begin + r;
+    const float c = ws.flag[t] ? ws.coef[t] : 0.f;
+    const float g = gscale * c;
+    BwdRec o;
+    o.r = static_cast<int32_t>(r);
+    o.pad[0] = o.pad[1] = o.pad[2] = 0.f;
+    if (g != 0.f) {
+      o.y = ws.y[t];
+      o.ng = -g;
+      o.nlseL = -ws.lse[t] * kLog2e;
+      o.gq = g * ws.q[t];
+    } else {
+      o.y = zero_fill ? -1 : -2;
+      o.ng = o.nlseL = o.gq = 0.f;
+    }
+    rec[r] = o;
+  }
+}
+
 }  // namespace espo
