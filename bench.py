@@ -390,7 +390,7 @@ def main_ours(args):
             "active_tokens": n_act, "clipped_tokens": n_clip,
             "zv_groups": st["n_zv_groups"], "groups": st["n_groups"],
         },
-        "roofline": {"bound": "hbm", "kernel": "espo_loss_bwd sweep (k_bwd_rows + k_dlogits)",
+        "roofline": {"bound": "hbm", "kernel": "espo_loss_bwd sweep (k_bwd_recs + k_dlogits_tile)",
                      "achieved": bwd_gbs, "peak": peak, "unit": "GB/s",
                      "frac": bwd_gbs / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": bwd_bytes / n_chunks},

@@ -60,7 +60,7 @@ def traffic(csv_path):
         b = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
         if k.startswith(("k_rowstats", "k_fwd_rows")):
             fwd.append((int(i), k, b, m.get("gpu__time_duration.sum", 0)))
-        if k.startswith(("k_dlogits", "k_bwd_rows")):
+        if k.startswith(("k_dlogits", "k_bwd_rows", "k_bwd_recs")):
             bwd.append((int(i), k, b, m.get("gpu__time_duration.sum", 0)))
     nf = len([x for x in fwd if x[1].startswith("k_rowstats")])
     nb = len([x for x in bwd if x[1].startswith("k_dlogits")])
