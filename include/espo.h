@@ -92,6 +92,13 @@ typedef enum { ESPO_PART_QUANTILE = 0, ESPO_PART_WHOLE = 1, ESPO_PART_SINGLETON 
  * (PAPER.md:105). TOKEN: J = (1/T_active) Σ_t ℓ_t. */
 typedef enum { ESPO_NORM_SEQ = 0, ESPO_NORM_TOKEN = 1 } espo_norm;
 
+/* Zero-variance groups (§2.4.1). MASK (default, north_star): eliminated — Â = 0, rows never
+ * read, not counted in N. RLZVP: ZVE stage 3 "advantage reshaping" with the
+ * RL-ZVP instantiation of SPEC.md:338-343 — the group's rows are read and token t of rollout
+ * i gets Â_t = β·s·(e_t − ē_i)/log|V|, s = +1 if the group's reward < zvp_threshold else −1,
+ * ē_i the rollout's mean token entropy; such rollouts count in N. */
+typedef enum { ESPO_ZV_MASK = 0, ESPO_ZV_RLZVP = 1 } espo_zv_mode;
+
 typedef struct {
   int32_t vocab;               /* V: row width; log|V| of Eq. 3 (Q6) */
   float alpha;                 /* Eq. 3 α (Q5), default 0.4 */
@@ -111,7 +118,10 @@ typedef struct {
   int32_t grad_dtype;          /* espo_dtype of dlogits (bf16 logits may emit f32 grads) */
   int32_t zero_fill_inactive_rows; /* 1 (default): bwd writes 0 to rows of masked tokens,
                                       ZV groups and clipped tokens; 0: leaves them as-is */
-  int32_t reserved[7];
+  int32_t zv_mode;             /* espo_zv_mode, default MASK */
+  float zvp_beta;              /* RL-ZVP β, default 0.05 (|Â_t| ≤ β) */
+  float zvp_threshold;         /* RL-ZVP success threshold on the uniform reward, default 0.5 */
+  int32_t reserved[4];
 } espo_config;
 
 /* Device-written statistics (all fp64). Per-bucket arrays are indexed by the pre-drop

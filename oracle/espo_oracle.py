@@ -53,6 +53,9 @@ RATIO_LITERAL_OLD = 1  # reading R1
 NORM_SEQ = 0  # paper: 1/N_rollouts · 1/#buckets · 1/|y_τ|
 NORM_TOKEN = 1  # 1/T_active
 
+ZV_MASK = 0   # zero-variance groups eliminated (north_star default)
+ZV_RLZVP = 1  # ZVE stage 3: RL-ZVP entropy-guided advantages
+
 MAX_STAT_BUCKETS = 4
 
 
@@ -80,6 +83,9 @@ class OracleConfig:
     zv_var_eps: float = 0.0
     logit_scale: float = 1.0
     log_ratio_clamp: float = 20.0
+    zv_mode: int = ZV_MASK
+    zvp_beta: float = 0.05
+    zvp_threshold: float = 0.5
 
 
 # ----------------------------------------------------------------------------------------
@@ -154,6 +160,17 @@ def group_advantages(rewards, group_ids, cfg: OracleConfig) -> dict:
         "n_groups": len(groups),
         "n_zv_groups": int(sum(zv_g)),
     }
+
+
+def zvp_token_advantages(H, reward: float, cfg: OracleConfig):
+    """O1' (RL-ZVP, ZVE stage 3 "Advantage reshaping"; instantiation of the cited
+    method from SPEC.md:338-343): for a rollout of a zero-variance group with reward r,
+    a_t = β·s·(e_t − ē)/log|V|, s = +1 if r < threshold (all fail: favour exploration) else −1,
+    ē = the rollout's mean token entropy. |a_t| ≤ β and Σ_t a_t = 0."""
+    H = np.asarray(H, dtype=np.float64)
+    sgn = 1.0 if reward < cfg.zvp_threshold else -1.0
+    hbar = float(sum(H.tolist())) / len(H)
+    return np.array([cfg.zvp_beta * sgn * (h - hbar) / math.log(cfg.vocab) for h in H.tolist()])
 
 
 # ----------------------------------------------------------------------------------------
@@ -280,6 +297,7 @@ class OracleResult:
     eps_tok: np.ndarray      # ε_τ of the token's bucket
     s_tok: np.ndarray        # s_τ of the token's bucket
     coef: np.ndarray         # c_t = ∂J_i/∂lp_t (before 1/D)
+    adv_tok: np.ndarray      # advantage used for each token (NaN if not evaluated)
     w_tok: np.ndarray        # normaliser weight of the token inside J_i
     theta: dict = field(default_factory=dict)   # rollout -> thresholds (quantile mode)
     stats: dict = field(default_factory=dict)
@@ -332,8 +350,11 @@ def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
     sum_H = 0.0
     n_clipped = 0
 
+    rewards32 = np.asarray(rewards, dtype=np.float32)
+    adv_tok = np.full(T, np.nan)
     for i in range(R):
-        if grp["zv"][i]:
+        zvp = bool(grp["zv"][i]) and cfg.zv_mode == ZV_RLZVP
+        if grp["zv"][i] and not zvp:
             continue                       # eliminated group: never read (P3)
         rows = np.arange(seq_offsets[i], seq_offsets[i + 1])
         valid = rows[mask[rows]]
@@ -357,6 +378,9 @@ def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
             lse_a[t], lp_a[t], H_a[t], q_a[t] = st
             lp[j], H[j] = st[1], st[2]
         old = old_logp[valid]
+        # per-token advantages: the group's Â broadcast, or RL-ZVP's a_t
+        A_t = zvp_token_advantages(H, float(rewards32[i]), cfg) if zvp else np.full(n, A)
+        adv_tok[valid] = A_t
 
         # O3 partition
         b, nb = partition(H, cfg)
@@ -381,11 +405,12 @@ def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
                     v = s                     # sg[s_τ]·π_θ/sg[π_θ]: value s_τ
                 else:
                     v = s * math.exp(lp[j] - old[j])
-                ell, kap = token_surrogate(v, A, eps)
+                At = float(A_t[j])
+                ell, kap = token_surrogate(v, At, eps)
                 if inject_kappa is not None:
                     kap = bool(np.asarray(inject_kappa)[t])
                 Ji += w * ell
-                coef_a[t] = A * v * w if kap else 0.0
+                coef_a[t] = At * v * w if kap else 0.0
                 sk = 0 if cfg.partition != PARTITION_QUANTILE else k
                 bucket_a[t] = sk
                 kappa_a[t] = 1 if kap else 0
@@ -422,7 +447,8 @@ def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
     return OracleResult(loss=loss, J_sum=J_sum, denom=denom, adv=grp["adv"], zv=grp["zv"],
                         active=active, n_valid=n_valid, J_i=J_i, nb=nb_a, lse=lse_a,
                         lp=lp_a, H=H_a, q=q_a, bucket=bucket_a, kappa=kappa_a, v=v_a,
-                        eps_tok=eps_a, s_tok=s_a, coef=coef_a, w_tok=w_a, theta=theta,
+                        eps_tok=eps_a, s_tok=s_a, coef=coef_a, adv_tok=adv_tok, w_tok=w_a,
+                        theta=theta,
                         stats=stats,
                         group=grp)
 
@@ -456,10 +482,10 @@ def frozen_surrogate_loss(logits_eval, res: OracleResult, tokens, old_logp, seq_
     for i in range(R):
         if not res.active[i]:
             continue
-        A = float(res.adv[i])
         for t in range(int(seq_offsets[i]), int(seq_offsets[i + 1])):
             if res.kappa[t] < 0:
                 continue
+            A = float(res.adv_tok[t])
             _, lp_z, _, _ = row_stats(logits_eval[t], int(tokens[t]), cfg.logit_scale)
             if cfg.ratio_mode == RATIO_GSPO_TOKEN:
                 v = res.s_tok[t] * math.exp(lp_z - res.lp[t])

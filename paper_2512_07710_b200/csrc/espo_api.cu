@@ -112,6 +112,9 @@ espo_status validate_config(const espo_config& c) {
       (c.grad_dtype != ESPO_F32 && c.grad_dtype != ESPO_BF16))
     return ESPO_ERR_INVALID_ARGUMENT;
   if (c.logits_dtype == ESPO_F32 && c.grad_dtype == ESPO_BF16) return ESPO_ERR_UNSUPPORTED;
+  if (c.zv_mode < 0 || c.zv_mode > 1 || !(c.zvp_beta >= 0.f) || !std::isfinite(c.zvp_beta) ||
+      !std::isfinite(c.zvp_threshold))
+    return ESPO_ERR_INVALID_ARGUMENT;
   return ESPO_OK;
 }
 
@@ -149,13 +152,14 @@ espo_status ensure_workspace(espo_ctx_t c, int R, int64_t T) {
     const size_t a4 = round_up(size_t(cap) * 4, 256);
     const size_t ath = round_up(size_t(cap) * (kMaxK - 1) * 4, 256);
     const size_t ared = round_up(size_t(cap) * kRedLen * 8, 256);
-    ESPO_CUDA(cudaMalloc(&c->blocks_roll, 3 * a8 + 3 * a1 + a4 + ath + ared));
+    ESPO_CUDA(cudaMalloc(&c->blocks_roll, 3 * a8 + 4 * a1 + a4 + ath + ared));
     char* p = static_cast<char*>(c->blocks_roll);
     auto take = [&](size_t n) { char* r = p; p += n; return r; };
     c->ws.seq_off = reinterpret_cast<int64_t*>(take(a8));
     c->ws.adv = reinterpret_cast<double*>(take(a8));
     c->ws.J = reinterpret_cast<double*>(take(a8));
     c->ws.cand = reinterpret_cast<uint8_t*>(take(a1));
+    c->ws.zsign = reinterpret_cast<int8_t*>(take(a1));
     c->ws.ghead = reinterpret_cast<uint8_t*>(take(a1));
     c->ws.active = reinterpret_cast<uint8_t*>(take(a1));
     c->ws.nb = reinterpret_cast<int32_t*>(take(a4));
@@ -214,6 +218,9 @@ void espo_config_default(espo_config* cfg, int32_t vocab) {
   cfg->logits_dtype = ESPO_BF16;
   cfg->grad_dtype = ESPO_BF16;
   cfg->zero_fill_inactive_rows = 1;
+  cfg->zv_mode = ESPO_ZV_MASK;
+  cfg->zvp_beta = 0.05f;
+  cfg->zvp_threshold = 0.5f;
 }
 
 const char* espo_status_string(espo_status s) {
@@ -348,6 +355,8 @@ espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* grou
   p.std_unbiased = c->cfg.std_unbiased;
   p.adv_eps = c->cfg.adv_eps;
   p.zv_var_eps = c->cfg.zv_var_eps;
+  p.zv_mode = c->cfg.zv_mode;
+  p.zvp_threshold = c->cfg.zvp_threshold;
   p.adv_out = adv_out;
   p.zv_out = zv_out;
   p.ws = c->ws;
@@ -445,6 +454,7 @@ espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_
     sp.norm = cf.norm;
     sp.log_ratio_clamp = cf.log_ratio_clamp;
     sp.inv_logV = 1.0 / std::log(static_cast<double>(cf.vocab));
+    sp.zvp_beta = cf.zvp_beta;
     sp.ws = c->ws;
     k_seq_reduce<<<c->R, kSeqThreads, 0, s>>>(sp);
     ESPO_LAUNCHED(c);

@@ -15,6 +15,8 @@ struct PrepParams {
   int64_t T;
   int std_unbiased;
   double adv_eps, zv_var_eps;
+  int zv_mode;
+  float zvp_threshold;
   float* adv_out;   // nullable
   uint8_t* zv_out;  // nullable
   Workspace ws;
@@ -61,10 +63,12 @@ __global__ void k_prepare_groups(const PrepParams p) {
   else if (p.zv_var_eps > 0.0) zv = var <= p.zv_var_eps;
   else zv = all_eq;
   const double den = __dadd_rn(sigma, p.adv_eps);
+  const bool zvp = zv && p.zv_mode == ESPO_ZV_RLZVP;
   for (int j = i; j < e; ++j) {
     const double a = zv ? 0.0 : __ddiv_rn(__dsub_rn(static_cast<double>(p.rewards[j]), mu), den);
     p.ws.adv[j] = a;
-    p.ws.cand[j] = zv ? 0 : 1;
+    p.ws.cand[j] = (zv && !zvp) ? 0 : 1;
+    p.ws.zsign[j] = zvp ? (p.rewards[j] < p.zvp_threshold ? 1 : -1) : 0;
     p.ws.ghead[j] = (j == i) ? (zv ? 2 : 1) : 0;
     if (p.adv_out) p.adv_out[j] = static_cast<float>(a);
     if (p.zv_out) p.zv_out[j] = zv ? 1 : 0;
@@ -88,6 +92,7 @@ struct SeqParams {
   int partition, ratio_mode, norm;
   double log_ratio_clamp;
   double inv_logV;
+  double zvp_beta;
   Workspace ws;
 };
 
@@ -194,6 +199,16 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_reduce(const SeqParams p) {
     return;
   }
   const double A = ws.adv[i];
+  const int zs = ws.zsign[i];
+  // RL-ZVP: ē_i (fp64, fixed order) for Â_t = β·s·(e_t − ē_i)/log|V|
+  double hbar = 0.0;
+  if (zs != 0) {
+    double hl = 0.0;
+    for (int64_t t = b + threadIdx.x; t < e; t += blockDim.x)
+      if (ws.flag[t]) hl += static_cast<double>(ws.H[t]);
+    hbar = block_sum<double>(hl, shd) / static_cast<double>(n);
+  }
+  const double zscale = p.zvp_beta * static_cast<double>(zs) * p.inv_logV;
   const bool quant = (p.partition == ESPO_PART_QUANTILE) && p.K > 1;
   const bool single = (p.partition == ESPO_PART_SINGLETON);
   const int K = quant ? p.K : 1;
@@ -286,12 +301,13 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_reduce(const SeqParams p) {
       s = s_s[bk]; eps = s_eps[bk]; w = s_w[bk];
     }
     const double v = (p.ratio_mode == ESPO_RATIO_GSPO_TOKEN) ? s : s * exp(lp - old);
+    const double At = zs ? zscale * (h - hbar) : A;
     const double lo = 1.0 - eps, hi = 1.0 + eps;
     const double vc = fmin(fmax(v, lo), hi);
-    const double ell = fmin(v * A, vc * A);
-    const bool clipped = (A > 0 && v > hi) || (A < 0 && v < lo);
+    const double ell = fmin(v * At, vc * At);
+    const bool clipped = (At > 0 && v > hi) || (At < 0 && v < lo);
     Jl += w * ell;
-    ws.coef[t] = clipped ? 0.f : static_cast<float>(A * v * w);
+    ws.coef[t] = clipped ? 0.f : static_cast<float>(At * v * w);
     const int sb = quant ? bk : 0;
     ws.bucket[t] = static_cast<uint8_t>(sb);
     ws.clip[t] = clipped ? 1 : 0;

@@ -22,7 +22,8 @@ struct Workspace {
   // ---- per rollout [R] ----
   int64_t* seq_off = nullptr;  // [R+1] copy of seq_offsets       (K1)
   double* adv = nullptr;       // Â_i (0 for ZV)                  (K1)
-  uint8_t* cand = nullptr;     // 1 = group not eliminated        (K1)
+  uint8_t* cand = nullptr;     // 1 = rows are read (group not eliminated) (K1)
+  int8_t* zsign = nullptr;     // RL-ZVP: +1 / −1 reshaped ZV rollout, 0 otherwise (K1)
   uint8_t* ghead = nullptr;    // 1 = first rollout of a group, 2 = first of a ZV group
   uint8_t* active = nullptr;   // cand ∧ n_i ≥ 1                  (K3)
   int32_t* nb = nullptr;       // non-empty buckets               (K3)

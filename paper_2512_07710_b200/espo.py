@@ -24,6 +24,7 @@ F32, BF16 = 0, 1
 PART_QUANTILE, PART_WHOLE, PART_SINGLETON = 0, 1, 2
 RATIO_GSPO_TOKEN, RATIO_LITERAL_OLD = 0, 1
 NORM_SEQ, NORM_TOKEN = 0, 1
+ZV_MASK, ZV_RLZVP = 0, 1
 OPT_FWD_IMPL, OPT_BWD_IMPL, OPT_BLOCKS_PER_SM = 0, 1, 2
 
 STATUS = {
@@ -58,7 +59,8 @@ class Config(ctypes.Structure):
         ("zv_var_eps", ctypes.c_double), ("logit_scale", ctypes.c_float),
         ("log_ratio_clamp", ctypes.c_float), ("logits_dtype", ctypes.c_int32),
         ("grad_dtype", ctypes.c_int32), ("zero_fill_inactive_rows", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 7),
+        ("zv_mode", ctypes.c_int32), ("zvp_beta", ctypes.c_float),
+        ("zvp_threshold", ctypes.c_float), ("reserved", ctypes.c_int32 * 4),
     ]
 
 
@@ -146,8 +148,8 @@ class Espo:
                  partition=PART_QUANTILE, ratio_mode=RATIO_GSPO_TOKEN, norm=NORM_SEQ,
                  std_unbiased=False, adv_eps=1e-6, zv_var_eps=0.0, logit_scale=1.0,
                  log_ratio_clamp=20.0, logits_dtype=torch.bfloat16, grad_dtype=None,
-                 zero_fill_inactive_rows=True, device=None, rank=0, world=1,
-                 process_group=None):
+                 zero_fill_inactive_rows=True, zv_mode=ZV_MASK, zvp_beta=0.05,
+                 zvp_threshold=0.5, device=None, rank=0, world=1, process_group=None):
         lib = load_library()
         self._lib = lib
         cfg = Config()
@@ -163,6 +165,8 @@ class Espo:
         self.grad_dtype = grad_dtype if grad_dtype is not None else logits_dtype
         cfg.logits_dtype, cfg.grad_dtype = _DT[self.logits_dtype], _DT[self.grad_dtype]
         cfg.zero_fill_inactive_rows = int(bool(zero_fill_inactive_rows))
+        cfg.zv_mode = int(zv_mode)
+        cfg.zvp_beta, cfg.zvp_threshold = float(zvp_beta), float(zvp_threshold)
         self.cfg = cfg
         self.vocab = int(vocab)
         if device is None:

@@ -14,7 +14,7 @@ GPU_TO_ORACLE = dict(alpha="alpha", eps_min="eps_min", n_buckets="n_buckets",
                      partition="partition", ratio_mode="ratio_mode", norm="norm",
                      std_unbiased="std_unbiased", adv_eps="adv_eps", zv_var_eps="zv_var_eps",
                      logit_scale="logit_scale", log_ratio_clamp="log_ratio_clamp")
-F32_FIELDS = ("alpha", "eps_min", "logit_scale", "log_ratio_clamp")
+F32_FIELDS = ("alpha", "eps_min", "logit_scale", "log_ratio_clamp", "zvp_beta", "zvp_threshold")
 
 
 def require_cuda():
@@ -25,7 +25,8 @@ def require_cuda():
 
 def oracle_cfg(V, **kw):
     """The oracle sees exactly the values the C config holds (float fields are f32)."""
-    d = dict(alpha=0.4, eps_min=0.01, logit_scale=1.0, log_ratio_clamp=20.0)
+    d = dict(alpha=0.4, eps_min=0.01, logit_scale=1.0, log_ratio_clamp=20.0, zvp_beta=0.05,
+             zvp_threshold=0.5)
     d.update(kw)
     for k in F32_FIELDS:
         d[k] = float(np.float32(d[k]))

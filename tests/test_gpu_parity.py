@@ -149,3 +149,39 @@ def test_bf16_ragged_vocab(dev, impl):
     g = run_gpu(inst, dev, logits_dtype=torch.bfloat16, grad_dtype=torch.float32, ld_pad=5,
                 fwd_impl=impl, bwd_impl=impl)
     full_check(g, inst, oracle_cfg(inst.V))
+
+
+def test_rlzvp_mode(dev):
+    """ZVE stage 3 as RL-ZVP: zero-variance groups are read and get entropy-
+    guided token advantages. The token advantage β·s·(e_t − ē)/log V is a difference of
+    entropies, so its fp32-vs-fp64 error is absolute (≈ β·1e-6/log V): coefficients and
+    gradient rows of ZV rollouts are compared at that absolute scale."""
+    inst = workload_instance("C0")
+    kw = dict(zv_mode=O.ZV_RLZVP, zvp_beta=0.2)
+    g = run_gpu(inst, dev, cfgkw=kw)
+    cfg = oracle_cfg(inst.V, **kw)
+    ref = inst.run(cfg)
+    check_exact_fields(g, ref)
+    check_token_stats(g, ref)
+    assert g["stats"]["n_zv_groups"] == 1 and ref.active.all()
+    ref2, _ = decision_aware_reference(g, inst, ref, cfg)
+    check_loss(g, ref2, 1e-5)
+    zv_rows = np.zeros(inst.T, bool)
+    for i in range(inst.R):
+        if ref.zv[i]:
+            zv_rows[inst.seq_offsets[i]:inst.seq_offsets[i + 1]] = True
+    v = ref2.kappa >= 0
+    atol_c = cfg.zvp_beta / np.log(inst.V) * 2e-5 * np.nanmax(ref2.w_tok) * 1.1
+    dc = np.abs(g["tok"]["coef"].astype(np.float64) - ref2.coef)
+    assert np.all(dc[v & ~zv_rows] <= 1e-5 * np.abs(ref2.coef[v & ~zv_rows]) + 1e-12)
+    assert np.all(dc[v & zv_rows] <= 1e-5 * np.abs(ref2.coef[v & zv_rows]) + atol_c)
+    rows = np.arange(inst.T)
+    want = oracle_dlogits(ref2, inst, cfg, rows)
+    check_dlogits_f32(g["dlogits"][~zv_rows], want[~zv_rows])
+    scale = np.abs(want[zv_rows]).max()
+    assert np.abs(g["dlogits"][zv_rows] - want[zv_rows]).max() <= 1e-4 * scale
+    # with every group mixed, RL-ZVP and masking coincide bitwise
+    inst2 = tiny_instance(21, V=1024, group_sizes=(4, 4), L=24, sigma_seq=0.08)
+    a = run_gpu(inst2, dev)
+    b = run_gpu(inst2, dev, cfgkw=kw)
+    assert a["loss"] == b["loss"] and np.array_equal(a["dlogits"], b["dlogits"])

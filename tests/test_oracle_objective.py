@@ -290,10 +290,10 @@ def _torch_frozen_loss(z, inst, res, cfg, grad_loss):
     for i in range(inst.R):
         if not res.active[i]:
             continue
-        A = float(res.adv[i])
         for t in range(inst.seq_offsets[i], inst.seq_offsets[i + 1]):
             if res.kappa[t] < 0:
                 continue
+            A = float(res.adv_tok[t])
             lpt = lp[t, int(inst.tokens[t])]
             base = res.lp[t] if cfg.ratio_mode == O.RATIO_GSPO_TOKEN else float(inst.old_logp[t])
             v = res.s_tok[t] * torch.exp(lpt - base)
@@ -366,3 +366,60 @@ def test_gradient_sign():
         dz = O.dlogits_row(res, t, inst.logits[t], y, cfg)
         A = res.adv[0] if t < inst.seq_offsets[1] else res.adv[1]
         assert np.sign(dz[y]) == -np.sign(A)
+
+
+# ------------------------------------------------------------------- RL-ZVP (ZVE stage 3)
+def test_zvp_spec_examples():
+    """SPEC.md:342 examples and SPEC.md:354 invariants for the RL-ZVP instantiation of the
+    cited method."""
+    cfg = O.OracleConfig(vocab=1000)
+    a = O.zvp_token_advantages(np.full(7, 1.3), 0.0, cfg)          # all entropies equal
+    assert np.all(a == 0.0)
+    H = np.array([0.01, 0.02, 3.5, 0.01])                         # one high-entropy token
+    a = O.zvp_token_advantages(H, 0.0, cfg)                       # all-fail group (r < 0.5)
+    assert a[2] > 0 and np.all(a[[0, 1, 3]] < 0)
+    a1 = O.zvp_token_advantages(H, 1.0, cfg)                      # all-pass: sign flips
+    np.testing.assert_allclose(a1, -a, rtol=0, atol=0)
+    rng = np.random.default_rng(4)
+    for _ in range(100):
+        H = rng.uniform(0, np.log(1000), size=int(rng.integers(1, 50)))
+        a = O.zvp_token_advantages(H, float(rng.uniform()), cfg)
+        assert np.all(np.abs(a) <= cfg.zvp_beta + 1e-15)
+        assert abs(a.mean()) < 1e-9
+
+
+def test_zvp_without_zv_groups_equals_mask_mode():
+    inst = tiny_instance(12, V=64, group_sizes=(4, 3), L=6, sigma_seq=0.1)
+    a = inst.run(O.OracleConfig(vocab=64))
+    b = inst.run(O.OracleConfig(vocab=64, zv_mode=O.ZV_RLZVP))
+    assert a.loss == b.loss and np.array_equal(a.coef, b.coef)
+
+
+def test_zvp_reads_zv_rows_and_bounds_advantages():
+    inst = tiny_instance(13, V=64, group_sizes=(4, 3, 2, 1), L=7, mask_tail=2,
+                         rewards=[1, 0, 1, 0, 1, 1, 1, 0, 0, 0.3])
+    m = inst.run(O.OracleConfig(vocab=64))
+    z = inst.run(O.OracleConfig(vocab=64, zv_mode=O.ZV_RLZVP))
+    assert m.active.sum() == 4 and z.active.sum() == inst.R
+    zv_rows = np.concatenate([np.arange(inst.seq_offsets[i], inst.seq_offsets[i + 1])
+                              for i in range(inst.R) if z.zv[i]])
+    v = z.kappa[zv_rows] >= 0
+    assert np.all(np.abs(z.adv_tok[zv_rows][v]) <= 0.05 + 1e-15)
+    # non-ZV rollouts keep their GRPO advantage and bucket machinery; N grows
+    assert z.denom == inst.R and m.denom == 4
+    np.testing.assert_allclose(z.J_i[:4], m.J_i[:4], rtol=1e-14)
+
+
+def test_zvp_gradient_matches_torch_autograd():
+    for seed in range(3):
+        inst = tiny_instance(seed + 40, V=13, group_sizes=(3, 3, 2), L=8, mask_tail=2,
+                             sigma_seq=0.1, rewards=[1, 0, 1, 1, 1, 1, 0, 0])
+        cfg = O.OracleConfig(vocab=13, zv_mode=O.ZV_RLZVP, zvp_beta=0.3)
+        res = inst.run(cfg)
+        z = torch.tensor(inst.logits.astype(np.float64), requires_grad=True)
+        loss = _torch_frozen_loss(z, inst, res, cfg, grad_loss=1.0)
+        assert float(loss) == pytest.approx(res.loss, rel=1e-12, abs=1e-15)
+        loss.backward()
+        for t in range(inst.T):
+            dz = O.dlogits_row(res, t, inst.logits[t], int(inst.tokens[t]), cfg)
+            np.testing.assert_allclose(dz, z.grad[t].numpy(), rtol=1e-10, atol=1e-14)
