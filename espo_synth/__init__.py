@@ -128,10 +128,12 @@ def make_mask(w: Workload, seq_offsets: np.ndarray, seed: int) -> np.ndarray:
 def round_to_bf16(a: np.ndarray) -> np.ndarray:
     """Round float32 → bfloat16 (round-to-nearest-even); returned widened as float32."""
     a = np.ascontiguousarray(a, dtype=np.float32)
-    u = a.view(np.uint32).astype(np.uint64)
-    rounding = ((u >> 16) & 1) + 0x7FFF
-    b = ((u + rounding) >> 16).astype(np.uint32) << 16
-    out = b.astype(np.uint32).view(np.float32).reshape(a.shape)
+    u = a.view(np.uint32)
+    b = (u >> 16) & np.uint32(1)
+    b += np.uint32(0x7FFF)
+    b += u                                   # uint32 wrap only for NaN payloads (fixed below)
+    b &= np.uint32(0xFFFF0000)
+    out = b.view(np.float32).reshape(a.shape)
     nan = np.isnan(a)
     if nan.any():
         out = out.copy()
@@ -155,8 +157,8 @@ def make_logit_rows(n_rows: int, V: int, seed: int, stream: int = 4,
     for r in range(n_rows):
         if high[r]:
             k = int(rng.integers(2, 9))
-            ids = rng.choice(V, size=k, replace=False)
-            z[r, ids] = rng.standard_normal(k).astype(np.float32)
+            ids = np.unique(rng.integers(0, V, size=k))   # distinct candidate ids
+            z[r, ids] = rng.standard_normal(len(ids)).astype(np.float32)
         else:
             z[r, int(rng.integers(0, V))] = np.float32(rng.uniform(2.0, 8.0))
     if dtype == "bf16":

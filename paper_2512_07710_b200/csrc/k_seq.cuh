@@ -414,7 +414,7 @@ __global__ void k_export_rollouts(const Workspace ws, int R, double* adv, uint8_
                                   uint8_t* active, double* J, int32_t* nb, float* theta) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < R; i += gridDim.x * blockDim.x) {
     if (adv) adv[i] = ws.adv[i];
-    if (zv) zv[i] = ws.cand[i] ? 0 : 1;
+    if (zv) zv[i] = (ws.cand[i] && ws.zsign[i] == 0) ? 0 : 1;
     if (active) active[i] = ws.active[i];
     if (J) J[i] = ws.J[i];
     if (nb) nb[i] = ws.nb[i];
