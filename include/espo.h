@@ -121,7 +121,10 @@ typedef struct {
   int32_t zv_mode;             /* espo_zv_mode, default MASK */
   float zvp_beta;              /* RL-ZVP β, default 0.05 (|Â_t| ≤ β) */
   float zvp_threshold;         /* RL-ZVP success threshold on the uniform reward, default 0.5 */
-  int32_t reserved[4];
+  int32_t vocab_begin;         /* vocabulary-parallel shard: this context's logits chunks hold */
+  int32_t vocab_local;         /* columns [vocab_begin, vocab_begin + vocab_local) of the full
+                                  `vocab`; vocab_local = 0 (default): unsharded */
+  int32_t reserved[2];
 } espo_config;
 
 /* Device-written statistics (all fp64). Per-bucket arrays are indexed by the pre-drop
@@ -187,6 +190,30 @@ espo_status espo_loss_finalize(espo_ctx_t ctx, float* loss_dev, espo_stats* stat
 espo_status espo_loss_bwd(espo_ctx_t ctx, const void* logits, int64_t ld, void* dlogits,
                           int64_t ldg, const float* grad_loss_dev, int64_t row_begin,
                           int64_t n_rows, espo_stream_t stream);
+
+/* ---- vocabulary-parallel ESPO (logits sharded by vocabulary over TP ranks) ----
+ * With cfg.vocab_local > 0 every rank holds the same token rows but only its vocabulary
+ * columns. The forward sweep then produces, per row, a 16-byte partial
+ * {R, S, W, u_y} (base-2 reference, Σ_{v≠y} 2^{u_v−R}, Σ 2^{u_v−R}(u_v−R) over the local
+ * columns, and λ·log2(e)·z_y on the rank owning the target, NaN elsewhere); the partials of
+ * all shards are combined into the exact row statistics (lse, lp, H, q). The backward sweep
+ * writes the local columns of dlogits (no collective). */
+
+/* Forward sweep of the local shard → partials (device f32[n_rows·4]); no coverage update. */
+espo_status espo_loss_fwd_partial(espo_ctx_t ctx, const void* logits, int64_t ld,
+                                  const int32_t* tokens, const float* old_logp,
+                                  const uint8_t* mask, int64_t row_begin, int64_t n_rows,
+                                  float* partial, espo_stream_t stream);
+/* Combines partials laid out [n_shards][n_rows][4] (device) into the row statistics and
+ * records the rows as covered (the same call order rules as espo_loss_fwd). */
+espo_status espo_loss_fwd_combine(espo_ctx_t ctx, const float* partials, int32_t n_shards,
+                                  int64_t row_begin, int64_t n_rows, espo_stream_t stream);
+/* Attaches a tensor-parallel NCCL communicator (collective over the TP ranks, id broadcast by
+ * the caller). Afterwards espo_loss_fwd on this context runs partial → ncclAllGather of the
+ * partials over the TP group → combine. The DP all-reduce of espo_loss_finalize stays on the
+ * communicator given to espo_create. */
+espo_status espo_attach_tp(espo_ctx_t ctx, const void* tp_unique_id, int32_t tp_rank,
+                           int32_t tp_world);
 
 /* Synchronises `stream`, then returns the sticky device error (ESPO_OK if none) or
  * ESPO_ERR_CUDA if a CUDA error is pending. */

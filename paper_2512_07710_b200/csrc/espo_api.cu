@@ -27,7 +27,9 @@ typedef int (*fn_get_uid)(nccl_uid*);
 typedef int (*fn_init_rank)(nccl_comm*, int, nccl_uid, int);
 typedef int (*fn_allreduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t);
 typedef int (*fn_destroy)(nccl_comm);
+typedef int (*fn_allgather)(const void*, void*, size_t, int, nccl_comm, cudaStream_t);
 constexpr int kNcclFloat64 = 8;  // ncclFloat64
+constexpr int kNcclFloat32 = 7;  // ncclFloat32
 constexpr int kNcclSum = 0;      // ncclSum
 
 struct NcclApi {
@@ -36,6 +38,7 @@ struct NcclApi {
   fn_init_rank init_rank = nullptr;
   fn_allreduce allreduce = nullptr;
   fn_destroy destroy = nullptr;
+  fn_allgather allgather = nullptr;
   bool load() {
     if (lib) return true;
     lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -44,7 +47,8 @@ struct NcclApi {
     init_rank = reinterpret_cast<fn_init_rank>(dlsym(lib, "ncclCommInitRank"));
     allreduce = reinterpret_cast<fn_allreduce>(dlsym(lib, "ncclAllReduce"));
     destroy = reinterpret_cast<fn_destroy>(dlsym(lib, "ncclCommDestroy"));
-    return get_uid && init_rank && allreduce && destroy;
+    allgather = reinterpret_cast<fn_allgather>(dlsym(lib, "ncclAllGather"));
+    return get_uid && init_rank && allreduce && destroy && allgather;
   }
 };
 NcclApi g_nccl;
@@ -55,7 +59,9 @@ enum class State { Created, Prepared, Finalized };
 struct espo_ctx_s {
   espo_config cfg{};
   int device = 0, rank = 0, world = 1;
-  nccl_comm comm = nullptr;
+  nccl_comm comm = nullptr;     // data-parallel group (loss all-reduce)
+  nccl_comm tp_comm = nullptr;  // vocabulary-parallel group (partials all-gather)
+  int tp_world = 1;
   int num_sms = 148;
   Workspace ws;
   int64_t cap_T = 0;
@@ -112,6 +118,9 @@ espo_status validate_config(const espo_config& c) {
       (c.grad_dtype != ESPO_F32 && c.grad_dtype != ESPO_BF16))
     return ESPO_ERR_INVALID_ARGUMENT;
   if (c.logits_dtype == ESPO_F32 && c.grad_dtype == ESPO_BF16) return ESPO_ERR_UNSUPPORTED;
+  if (c.vocab_local < 0 || (c.vocab_local > 0 && (c.vocab_begin < 0 ||
+                                                   int64_t(c.vocab_begin) + c.vocab_local > c.vocab)))
+    return ESPO_ERR_INVALID_ARGUMENT;
   if (c.zv_mode < 0 || c.zv_mode > 1 || !(c.zvp_beta >= 0.f) || !std::isfinite(c.zvp_beta) ||
       !std::isfinite(c.zvp_threshold))
     return ESPO_ERR_INVALID_ARGUMENT;
@@ -126,7 +135,10 @@ espo_status ensure_workspace(espo_ctx_t c, int R, int64_t T) {
     // 6 f32 + 2 i32 + 3 u8 arrays, each 256-byte aligned
     const size_t a4 = round_up(size_t(cap) * 4, 256), a1 = round_up(size_t(cap), 256);
     const size_t a32 = round_up(size_t(cap) * 32, 256);
-    ESPO_CUDA(cudaMalloc(&c->blocks_tok, 9 * a4 + 3 * a1 + a32));
+    const bool sharded = c->cfg.vocab_local > 0;
+    const size_t a16 = sharded ? round_up(size_t(cap) * 16, 256) : 0;
+    const size_t agath = c->tp_comm ? round_up(size_t(cap) * 16 * c->tp_world, 256) : 0;
+    ESPO_CUDA(cudaMalloc(&c->blocks_tok, 9 * a4 + 3 * a1 + a32 + a16 + agath));
     char* p = static_cast<char*>(c->blocks_tok);
     auto take = [&](size_t n) { char* r = p; p += n; return r; };
     c->ws.lse = reinterpret_cast<float*>(take(a4));
@@ -142,6 +154,8 @@ espo_status ensure_workspace(espo_ctx_t c, int R, int64_t T) {
     c->ws.clip = reinterpret_cast<uint8_t*>(take(a1));
     c->ws.list = take(a32);
     c->ws.zlist = reinterpret_cast<int32_t*>(take(a4));
+    c->ws.partial = sharded ? reinterpret_cast<float*>(take(a16)) : nullptr;
+    c->ws.gathered = c->tp_comm ? reinterpret_cast<float*>(take(agath)) : nullptr;
     c->cap_T = cap;
   }
   if (R > c->cap_R) {
@@ -302,6 +316,7 @@ espo_status espo_destroy(espo_ctx_t c) {
     DevGuard g(c->device);
     cudaDeviceSynchronize();
     if (c->comm) g_nccl.destroy(c->comm);
+    if (c->tp_comm) g_nccl.destroy(c->tp_comm);
     if (c->blocks_tok) cudaFree(c->blocks_tok);
     if (c->blocks_roll) cudaFree(c->blocks_roll);
     if (c->blocks_scalar) cudaFree(c->blocks_scalar);
@@ -370,28 +385,43 @@ espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* grou
   return ESPO_OK;
 }
 
-espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
-                          const float* old_logp, const uint8_t* mask, int64_t row_begin,
-                          int64_t n_rows, uint32_t flags, espo_stream_t stream) {
+}  // extern "C"
+
+namespace {
+// vocabulary columns held by this context: [v0, v0 + Vl)
+inline int shard_begin(espo_ctx_t c) { return c->cfg.vocab_local > 0 ? c->cfg.vocab_begin : 0; }
+inline int shard_width(espo_ctx_t c) {
+  return c->cfg.vocab_local > 0 ? c->cfg.vocab_local : c->cfg.vocab;
+}
+
+espo_status check_fwd_args(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
+                           const float* old_logp, int64_t row_begin, int64_t n_rows) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
-  if (flags != 0 || n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T)
+  if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T)
     return ESPO_ERR_INVALID_ARGUMENT;
   if (n_rows == 0) return ESPO_OK;
   if (!logits || !tokens || !old_logp) return ESPO_ERR_INVALID_ARGUMENT;
   const size_t es = dsize(c->cfg.logits_dtype);
-  if (ld < c->cfg.vocab) return ESPO_ERR_INVALID_ARGUMENT;
+  if (ld < shard_width(c)) return ESPO_ERR_INVALID_ARGUMENT;
   if (!aligned16(logits) || (size_t(ld) * es) % 16 != 0) return ESPO_ERR_ALIGNMENT;
-  // chunk coverage: reject overlaps with earlier chunks
-  const int64_t b = row_begin, e = row_begin + n_rows;
+  return ESPO_OK;
+}
+
+espo_status check_coverage(espo_ctx_t c, int64_t b, int64_t e) {
   auto it = c->covered.upper_bound(b);
   if (it != c->covered.begin()) {
     auto pv = std::prev(it);
     if (pv->second > b) return ESPO_ERR_BAD_STATE;
   }
   if (it != c->covered.end() && it->first < e) return ESPO_ERR_BAD_STATE;
-  DevGuard g(c->device);
-  cudaStream_t s = S(stream);
+  return ESPO_OK;
+}
+
+// K2 (+ its row-list pre-pass) over one chunk; writes statistics, or partials if `partial`.
+espo_status launch_sweep_fwd(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
+                             const float* old_logp, const uint8_t* mask, int64_t row_begin,
+                             int64_t n_rows, float* partial, cudaStream_t s) {
   FwdParams p;
   p.logits = logits;
   p.ld = ld;
@@ -400,19 +430,22 @@ espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const in
   p.mask = mask;
   p.row_begin = row_begin;
   p.n_rows = n_rows;
-  p.V = c->cfg.vocab;
+  p.V = shard_width(c);
   p.lam_log2e = c->cfg.logit_scale * kLog2e;
+  p.partial = partial;
   p.ws = c->ws;
+  const int V = c->cfg.vocab, v0 = shard_begin(c);
   const bool bf = c->cfg.logits_dtype == ESPO_BF16;
   FwdRec* list = static_cast<FwdRec*>(c->ws.list);
   ESPO_CUDA(cudaMemsetAsync(c->ws.count, 0, 2 * sizeof(int), s));
   const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
   if (bf)
     k_fwd_rows<__nv_bfloat16><<<pre_grid, 256, 0, s>>>(logits, ld, tokens, old_logp, mask, row_begin,
-                                                       n_rows, p.V, p.lam_log2e, c->ws, list, c->ws.count);
+                                                       n_rows, V, v0, p.V, p.lam_log2e, c->ws, list,
+                                                       c->ws.count);
   else
     k_fwd_rows<float><<<pre_grid, 256, 0, s>>>(logits, ld, tokens, old_logp, mask, row_begin, n_rows,
-                                               p.V, p.lam_log2e, c->ws, list, c->ws.count);
+                                               V, v0, p.V, p.lam_log2e, c->ws, list, c->ws.count);
   ESPO_LAUNCHED(c);
   if (c->fwd_impl == 1) {
     if (bf) {
@@ -428,8 +461,94 @@ espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const in
     if (le != cudaSuccess) return cuda_status(le);
   }
   ESPO_LAUNCHED(c);
-  c->covered[b] = e;
+  return ESPO_OK;
+}
+
+espo_status launch_combine(espo_ctx_t c, const float* partials, int n_shards, int64_t row_begin,
+                           int64_t n_rows, cudaStream_t s) {
+  const int grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  k_fwd_combine<<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(partials), n_shards, row_begin,
+                                     n_rows, c->ws);
+  ESPO_LAUNCHED(c);
+  return ESPO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
+                          const float* old_logp, const uint8_t* mask, int64_t row_begin,
+                          int64_t n_rows, uint32_t flags, espo_stream_t stream) {
+  if (flags != 0) return ESPO_ERR_INVALID_ARGUMENT;
+  espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
+  if (st != ESPO_OK || n_rows == 0) return st;
+  const bool sharded = c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab;
+  if (sharded && !c->tp_comm) return ESPO_ERR_BAD_STATE;  // use partial + combine
+  if ((st = check_coverage(c, row_begin, row_begin + n_rows)) != ESPO_OK) return st;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  if (sharded) {
+    // vocabulary-parallel: partial → all-gather over the TP group → combine
+    float* part = c->ws.partial;
+    float* gath = c->ws.gathered;
+    if ((st = launch_sweep_fwd(c, logits, ld, tokens, old_logp, mask, row_begin, n_rows, part, s)) != ESPO_OK)
+      return st;
+    if (g_nccl.allgather(part, gath, size_t(n_rows) * 4, kNcclFloat32, c->tp_comm, s) != 0)
+      return ESPO_ERR_NCCL;
+    if ((st = launch_combine(c, gath, c->tp_world, row_begin, n_rows, s)) != ESPO_OK) return st;
+  } else {
+    if ((st = launch_sweep_fwd(c, logits, ld, tokens, old_logp, mask, row_begin, n_rows, nullptr, s)) != ESPO_OK)
+      return st;
+  }
+  c->covered[row_begin] = row_begin + n_rows;
   c->n_covered += n_rows;
+  return ESPO_OK;
+}
+
+espo_status espo_loss_fwd_partial(espo_ctx_t c, const void* logits, int64_t ld,
+                                  const int32_t* tokens, const float* old_logp,
+                                  const uint8_t* mask, int64_t row_begin, int64_t n_rows,
+                                  float* partial, espo_stream_t stream) {
+  espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
+  if (st != ESPO_OK || n_rows == 0) return st;
+  if (!partial || !aligned16(partial)) return ESPO_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return launch_sweep_fwd(c, logits, ld, tokens, old_logp, mask, row_begin, n_rows, partial, S(stream));
+}
+
+espo_status espo_loss_fwd_combine(espo_ctx_t c, const float* partials, int32_t n_shards,
+                                  int64_t row_begin, int64_t n_rows, espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
+  if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T ||
+      n_shards < 1 || n_shards > 1024)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rows == 0) return ESPO_OK;
+  if (!partials || !aligned16(partials)) return ESPO_ERR_INVALID_ARGUMENT;
+  espo_status st = check_coverage(c, row_begin, row_begin + n_rows);
+  if (st != ESPO_OK) return st;
+  DevGuard g(c->device);
+  if ((st = launch_combine(c, partials, n_shards, row_begin, n_rows, S(stream))) != ESPO_OK) return st;
+  c->covered[row_begin] = row_begin + n_rows;
+  c->n_covered += n_rows;
+  return ESPO_OK;
+}
+
+espo_status espo_attach_tp(espo_ctx_t c, const void* tp_unique_id, int32_t tp_rank,
+                           int32_t tp_world) {
+  if (!c || !tp_unique_id || tp_world < 2 || tp_rank < 0 || tp_rank >= tp_world)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->cfg.vocab_local <= 0 || c->tp_comm) return ESPO_ERR_BAD_STATE;
+  if (!g_nccl.load()) return ESPO_ERR_NCCL;
+  DevGuard g(c->device);
+  nccl_uid id;
+  std::memcpy(&id, tp_unique_id, sizeof(id));
+  if (g_nccl.init_rank(&c->tp_comm, tp_world, id, tp_rank) != 0) {
+    c->tp_comm = nullptr;
+    return ESPO_ERR_NCCL;
+  }
+  c->tp_world = tp_world;
+  c->cap_T = 0;  // re-size the workspace at the next prepare (adds the gather buffer)
   return ESPO_OK;
 }
 
@@ -484,7 +603,7 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
   if (!logits || !dlogits) return ESPO_ERR_INVALID_ARGUMENT;
   const espo_config& cf = c->cfg;
   const size_t ei = dsize(cf.logits_dtype), eo = dsize(cf.grad_dtype);
-  if (ld < cf.vocab || ldg < cf.vocab) return ESPO_ERR_INVALID_ARGUMENT;
+  if (ld < shard_width(c) || ldg < shard_width(c)) return ESPO_ERR_INVALID_ARGUMENT;
   if (!aligned16(logits) || !aligned16(dlogits) || (size_t(ld) * ei) % 16 || (size_t(ldg) * eo) % 16)
     return ESPO_ERR_ALIGNMENT;
   const bool aliased = logits == dlogits;
@@ -499,7 +618,7 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
   p.grad_loss = grad_loss_dev;
   p.row_begin = row_begin;
   p.n_rows = n_rows;
-  p.V = cf.vocab;
+  p.V = shard_width(c);
   p.lam_log2e = cf.logit_scale * kLog2e;
   p.zero_fill = cf.zero_fill_inactive_rows;
   p.aliased = aliased ? 1 : 0;
@@ -511,10 +630,11 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
   const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
   if (c->bwd_impl == 0 || c->bwd_impl == 7) {
     // tiled (default): per-row records indexed by row, non-persistent (row, tile) grid
-    k_bwd_recs<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, p.zero_fill, c->ws, list);
+    k_bwd_recs<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, p.zero_fill,
+                                        shard_begin(c), p.V, c->ws, list);
     ESPO_LAUNCHED(c);
     const int epv = bi ? 8 : 4;
-    const int nvec = (cf.vocab + epv - 1) / epv;
+    const int nvec = (p.V + epv - 1) / epv;
     const int vpt = (c->bwd_impl == 7) ? 4 : 8;  // default 0: 32 KB tiles (measured best)
     const int ntiles = (nvec + 256 * vpt - 1) / (256 * vpt);
     const int64_t grid = n_rows * int64_t(ntiles);
@@ -532,7 +652,8 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
     return ESPO_OK;
   }
   ESPO_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), s));
-  k_bwd_rows<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, p.zero_fill, c->ws, list, zl, cnt);
+  k_bwd_rows<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, p.zero_fill, shard_begin(c),
+                                      p.V, c->ws, list, zl, cnt);
   ESPO_LAUNCHED(c);
   if (c->bwd_impl == 1) {
     if (bi && bo) {

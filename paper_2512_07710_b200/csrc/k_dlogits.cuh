@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256) k_dlogits_ldg(const BwdParams p, const Bw
     const BwdRec rec = list[k];
     const char* row = static_cast<const char*>(p.logits) + int64_t(rec.r) * p.ld * int64_t(sizeof(Tin));
     char* orow = static_cast<char*>(p.dlogits) + int64_t(rec.r) * p.ldg * int64_t(sizeof(Tout));
-    const int vy = rec.y / EPV, yoff = rec.y % EPV;
+    const int vy = rec.yl >= 0 ? rec.yl / EPV : -1, yoff = rec.yl >= 0 ? rec.yl % EPV : 0;
     for (int j0 = lane; j0 < nvec; j0 += 32 * U) {
       uint4 v[U];
 #pragma unroll
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dlogits_tma(const BwdParams p, c
     const BwdRec rec = rec_next;
     if (k + nw < n) rec_next = list[k + nw];
     char* orow = static_cast<char*>(p.dlogits) + int64_t(rec.r) * p.ldg * int64_t(sizeof(Tout));
-    const int vy = rec.y / EPV, yoff = rec.y % EPV;
+    const int vy = rec.yl >= 0 ? rec.yl / EPV : -1, yoff = rec.yl >= 0 ? rec.yl % EPV : 0;
     for (int c = 0; c < nch; ++c) {
       const int slot = consumed % STAGES;
       mbar_wait(&bars[slot], (consumed / STAGES) & 1u);
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256) k_dlogits_tile(const BwdParams p, const B
   }
   const char* row = static_cast<const char*>(p.logits) + int64_t(rc.r) * p.ld * int64_t(sizeof(Tin));
   const float lamL = p.lam_log2e;
-  const int vy = rc.y / EPV, yoff = rc.y % EPV;
+  const int vy = rc.yl >= 0 ? rc.yl / EPV : -1, yoff = rc.yl >= 0 ? rc.yl % EPV : 0;
   uint4 v[VPT];
 #pragma unroll
   for (int u = 0; u < VPT; ++u) {

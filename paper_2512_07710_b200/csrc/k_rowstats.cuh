@@ -23,8 +23,9 @@ struct FwdParams {
   const float* old_logp;
   const uint8_t* mask;  // nullable
   int64_t row_begin, n_rows;
-  int V;
+  int V;                // columns of a logits row held here (the shard width if sharded)
   float lam_log2e;      // λ·log2(e)
+  float* partial;       // vocabulary-parallel: per-row {R, S, W, u_y} instead of statistics
   Workspace ws;
 };
 
@@ -68,17 +69,11 @@ __device__ __forceinline__ void kahan_add(float& s, float& c, float x) {
   s = t;
 }
 
-// Row epilogue: combine lanes (each lane may hold its own reference r), write lse/lp/H/q.
-__device__ __forceinline__ void row_finish(float r, float S, float W, float uy, const Workspace& ws,
-                                           int64_t t, int lane) {
-  const float R = warp_max(r);
-  const float d = r - R;
-  const float sc = ex2(d);
-  W = sc * fmaf(d, S, W);
-  S = sc * S;
-  S = warp_sum(S);
-  W = warp_sum(W);
-  if (lane == 0) {
+// Final statistics from (R, S, W) = (reference, Σ_{v≠y} 2^{u_v−R}, Σ 2^{u_v−R}(u_v−R)) and
+// the target's u_y ≤ R: lse, lp = log p_y, H, q = 1 − p_y.
+__device__ __forceinline__ void finish_stats(float R, float S, float W, float uy,
+                                             const Workspace& ws, int64_t t) {
+  {
     const float ty = uy - R;               // ≤ 0
     const float ey = ex2(ty);              // = 1 when no lane moved its reference
     const float Stot = ey + S;
@@ -98,6 +93,71 @@ __device__ __forceinline__ void row_finish(float r, float S, float W, float uy, 
     ws.lp[t] = lp;
     ws.H[t] = H;
     ws.q[t] = S / Stot;
+  }
+}
+
+// Rescales (S, W) from reference r to R ≥ r (r = −inf: nothing accumulated yet).
+__device__ __forceinline__ void rebase(float r, float R, float& S, float& W) {
+  if (r == R) return;
+  if (r == -INFINITY || (S == 0.f && W == 0.f)) {
+    S = 0.f;
+    W = 0.f;
+    return;
+  }
+  const float d = r - R;
+  const float sc = ex2(d);
+  W = sc * fmaf(d, S, W);
+  S = sc * S;
+}
+
+// Row epilogue: combine lanes (each lane may hold its own reference r), then write the row
+// statistics — or, for a vocabulary shard, the row's partial {R, S, W, u_y}.
+__device__ __forceinline__ void row_finish(float r, float S, float W, float uy, const Workspace& ws,
+                                           int64_t t, int lane, float* partial = nullptr,
+                                           int64_t pr = 0) {
+  const float R = warp_max(r);
+  if (R == -INFINITY) {
+    S = 0.f;
+    W = 0.f;
+  } else {
+    rebase(r, R, S, W);
+  }
+  S = warp_sum(S);
+  W = warp_sum(W);
+  if (lane == 0) {
+    if (partial) {
+      reinterpret_cast<float4*>(partial)[pr] = make_float4(R, S, W, uy);
+    } else {
+      finish_stats(R, S, W, uy, ws, t);
+    }
+  }
+}
+
+// Vocabulary-parallel combine: one thread per valid row merges the shards' partials
+// {R_k, S_k, W_k, u_y (owner only)} laid out [n_shards][n_rows] into the row statistics.
+__global__ void __launch_bounds__(256) k_fwd_combine(const float4* partials, int n_shards,
+                                                     int64_t row_begin, int64_t n_rows,
+                                                     Workspace ws) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = row_begin + r;
+    if (!ws.flag[t]) continue;
+    float R = -INFINITY, uy = __int_as_float(0x7fc00000);
+    for (int k = 0; k < n_shards; ++k) {
+      const float4 a = partials[int64_t(k) * n_rows + r];
+      R = fmaxf(R, a.x);
+      if (!isnan(a.w)) uy = a.w;
+    }
+    float S = 0.f, W = 0.f;
+    for (int k = 0; k < n_shards; ++k) {
+      const float4 a = partials[int64_t(k) * n_rows + r];
+      float s = a.y, w = a.z;
+      rebase(a.x, R, s, w);
+      S += s;
+      W += w;
+    }
+    if (isnan(uy)) set_error(ws.err, ESPO_ERR_INVALID_ARGUMENT);  // no shard owns the target
+    finish_stats(R, S, W, uy, ws, t);
   }
 }
 
@@ -131,10 +191,7 @@ __device__ __forceinline__ void batch_slow(const uint4* v, int j0, int nvec, int
     return;
   }
   if (bm > r + 60.f) {  // keep r = u_y (exact e_y = 1) unless the batch could overflow
-    const float d = r - bm;
-    const float sc = ex2(d);
-    W = sc * fmaf(d, S, W);
-    S = sc * S;
+    rebase(r, bm, S, W);
     r = bm;
   }
   bS = 0.f;
@@ -222,8 +279,8 @@ __global__ void __launch_bounds__(256) k_rowstats_ldg(const FwdParams p, const F
   for (int k = gw; k < n; k += nw) {
     const FwdRec rec = list[k];
     const char* row = static_cast<const char*>(p.logits) + int64_t(rec.r) * p.ld * int64_t(sizeof(Tin));
-    const int vy = rec.y / EPV, yoff = rec.y % EPV;
-    float ref = rec.uy, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f;
+    const int vy = rec.yl >= 0 ? rec.yl / EPV : -1, yoff = rec.yl >= 0 ? rec.yl % EPV : 0;
+    float ref = rec.yl >= 0 ? rec.uy : -INFINITY, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f;
     for (int j0 = lane; j0 < nvec; j0 += 32 * U) {
       uint4 v[U];
 #pragma unroll
@@ -242,7 +299,7 @@ __global__ void __launch_bounds__(256) k_rowstats_ldg(const FwdParams p, const F
       kahan_add(S, cS, bS);
       kahan_add(W, cW, bW);
     }
-    row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane);
+    row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane, p.partial, rec.r);
   }
 }
 
@@ -310,9 +367,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
   for (int k = gw; k < n; k += nw) {
     const FwdRec rec = rec_next;
     if (k + nw < n) rec_next = list[k + nw];
-    const int vy = rec.y / EPV, yoff = rec.y % EPV;
-    float ref = rec.uy, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f;
-    const int cy = vy / VPC;  // chunk holding the target; the ragged vector is in the last
+    const int vy = rec.yl >= 0 ? rec.yl / EPV : -1, yoff = rec.yl >= 0 ? rec.yl % EPV : 0;
+    float ref = rec.yl >= 0 ? rec.uy : -INFINITY, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f;
+    const int cy = vy >= 0 ? vy / VPC : -1;  // chunk holding the target; the ragged vector is in the last
     for (int c = 0; c < nch; ++c, ++q) {
       const int slot = q % STAGES;
       mbar_wait(&bars[slot], (q / STAGES) & 1u);
@@ -376,7 +433,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
         kahan_add(W, cW, bW);
       }
     }
-    row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane);
+    row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane, p.partial, rec.r);
   }
 }
 

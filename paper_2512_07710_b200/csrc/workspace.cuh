@@ -19,6 +19,8 @@ struct Workspace {
   uint8_t* clip = nullptr;   // 1 = gradient clipped              (K3)
   void* list = nullptr;      // per-chunk row records (FwdRec / BwdRec), 32 B × T
   int32_t* zlist = nullptr;  // per-chunk zero-fill rows (bwd), 4 B × T
+  float* partial = nullptr;  // vocabulary shard: per-row {R, S, W, u_y}, 16 B × T
+  float* gathered = nullptr; // TP all-gather target [tp_world][rows][4]
   // ---- per rollout [R] ----
   int64_t* seq_off = nullptr;  // [R+1] copy of seq_offsets       (K1)
   double* adv = nullptr;       // Â_i (0 for ZV)                  (K1)

@@ -38,7 +38,8 @@ EXPORTED_SYMBOLS = [
     "espo_config_default", "espo_get_unique_id", "espo_create", "espo_destroy", "espo_prepare",
     "espo_loss_fwd", "espo_loss_finalize", "espo_loss_bwd", "espo_get_error",
     "espo_status_string", "espo_export_token_stats", "espo_export_rollout_stats",
-    "espo_launch_count", "espo_set_option",
+    "espo_launch_count", "espo_set_option", "espo_loss_fwd_partial", "espo_loss_fwd_combine",
+    "espo_attach_tp",
 ]
 
 
@@ -60,7 +61,8 @@ class Config(ctypes.Structure):
         ("log_ratio_clamp", ctypes.c_float), ("logits_dtype", ctypes.c_int32),
         ("grad_dtype", ctypes.c_int32), ("zero_fill_inactive_rows", ctypes.c_int32),
         ("zv_mode", ctypes.c_int32), ("zvp_beta", ctypes.c_float),
-        ("zvp_threshold", ctypes.c_float), ("reserved", ctypes.c_int32 * 4),
+        ("zvp_threshold", ctypes.c_float), ("vocab_begin", ctypes.c_int32),
+        ("vocab_local", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2),
     ]
 
 
@@ -107,6 +109,9 @@ def load_library():
         "espo_export_rollout_stats": (I32, [P, P, P, P, P, P, P, P]),
         "espo_launch_count": (ctypes.c_uint64, [P]),
         "espo_set_option": (I32, [P, I32, I64]),
+        "espo_loss_fwd_partial": (I32, [P, P, I64, P, P, P, I64, I64, P, P]),
+        "espo_loss_fwd_combine": (I32, [P, P, I32, I64, I64, P]),
+        "espo_attach_tp": (I32, [P, P, I32, I32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -149,7 +154,8 @@ class Espo:
                  std_unbiased=False, adv_eps=1e-6, zv_var_eps=0.0, logit_scale=1.0,
                  log_ratio_clamp=20.0, logits_dtype=torch.bfloat16, grad_dtype=None,
                  zero_fill_inactive_rows=True, zv_mode=ZV_MASK, zvp_beta=0.05,
-                 zvp_threshold=0.5, device=None, rank=0, world=1, process_group=None):
+                 zvp_threshold=0.5, vocab_shard=None, device=None, rank=0, world=1,
+                 process_group=None, tp_rank=0, tp_world=1, tp_group=None):
         lib = load_library()
         self._lib = lib
         cfg = Config()
@@ -167,6 +173,8 @@ class Espo:
         cfg.zero_fill_inactive_rows = int(bool(zero_fill_inactive_rows))
         cfg.zv_mode = int(zv_mode)
         cfg.zvp_beta, cfg.zvp_threshold = float(zvp_beta), float(zvp_threshold)
+        if vocab_shard is not None:                  # (begin, width) of this rank's columns
+            cfg.vocab_begin, cfg.vocab_local = int(vocab_shard[0]), int(vocab_shard[1])
         self.cfg = cfg
         self.vocab = int(vocab)
         if device is None:
@@ -183,6 +191,10 @@ class Espo:
         self._h = h
         self.n_tokens = 0
         self.n_rollouts = 0
+        if tp_world > 1:
+            tuid = ctypes.create_string_buffer(bootstrap_unique_id(tp_rank, tp_group), 128)
+            _check(lib.espo_attach_tp(self._h, tuid, int(tp_rank), int(tp_world)),
+                   "espo_attach_tp")
 
     # -- lifecycle ------------------------------------------------------------------------
     def close(self):
@@ -225,6 +237,24 @@ class Espo:
         _check(self._lib.espo_loss_fwd(self._h, _ptr(logits), int(logits.stride(0)),
                                        _ptr(tokens), _ptr(old_logp), _ptr(mask), int(row_begin),
                                        n, 0, self._stream()), "espo_loss_fwd")
+
+    def loss_fwd_partial(self, logits, tokens, old_logp, mask=None, row_begin=0, partial=None):
+        """espo_loss_fwd_partial: this vocabulary shard's per-row {R, S, W, u_y} (f32[n, 4])."""
+        n = int(logits.shape[0])
+        if partial is None:
+            partial = torch.empty((n, 4), dtype=torch.float32, device=logits.device)
+        _check(self._lib.espo_loss_fwd_partial(self._h, _ptr(logits), int(logits.stride(0)),
+                                               _ptr(tokens), _ptr(old_logp), _ptr(mask),
+                                               int(row_begin), n, _ptr(partial), self._stream()),
+               "espo_loss_fwd_partial")
+        return partial
+
+    def loss_fwd_combine(self, partials, row_begin=0):
+        """espo_loss_fwd_combine over partials [n_shards, n_rows, 4] (device)."""
+        partials = partials.contiguous()
+        _check(self._lib.espo_loss_fwd_combine(self._h, _ptr(partials), int(partials.shape[0]),
+                                               int(row_begin), int(partials.shape[1]),
+                                               self._stream()), "espo_loss_fwd_combine")
 
     def loss_finalize(self, loss_out=None, stats_out=None):
         """espo_loss_finalize → (loss f32[1], stats f64[STATS_LEN]) device tensors."""

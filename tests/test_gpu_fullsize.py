@@ -168,8 +168,11 @@ def test_full_size_sampled_groups(name):
         r0, r1 = g * G, (g + 1) * G
         t0, t1 = int(b.seq_offsets[r0]), int(b.seq_offsets[r1])
         so = b.seq_offsets[r0:r1 + 1] - t0
+        memo = {}
+        key = (lambda u, t0=t0: (u + t0) % U_ROWS)   # distinct row of local row u
         sub = O.espo_loss(Cycled(np.roll(b.rows, -(t0 % U_ROWS), axis=0)), b.tokens[t0:t1],
-                          b.old[t0:t1], None, b.rewards[r0:r1], b.group_ids[r0:r1], so, cfg)
+                          b.old[t0:t1], None, b.rewards[r0:r1], b.group_ids[r0:r1], so, cfg,
+                          row_key=key, stats_cache=memo)
         assert np.array_equal(rol["adv"][r0:r1], sub.adv)
         assert np.array_equal(rol["active"][r0:r1].astype(bool), sub.active)
         tok = {k: v.cpu().numpy() for k, v in ctx.export_token_stats(t0, t1 - t0).items()}
@@ -192,7 +195,8 @@ def test_full_size_sampled_groups(name):
                 def run(c, **kw):
                     return O.espo_loss(Cycled(np.roll(b.rows, -(t0 % U_ROWS), axis=0)),
                                        b.tokens[t0:t1], b.old[t0:t1], None, b.rewards[r0:r1],
-                                       b.group_ids[r0:r1], so, c, **kw)
+                                       b.group_ids[r0:r1], so, c, row_key=key,
+                                       stats_cache=memo, **kw)
             sub2, _ = decision_aware_reference({"tok": tok}, Inst, sub, cfg)
             np.testing.assert_allclose(rol["J"][r0:r1], sub2.J_i, rtol=1e-5,
                                        atol=1e-5 * np.abs(sub2.J_i).max())
