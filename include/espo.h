@@ -215,6 +215,18 @@ espo_status espo_loss_fwd_combine(espo_ctx_t ctx, const float* partials, int32_t
 espo_status espo_attach_tp(espo_ctx_t ctx, const void* tp_unique_id, int32_t tp_rank,
                            int32_t tp_world);
 
+/* ---- fused LM head + forward statistics (tcgen05) ----
+ * Computes the same row statistics as espo_loss_fwd for logits = λ·(hidden · weightᵀ) without
+ * writing the logits: hidden bf16 [n_rows, ldh ≥ d] (row row_begin of the chunk first),
+ * weight bf16 [vocab, ldw ≥ d] (the LM-head matrix, row v = vocabulary entry v), fp32
+ * accumulation on the tensor cores; tokens/old_logp/mask as in espo_loss_fwd. 16-byte aligned
+ * bases and pitches. Counts as the forward call for these rows. The first call may allocate
+ * a small per-row partial buffer (16 B × rows × vocabulary parts). Unsharded contexts only. */
+espo_status espo_lmhead_fwd(espo_ctx_t ctx, const void* hidden, int64_t ldh, const void* weight,
+                            int64_t ldw, int32_t d, const int32_t* tokens, const float* old_logp,
+                            const uint8_t* mask, int64_t row_begin, int64_t n_rows,
+                            espo_stream_t stream);
+
 /* Synchronises `stream`, then returns the sticky device error (ESPO_OK if none) or
  * ESPO_ERR_CUDA if a CUDA error is pending. */
 espo_status espo_get_error(espo_ctx_t ctx, espo_stream_t stream);

@@ -13,7 +13,10 @@
 #include "k_rowstats.cuh"
 #include "k_rowlist.cuh"
 #include "k_seq.cuh"
+#include "k_lmhead.cuh"
 #include "workspace.cuh"
+
+#include <cudaTypedefs.h>
 
 using namespace espo;
 
@@ -77,6 +80,8 @@ struct espo_ctx_s {
   void* blocks_tok = nullptr;  // one allocation for all per-token arrays
   void* blocks_roll = nullptr; // one allocation for all per-rollout arrays
   void* blocks_scalar = nullptr;
+  float* lmh_partial = nullptr;  // fused LM-head: [parts][rows] float4, grown on demand
+  size_t lmh_cap = 0;
 };
 
 namespace {
@@ -320,6 +325,7 @@ espo_status espo_destroy(espo_ctx_t c) {
     if (c->blocks_tok) cudaFree(c->blocks_tok);
     if (c->blocks_roll) cudaFree(c->blocks_roll);
     if (c->blocks_scalar) cudaFree(c->blocks_scalar);
+    if (c->lmh_partial) cudaFree(c->lmh_partial);
   }
   delete c;
   return ESPO_OK;
@@ -529,6 +535,94 @@ espo_status espo_loss_fwd_combine(espo_ctx_t c, const float* partials, int32_t n
   if (st != ESPO_OK) return st;
   DevGuard g(c->device);
   if ((st = launch_combine(c, partials, n_shards, row_begin, n_rows, S(stream))) != ESPO_OK) return st;
+  c->covered[row_begin] = row_begin + n_rows;
+  c->n_covered += n_rows;
+  return ESPO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                   uint64_t pitch_bytes, uint32_t box_rows) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_encode),
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_bytes};
+  cuuint32_t box[2] = {uint32_t(kLmBK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+}  // namespace
+
+extern "C" {
+
+espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const void* weight,
+                            int64_t ldw, int32_t d, const int32_t* tokens, const float* old_logp,
+                            const uint8_t* mask, int64_t row_begin, int64_t n_rows,
+                            espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
+  if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T || d < 1)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rows == 0) return ESPO_OK;
+  if (!hidden || !weight || !tokens || !old_logp || ldh < d || ldw < d) return ESPO_ERR_INVALID_ARGUMENT;
+  if (!aligned16(hidden) || !aligned16(weight) || (ldh * 2) % 16 || (ldw * 2) % 16)
+    return ESPO_ERR_ALIGNMENT;
+  if (c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab) return ESPO_ERR_UNSUPPORTED;
+  espo_status st = check_coverage(c, row_begin, row_begin + n_rows);
+  if (st != ESPO_OK) return st;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  const int V = c->cfg.vocab;
+  const int mblocks = int((n_rows + kLmBM - 1) / kLmBM);
+  const int ntiles = (V + kLmBN - 1) / kLmBN;
+  int parts = (2 * c->num_sms + mblocks - 1) / mblocks;   // ≥ 2 waves of CTAs
+  parts = std::max(1, std::min(parts, std::min(16, ntiles)));
+  const size_t need = size_t(parts) * size_t(n_rows) * 16;
+  if (need > c->lmh_cap) {
+    if (c->lmh_partial) cudaFree(c->lmh_partial);
+    c->lmh_partial = nullptr;
+    ESPO_CUDA(cudaMalloc(&c->lmh_partial, need));
+    c->lmh_cap = need;
+  }
+  CUtensorMap mh, mw;
+  if (!make_map_bf16(&mh, hidden, uint64_t(n_rows), uint64_t(d), uint64_t(ldh) * 2, kLmBM) ||
+      !make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, kLmBN))
+    return ESPO_ERR_CUDA;
+  const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  k_lmh_rows<<<pre_grid, 256, 0, s>>>(tokens, old_logp, mask, row_begin, n_rows, V, c->ws);
+  ESPO_LAUNCHED(c);
+  static bool attr = false;
+  if (!attr) {
+    ESPO_CUDA(cudaFuncSetAttribute(k_lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kLmSmem)));
+    attr = true;
+  }
+  LmParams lp;
+  lp.n_rows = int(n_rows);
+  lp.row_begin = row_begin;
+  lp.d = d;
+  lp.V = V;
+  lp.ntiles = ntiles;
+  lp.parts = parts;
+  lp.lam_log2e = c->cfg.logit_scale * kLog2e;
+  lp.tokens = tokens;
+  lp.partial = c->lmh_partial;
+  lp.ws = c->ws;
+  k_lmhead_fwd<<<dim3(mblocks, parts), kLmThreads, kLmSmem, s>>>(mh, mw, lp);
+  ESPO_LAUNCHED(c);
+  if ((st = launch_combine(c, c->lmh_partial, parts, row_begin, n_rows, s)) != ESPO_OK) return st;
   c->covered[row_begin] = row_begin + n_rows;
   c->n_covered += n_rows;
   return ESPO_OK;

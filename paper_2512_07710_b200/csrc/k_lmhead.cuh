@@ -1,0 +1,286 @@
+// k_lmhead.cuh — fused LM head + ESPO forward statistics on the 5th-gen tensor cores
+// (SURVEY §8(f) row 1): logits z = h·Wᵀ are produced tile by tile in TMEM by tcgen05.mma and
+// reduced on the fly into the row statistics (lse, lp, H, q) — the [T, V] logits never exist
+// in HBM.
+//
+// CTA = one 128-row block of hidden states × one contiguous part of the vocabulary (P parts).
+// Warp roles (192 threads): warp 0 — TMA producer (cp.async.bulk.tensor 2D, 128-byte swizzle,
+// 4-stage smem ring of {A: 128×64 bf16, B: 256×64 bf16}); warp 1 — TMEM allocator and MMA
+// issuer (one thread, tcgen05.mma.cta_group::1.kind::f16, M=128, N=256, K=16, fp32
+// accumulators in two 256-column TMEM buffers); warps 2–5 — epilogue: thread i owns row i
+// (TMEM lane i), reads its 256 logits per tile with tcgen05.ld.32x32b.x32 and runs the same
+// base-2 online (max, S, W) reduction as K2. Each CTA writes a 16-byte partial
+// {R, S, W, u_y} per row; k_fwd_combine merges the P parts (the vocabulary-parallel merge).
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "k_rowstats.cuh"
+#include "workspace.cuh"
+
+namespace espo {
+
+constexpr int kLmBM = 128;          // rows per CTA (UMMA M)
+constexpr int kLmBN = 256;          // vocabulary columns per tile (UMMA N)
+constexpr int kLmBK = 64;           // K per stage (128 bytes of bf16: one swizzle atom)
+constexpr int kLmStages = 4;
+constexpr int kLmABytes = kLmBM * kLmBK * 2;   // 16 KB
+constexpr int kLmBBytes = kLmBN * kLmBK * 2;   // 32 KB
+constexpr int kLmStageBytes = kLmABytes + kLmBBytes;
+constexpr int kLmThreads = 192;
+constexpr size_t kLmSmem = size_t(kLmStages) * kLmStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+struct LmParams {
+  int n_rows;            // rows of this chunk
+  int64_t row_begin;
+  int d;                 // hidden size (K)
+  int V;                 // vocabulary rows of W
+  int ntiles;            // ceil(V / 256)
+  int parts;             // vocabulary parts (gridDim.y)
+  float lam_log2e;
+  const int32_t* tokens; // chunk-relative
+  float* partial;        // [parts][n_rows] float4
+  Workspace ws;
+};
+
+// --------------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle (rows of 128 B, 8-row groups
+// 1024 B apart), sm100 version field = 1.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr & 0x3FFFF) >> 4);        // start address
+  d |= uint64_t(1) << 16;                       // LBO (unused for swizzled K-major) = 1
+  d |= uint64_t(1024 >> 4) << 32;               // SBO = 1024 B
+  d |= uint64_t(1) << 46;                       // version (Blackwell)
+  d |= uint64_t(2) << 61;                       // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: bf16 × bf16 → f32, K-major A and B, M = 128, N = 256
+constexpr uint32_t kLmIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kLmBN >> 3) << 17) |
+                              (uint32_t(kLmBM >> 4) << 24);
+
+__global__ void __launch_bounds__(kLmThreads, 1)
+    k_lmhead_fwd(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w,
+                 const LmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);   // 1024-B aligned (SW128)
+  uint8_t* sA = smem;                                             // [stages][16 KB]
+  uint8_t* sB = smem + kLmStages * kLmABytes;                     // [stages][32 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kLmStages * kLmStageBytes);
+  uint64_t* empty = full + kLmStages;
+  uint64_t* tfull = empty + kLmStages;   // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_any = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * kLmBM;
+  const int part = blockIdx.y;
+  const int t_begin = int((int64_t(p.ntiles) * part) / p.parts);
+  const int t_end = int((int64_t(p.ntiles) * (part + 1)) / p.parts);
+  const int nk = (p.d + kLmBK - 1) / kLmBK;
+
+  // skip blocks without a valid row (eliminated groups, masked tails)
+  if (threadIdx.x == 0) *s_any = 0;
+  __syncthreads();
+  if (threadIdx.x < kLmBM) {
+    const int r = m0 + threadIdx.x;
+    if (r < p.n_rows && p.ws.flag[p.row_begin + r]) *s_any = 1;
+  }
+  __syncthreads();
+  if (*s_any == 0 || t_begin >= t_end) return;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kLmStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kLmBM);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {   // TMEM: two 256-column fp32 accumulators (all 512 columns)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t q = 0;
+      for (int tile = t_begin; tile < t_end; ++tile) {
+        for (int kb = 0; kb < nk; ++kb, ++q) {
+          const int s = q % kLmStages;
+          mbar_wait(&empty[s], ((q / kLmStages) & 1u) ^ 1u);
+          mbar_arrive_tx(&full[s], kLmStageBytes);
+          tma_load_2d(sA + s * kLmABytes, &tmap_h, kb * kLmBK, m0, &full[s]);
+          tma_load_2d(sB + s * kLmBBytes, &tmap_w, kb * kLmBK, tile * kLmBN, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      uint32_t q = 0;
+      int i = 0;
+      for (int tile = t_begin; tile < t_end; ++tile, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tempty[acc], ((i >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t dt = tmem + uint32_t(acc * kLmBN);
+        for (int kb = 0; kb < nk; ++kb, ++q) {
+          const int s = q % kLmStages;
+          mbar_wait(&full[s], (q / kLmStages) & 1u);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * kLmABytes), b0 = smem_u32(sB + s * kLmBBytes);
+#pragma unroll
+          for (int k = 0; k < kLmBK / 16; ++k)   // K = 16 per MMA: +32 bytes inside the atom
+            tc_mma(dt, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), kLmIdesc,
+                   (kb | k) != 0);
+          tc_commit(&empty[s]);                  // smem stage free once these MMAs finish
+        }
+        tc_commit(&tfull[acc]);                  // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue
+    const int quarter = warp & 3;                // TMEM lanes this warp may access
+    const int row = quarter * 32 + lane;
+    const int r = m0 + row;
+    const bool valid = r < p.n_rows && p.ws.flag[p.row_begin + r];
+    const int y = valid ? p.tokens[r] : -1;
+    const float lamL = p.lam_log2e;
+    float R = -INFINITY, S = 0.f, W = 0.f, uy = __int_as_float(0x7fc00000);
+    int i = 0;
+    for (int tile = t_begin; tile < t_end; ++tile, ++i) {
+      const int acc = i & 1;
+      mbar_wait(&tfull[acc], (i >> 1) & 1u);
+      tc_fence_after();
+      const uint32_t base = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kLmBN);
+#pragma unroll 1
+      for (int c = 0; c < kLmBN / 32; ++c) {
+        float x[32];
+        __syncwarp();                              // tcgen05.ld is .sync.aligned
+        tmem_ld32(base + uint32_t(c * 32), x);
+        const int col0 = tile * kLmBN + c * 32;
+        if (!valid) continue;
+        const bool special = (y >= col0 && y < col0 + 32) || (col0 + 32 > p.V);
+        if (special) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int col = col0 + e;
+            if (col == y) uy = x[e] * lamL;
+            if (col == y || col >= p.V) x[e] = -INFINITY;
+          }
+        }
+        float m = x[0];
+#pragma unroll
+        for (int e = 1; e < 32; ++e) m = fmaxf(m, x[e]);
+        m *= lamL;
+        if (m > R) {
+          rebase(R, m, S, W);
+          R = m;
+        }
+        if (R == -INFINITY) continue;
+        const float nR = -R;
+        float s0 = 0.f, s1 = 0.f, w0 = 0.f, w1 = 0.f;
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float ta = max_nan(fmaf(x[e], lamL, nR), -127.f);
+          const float tb = max_nan(fmaf(x[e + 1], lamL, nR), -127.f);
+          const float ea = ex2(ta), eb = ex2(tb);
+          s0 += ea;
+          s1 += eb;
+          w0 = fmaf(ea, ta, w0);
+          w1 = fmaf(eb, tb, w1);
+        }
+        S += s0 + s1;
+        W += w0 + w1;
+      }
+      __syncwarp();
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+    if (valid)
+      reinterpret_cast<float4*>(p.partial)[int64_t(part) * p.n_rows + r] = make_float4(R, S, W, uy);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
+                 : "memory");
+  }
+}
+
+// Row flags / token copies for the fused path (no logits to read the target from).
+__global__ void __launch_bounds__(256) k_lmh_rows(const int32_t* tokens, const float* old_logp,
+                                                  const uint8_t* mask, int64_t row_begin,
+                                                  int64_t n_rows, int V, Workspace ws) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = row_begin + r;
+    const int y = tokens[r];
+    ws.old[t] = old_logp[r];
+    ws.y[t] = y;
+    bool valid = (mask ? mask[r] != 0 : true) && ws.cand[ws.row_seq[t]];
+    if (valid && (y < 0 || y >= V)) {
+      set_error(ws.err, ESPO_ERR_TOKEN_OUT_OF_RANGE);
+      valid = false;
+    }
+    ws.flag[t] = valid ? 1 : 0;
+  }
+}
+
+}  // namespace espo

@@ -39,7 +39,7 @@ EXPORTED_SYMBOLS = [
     "espo_loss_fwd", "espo_loss_finalize", "espo_loss_bwd", "espo_get_error",
     "espo_status_string", "espo_export_token_stats", "espo_export_rollout_stats",
     "espo_launch_count", "espo_set_option", "espo_loss_fwd_partial", "espo_loss_fwd_combine",
-    "espo_attach_tp",
+    "espo_attach_tp", "espo_lmhead_fwd",
 ]
 
 
@@ -112,6 +112,7 @@ def load_library():
         "espo_loss_fwd_partial": (I32, [P, P, I64, P, P, P, I64, I64, P, P]),
         "espo_loss_fwd_combine": (I32, [P, P, I32, I64, I64, P]),
         "espo_attach_tp": (I32, [P, P, I32, I32]),
+        "espo_lmhead_fwd": (I32, [P, P, I64, P, I64, I32, P, P, P, I64, I64, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -255,6 +256,15 @@ class Espo:
         _check(self._lib.espo_loss_fwd_combine(self._h, _ptr(partials), int(partials.shape[0]),
                                                int(row_begin), int(partials.shape[1]),
                                                self._stream()), "espo_loss_fwd_combine")
+
+    def lmhead_fwd(self, hidden, weight, tokens, old_logp, mask=None, row_begin=0):
+        """espo_lmhead_fwd: fused LM head (tcgen05) + forward statistics; logits never
+        materialised. hidden bf16 [n, d], weight bf16 [vocab, d]."""
+        n, d = int(hidden.shape[0]), int(hidden.shape[1])
+        _check(self._lib.espo_lmhead_fwd(self._h, _ptr(hidden), int(hidden.stride(0)),
+                                         _ptr(weight), int(weight.stride(0)), d, _ptr(tokens),
+                                         _ptr(old_logp), _ptr(mask), int(row_begin), n,
+                                         self._stream()), "espo_lmhead_fwd")
 
     def loss_finalize(self, loss_out=None, stats_out=None):
         """espo_loss_finalize → (loss f32[1], stats f64[STATS_LEN]) device tensors."""

@@ -1,0 +1,98 @@
+"""Fused LM head + ESPO forward on tcgen05: the row statistics computed
+from hidden states and the LM-head matrix without materialising logits must equal those of
+the logits path on the same fp32 logits (h·Wᵀ with fp32 accumulation), and the oracle's on
+fp64 logits within the fp32-accumulation error of the GEMM."""
+import numpy as np
+import pytest
+import torch
+
+import espo_synth as S
+from oracle import espo_oracle as O
+from paper_2512_07710_b200.espo import Espo, stats_to_dict
+from tests.gpu_common import oracle_cfg, require_cuda, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def make_case(seed, n_groups, G, L, V, d, zv_group=None):
+    rng = np.random.default_rng(seed)
+    R = n_groups * G
+    T = R * L
+    h = (rng.standard_normal((T, d)) / np.sqrt(d) * 3).astype(np.float32)
+    W = rng.standard_normal((V, d)).astype(np.float32)
+    W[rng.integers(0, V, size=V // 50)] *= 3.0                  # a few strong tokens
+    h, W = S.round_to_bf16(h), S.round_to_bf16(W)
+    z64 = h.astype(np.float64) @ W.astype(np.float64).T
+    tokens = S.sample_tokens_gumbel(z64.astype(np.float32), seed)
+    group_ids = np.repeat(np.arange(n_groups, dtype=np.int32), G)
+    so = np.arange(R + 1, dtype=np.int64) * L
+    rewards = (rng.uniform(size=R) < 0.5).astype(np.float32)
+    for g in range(n_groups):
+        rewards[g * G] = 1.0
+        rewards[g * G + 1] = 0.0
+    if zv_group is not None:
+        rewards[zv_group * G:(zv_group + 1) * G] = 1.0
+    lp = np.array([O.row_stats(z64[t], int(tokens[t]))[1] for t in range(T)])
+    old = S.drift_old_logp(lp, so, seed)
+    mask = np.ones(T, np.uint8)
+    mask[L - 5:L] = 0
+    return dict(h=h, W=W, z64=z64, tokens=tokens, group_ids=group_ids, so=so, rewards=rewards,
+                old=old, mask=mask, T=T, R=R)
+
+
+def run_path(case, dev, fused, V):
+    ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
+    tok = to_dev(case["tokens"], torch.int32, dev)
+    old = to_dev(case["old"], torch.float32, dev)
+    mask = to_dev(case["mask"], torch.uint8, dev)
+    ctx.prepare(to_dev(case["rewards"], torch.float32, dev), to_dev(case["group_ids"], torch.int32, dev),
+                to_dev(case["so"], torch.int64, dev), n_tokens=case["T"])
+    h = to_dev(case["h"], torch.bfloat16, dev)
+    W = to_dev(case["W"], torch.bfloat16, dev)
+    if fused:
+        half = case["T"] // 2 + 37                   # two chunks, the first not a multiple of 128
+        ctx.lmhead_fwd(h[:half], W, tok[:half], old[:half], mask[:half], row_begin=0)
+        ctx.lmhead_fwd(h[half:], W, tok[half:], old[half:], mask[half:], row_begin=half)
+    else:
+        ld = (V + 3) // 4 * 4
+        z = torch.zeros((case["T"], ld), dtype=torch.float32, device=dev)
+        z[:, :V] = h.float() @ W.float().T
+        ctx.loss_fwd(z, tok, old, mask)
+    loss, stats = ctx.loss_finalize()
+    ctx.get_error()
+    out = dict(loss=float(loss.item()), stats=stats_to_dict(stats),
+               tok={k: v.cpu().numpy() for k, v in ctx.export_token_stats().items()})
+    ctx.close()
+    return out
+
+
+@pytest.mark.parametrize("shape", [(4, 4, 40, 1000, 200), (2, 8, 64, 4099, 512)],
+                         ids=["V1000_d200", "V4099_d512"])
+def test_lmhead_fwd_matches_logits_path(shape):
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dev = require_cuda()
+    ng, G, L, V, d = shape
+    case = make_case(5, ng, G, L, V, d, zv_group=1)
+    f = run_path(case, dev, True, V)
+    u = run_path(case, dev, False, V)
+    v = u["tok"]["valid"].astype(bool)
+    assert np.array_equal(f["tok"]["valid"], u["tok"]["valid"])
+    assert f["stats"]["n_active_tokens"] == u["stats"]["n_active_tokens"]
+    # both paths accumulate h·Wᵀ in fp32 (different orders): per-row logit error bound
+    hb = np.abs(case["h"].astype(np.float64)) @ np.abs(case["W"].astype(np.float64)).T
+    bound = d * 2.0 ** -24 * hb.max(axis=1)[v]
+    for k, tol, kb in (("lse", 2e-6, 2), ("lp", 2e-6, 4), ("H", 1e-5, 8)):
+        a, b = f["tok"][k][v].astype(np.float64), u["tok"][k][v].astype(np.float64)
+        lim = tol * np.maximum(1, np.abs(b)) + kb * bound
+        assert np.all(np.abs(a - b) <= lim), (k, np.max(np.abs(a - b) / lim))
+    assert f["loss"] == pytest.approx(u["loss"], rel=1e-3, abs=1e-6)
+    # oracle on fp64 logits: within the fused GEMM's fp32-accumulation error
+    cfg = oracle_cfg(V)
+    ref = O.espo_loss(case["z64"], case["tokens"], case["old"], case["mask"], case["rewards"],
+                      case["group_ids"], case["so"], cfg)
+    assert np.array_equal(ref.kappa >= 0, v)
+    for k, tol, kb in (("lse", 2e-6, 1), ("lp", 2e-6, 2), ("H", 1e-5, 4)):
+        diff = np.abs(f["tok"][k][v].astype(np.float64) - getattr(ref, k)[v])
+        lim = tol * np.maximum(1, np.abs(getattr(ref, k)[v])) + kb * bound
+        assert np.all(diff <= lim), (k, np.max(diff / lim))
+    assert f["stats"]["n_zv_groups"] == ref.stats["n_zv_groups"] == 1
