@@ -587,8 +587,14 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   const int V = c->cfg.vocab;
   const int mblocks = int((n_rows + kLmBM - 1) / kLmBM);
   const int ntiles = (V + kLmBN - 1) / kLmBN;
-  int parts = (2 * c->num_sms + mblocks - 1) / mblocks;   // ≥ 2 waves of CTAs
-  parts = std::max(1, std::min(parts, std::min(16, ntiles)));
+  // vocabulary parts: ≥ 2 waves of CTAs, and few enough distinct row blocks resident at once
+  // that their A tiles (128 × d bf16 each) stay in L2 (≤ ~40 MB of the 126 MB)
+  int parts = (2 * c->num_sms + mblocks - 1) / mblocks;
+  const int64_t a_bytes = int64_t(kLmBM) * d * 2;
+  const int l2_parts = int((int64_t(c->num_sms) * a_bytes + (40ll << 20) - 1) / (40ll << 20));
+  parts = std::max(parts, l2_parts);
+  parts = std::max(1, std::min(parts, std::min(32, ntiles)));
+  if (mblocks > 65535) return ESPO_ERR_INVALID_ARGUMENT;
   const size_t need = size_t(parts) * size_t(n_rows) * 16;
   if (need > c->lmh_cap) {
     if (c->lmh_partial) cudaFree(c->lmh_partial);
@@ -620,7 +626,7 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   lp.tokens = tokens;
   lp.partial = c->lmh_partial;
   lp.ws = c->ws;
-  k_lmhead_fwd<<<dim3(mblocks, parts), kLmThreads, kLmSmem, s>>>(mh, mw, lp);
+  k_lmhead_fwd<<<dim3(parts, mblocks), kLmThreads, kLmSmem, s>>>(mh, mw, lp);
   ESPO_LAUNCHED(c);
   if ((st = launch_combine(c, c->lmh_partial, parts, row_begin, n_rows, s)) != ESPO_OK) return st;
   c->covered[row_begin] = row_begin + n_rows;

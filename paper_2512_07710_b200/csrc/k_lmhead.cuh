@@ -3,7 +3,8 @@
 // reduced on the fly into the row statistics (lse, lp, H, q) — the [T, V] logits never exist
 // in HBM.
 //
-// CTA = one 128-row block of hidden states × one contiguous part of the vocabulary (P parts).
+// CTA = one 128-row block of hidden states × one contiguous part of the vocabulary (P parts;
+// grid = (P, row blocks), P chosen so the A tiles of the resident CTAs fit in L2).
 // Warp roles (192 threads): warp 0 — TMA producer (cp.async.bulk.tensor 2D, 128-byte swizzle,
 // 4-stage smem ring of {A: 128×64 bf16, B: 256×64 bf16}); warp 1 — TMEM allocator and MMA
 // issuer (one thread, tcgen05.mma.cta_group::1.kind::f16, M=128, N=256, K=16, fp32
@@ -118,8 +119,10 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   int* s_any = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kLmBM;
-  const int part = blockIdx.y;
+  // vocabulary part fastest-varying: the CTAs resident together share a few row blocks (their
+  // A tiles stay in L2) and read the same W tiles in step
+  const int m0 = blockIdx.y * kLmBM;
+  const int part = blockIdx.x;
   const int t_begin = int((int64_t(p.ntiles) * part) / p.parts);
   const int t_end = int((int64_t(p.ntiles) * (part + 1)) / p.parts);
   const int nk = (p.d + kLmBK - 1) / kLmBK;
