@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
     const bool valid = r < p.n_rows && p.ws.flag[p.row_begin + r];
     const int y = valid ? p.tokens[r] : -1;
     const float lamL = p.lam_log2e;
-    float R = -INFINITY, S = 0.f, W = 0.f, uy = __int_as_float(0x7fc00000);
+    float R = -INFINITY, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f, uy = __int_as_float(0x7fc00000);
     int i = 0;
     for (int tile = t_begin; tile < t_end; ++tile, ++i) {
       const int acc = i & 1;
@@ -227,36 +227,67 @@ __global__ void __launch_bounds__(kLmThreads, 1)
             if (col == y || col >= p.V) x[e] = -INFINITY;
           }
         }
-        float m = x[0];
+        if (R == -INFINITY) {                      // first chunk: reference = its max
+          float m = x[0];
 #pragma unroll
-        for (int e = 1; e < 32; ++e) m = fmaxf(m, x[e]);
-        m *= lamL;
-        if (m > R) {
-          rebase(R, m, S, W);
-          R = m;
+          for (int e = 1; e < 32; ++e) m = fmaxf(m, x[e]);
+          R = m * lamL;
+          if (R == -INFINITY) continue;
         }
-        if (R == -INFINITY) continue;
-        const float nR = -R;
-        float s0 = 0.f, s1 = 0.f, w0 = 0.f, w1 = 0.f;
+        // fast chunk: no clamp, no max (logits are finite; masked columns are −inf and go
+        // through the checked path below via NaN = 0·(−inf))
+        float bS, bW;
+        {
+          const float nR = -R;
+          float s0 = 0.f, s1 = 0.f, w0 = 0.f, w1 = 0.f;
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float ta = max_nan(fmaf(x[e], lamL, nR), -127.f);
-          const float tb = max_nan(fmaf(x[e + 1], lamL, nR), -127.f);
-          const float ea = ex2(ta), eb = ex2(tb);
-          s0 += ea;
-          s1 += eb;
-          w0 = fmaf(ea, ta, w0);
-          w1 = fmaf(eb, tb, w1);
+          for (int e = 0; e < 32; e += 2) {
+            const float ta = fmaf(x[e], lamL, nR), tb = fmaf(x[e + 1], lamL, nR);
+            const float ea = ex2(ta), eb = ex2(tb);
+            s0 += ea;
+            s1 += eb;
+            w0 = fmaf(ea, ta, w0);
+            w1 = fmaf(eb, tb, w1);
+          }
+          bS = s0 + s1;
+          bW = w0 + w1;
         }
-        S += s0 + s1;
-        W += w0 + w1;
+        if (!(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {  // overflow / −inf / NaN: checked
+          S -= cS;
+          W -= cW;
+          cS = cW = 0.f;
+          float m = -INFINITY;
+          bool bad = false;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            bad |= isnan(x[e]) || x[e] == INFINITY;
+            m = fmaxf(m, x[e] * lamL);
+          }
+          if (bad) set_error(p.ws.err, ESPO_ERR_NONFINITE_INPUT);
+          if (m > R + 60.f) {
+            rebase(R, m, S, W);
+            R = m;
+          }
+          bS = 0.f;
+          bW = 0.f;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float t = max_nan(fmaf(x[e], lamL, -R), -127.f);
+            const float ex = ex2(t);
+            bS += ex;
+            bW = fmaf(ex, t, bW);
+          }
+        }
+        kahan_add(S, cS, bS);
+        kahan_add(W, cW, bW);
       }
       __syncwarp();
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
     if (valid)
-      reinterpret_cast<float4*>(p.partial)[int64_t(part) * p.n_rows + r] = make_float4(R, S, W, uy);
+      reinterpret_cast<float4*>(p.partial)[int64_t(part) * p.n_rows + r] =
+          make_float4(R, S - cS, W - cW, uy);
   }
   tc_fence_before();
   __syncthreads();
