@@ -39,7 +39,9 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="C1")
+    p.add_argument("--config", default="C1", help="C1 (default), C2, C3, C4 (BASELINE.json)")
+    p.add_argument("--compact", action="store_true",
+                   help="compact mode: rows without gradient are not zero-filled (C3)")
     p.add_argument("--buffer-rows", type=int, default=32768)
     p.add_argument("--fwd-impl", type=int, default=0, help="0/2/3/4 = TMA ring variants, 1 = LDG")
     p.add_argument("--bwd-impl", type=int, default=0, help="0/7 = tiled grid, 1 = LDG, 2-6 = TMA rings")
@@ -296,7 +298,8 @@ def main_ours(args):
     w = S.WORKLOADS[args.config]
     seed = S.config_seed(w.index) ^ (rank * 0x9E3779B9)
     d = make_batch(w, seed, dev, args.buffer_rows, log)
-    ctx = Espo(w.V, logits_dtype=torch.bfloat16, device=local, rank=rank, world=world)
+    ctx = Espo(w.V, logits_dtype=torch.bfloat16, device=local, rank=rank, world=world,
+               zero_fill_inactive_rows=not args.compact)
     ctx.set_option(OPT_FWD_IMPL, args.fwd_impl)
     ctx.set_option(OPT_BWD_IMPL, args.bwd_impl)
     ctx.set_option(OPT_BLOCKS_PER_SM, args.blocks_per_sm)
@@ -336,7 +339,9 @@ def main_ours(args):
     n_act = st["n_active_tokens"] / world      # stats are global (all-reduced)
     n_clip = st["n_clipped_tokens"] / world
     fwd_bytes = n_act * (2 * V + 4 + 4 + 16) + T * (4 + 4 + 1 + 8)
-    bwd_bytes = (n_act - n_clip) * 2 * V + T * 2 * V + T * 12
+    bwd_bytes = (n_act - n_clip) * 2 * V + (0 if args.compact else T) * 2 * V + T * 12
+    if args.compact:
+        bwd_bytes += (n_act - n_clip) * 2 * V      # swept rows are still written
     step_bytes = fwd_bytes + bwd_bytes
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["fwd"])
     bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["bwd"])
@@ -377,7 +382,7 @@ def main_ours(args):
                 "Bernoulli rewards, drifted old log-probs)",
         "config": {
             "workload": f"{w.name}: {w.n_prompts} prompts x {w.G} rollouts x {w.L} tokens per GPU, "
-                        f"vocab {V}, bf16 logits/grads",
+                        f"vocab {V}, bf16 logits/grads" + (", compact dlogits" if args.compact else ""),
             "global_batch_tokens": T * world, "seq_len": w.L, "parallelism": f"dp{world} (prompt-group sharded)",
             "chunk_rows": d["Rc"], "l2": "inputs larger than L2 (chunk buffer "
                                          f"{d['Rc'] * V * 2 / 1e9:.2f} GB > 126 MB)",

@@ -1,4 +1,6 @@
 set -u
-true
-for a in "0 7" "2 7" "4 7" "6 7" "1 7" "2 0"; do set -- $a; timeout 400 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --fwd-impl $1 --bwd-impl $2 > gpurun_out/bench_$1$2.json 2> gpurun_out/bench_$1$2.err; python -c "
-import json;d=json.load(open('gpurun_out/bench_$1$2.json'));c=d['config'];print('fwd $1 bwd $2: tok/s %.3e ms %.1f fwdGBs %.0f fwdms %.3f bwdms %.3f bwdGBs %.0f' % (d['value'],d['ms_per_step'],c['fwd_sweep_gbs'],c['fwd_sweep_ms_per_chunk'],c['bwd_sweep_ms_per_chunk'],d['roofline']['achieved']))" || tail -3 gpurun_out/bench_$1$2.err; done
+for c in "C2" "C3" "C3 --compact" "C4"; do
+  n=$(echo $c | tr -d ' -'); timeout 900 python bench.py --config $c --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_$n.json 2> gpurun_out/bench_$n.err; echo "$c exit=$?"
+  python -c "
+import json;d=json.load(open('gpurun_out/bench_$n.json'));c=d['config'];print('$c tok/s %.3e ms %.1f step TB/s %.2f (%.0f%% of 8) fwd %.0f bwd %.0f' % (d['value'],d['ms_per_step'],c['achieved_hbm_gbs_step']/1e3,100*c['frac_of_8TBs_step'],c['fwd_sweep_gbs'],d['roofline']['achieved']))" || tail -3 gpurun_out/bench_$n.err
+done
