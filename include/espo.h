@@ -259,7 +259,8 @@ typedef enum {
                                   row, 2..7 = other ring geometries (K2) */
   ESPO_OPT_BWD_IMPL = 1,       /* 0 = tiled (row, 32 KB tile) grid (default), 1 = LDG.128 warp
                                   per row, 2..6 = TMA ring geometries, 7 = 16 KB tiles */
-  ESPO_OPT_BLOCKS_PER_SM = 2   /* persistent grid = blocks_per_sm × SM count (0 = auto) */
+  ESPO_OPT_BLOCKS_PER_SM = 2,  /* persistent grid = blocks_per_sm × SM count (0 = auto) */
+  ESPO_OPT_LMHEAD_PARTS = 3    /* espo_lmhead_fwd vocabulary parts per row block (0 = auto) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

@@ -77,6 +77,7 @@ struct espo_ctx_s {
   uint64_t launches = 0;
   int fwd_impl = 0, bwd_impl = 0;
   int blocks_per_sm = 0;
+  int lmh_parts = 0;  // 0 = auto
   void* blocks_tok = nullptr;  // one allocation for all per-token arrays
   void* blocks_roll = nullptr; // one allocation for all per-rollout arrays
   void* blocks_scalar = nullptr;
@@ -346,6 +347,10 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       if (value < 0 || value > 32) return ESPO_ERR_INVALID_ARGUMENT;
       c->blocks_per_sm = static_cast<int>(value);
       return ESPO_OK;
+    case ESPO_OPT_LMHEAD_PARTS:
+      if (value < 0 || value > 64) return ESPO_ERR_INVALID_ARGUMENT;
+      c->lmh_parts = static_cast<int>(value);
+      return ESPO_OK;
   }
   return ESPO_ERR_INVALID_ARGUMENT;
 }
@@ -587,13 +592,14 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   const int V = c->cfg.vocab;
   const int mblocks = int((n_rows + kLmBM - 1) / kLmBM);
   const int ntiles = (V + kLmBN - 1) / kLmBN;
-  // vocabulary parts: ≥ 2 waves of CTAs, and few enough distinct row blocks resident at once
-  // that their A tiles (128 × d bf16 each) stay in L2 (≤ ~40 MB of the 126 MB)
+  // vocabulary parts per row block: enough CTAs for ≥ 2 waves; beyond that the best split
+  // measured on B200 (tools/bench_lmhead.py, n = 32,768, V = 151,936) is 4 parts for
+  // d ≤ 4096 and 2 for d = 8192 (fewer parts keep fewer W tiles live in L2, more parts keep
+  // fewer A row blocks live)
   int parts = (2 * c->num_sms + mblocks - 1) / mblocks;
-  const int64_t a_bytes = int64_t(kLmBM) * d * 2;
-  const int l2_parts = int((int64_t(c->num_sms) * a_bytes + (40ll << 20) - 1) / (40ll << 20));
-  parts = std::max(parts, l2_parts);
-  parts = std::max(1, std::min(parts, std::min(32, ntiles)));
+  parts = std::max(parts, std::max(2, std::min(4, 16384 / d)));
+  if (c->lmh_parts > 0) parts = c->lmh_parts;
+  parts = std::max(1, std::min(parts, std::min(64, ntiles)));
   if (mblocks > 65535) return ESPO_ERR_INVALID_ARGUMENT;
   const size_t need = size_t(parts) * size_t(n_rows) * 16;
   if (need > c->lmh_cap) {
