@@ -191,6 +191,29 @@ espo_status espo_loss_bwd(espo_ctx_t ctx, const void* logits, int64_t ld, void* 
                           int64_t ldg, const float* grad_loss_dev, int64_t row_begin,
                           int64_t n_rows, espo_stream_t stream);
 
+/* ---- ZVE stage 2: reward reshaping ----
+ * final_i = base_i + length_penalty_i + repetition_penalty_i for rollout i with response
+ * tokens tokens[seq_offsets[i] .. seq_offsets[i+1]) (device). length_penalty = 0 if
+ * len ≤ max_len − buffer, −(len − (max_len − buffer))/buffer on the ramp, −1 from max_len on;
+ * repetition_penalty = −gamma_rep·max(0, f − rep_thresh), f = fraction of the len − ngram + 1
+ * positions whose n-gram occurred earlier in the response. Arithmetic in fp64, results f32.
+ * Run before espo_prepare (the reshaped rewards feed the zero-variance test). May allocate
+ * scratch (12 B × 4 × n_tokens) on first use or growth. */
+typedef struct {
+  int32_t max_len;      /* ≥ 1 */
+  int32_t buffer;       /* ramp length; 0 = ⌈max_len / 8⌉ */
+  int32_t ngram;        /* 1..16, default 4 */
+  float gamma_rep;      /* default 1.0 */
+  float rep_thresh;     /* default 0.2 */
+  int32_t reserved[3];
+} espo_reward_shaping;
+void espo_reward_shaping_default(espo_reward_shaping* p, int32_t max_len);
+espo_status espo_reshape_rewards(espo_ctx_t ctx, const espo_reward_shaping* params,
+                                 const float* base_rewards, const int32_t* tokens,
+                                 const int64_t* seq_offsets, int32_t n_rollouts,
+                                 int64_t n_tokens, float* rewards_out, float* len_pen_out,
+                                 float* rep_pen_out, espo_stream_t stream);
+
 /* ---- vocabulary-parallel ESPO (logits sharded by vocabulary over TP ranks) ----
  * With cfg.vocab_local > 0 every rank holds the same token rows but only its vocabulary
  * columns. The forward sweep then produces, per row, a 16-byte partial

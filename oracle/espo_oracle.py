@@ -173,6 +173,35 @@ def zvp_token_advantages(H, reward: float, cfg: OracleConfig):
     return np.array([cfg.zvp_beta * sgn * (h - hbar) / math.log(cfg.vocab) for h in H.tolist()])
 
 
+def reshape_reward(base: float, response, max_len: int, buffer: int = 0, ngram: int = 4,
+                   gamma_rep: float = 1.0, rep_thresh: float = 0.2):
+    """ZVE stage 2 "Reward reshaping" (length and repetition penalties; concrete
+    form SPEC.md:262-265). Length penalty: 0 if len ≤ max_len − buffer, else linear from 0 to
+    −1 on [max_len − buffer, max_len] (buffer = ⌈max_len/8⌉ by default), −1 beyond.
+    Repetition penalty: −γ·max(0, f − thresh), f = fraction of the len−n+1 positions whose
+    n-gram occurred at an earlier position. Returns (final, length_penalty, rep_penalty)."""
+    toks = [int(t) for t in response]
+    n = len(toks)
+    buf = buffer if buffer > 0 else -(-max_len // 8)
+    start = max_len - buf
+    if n <= start:
+        lpen = 0.0
+    elif n >= max_len:
+        lpen = -1.0
+    else:
+        lpen = -(n - start) / buf
+    seen = set()
+    rep = 0
+    for p in range(n - ngram + 1):
+        g = tuple(toks[p:p + ngram])
+        if g in seen:
+            rep += 1
+        seen.add(g)
+    frac = rep / (n - ngram + 1) if n >= ngram else 0.0
+    rpen = -gamma_rep * max(0.0, frac - rep_thresh)
+    return base + lpen + rpen, lpen, rpen
+
+
 # ----------------------------------------------------------------------------------------
 # O2 — per-token log-softmax statistics
 # ----------------------------------------------------------------------------------------

@@ -14,6 +14,7 @@
 #include "k_rowlist.cuh"
 #include "k_seq.cuh"
 #include "k_lmhead.cuh"
+#include "k_reward.cuh"
 #include "workspace.cuh"
 
 #include <cudaTypedefs.h>
@@ -83,6 +84,8 @@ struct espo_ctx_s {
   void* blocks_scalar = nullptr;
   float* lmh_partial = nullptr;  // fused LM-head: [parts][rows] float4, grown on demand
   size_t lmh_cap = 0;
+  void* rs_scratch = nullptr;    // reward reshaping hash tables, grown on demand
+  int64_t rs_cap = 0;
 };
 
 namespace {
@@ -327,6 +330,7 @@ espo_status espo_destroy(espo_ctx_t c) {
     if (c->blocks_roll) cudaFree(c->blocks_roll);
     if (c->blocks_scalar) cudaFree(c->blocks_scalar);
     if (c->lmh_partial) cudaFree(c->lmh_partial);
+    if (c->rs_scratch) cudaFree(c->rs_scratch);
   }
   delete c;
   return ESPO_OK;
@@ -604,6 +608,7 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   const size_t need = size_t(parts) * size_t(n_rows) * 16;
   if (need > c->lmh_cap) {
     if (c->lmh_partial) cudaFree(c->lmh_partial);
+    if (c->rs_scratch) cudaFree(c->rs_scratch);
     c->lmh_partial = nullptr;
     ESPO_CUDA(cudaMalloc(&c->lmh_partial, need));
     c->lmh_cap = need;
@@ -637,6 +642,57 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   if ((st = launch_combine(c, c->lmh_partial, parts, row_begin, n_rows, s)) != ESPO_OK) return st;
   c->covered[row_begin] = row_begin + n_rows;
   c->n_covered += n_rows;
+  return ESPO_OK;
+}
+
+void espo_reward_shaping_default(espo_reward_shaping* p, int32_t max_len) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->max_len = max_len;
+  p->buffer = 0;
+  p->ngram = 4;
+  p->gamma_rep = 1.0f;
+  p->rep_thresh = 0.2f;
+}
+
+espo_status espo_reshape_rewards(espo_ctx_t c, const espo_reward_shaping* prm,
+                                 const float* base_rewards, const int32_t* tokens,
+                                 const int64_t* seq_offsets, int32_t n_rollouts,
+                                 int64_t n_tokens, float* rewards_out, float* len_pen_out,
+                                 float* rep_pen_out, espo_stream_t stream) {
+  if (!c || !prm || !base_rewards || !seq_offsets || !rewards_out || n_rollouts < 0 ||
+      n_tokens < 0 || (n_tokens > 0 && !tokens))
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (prm->max_len < 1 || prm->buffer < 0 || prm->buffer > prm->max_len || prm->ngram < 1 ||
+      prm->ngram > 16 || !(prm->gamma_rep >= 0.f) || !std::isfinite(prm->gamma_rep) ||
+      !std::isfinite(prm->rep_thresh))
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rollouts == 0) return ESPO_OK;
+  DevGuard g(c->device);
+  const int64_t need = std::max<int64_t>(4 * n_tokens, 1);
+  if (need > c->rs_cap) {
+    if (c->rs_scratch) cudaFree(c->rs_scratch);
+    c->rs_scratch = nullptr;
+    ESPO_CUDA(cudaMalloc(&c->rs_scratch, size_t(need) * 12));
+    c->rs_cap = need;
+  }
+  ReshapeParams rp;
+  rp.base = base_rewards;
+  rp.tokens = tokens;
+  rp.seq_off = seq_offsets;
+  rp.R = n_rollouts;
+  rp.max_len = prm->max_len;
+  rp.buffer = prm->buffer;
+  rp.ngram = prm->ngram;
+  rp.gamma_rep = prm->gamma_rep;
+  rp.rep_thresh = prm->rep_thresh;
+  rp.out = rewards_out;
+  rp.len_pen = len_pen_out;
+  rp.rep_pen = rep_pen_out;
+  rp.keys = static_cast<uint64_t*>(c->rs_scratch);
+  rp.first = reinterpret_cast<int32_t*>(static_cast<char*>(c->rs_scratch) + size_t(c->rs_cap) * 8);
+  k_reshape_rewards<<<n_rollouts, 256, 0, S(stream)>>>(rp);
+  ESPO_LAUNCHED(c);
   return ESPO_OK;
 }
 

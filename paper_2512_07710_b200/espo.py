@@ -39,7 +39,8 @@ EXPORTED_SYMBOLS = [
     "espo_loss_fwd", "espo_loss_finalize", "espo_loss_bwd", "espo_get_error",
     "espo_status_string", "espo_export_token_stats", "espo_export_rollout_stats",
     "espo_launch_count", "espo_set_option", "espo_loss_fwd_partial", "espo_loss_fwd_combine",
-    "espo_attach_tp", "espo_lmhead_fwd",
+    "espo_attach_tp", "espo_lmhead_fwd", "espo_reward_shaping_default",
+    "espo_reshape_rewards",
 ]
 
 
@@ -64,6 +65,12 @@ class Config(ctypes.Structure):
         ("zvp_threshold", ctypes.c_float), ("vocab_begin", ctypes.c_int32),
         ("vocab_local", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2),
     ]
+
+
+class RewardShaping(ctypes.Structure):
+    _fields_ = [("max_len", ctypes.c_int32), ("buffer", ctypes.c_int32),
+                ("ngram", ctypes.c_int32), ("gamma_rep", ctypes.c_float),
+                ("rep_thresh", ctypes.c_float), ("reserved", ctypes.c_int32 * 3)]
 
 
 STATS_FIELDS = ["loss", "n_active_rollouts", "n_active_tokens", "n_zv_groups", "n_groups",
@@ -113,6 +120,9 @@ def load_library():
         "espo_loss_fwd_combine": (I32, [P, P, I32, I64, I64, P]),
         "espo_attach_tp": (I32, [P, P, I32, I32]),
         "espo_lmhead_fwd": (I32, [P, P, I64, P, I64, I32, P, P, P, I64, I64, P]),
+        "espo_reward_shaping_default": (None, [ctypes.POINTER(RewardShaping), I32]),
+        "espo_reshape_rewards": (I32, [P, ctypes.POINTER(RewardShaping), P, P, P, I32, I64, P,
+                                       P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -265,6 +275,21 @@ class Espo:
                                          _ptr(weight), int(weight.stride(0)), d, _ptr(tokens),
                                          _ptr(old_logp), _ptr(mask), int(row_begin), n,
                                          self._stream()), "espo_lmhead_fwd")
+
+    def reshape_rewards(self, base_rewards, tokens, seq_offsets, n_tokens, max_len, buffer=0,
+                        ngram=4, gamma_rep=1.0, rep_thresh=0.2):
+        """espo_reshape_rewards (ZVE stage 2): returns (rewards, length_pen, rep_pen) f32[R]."""
+        prm = RewardShaping()
+        self._lib.espo_reward_shaping_default(ctypes.byref(prm), int(max_len))
+        prm.buffer, prm.ngram = int(buffer), int(ngram)
+        prm.gamma_rep, prm.rep_thresh = float(gamma_rep), float(rep_thresh)
+        R = int(base_rewards.shape[0])
+        out = [torch.empty(R, dtype=torch.float32, device=base_rewards.device) for _ in range(3)]
+        _check(self._lib.espo_reshape_rewards(self._h, ctypes.byref(prm), _ptr(base_rewards),
+                                              _ptr(tokens), _ptr(seq_offsets), R, int(n_tokens),
+                                              *[_ptr(o) for o in out], self._stream()),
+               "espo_reshape_rewards")
+        return tuple(out)
 
     def loss_finalize(self, loss_out=None, stats_out=None):
         """espo_loss_finalize → (loss f32[1], stats f64[STATS_LEN]) device tensors."""

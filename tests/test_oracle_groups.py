@@ -104,3 +104,44 @@ def test_errors():
     with pytest.raises(O.OracleInputError) as e:
         O.group_advantages(np.array([0, np.nan], np.float32), np.zeros(2, np.int32), cfg())
     assert e.value.code == "ESPO_ERR_NONFINITE_INPUT"
+
+
+# --------------------------------------------------- ZVE stage 2: reward reshaping
+def test_reshape_reward_spec_examples():
+    """short non-repetitive → no penalty; len = max_len → −1; a fully
+    periodic "ab ab ab …" response → rep fraction from an independent scan."""
+    final, lp_, rp = O.reshape_reward(0.7, list(range(20)), max_len=64)
+    assert (final, lp_, rp) == (0.7, 0.0, 0.0)
+    _, lp_, _ = O.reshape_reward(1.0, list(range(64)), max_len=64)
+    assert lp_ == -1.0
+    periodic = [1, 2] * 32                                   # 64 tokens
+    _, _, rp = O.reshape_reward(1.0, periodic, max_len=1000)
+    # 4-grams: positions 0 and 1 are new, the other 59 of 61 repeat → −(59/61 − 0.2)
+    assert rp == pytest.approx(-(59 / 61 - 0.2), rel=1e-15)
+
+
+def test_reshape_reward_length_ramp_and_brute_force_repetition():
+    # buffer = ceil(100/8) = 13: ramp on [87, 100]
+    for n, want in ((87, 0.0), (88, -1 / 13), (93, -6 / 13), (100, -1.0), (150, -1.0)):
+        assert O.reshape_reward(0.0, list(range(n)), 100)[1] == pytest.approx(want)
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        n = int(rng.integers(0, 40))
+        toks = rng.integers(0, 3, size=n).tolist()
+        _, _, rp = O.reshape_reward(0.0, toks, 10 ** 6, gamma_rep=2.0, rep_thresh=0.1)
+        m = n - 3
+        rep = sum(1 for p in range(max(m, 0))
+                  if any(toks[q:q + 4] == toks[p:p + 4] for q in range(p)))
+        frac = rep / m if m > 0 else 0.0
+        assert rp == pytest.approx(-2.0 * max(0.0, frac - 0.1), abs=1e-15)
+
+
+def test_reshaping_breaks_zero_variance_ties():
+    """with penalties an all-correct group of different lengths is no longer
+    zero-variance (PAPER.md:90: reshaping "leverages negative samples")."""
+    lengths = [30, 60, 95, 120]
+    base = np.ones(4, np.float32)
+    assert O.group_advantages(base, np.zeros(4, np.int32), cfg())["zv_group"][0]
+    shaped = np.array([O.reshape_reward(1.0, list(range(n)), 100)[0] for n in lengths],
+                      np.float32)
+    assert not O.group_advantages(shaped, np.zeros(4, np.int32), cfg())["zv_group"][0]
