@@ -163,6 +163,21 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
   return r;
 }
 
+// Per-(kernel, device) one-time opt-in to large dynamic shared memory: the attribute is a
+// property of the function on the *current* device, so a process driving several GPUs sets it
+// once per device (bit d of a per-kernel mask; the race on first use is benign).
+template <typename K>
+inline cudaError_t ensure_smem_attr(K kernel, int bytes, unsigned long long& done_mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done_mask & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done_mask |= bit;
+  return e;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -620,12 +620,8 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
   k_lmh_rows<<<pre_grid, 256, 0, s>>>(tokens, old_logp, mask, row_begin, n_rows, V, c->ws);
   ESPO_LAUNCHED(c);
-  static bool attr = false;
-  if (!attr) {
-    ESPO_CUDA(cudaFuncSetAttribute(k_lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kLmSmem)));
-    attr = true;
-  }
+  static unsigned long long attr_mask = 0;
+  ESPO_CUDA(ensure_smem_attr(k_lmhead_fwd, int(kLmSmem), attr_mask));
   LmParams lp;
   lp.n_rows = int(n_rows);
   lp.row_begin = row_begin;

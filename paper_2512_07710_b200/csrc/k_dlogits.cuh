@@ -265,12 +265,9 @@ inline cudaError_t launch_dlogits_tma_cfg(const BwdParams& p, const BwdRec* list
                                           int blocks_per_sm, cudaStream_t s) {
   constexpr size_t smem = size_t(NW) * STAGES * CHUNK + size_t(NW) * STAGES * 8;
   auto k = k_dlogits_tma<Tin, Tout, NW, STAGES, CHUNK>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static unsigned long long attr_mask = 0;
+  cudaError_t e = ensure_smem_attr(k, int(smem), attr_mask);
+  if (e != cudaSuccess) return e;
   const int bps = blocks_per_sm > 0 ? blocks_per_sm : 1;
   k<<<num_sms * bps, NW * 32, smem, s>>>(p, list, zlist, count);
   return cudaGetLastError();

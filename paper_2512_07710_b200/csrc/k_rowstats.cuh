@@ -442,12 +442,9 @@ inline cudaError_t launch_rowstats_tma_cfg(const FwdParams& p, const FwdRec* lis
                                            int num_sms, int blocks_per_sm, cudaStream_t s) {
   constexpr size_t smem = size_t(NW) * STAGES * CHUNK + size_t(NW) * STAGES * 8;
   auto k = k_rowstats_tma<Tin, NW, STAGES, CHUNK, SUB, NPOLY>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static unsigned long long attr_mask = 0;
+  cudaError_t e = ensure_smem_attr(k, int(smem), attr_mask);
+  if (e != cudaSuccess) return e;
   const int bps = blocks_per_sm > 0 ? blocks_per_sm : 1;
   k<<<num_sms * bps, NW * 32, smem, s>>>(p, list, count);
   return cudaGetLastError();
