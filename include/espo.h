@@ -73,7 +73,8 @@ typedef enum {
   ESPO_ERR_OUT_OF_MEMORY = 7,
   ESPO_ERR_CUDA = 8,
   ESPO_ERR_NCCL = 9,
-  ESPO_ERR_UNSUPPORTED = 10
+  ESPO_ERR_UNSUPPORTED = 10,
+  ESPO_ERR_BLAS = 11                 /* libcublas missing or a cuBLAS call failed */
 } espo_status;
 
 typedef enum { ESPO_F32 = 0, ESPO_BF16 = 1 } espo_dtype;
@@ -239,8 +240,8 @@ espo_status espo_attach_tp(espo_ctx_t ctx, const void* tp_unique_id, int32_t tp_
                            int32_t tp_world);
 
 /* ---- fused LM head + forward statistics (tcgen05) ----
- * Computes the same row statistics as espo_loss_fwd for logits = λ·(hidden · weightᵀ) without
- * writing the logits: hidden bf16 [n_rows, ldh ≥ d] (row row_begin of the chunk first),
+ * Computes the same row statistics as espo_loss_fwd for logits z = hidden · weightᵀ (softmax
+ * of λ·z as there) without writing the logits: hidden bf16 [n_rows, ldh ≥ d] (row row_begin of the chunk first),
  * weight bf16 [vocab, ldw ≥ d] (the LM-head matrix, row v = vocabulary entry v), fp32
  * accumulation on the tensor cores; tokens/old_logp/mask as in espo_loss_fwd. 16-byte aligned
  * bases and pitches. Counts as the forward call for these rows. The first call may allocate
@@ -249,6 +250,26 @@ espo_status espo_lmhead_fwd(espo_ctx_t ctx, const void* hidden, int64_t ldh, con
                             int64_t ldw, int32_t d, const int32_t* tokens, const float* old_logp,
                             const uint8_t* mask, int64_t row_begin, int64_t n_rows,
                             espo_stream_t stream);
+
+/* ---- fused LM head backward (tcgen05 recompute + bf16 dz tile + two GEMMs) ----
+ * Gradients of grad_loss·loss through logits z = hidden·weightᵀ for the
+ * rows [row_begin, row_begin + n_rows) of a finalized context whose forward ran through
+ * espo_lmhead_fwd with the same hidden/weight:
+ *   dz    = ∂(grad_loss·loss)/∂z, exactly K5's formula, recomputed tile by tile on the tensor
+ *           cores (same pipeline and K order as the forward, so the logits are bitwise the
+ *           forward's) and rounded to bf16 into a context-owned scratch of
+ *           ESPO_OPT_LMHEAD_BWD_ROWS × round_up(vocab, 256) bf16 (allocated on first use);
+ *   dhidden[r, :] = Σ_v dz[r, v]·weight[v, :]          (overwritten; f32 or bf16 per dh_dtype)
+ *   dweight[v, :] += Σ_r dz[r, v]·hidden[r, :]          (f32, ACCUMULATED: zero it once)
+ * The two contractions are plain bf16 GEMMs with fp32 accumulation, run by cuBLAS (loaded
+ * at run time from libcublas.so.12) on `stream`. Either output may be NULL (skipped). Shapes
+ * and alignment as espo_lmhead_fwd; dhidden pitch lddh ≥ d, dweight pitch lddw ≥ d (16-byte
+ * aligned). grad_loss_dev as espo_loss_bwd. Errors: ESPO_ERR_BAD_STATE before finalize,
+ * ESPO_ERR_UNSUPPORTED on a vocabulary-sharded context, ESPO_ERR_BLAS if cuBLAS fails. */
+espo_status espo_lmhead_bwd(espo_ctx_t ctx, const void* hidden, int64_t ldh, const void* weight,
+                            int64_t ldw, int32_t d, void* dhidden, int64_t lddh, int32_t dh_dtype,
+                            float* dweight, int64_t lddw, const float* grad_loss_dev,
+                            int64_t row_begin, int64_t n_rows, espo_stream_t stream);
 
 /* Synchronises `stream`, then returns the sticky device error (ESPO_OK if none) or
  * ESPO_ERR_CUDA if a CUDA error is pending. */
@@ -283,7 +304,9 @@ typedef enum {
   ESPO_OPT_BWD_IMPL = 1,       /* 0 = tiled (row, 32 KB tile) grid (default), 1 = LDG.128 warp
                                   per row, 2..6 = TMA ring geometries, 7 = 16 KB tiles */
   ESPO_OPT_BLOCKS_PER_SM = 2,  /* persistent grid = blocks_per_sm × SM count (0 = auto) */
-  ESPO_OPT_LMHEAD_PARTS = 3    /* espo_lmhead_fwd vocabulary parts per row block (0 = auto) */
+  ESPO_OPT_LMHEAD_PARTS = 3,   /* espo_lmhead_fwd/bwd vocabulary parts per row block (0 = auto) */
+  ESPO_OPT_LMHEAD_BWD_ROWS = 4 /* espo_lmhead_bwd rows per dz sub-chunk (multiple of 128;
+                                  0 = default 8192) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

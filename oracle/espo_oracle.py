@@ -22,6 +22,9 @@ order the paper states the method; citations are ``PAPER.md:<line> (<section/eq>
   O6  espo_loss          PAPER.md:105 (expectation, 1/G, 1/|τ|, 1/|y_τ| normalisers)
   O7  dlogits            chain rule through log-softmax of the Eq. 1 numerator; every
                          sg[·] term is constant (PAPER.md:113)
+  O8  frozen_surrogate   the sg-frozen objective used by the finite-difference pins
+  O9  lmhead_grads       (§8(f) row 1) dh = dz·W, dW = dzᵀ·h for logits z = h·Wᵀ
+                         (Megatron log-prob recompute)
 
 Readings where the paper is silent/garbled (IDs from SURVEY.md §8(c)-2; all listed in
 DESIGN.md "Readings"): Q1 ratio reading R2 (GSPO-token sg[π_θ] denominator) is the
@@ -523,3 +526,18 @@ def frozen_surrogate_loss(logits_eval, res: OracleResult, tokens, old_logp, seq_
             ell, _ = token_surrogate(v, A, res.eps_tok[t])
             J += res.w_tok[t] * ell
     return -grad_loss * J / res.denom if res.denom > 0 else 0.0
+
+
+def lmhead_grads(res: OracleResult, hidden, weight, tokens, cfg: OracleConfig,
+                 grad_loss: float = 1.0):
+    """O9 (the LM head in front of the path; Megatron log-prob recompute,
+    PAPER.md:129-131). With logits z = h·Wᵀ (row t: z_t = W h_t), the chain rule through
+    O7 gives dL/dh_t = Σ_v dz_{t,v} W_v and dL/dW_v = Σ_t dz_{t,v} h_t, i.e.
+    dh = dz·W and dW = dzᵀ·h, where dz is O7's matrix on z = h·Wᵀ in fp64.
+    Returns (dz, dh, dW), all fp64."""
+    h = np.asarray(hidden, dtype=np.float64)
+    W = np.asarray(weight, dtype=np.float64)
+    z = h @ W.T
+    dz = np.stack([dlogits_row(res, t, z[t], int(tokens[t]), cfg, grad_loss)
+                   for t in range(h.shape[0])])
+    return dz, dz @ W, dz.T @ h

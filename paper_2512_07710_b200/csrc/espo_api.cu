@@ -17,6 +17,7 @@
 #include "k_reward.cuh"
 #include "workspace.cuh"
 
+#include <cublas_v2.h>
 #include <cudaTypedefs.h>
 
 using namespace espo;
@@ -57,6 +58,40 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
+// ------------------------------------------------------------------------------ cuBLAS
+// The LM-head backward's two plain GEMMs (dh = dz·W, dW += dzᵀ·h). Resolved at run time from
+// libcublas.so.12 (the copy torch already loaded, when present); no link-time dependency.
+typedef int (*fn_blas_create)(cublasHandle_t*);
+typedef int (*fn_blas_destroy)(cublasHandle_t);
+typedef int (*fn_blas_stream)(cublasHandle_t, cudaStream_t);
+typedef int (*fn_blas_workspace)(cublasHandle_t, void*, size_t);
+typedef int (*fn_blas_gemm)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
+                            const void*, const void*, cudaDataType, int, const void*, cudaDataType,
+                            int, const void*, void*, cudaDataType, int, cublasComputeType_t,
+                            cublasGemmAlgo_t);
+struct BlasApi {
+  void* lib = nullptr;
+  fn_blas_create create = nullptr;
+  fn_blas_destroy destroy = nullptr;
+  fn_blas_stream set_stream = nullptr;
+  fn_blas_workspace set_workspace = nullptr;
+  fn_blas_gemm gemm = nullptr;
+  bool load() {
+    if (lib) return true;
+    lib = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("/usr/local/cuda/lib64/libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return false;
+    create = reinterpret_cast<fn_blas_create>(dlsym(lib, "cublasCreate_v2"));
+    destroy = reinterpret_cast<fn_blas_destroy>(dlsym(lib, "cublasDestroy_v2"));
+    set_stream = reinterpret_cast<fn_blas_stream>(dlsym(lib, "cublasSetStream_v2"));
+    set_workspace = reinterpret_cast<fn_blas_workspace>(dlsym(lib, "cublasSetWorkspace_v2"));
+    gemm = reinterpret_cast<fn_blas_gemm>(dlsym(lib, "cublasGemmEx"));
+    return create && destroy && set_stream && set_workspace && gemm;
+  }
+};
+BlasApi g_blas;
+constexpr size_t kBlasWorkspace = size_t(32) << 20;
+
 enum class State { Created, Prepared, Finalized };
 }  // namespace
 
@@ -86,6 +121,11 @@ struct espo_ctx_s {
   size_t lmh_cap = 0;
   void* rs_scratch = nullptr;    // reward reshaping hash tables, grown on demand
   int64_t rs_cap = 0;
+  int lmh_bwd_rows = 8192;       // LM-head backward dz sub-chunk rows
+  void* lmh_dz = nullptr;        // [lmh_bwd_rows][round_up(V, 256)] bf16, grown on demand
+  size_t lmh_dz_cap = 0;
+  cublasHandle_t blas = nullptr;
+  void* blas_ws = nullptr;
 };
 
 namespace {
@@ -259,6 +299,7 @@ const char* espo_status_string(espo_status s) {
     case ESPO_ERR_CUDA: return "ESPO_ERR_CUDA";
     case ESPO_ERR_NCCL: return "ESPO_ERR_NCCL";
     case ESPO_ERR_UNSUPPORTED: return "ESPO_ERR_UNSUPPORTED";
+    case ESPO_ERR_BLAS: return "ESPO_ERR_BLAS";
   }
   return "ESPO_ERR_UNKNOWN";
 }
@@ -331,6 +372,9 @@ espo_status espo_destroy(espo_ctx_t c) {
     if (c->blocks_scalar) cudaFree(c->blocks_scalar);
     if (c->lmh_partial) cudaFree(c->lmh_partial);
     if (c->rs_scratch) cudaFree(c->rs_scratch);
+    if (c->lmh_dz) cudaFree(c->lmh_dz);
+    if (c->blas) g_blas.destroy(c->blas);
+    if (c->blas_ws) cudaFree(c->blas_ws);
   }
   delete c;
   return ESPO_OK;
@@ -354,6 +398,10 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
     case ESPO_OPT_LMHEAD_PARTS:
       if (value < 0 || value > 64) return ESPO_ERR_INVALID_ARGUMENT;
       c->lmh_parts = static_cast<int>(value);
+      return ESPO_OK;
+    case ESPO_OPT_LMHEAD_BWD_ROWS:
+      if (value < 0 || value > (1 << 20) || value % kLmBM) return ESPO_ERR_INVALID_ARGUMENT;
+      c->lmh_bwd_rows = value ? static_cast<int>(value) : 8192;
       return ESPO_OK;
   }
   return ESPO_ERR_INVALID_ARGUMENT;
@@ -572,6 +620,16 @@ bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
+// vocabulary parts per row block: enough CTAs for ≥ 2 waves; beyond that the best split
+// measured on B200 (tools/bench_lmhead.py, n = 32,768, V = 151,936) is 4 parts for d ≤ 4096
+// and 2 for d = 8192 (fewer parts keep fewer W tiles live in L2, more parts keep fewer A row
+// blocks live)
+int lmhead_parts(const espo_ctx_s* c, int mblocks, int ntiles, int d) {
+  int parts = (2 * c->num_sms + mblocks - 1) / mblocks;
+  parts = std::max(parts, std::max(2, std::min(4, 16384 / d)));
+  if (c->lmh_parts > 0) parts = c->lmh_parts;
+  return std::max(1, std::min(parts, std::min(64, ntiles)));
+}
 }  // namespace
 
 extern "C" {
@@ -596,19 +654,11 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   const int V = c->cfg.vocab;
   const int mblocks = int((n_rows + kLmBM - 1) / kLmBM);
   const int ntiles = (V + kLmBN - 1) / kLmBN;
-  // vocabulary parts per row block: enough CTAs for ≥ 2 waves; beyond that the best split
-  // measured on B200 (tools/bench_lmhead.py, n = 32,768, V = 151,936) is 4 parts for
-  // d ≤ 4096 and 2 for d = 8192 (fewer parts keep fewer W tiles live in L2, more parts keep
-  // fewer A row blocks live)
-  int parts = (2 * c->num_sms + mblocks - 1) / mblocks;
-  parts = std::max(parts, std::max(2, std::min(4, 16384 / d)));
-  if (c->lmh_parts > 0) parts = c->lmh_parts;
-  parts = std::max(1, std::min(parts, std::min(64, ntiles)));
+  const int parts = lmhead_parts(c, mblocks, ntiles, d);
   if (mblocks > 65535) return ESPO_ERR_INVALID_ARGUMENT;
   const size_t need = size_t(parts) * size_t(n_rows) * 16;
   if (need > c->lmh_cap) {
     if (c->lmh_partial) cudaFree(c->lmh_partial);
-    if (c->rs_scratch) cudaFree(c->rs_scratch);
     c->lmh_partial = nullptr;
     ESPO_CUDA(cudaMalloc(&c->lmh_partial, need));
     c->lmh_cap = need;
@@ -638,6 +688,99 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   if ((st = launch_combine(c, c->lmh_partial, parts, row_begin, n_rows, s)) != ESPO_OK) return st;
   c->covered[row_begin] = row_begin + n_rows;
   c->n_covered += n_rows;
+  return ESPO_OK;
+}
+
+espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const void* weight,
+                            int64_t ldw, int32_t d, void* dhidden, int64_t lddh, int32_t dh_dtype,
+                            float* dweight, int64_t lddw, const float* grad_loss_dev,
+                            int64_t row_begin, int64_t n_rows, espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Finalized) return ESPO_ERR_BAD_STATE;
+  if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T || d < 1)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rows == 0) return ESPO_OK;
+  if (!hidden || !weight || ldh < d || ldw < d) return ESPO_ERR_INVALID_ARGUMENT;
+  if (dh_dtype != ESPO_F32 && dh_dtype != ESPO_BF16) return ESPO_ERR_INVALID_ARGUMENT;
+  if ((dhidden && lddh < d) || (dweight && lddw < d)) return ESPO_ERR_INVALID_ARGUMENT;
+  if (!aligned16(hidden) || !aligned16(weight) || (ldh * 2) % 16 || (ldw * 2) % 16 ||
+      (dhidden && (!aligned16(dhidden) || (lddh * int64_t(dsize(dh_dtype))) % 16)) ||
+      (dweight && (!aligned16(dweight) || (lddw * 4) % 16)))
+    return ESPO_ERR_ALIGNMENT;
+  if (c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab) return ESPO_ERR_UNSUPPORTED;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  const int V = c->cfg.vocab;
+  const int ntiles = (V + kLmBN - 1) / kLmBN;
+  const int64_t ldz = int64_t(ntiles) * kLmBN;
+  const int sub = int(std::min<int64_t>(c->lmh_bwd_rows, round_up(size_t(n_rows), kLmBM)));
+  const size_t need = size_t(sub) * size_t(ldz) * 2;
+  if (need > c->lmh_dz_cap) {
+    if (c->lmh_dz) cudaFree(c->lmh_dz);
+    c->lmh_dz = nullptr;
+    c->lmh_dz_cap = 0;
+    ESPO_CUDA(cudaMalloc(&c->lmh_dz, need));
+    c->lmh_dz_cap = need;
+  }
+  if (!c->blas) {
+    if (!g_blas.load()) return ESPO_ERR_BLAS;
+    if (g_blas.create(&c->blas) != 0) {
+      c->blas = nullptr;
+      return ESPO_ERR_BLAS;
+    }
+    ESPO_CUDA(cudaMalloc(&c->blas_ws, kBlasWorkspace));
+    if (g_blas.set_workspace(c->blas, c->blas_ws, kBlasWorkspace) != 0) return ESPO_ERR_BLAS;
+  }
+  if (g_blas.set_stream(c->blas, s) != 0) return ESPO_ERR_BLAS;
+  // per-row records {g, −lse·log2e, g·q, y} for the whole chunk (K5's k_bwd_recs, zero-filling)
+  BwdRec* rec = static_cast<BwdRec*>(c->ws.list);
+  const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  k_bwd_recs<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, 1, 0, V, c->ws, rec);
+  ESPO_LAUNCHED(c);
+  static unsigned long long attr_mask = 0;
+  ESPO_CUDA(ensure_smem_attr(k_lmhead_dz, int(kLmSmem), attr_mask));
+  CUtensorMap mw;
+  if (!make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, kLmBN))
+    return ESPO_ERR_CUDA;
+  const float one = 1.f, zero = 0.f;
+  const char* hb = static_cast<const char*>(hidden);
+  for (int64_t r0 = 0; r0 < n_rows; r0 += sub) {
+    const int n = int(std::min<int64_t>(sub, n_rows - r0));
+    const int mblocks = (n + kLmBM - 1) / kLmBM;
+    const int parts = lmhead_parts(c, mblocks, ntiles, d);
+    CUtensorMap mh;
+    if (!make_map_bf16(&mh, hb + r0 * ldh * 2, uint64_t(n), uint64_t(d), uint64_t(ldh) * 2, kLmBM))
+      return ESPO_ERR_CUDA;
+    LmParams lp{};
+    lp.n_rows = n;
+    lp.row_begin = row_begin + r0;
+    lp.d = d;
+    lp.V = V;
+    lp.ntiles = ntiles;
+    lp.parts = parts;
+    lp.lam_log2e = c->cfg.logit_scale * kLog2e;
+    lp.rec = rec + r0;
+    lp.dz = static_cast<__nv_bfloat16*>(c->lmh_dz);
+    lp.ldz = ldz;
+    lp.ws = c->ws;
+    k_lmhead_dz<<<dim3(parts, mblocks), kLmThreads, kLmSmem, s>>>(mh, mw, lp);
+    ESPO_LAUNCHED(c);
+    // z = h·Wᵀ (dz already carries λ, as K5's) ⇒ dh = dz·W and dW = dzᵀ·h
+    if (dhidden) {   // column-major view: dhᵀ[d, n] = Wᵀ[d, V] · dzᵀ[V, n]
+      char* dh = static_cast<char*>(dhidden) + r0 * lddh * int64_t(dsize(dh_dtype));
+      if (g_blas.gemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, d, n, V, &one, weight, CUDA_R_16BF,
+                      int(ldw), c->lmh_dz, CUDA_R_16BF, int(ldz), &zero, dh,
+                      dh_dtype == ESPO_BF16 ? CUDA_R_16BF : CUDA_R_32F, int(lddh),
+                      CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != 0)
+        return ESPO_ERR_BLAS;
+    }
+    if (dweight) {   // column-major view: dWᵀ[d, V] += hᵀ[d, n] · dz[n, V]
+      if (g_blas.gemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_T, d, V, n, &one, hb + r0 * ldh * 2,
+                      CUDA_R_16BF, int(ldh), c->lmh_dz, CUDA_R_16BF, int(ldz), &one, dweight,
+                      CUDA_R_32F, int(lddw), CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != 0)
+        return ESPO_ERR_BLAS;
+    }
+  }
   return ESPO_OK;
 }
 

@@ -16,6 +16,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "k_rowlist.cuh"
 #include "k_rowstats.cuh"
 #include "workspace.cuh"
 
@@ -40,7 +41,10 @@ struct LmParams {
   int parts;             // vocabulary parts (gridDim.y)
   float lam_log2e;
   const int32_t* tokens; // chunk-relative
-  float* partial;        // [parts][n_rows] float4
+  float* partial;        // [parts][n_rows] float4 (forward)
+  const BwdRec* rec;     // per-row backward records, chunk-relative (k_lmhead_dz)
+  __nv_bfloat16* dz;     // [n_rows][ldz] bf16 gradient tile output (k_lmhead_dz)
+  int64_t ldz;           // ≥ ntiles·256 elements
   Workspace ws;
 };
 
@@ -103,9 +107,42 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 constexpr uint32_t kLmIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kLmBN >> 3) << 17) |
                               (uint32_t(kLmBM >> 4) << 24);
 
-__global__ void __launch_bounds__(kLmThreads, 1)
-    k_lmhead_fwd(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w,
-                 const LmParams p) {
+// Epilogue of the backward recompute (kDz): the gradient of the 32 logits x[] of row `rc`
+// starting at column col0, rounded to bf16 and stored (64 contiguous bytes of the row):
+// dz_v = λ·g·(1[v = y] − p_v) — the same per-element formula as K5 (k_dlogits.cuh dz_vec).
+__device__ __forceinline__ void lm_store_dz(const float* x, const BwdRec& rc, int col0, int V,
+                                            float lamL, __nv_bfloat16* out) {
+  uint32_t w[16];
+  if (rc.ng != 0.f) {
+    const bool special = (rc.y >= col0 && rc.y < col0 + 32) || (col0 + 32 > V);
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float a = rc.ng * ex2(fmaf(x[e], lamL, rc.nlseL));
+      float b = rc.ng * ex2(fmaf(x[e + 1], lamL, rc.nlseL));
+      if (special) {
+        if (col0 + e == rc.y) a = rc.gq;
+        if (col0 + e + 1 == rc.y) b = rc.gq;
+        if (col0 + e >= V) a = 0.f;
+        if (col0 + e + 1 >= V) b = 0.f;
+      }
+      const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+      w[e >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) w[e] = 0u;
+  }
+  uint4* o = reinterpret_cast<uint4*>(out);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) o[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+}
+
+// kDz = false: forward statistics (k_lmhead_fwd); kDz = true: backward recompute writing the
+// bf16 gradient tile dz = ∂(grad·loss)/∂z (k_lmhead_dz). Same TMA/MMA pipeline, same tile
+// order and K order, so the recomputed logits are bitwise the forward's.
+template <bool kDz>
+__device__ __forceinline__ void lmhead_body(const CUtensorMap& tmap_h, const CUtensorMap& tmap_w,
+                                            const LmParams& p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);   // 1024-B aligned (SW128)
@@ -132,10 +169,27 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   __syncthreads();
   if (threadIdx.x < kLmBM) {
     const int r = m0 + threadIdx.x;
-    if (r < p.n_rows && p.ws.flag[p.row_begin + r]) *s_any = 1;
+    if (r < p.n_rows) {
+      if constexpr (kDz) {
+        if (p.rec[r].ng != 0.f) *s_any = 1;
+      } else {
+        if (p.ws.flag[p.row_begin + r]) *s_any = 1;
+      }
+    }
   }
   __syncthreads();
-  if (*s_any == 0 || t_begin >= t_end) return;
+  if (t_begin >= t_end) return;
+  if (*s_any == 0) {
+    if constexpr (kDz) {   // no gradient in this block: zero its rows of this part's columns
+      const int c0 = t_begin * kLmBN / 8, c1 = t_end * kLmBN / 8;   // uint4 columns
+      const int nr = min(kLmBM, p.n_rows - m0);
+      for (int rr = 0; rr < nr; ++rr) {
+        uint4* o = reinterpret_cast<uint4*>(p.dz + int64_t(m0 + rr) * p.ldz);
+        for (int c = c0 + int(threadIdx.x); c < c1; c += kLmThreads) o[c] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    return;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kLmStages; ++s) {
@@ -201,6 +255,30 @@ __global__ void __launch_bounds__(kLmThreads, 1)
     const int quarter = warp & 3;                // TMEM lanes this warp may access
     const int row = quarter * 32 + lane;
     const int r = m0 + row;
+    if constexpr (kDz) {
+      BwdRec rc;
+      rc.ng = 0.f;
+      rc.y = -1;
+      if (r < p.n_rows) rc = p.rec[r];
+      int i = 0;
+      for (int tile = t_begin; tile < t_end; ++tile, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tfull[acc], (i >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t base = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kLmBN);
+#pragma unroll 1
+        for (int c = 0; c < kLmBN / 32; ++c) {
+          float x[32];
+          __syncwarp();
+          tmem_ld32(base + uint32_t(c * 32), x);
+          const int col0 = tile * kLmBN + c * 32;
+          if (r < p.n_rows) lm_store_dz(x, rc, col0, p.V, p.lam_log2e, p.dz + int64_t(r) * p.ldz + col0);
+        }
+        __syncwarp();
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
+    } else {
     const bool valid = r < p.n_rows && p.ws.flag[p.row_begin + r];
     const int y = valid ? p.tokens[r] : -1;
     const float lamL = p.lam_log2e;
@@ -288,6 +366,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
     if (valid)
       reinterpret_cast<float4*>(p.partial)[int64_t(part) * p.n_rows + r] =
           make_float4(R, S - cS, W - cW, uy);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -296,6 +375,18 @@ __global__ void __launch_bounds__(kLmThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
                  : "memory");
   }
+}
+
+__global__ void __launch_bounds__(kLmThreads, 1)
+    k_lmhead_fwd(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w,
+                 const LmParams p) {
+  lmhead_body<false>(tmap_h, tmap_w, p);
+}
+
+__global__ void __launch_bounds__(kLmThreads, 1)
+    k_lmhead_dz(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w,
+                const LmParams p) {
+  lmhead_body<true>(tmap_h, tmap_w, p);
 }
 
 // Row flags / token copies for the fused path (no logits to read the target from).

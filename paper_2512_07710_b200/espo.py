@@ -25,7 +25,7 @@ PART_QUANTILE, PART_WHOLE, PART_SINGLETON = 0, 1, 2
 RATIO_GSPO_TOKEN, RATIO_LITERAL_OLD = 0, 1
 NORM_SEQ, NORM_TOKEN = 0, 1
 ZV_MASK, ZV_RLZVP = 0, 1
-OPT_FWD_IMPL, OPT_BWD_IMPL, OPT_BLOCKS_PER_SM, OPT_LMHEAD_PARTS = 0, 1, 2, 3
+OPT_FWD_IMPL, OPT_BWD_IMPL, OPT_BLOCKS_PER_SM, OPT_LMHEAD_PARTS, OPT_LMHEAD_BWD_ROWS = 0, 1, 2, 3, 4
 
 STATUS = {
     0: "ESPO_OK", 1: "ESPO_ERR_INVALID_ARGUMENT", 2: "ESPO_ERR_ALIGNMENT",
@@ -33,13 +33,14 @@ STATUS = {
     5: "ESPO_ERR_NONFINITE_INPUT", 6: "ESPO_ERR_TOKEN_OUT_OF_RANGE",
     7: "ESPO_ERR_OUT_OF_MEMORY", 8: "ESPO_ERR_CUDA", 9: "ESPO_ERR_NCCL",
     10: "ESPO_ERR_UNSUPPORTED",
+    11: "ESPO_ERR_BLAS",
 }
 EXPORTED_SYMBOLS = [
     "espo_config_default", "espo_get_unique_id", "espo_create", "espo_destroy", "espo_prepare",
     "espo_loss_fwd", "espo_loss_finalize", "espo_loss_bwd", "espo_get_error",
     "espo_status_string", "espo_export_token_stats", "espo_export_rollout_stats",
     "espo_launch_count", "espo_set_option", "espo_loss_fwd_partial", "espo_loss_fwd_combine",
-    "espo_attach_tp", "espo_lmhead_fwd", "espo_reward_shaping_default",
+    "espo_attach_tp", "espo_lmhead_fwd", "espo_lmhead_bwd", "espo_reward_shaping_default",
     "espo_reshape_rewards",
 ]
 
@@ -120,6 +121,7 @@ def load_library():
         "espo_loss_fwd_combine": (I32, [P, P, I32, I64, I64, P]),
         "espo_attach_tp": (I32, [P, P, I32, I32]),
         "espo_lmhead_fwd": (I32, [P, P, I64, P, I64, I32, P, P, P, I64, I64, P]),
+        "espo_lmhead_bwd": (I32, [P, P, I64, P, I64, I32, P, I64, I32, P, I64, P, I64, I64, P]),
         "espo_reward_shaping_default": (None, [ctypes.POINTER(RewardShaping), I32]),
         "espo_reshape_rewards": (I32, [P, ctypes.POINTER(RewardShaping), P, P, P, I32, I64, P,
                                        P, P, P]),
@@ -275,6 +277,24 @@ class Espo:
                                          _ptr(weight), int(weight.stride(0)), d, _ptr(tokens),
                                          _ptr(old_logp), _ptr(mask), int(row_begin), n,
                                          self._stream()), "espo_lmhead_fwd")
+
+    def lmhead_bwd(self, hidden, weight, dhidden=None, dweight=None, row_begin=0, grad_loss=None,
+                   dh_dtype=None):
+        """espo_lmhead_bwd: dhidden (overwritten, [n, d]) and dweight (f32 [vocab, d],
+        accumulated) for rows [row_begin, row_begin + n) of the fused LM head."""
+        n, d = int(hidden.shape[0]), int(hidden.shape[1])
+        if dhidden is None:
+            dhidden = torch.empty((n, d), dtype=dh_dtype or torch.float32, device=hidden.device)
+        dt = _DT[dhidden.dtype] if dhidden is not False else F32
+        dh = None if dhidden is False else dhidden
+        _check(self._lib.espo_lmhead_bwd(self._h, _ptr(hidden), int(hidden.stride(0)),
+                                         _ptr(weight), int(weight.stride(0)), d, _ptr(dh),
+                                         int(dh.stride(0)) if dh is not None else 0, dt,
+                                         _ptr(dweight),
+                                         int(dweight.stride(0)) if dweight is not None else 0,
+                                         _ptr(grad_loss), int(row_begin), n, self._stream()),
+               "espo_lmhead_bwd")
+        return dh, dweight
 
     def reshape_rewards(self, base_rewards, tokens, seq_offsets, n_tokens, max_len, buffer=0,
                         ngram=4, gamma_rep=1.0, rep_thresh=0.2):

@@ -96,3 +96,68 @@ def test_lmhead_fwd_matches_logits_path(shape):
         lim = tol * np.maximum(1, np.abs(getattr(ref, k)[v])) + kb * bound
         assert np.all(diff <= lim), (k, np.max(diff / lim))
     assert f["stats"]["n_zv_groups"] == ref.stats["n_zv_groups"] == 1
+
+
+@pytest.mark.parametrize("shape,sub,dh_bf16", [((4, 4, 40, 1000, 200), 0, False),
+                                               ((2, 8, 64, 4099, 512), 256, True)],
+                         ids=["V1000_d200", "V4099_d512_sub256_bf16"])
+def test_lmhead_bwd_matches_oracle(shape, sub, dh_bf16):
+    """espo_lmhead_bwd (tcgen05 recompute → bf16 dz → dh = dz·W, dW += dzᵀ·h) against O9 on
+    fp64 logits, with the GPU's bucket / clip decisions injected where they flipped. Bound:
+    dz is rounded to bf16 (2^-9) after an fp32 recompute whose logit error is ≤ the GEMM
+    bound b_t; the contractions accumulate in fp32 over V (resp. n) terms."""
+    from paper_2512_07710_b200.espo import OPT_LMHEAD_BWD_ROWS
+    from tests._instances import Instance
+    from tests.gpu_common import decision_aware_reference
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dev = require_cuda()
+    ng, G, L, V, d = shape
+    case = make_case(7, ng, G, L, V, d, zv_group=0)
+    T = case["T"]
+    ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
+    if sub:
+        ctx.set_option(OPT_LMHEAD_BWD_ROWS, sub)
+    tok = to_dev(case["tokens"], torch.int32, dev)
+    old = to_dev(case["old"], torch.float32, dev)
+    mask = to_dev(case["mask"], torch.uint8, dev)
+    ctx.prepare(to_dev(case["rewards"], torch.float32, dev), to_dev(case["group_ids"], torch.int32, dev),
+                to_dev(case["so"], torch.int64, dev), n_tokens=T)
+    h = to_dev(case["h"], torch.bfloat16, dev)
+    W = to_dev(case["W"], torch.bfloat16, dev)
+    ctx.lmhead_fwd(h, W, tok, old, mask)
+    ctx.loss_finalize()
+    gl = torch.tensor([0.75], dtype=torch.float32, device=dev)
+    dW = torch.zeros((V, d), dtype=torch.float32, device=dev)
+    dh = torch.full((T, d), float("nan"), dtype=torch.bfloat16 if dh_bf16 else torch.float32,
+                    device=dev)
+    cut = T // 3 + 5                                   # two backward chunks, dW accumulates
+    ctx.lmhead_bwd(h[:cut], W, dh[:cut], dW, row_begin=0, grad_loss=gl)
+    ctx.lmhead_bwd(h[cut:], W, dh[cut:], dW, row_begin=cut, grad_loss=gl)
+    ctx.get_error()
+    g = dict(tok={k: v.cpu().numpy() for k, v in ctx.export_token_stats().items()})
+    ctx.close()
+    inst = Instance(case["z64"], case["tokens"], case["old"], case["mask"], case["rewards"],
+                    case["group_ids"], case["so"], V)
+    cfg = oracle_cfg(V)
+    ref = inst.run(cfg)
+    ref2, _ = decision_aware_reference(g, inst, ref, cfg)
+    dz, dh_ref, dW_ref = O.lmhead_grads(ref2, case["h"], case["W"], case["tokens"], cfg, 0.75)
+    hb = np.abs(case["h"].astype(np.float64)) @ np.abs(case["W"].astype(np.float64)).T
+    b_t = d * 2.0 ** -24 * hb.max(axis=1)                    # per-row logit error bound
+    adz = np.abs(dz) * (2.0 ** -9 + 4 * b_t[:, None] + 1e-6)  # per-element dz error bound
+    Wa, ha = np.abs(case["W"].astype(np.float64)), np.abs(case["h"].astype(np.float64))
+    lim_dh = adz @ Wa + V * 2.0 ** -24 * (np.abs(dz) @ Wa) + 1e-30
+    lim_dW = adz.T @ ha + T * 2.0 ** -24 * (np.abs(dz).T @ ha) + 1e-30
+    got_dh = dh.float().cpu().numpy().astype(np.float64)
+    got_dW = dW.cpu().numpy().astype(np.float64)
+    if dh_bf16:
+        lim_dh = lim_dh + 2.0 ** -9 * np.abs(dh_ref) * 1.01
+    assert np.all(np.abs(got_dh - dh_ref) <= lim_dh), np.max(np.abs(got_dh - dh_ref) / lim_dh)
+    assert np.all(np.abs(got_dW - dW_ref) <= lim_dW), np.max(np.abs(got_dW - dW_ref) / lim_dW)
+    # norm-wise: 2e-3 (the north_star bf16 tolerance); a bf16 dh adds its own output rounding
+    for got, want, tol in ((got_dh, dh_ref, 2e-3 + (2.0 ** -9 if dh_bf16 else 0.0)),
+                           (got_dW, dW_ref, 2e-3)):
+        assert np.linalg.norm(got - want) <= tol * np.linalg.norm(want)
+    # rows of the zero-variance group and masked rows carry no gradient
+    zrows = ref2.kappa < 0
+    assert zrows.any() and np.all(got_dh[zrows] == 0)

@@ -423,3 +423,61 @@ def test_zvp_gradient_matches_torch_autograd():
         for t in range(inst.T):
             dz = O.dlogits_row(res, t, inst.logits[t], int(inst.tokens[t]), cfg)
             np.testing.assert_allclose(dz, z.grad[t].numpy(), rtol=1e-10, atol=1e-14)
+
+
+# --------------------------------------------------- O9: LM-head gradients (§8(f) row 1)
+def _lmhead_instance(seed, V=11, d=5, kw=None):
+    rng = np.random.default_rng(seed)
+    base = tiny_instance(seed + 300, V=V, group_sizes=(3, 2), L=6, mask_tail=2, sigma_seq=0.1,
+                         logit_scale=(kw or {}).get("logit_scale", 1.0))
+    h = rng.standard_normal((base.T, d))
+    W = rng.standard_normal((V, d))
+    z = h @ W.T
+    lp = np.array([O.row_stats(z[t], int(base.tokens[t]), (kw or {}).get("logit_scale", 1.0))[1]
+                   for t in range(base.T)])
+    old = (lp + rng.normal(0, 0.05, size=base.T)).astype(np.float32)
+    inst = type(base)(z, base.tokens, old, base.mask, base.rewards, base.group_ids,
+                      base.seq_offsets, V)
+    return inst, h, W
+
+
+@pytest.mark.parametrize("kw", CONFIGS[:3] + [dict(logit_scale=0.7)],
+                         ids=["default", "literal", "token_norm", "lambda0.7"])
+def test_lmhead_grads_match_torch_autograd(kw):
+    """O9 against autograd of the torch frozen surrogate through z = h·Wᵀ (a transposed or
+    swapped operand in O9 fails: h and W have different shapes)."""
+    inst, h, W = _lmhead_instance(3, kw=kw)
+    cfg = O.OracleConfig(vocab=inst.V, **kw)
+    res = inst.run(cfg)
+    ht = torch.tensor(h, requires_grad=True)
+    Wt = torch.tensor(W, requires_grad=True)
+    loss = _torch_frozen_loss(ht @ Wt.T, inst, res, cfg, grad_loss=1.3)
+    loss.backward()
+    dz, dh, dW = O.lmhead_grads(res, h, W, inst.tokens, cfg, grad_loss=1.3)
+    assert dz.shape == (inst.T, inst.V) and dh.shape == h.shape and dW.shape == W.shape
+    np.testing.assert_allclose(dh, ht.grad.numpy(), rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(dW, Wt.grad.numpy(), rtol=1e-10, atol=1e-14)
+    assert np.abs(dh).max() > 0 and np.abs(dW).max() > 0
+
+
+def test_lmhead_grads_match_finite_differences():
+    """fp64 central differences of the frozen surrogate F(h·Wᵀ) in single h and W entries."""
+    inst, h, W = _lmhead_instance(8)
+    cfg = O.OracleConfig(vocab=inst.V)
+    res = inst.run(cfg)
+    _, dh, dW = O.lmhead_grads(res, h, W, inst.tokens, cfg)
+    F = lambda hh, WW: O.frozen_surrogate_loss(hh @ WW.T, res, inst.tokens, inst.old_logp,
+                                               inst.seq_offsets, cfg)
+    eps = 1e-6
+    rng = np.random.default_rng(0)
+    for _ in range(12):
+        t, j = int(rng.integers(0, h.shape[0])), int(rng.integers(0, h.shape[1]))
+        hp, hm = h.copy(), h.copy()
+        hp[t, j] += eps
+        hm[t, j] -= eps
+        assert (F(hp, W) - F(hm, W)) / (2 * eps) == pytest.approx(dh[t, j], rel=1e-5, abs=1e-9)
+        v = int(rng.integers(0, W.shape[0]))
+        Wp, Wm = W.copy(), W.copy()
+        Wp[v, j] += eps
+        Wm[v, j] -= eps
+        assert (F(h, Wp) - F(h, Wm)) / (2 * eps) == pytest.approx(dW[v, j], rel=1e-5, abs=1e-9)
