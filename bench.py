@@ -51,6 +51,11 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-tokens", type=int, default=128, help="tokens per rollout")
+    p.add_argument("--zv-mode", default="mask", choices=["mask", "rlzvp"],
+                   help="zero-variance groups: eliminated (default) or RL-ZVP advantages")
+    p.add_argument("--vocab-shards", type=int, default=1,
+                   help="S > 1: vocabulary-parallel leg, S shard contexts back to back on this "
+                        "GPU (partials gathered by a device copy)")
     return p.parse_args()
 
 
@@ -179,6 +184,64 @@ def run_step(ctx, d, dlog, ev=None):
     return loss, stats
 
 
+class ShardedStep:
+    """Vocabulary-parallel leg on one GPU: S contexts, shard k owns columns [v0_k, v0_k + w_k)
+    of the same chunk buffer (a column view with the full row pitch); per chunk: S partial
+    sweeps → gathered partials (one device tensor) → S combines; after finalize, S backward
+    sweeps each writing its columns of the dlogits buffer."""
+
+    def __init__(self, ctxs, shards, Rc, dev):
+        import torch
+        self.ctxs, self.shards = ctxs, shards
+        self.part = torch.empty((len(ctxs), Rc, 4), dtype=torch.float32, device=dev)
+
+    @property
+    def launch_count(self):
+        return sum(c.launch_count for c in self.ctxs)
+
+    def get_error(self):
+        for c in self.ctxs:
+            c.get_error()
+
+    def close(self):
+        for c in self.ctxs:
+            c.close()
+
+
+def run_step_sharded(sh, d, dlog, ev=None):
+    import torch
+    T, Rc, buf = d["T"], d["Rc"], d["buf"]
+    for c in sh.ctxs:
+        c.prepare(d["rewards"], d["group_ids"], d["seq_offsets"], n_tokens=T)
+    for b in range(0, T, Rc):
+        e = min(T, b + Rc)
+        if ev is not None:
+            s0 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+        for k, (c, (v0, w)) in enumerate(zip(sh.ctxs, sh.shards)):
+            c.loss_fwd_partial(buf[:e - b, v0:v0 + w], d["tokens"][b:e], d["old"][b:e], None,
+                               row_begin=b, partial=sh.part[k, :e - b])
+        for c in sh.ctxs:
+            c.loss_fwd_combine(sh.part[:, :e - b], row_begin=b)
+        if ev is not None:
+            s1 = torch.cuda.Event(enable_timing=True)
+            s1.record()
+            ev["fwd"].append((s0, s1))
+    outs = [c.loss_finalize() for c in sh.ctxs]
+    for b in range(0, T, Rc):
+        e = min(T, b + Rc)
+        if ev is not None:
+            s0 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+        for c, (v0, w) in zip(sh.ctxs, sh.shards):
+            c.loss_bwd(buf[:e - b, v0:v0 + w], dlog[:e - b, v0:v0 + w], row_begin=b)
+        if ev is not None:
+            s1 = torch.cuda.Event(enable_timing=True)
+            s1.record()
+            ev["bwd"].append((s0, s1))
+    return outs[0]
+
+
 def run_e2e(ctx, d, dlog, args, dev):
     """End-to-end through the public API with HOST inputs: every step copies its inputs
     (rewards, group ids, offsets, tokens, old log-probs and every logits chunk, for the fwd
@@ -298,15 +361,32 @@ def main_ours(args):
     w = S.WORKLOADS[args.config]
     seed = S.config_seed(w.index) ^ (rank * 0x9E3779B9)
     d = make_batch(w, seed, dev, args.buffer_rows, log)
-    ctx = Espo(w.V, logits_dtype=torch.bfloat16, device=local, rank=rank, world=world,
-               zero_fill_inactive_rows=not args.compact)
-    ctx.set_option(OPT_FWD_IMPL, args.fwd_impl)
-    ctx.set_option(OPT_BWD_IMPL, args.bwd_impl)
-    ctx.set_option(OPT_BLOCKS_PER_SM, args.blocks_per_sm)
+    kw = dict(zero_fill_inactive_rows=not args.compact,
+              zv_mode=1 if args.zv_mode == "rlzvp" else 0)
+    S_ = args.vocab_shards
+    if S_ > 1:
+        if world > 1:
+            raise SystemExit("--vocab-shards is a single-GPU leg")
+        wd = [((w.V * (k + 1) // S_) // 8 * 8) - ((w.V * k // S_) // 8 * 8) for k in range(S_)]
+        wd[-1] = w.V - sum(wd[:-1])
+        shards = [(sum(wd[:k]), wd[k]) for k in range(S_)]
+        ctxs = [Espo(w.V, logits_dtype=torch.bfloat16, device=local, vocab_shard=sh, **kw)
+                for sh in shards]
+        for c in ctxs:
+            c.set_option(OPT_FWD_IMPL, args.fwd_impl)
+            c.set_option(OPT_BWD_IMPL, args.bwd_impl)
+        ctx = ShardedStep(ctxs, shards, d["Rc"], dev)
+        step_fn = run_step_sharded
+    else:
+        ctx = Espo(w.V, logits_dtype=torch.bfloat16, device=local, rank=rank, world=world, **kw)
+        ctx.set_option(OPT_FWD_IMPL, args.fwd_impl)
+        ctx.set_option(OPT_BWD_IMPL, args.bwd_impl)
+        ctx.set_option(OPT_BLOCKS_PER_SM, args.blocks_per_sm)
+        step_fn = run_step
     dlog = torch.empty((d["Rc"], w.V), dtype=torch.bfloat16, device=dev)
 
     for _ in range(args.warmup):
-        run_step(ctx, d, dlog)
+        step_fn(ctx, d, dlog)
     ctx.get_error()
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -319,7 +399,7 @@ def main_ours(args):
     torch.cuda.synchronize(dev)
     start.record()
     for _ in range(args.steps):
-        loss, stats = run_step(ctx, d, dlog, ev)
+        loss, stats = step_fn(ctx, d, dlog, ev)
     end.record()
     torch.cuda.synchronize(dev)
     launches = ctx.launch_count - launches0
@@ -357,7 +437,7 @@ def main_ours(args):
         traffic = tr.get("bwd_bytes_per_launch")
 
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and S_ == 1:
         tps, h2d, d2h, dt = run_e2e(ctx, d, dlog, args, dev)
         e2e = {"value": tps * world, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
@@ -382,7 +462,10 @@ def main_ours(args):
                 "Bernoulli rewards, drifted old log-probs)",
         "config": {
             "workload": f"{w.name}: {w.n_prompts} prompts x {w.G} rollouts x {w.L} tokens per GPU, "
-                        f"vocab {V}, bf16 logits/grads" + (", compact dlogits" if args.compact else ""),
+                        f"vocab {V}, bf16 logits/grads" + (", compact dlogits" if args.compact else "")
+                        + (", RL-ZVP advantages for zero-variance groups" if args.zv_mode == "rlzvp" else "")
+                        + (f", {S_} vocabulary shards back to back on one GPU (TP emulation, "
+                           "partials gathered by device copy)" if S_ > 1 else ""),
             "global_batch_tokens": T * world, "seq_len": w.L, "parallelism": f"dp{world} (prompt-group sharded)",
             "chunk_rows": d["Rc"], "l2": "inputs larger than L2 (chunk buffer "
                                          f"{d['Rc'] * V * 2 / 1e9:.2f} GB > 126 MB)",
