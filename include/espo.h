@@ -239,6 +239,30 @@ espo_status espo_loss_fwd_combine(espo_ctx_t ctx, const float* partials, int32_t
 espo_status espo_attach_tp(espo_ctx_t ctx, const void* tp_unique_id, int32_t tp_rank,
                            int32_t tp_world);
 
+/* ---- single-pass mode: forward and backward of a chunk in one call ----
+ * The loss normaliser D (N active rollouts; T_active in TOKEN mode) depends only on the
+ * zero-variance filter and the mask (readings Q10, Q11), and every other
+ * coupling (partition, s_τ, ε_τ) is within a rollout. So once D is fixed from the mask, a
+ * chunk holding COMPLETE rollouts can run forward → per-rollout K3 → backward at once, and a
+ * trainer produces each logits chunk once (no second pass over the logits or recompute of the
+ * LM head for the backward).
+ *
+ * espo_set_mask: after espo_prepare and before any forward call. mask u8[T] (device; NULL =
+ * all ones) is copied into the context; D is counted (and all-reduced over the DP
+ * communicator when world > 1 — a collective: every rank calls it). Switches the context to
+ * single-pass mode until the next espo_prepare: espo_loss_fwd / espo_loss_bwd then return
+ * ESPO_ERR_BAD_STATE.
+ * espo_loss_fwd_bwd: rows [row_begin, row_begin + n_rows) must start and end on rollout
+ * boundaries (device-checked: ESPO_ERR_INVALID_ARGUMENT via espo_get_error and a NaN loss);
+ * logits/tokens/old_logp as espo_loss_fwd, dlogits/grad_loss_dev as espo_loss_bwd (in place
+ * allowed). Chunks in any order, each row once; espo_loss_finalize afterwards only reduces
+ * the loss and statistics. Results are identical to the two-sweep path. */
+espo_status espo_set_mask(espo_ctx_t ctx, const uint8_t* mask, espo_stream_t stream);
+espo_status espo_loss_fwd_bwd(espo_ctx_t ctx, const void* logits, int64_t ld,
+                              const int32_t* tokens, const float* old_logp, void* dlogits,
+                              int64_t ldg, const float* grad_loss_dev, int64_t row_begin,
+                              int64_t n_rows, espo_stream_t stream);
+
 /* ---- fused LM head + forward statistics (tcgen05) ----
  * Computes the same row statistics as espo_loss_fwd for logits z = hidden · weightᵀ (softmax
  * of λ·z as there) without writing the logits: hidden bf16 [n_rows, ldh ≥ d] (row row_begin of the chunk first),

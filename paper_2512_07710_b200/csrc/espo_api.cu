@@ -108,6 +108,7 @@ struct espo_ctx_s {
   int R = 0;
   int64_t T = 0;
   State state = State::Created;
+  bool single_pass = false;  // espo_set_mask called: chunks run fwd → K3 → bwd at once
   std::map<int64_t, int64_t> covered;  // fwd chunks: begin → end
   int64_t n_covered = 0;
   uint64_t launches = 0;
@@ -187,7 +188,7 @@ espo_status ensure_workspace(espo_ctx_t c, int R, int64_t T) {
     const bool sharded = c->cfg.vocab_local > 0;
     const size_t a16 = sharded ? round_up(size_t(cap) * 16, 256) : 0;
     const size_t agath = c->tp_comm ? round_up(size_t(cap) * 16 * c->tp_world, 256) : 0;
-    ESPO_CUDA(cudaMalloc(&c->blocks_tok, 9 * a4 + 3 * a1 + a32 + a16 + agath));
+    ESPO_CUDA(cudaMalloc(&c->blocks_tok, 9 * a4 + 4 * a1 + a32 + a16 + agath));
     char* p = static_cast<char*>(c->blocks_tok);
     auto take = [&](size_t n) { char* r = p; p += n; return r; };
     c->ws.lse = reinterpret_cast<float*>(take(a4));
@@ -201,6 +202,7 @@ espo_status ensure_workspace(espo_ctx_t c, int R, int64_t T) {
     c->ws.flag = reinterpret_cast<uint8_t*>(take(a1));
     c->ws.bucket = reinterpret_cast<uint8_t*>(take(a1));
     c->ws.clip = reinterpret_cast<uint8_t*>(take(a1));
+    c->ws.pmask = reinterpret_cast<uint8_t*>(take(a1));
     c->ws.list = take(a32);
     c->ws.zlist = reinterpret_cast<int32_t*>(take(a4));
     c->ws.partial = sharded ? reinterpret_cast<float*>(take(a16)) : nullptr;
@@ -340,6 +342,7 @@ espo_status espo_create(const espo_config* cfg, const void* nccl_unique_id, int3
   char* p = static_cast<char*>(c->blocks_scalar);
   c->ws.red = reinterpret_cast<double*>(p);
   c->ws.bwd_scale = reinterpret_cast<float*>(p + 512);
+  c->ws.dpre = reinterpret_cast<double*>(p + 256);
   c->ws.err = reinterpret_cast<int*>(p + 768);
   c->ws.count = reinterpret_cast<int*>(p + 896);
   cudaMemset(c->blocks_scalar, 0, 1024);
@@ -424,6 +427,7 @@ espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* grou
   c->T = n_tokens;
   c->covered.clear();
   c->n_covered = 0;
+  c->single_pass = false;
   PrepParams p;
   p.rewards = rewards;
   p.group_ids = group_ids;
@@ -535,21 +539,13 @@ espo_status launch_combine(espo_ctx_t c, const float* partials, int n_shards, in
   ESPO_LAUNCHED(c);
   return ESPO_OK;
 }
-}  // namespace
 
-extern "C" {
-
-espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
-                          const float* old_logp, const uint8_t* mask, int64_t row_begin,
-                          int64_t n_rows, uint32_t flags, espo_stream_t stream) {
-  if (flags != 0) return ESPO_ERR_INVALID_ARGUMENT;
-  espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
-  if (st != ESPO_OK || n_rows == 0) return st;
+// Forward of one chunk (arguments and coverage already checked); records the coverage.
+espo_status fwd_chunk(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
+                      const float* old_logp, const uint8_t* mask, int64_t row_begin,
+                      int64_t n_rows, cudaStream_t s) {
+  espo_status st;
   const bool sharded = c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab;
-  if (sharded && !c->tp_comm) return ESPO_ERR_BAD_STATE;  // use partial + combine
-  if ((st = check_coverage(c, row_begin, row_begin + n_rows)) != ESPO_OK) return st;
-  DevGuard g(c->device);
-  cudaStream_t s = S(stream);
   if (sharded) {
     // vocabulary-parallel: partial → all-gather over the TP group → combine
     float* part = c->ws.partial;
@@ -566,6 +562,45 @@ espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const in
   c->covered[row_begin] = row_begin + n_rows;
   c->n_covered += n_rows;
   return ESPO_OK;
+}
+
+SeqParams seq_params(espo_ctx_t c, int64_t row_lo, int64_t row_hi) {
+  const espo_config& cf = c->cfg;
+  SeqParams sp;
+  sp.R = c->R;
+  sp.row_lo = row_lo;
+  sp.row_hi = row_hi;
+  sp.V = cf.vocab;
+  sp.alpha = cf.alpha;
+  sp.eps_min = cf.eps_min;
+  sp.K = cf.n_buckets;
+  sp.split_num = cf.split_num;
+  sp.split_den = cf.split_den;
+  sp.partition = cf.partition;
+  sp.ratio_mode = cf.ratio_mode;
+  sp.norm = cf.norm;
+  sp.log_ratio_clamp = cf.log_ratio_clamp;
+  sp.inv_logV = 1.0 / std::log(static_cast<double>(cf.vocab));
+  sp.zvp_beta = cf.zvp_beta;
+  sp.ws = c->ws;
+  return sp;
+}
+}  // namespace
+
+extern "C" {
+
+espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
+                          const float* old_logp, const uint8_t* mask, int64_t row_begin,
+                          int64_t n_rows, uint32_t flags, espo_stream_t stream) {
+  if (flags != 0) return ESPO_ERR_INVALID_ARGUMENT;
+  espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
+  if (st != ESPO_OK || n_rows == 0) return st;
+  const bool sharded = c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab;
+  if (sharded && !c->tp_comm) return ESPO_ERR_BAD_STATE;  // use partial + combine
+  if (c->single_pass) return ESPO_ERR_BAD_STATE;           // use espo_loss_fwd_bwd
+  if ((st = check_coverage(c, row_begin, row_begin + n_rows)) != ESPO_OK) return st;
+  DevGuard g(c->device);
+  return fwd_chunk(c, logits, ld, tokens, old_logp, mask, row_begin, n_rows, S(stream));
 }
 
 espo_status espo_loss_fwd_partial(espo_ctx_t c, const void* logits, int64_t ld,
@@ -861,23 +896,10 @@ espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_
   cudaStream_t s = S(stream);
   const espo_config& cf = c->cfg;
   if (c->R > 0) {
-    SeqParams sp;
-    sp.R = c->R;
-    sp.V = cf.vocab;
-    sp.alpha = cf.alpha;
-    sp.eps_min = cf.eps_min;
-    sp.K = cf.n_buckets;
-    sp.split_num = cf.split_num;
-    sp.split_den = cf.split_den;
-    sp.partition = cf.partition;
-    sp.ratio_mode = cf.ratio_mode;
-    sp.norm = cf.norm;
-    sp.log_ratio_clamp = cf.log_ratio_clamp;
-    sp.inv_logV = 1.0 / std::log(static_cast<double>(cf.vocab));
-    sp.zvp_beta = cf.zvp_beta;
-    sp.ws = c->ws;
-    k_seq_reduce<<<c->R, kSeqThreads, 0, s>>>(sp);
-    ESPO_LAUNCHED(c);
+    if (!c->single_pass || c->T == 0) {   // single-pass chunks ran K3 already
+      k_seq_reduce<<<c->R, kSeqThreads, 0, s>>>(seq_params(c, 0, c->T));
+      ESPO_LAUNCHED(c);
+    }
     k_reduce_rollouts<<<kRedLen, 256, 0, s>>>(c->ws, c->R);
     ESPO_LAUNCHED(c);
   } else {
@@ -893,24 +915,27 @@ espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_
   return ESPO_OK;
 }
 
-espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogits, int64_t ldg,
-                          const float* grad_loss_dev, int64_t row_begin, int64_t n_rows,
-                          espo_stream_t stream) {
-  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
-  if (c->state != State::Finalized) return ESPO_ERR_BAD_STATE;
-  if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T)
-    return ESPO_ERR_INVALID_ARGUMENT;
-  if (n_rows == 0) return ESPO_OK;
+}  // extern "C"
+
+namespace {
+espo_status check_bwd_args(espo_ctx_t c, const void* logits, int64_t ld, const void* dlogits,
+                           int64_t ldg) {
   if (!logits || !dlogits) return ESPO_ERR_INVALID_ARGUMENT;
   const espo_config& cf = c->cfg;
   const size_t ei = dsize(cf.logits_dtype), eo = dsize(cf.grad_dtype);
   if (ld < shard_width(c) || ldg < shard_width(c)) return ESPO_ERR_INVALID_ARGUMENT;
   if (!aligned16(logits) || !aligned16(dlogits) || (size_t(ld) * ei) % 16 || (size_t(ldg) * eo) % 16)
     return ESPO_ERR_ALIGNMENT;
+  if (logits == dlogits && (ld != ldg || ei != eo)) return ESPO_ERR_INVALID_ARGUMENT;
+  return ESPO_OK;
+}
+
+// K5 over one chunk (arguments checked).
+espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogits, int64_t ldg,
+                       const float* grad_loss_dev, int64_t row_begin, int64_t n_rows,
+                       cudaStream_t s) {
+  const espo_config& cf = c->cfg;
   const bool aliased = logits == dlogits;
-  if (aliased && (ld != ldg || ei != eo)) return ESPO_ERR_INVALID_ARGUMENT;
-  DevGuard g(c->device);
-  cudaStream_t s = S(stream);
   BwdParams p;
   p.logits = logits;
   p.ld = ld;
@@ -977,6 +1002,71 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
   }
   ESPO_LAUNCHED(c);
   return ESPO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogits, int64_t ldg,
+                          const float* grad_loss_dev, int64_t row_begin, int64_t n_rows,
+                          espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Finalized || c->single_pass) return ESPO_ERR_BAD_STATE;
+  if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rows == 0) return ESPO_OK;
+  espo_status st = check_bwd_args(c, logits, ld, dlogits, ldg);
+  if (st != ESPO_OK) return st;
+  DevGuard g(c->device);
+  return launch_bwd(c, logits, ld, dlogits, ldg, grad_loss_dev, row_begin, n_rows, S(stream));
+}
+
+espo_status espo_set_mask(espo_ctx_t c, const uint8_t* mask, espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Prepared || c->n_covered != 0) return ESPO_ERR_BAD_STATE;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  if (c->R > 0) {
+    k_mask_counts<<<c->R, 256, 0, s>>>(mask, c->ws, c->R);
+    ESPO_LAUNCHED(c);
+    k_mask_reduce<<<1, 256, 0, s>>>(c->ws, c->R);
+    ESPO_LAUNCHED(c);
+  } else {
+    ESPO_CUDA(cudaMemsetAsync(c->ws.dpre, 0, 2 * sizeof(double), s));
+  }
+  if (c->world > 1) {
+    if (g_nccl.allreduce(c->ws.dpre, c->ws.dpre, 2, kNcclFloat64, kNcclSum, c->comm, s) != 0)
+      return ESPO_ERR_NCCL;
+  }
+  k_mask_scale<<<1, 1, 0, s>>>(c->ws, c->cfg.norm, c->cfg.logit_scale);
+  ESPO_LAUNCHED(c);
+  c->single_pass = true;
+  return ESPO_OK;
+}
+
+espo_status espo_loss_fwd_bwd(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
+                              const float* old_logp, void* dlogits, int64_t ldg,
+                              const float* grad_loss_dev, int64_t row_begin, int64_t n_rows,
+                              espo_stream_t stream) {
+  espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
+  if (st != ESPO_OK) return st;
+  if (!c->single_pass) return ESPO_ERR_BAD_STATE;
+  if (n_rows == 0) return ESPO_OK;
+  const bool sharded = c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab;
+  if (sharded && !c->tp_comm) return ESPO_ERR_BAD_STATE;
+  if ((st = check_bwd_args(c, logits, ld, dlogits, ldg)) != ESPO_OK) return st;
+  if ((st = check_coverage(c, row_begin, row_begin + n_rows)) != ESPO_OK) return st;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  const int64_t row_end = row_begin + n_rows;
+  k_check_chunk<<<1, 1, 0, s>>>(c->ws, row_begin, row_end, c->T);
+  ESPO_LAUNCHED(c);
+  if ((st = fwd_chunk(c, logits, ld, tokens, old_logp, c->ws.pmask + row_begin, row_begin, n_rows, s)) != ESPO_OK)
+    return st;
+  k_seq_reduce<<<c->R, kSeqThreads, 0, s>>>(seq_params(c, row_begin, row_end));
+  ESPO_LAUNCHED(c);
+  return launch_bwd(c, logits, ld, dlogits, ldg, grad_loss_dev, row_begin, n_rows, s);
 }
 
 espo_status espo_get_error(espo_ctx_t c, espo_stream_t stream) {

@@ -85,6 +85,7 @@ __global__ void k_row_seq(const Workspace ws, int R) {
 // ------------------------------------------------------------------------------ K3
 struct SeqParams {
   int R;
+  int64_t row_lo, row_hi;  // rollouts inside [row_lo, row_hi] only (single-pass chunk)
   int V;
   float alpha, eps_min;
   int K;
@@ -179,6 +180,7 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_reduce(const SeqParams p) {
   const int i = blockIdx.x;
   const Workspace& ws = p.ws;
   const int64_t b = ws.seq_off[i], e = ws.seq_off[i + 1];
+  if (b < p.row_lo || e > p.row_hi) return;   // another chunk's rollout (single-pass)
   double* red = ws.red_r;  // SoA [kRedLen][R]
   auto put = [&](int k, double v) { if (threadIdx.x == 0) red[int64_t(k) * p.R + i] = v; };
 
@@ -344,6 +346,73 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_reduce(const SeqParams p) {
   put(5, ncl);
   put(6, al);
   put(7, hs);
+}
+
+// ------------------------------------------------------------------ K0 (single-pass mode)
+// The normaliser D of the loss (N active rollouts, or T_active tokens in TOKEN mode) depends
+// only on the zero-variance filter and the mask (Q10, Q11), never on logits, so
+// it can be fixed before the forward: then every chunk of complete rollouts can run
+// forward → K3 → backward at once (espo_loss_fwd_bwd).
+// K0a — one block per rollout: copies its mask rows, counts them, marks it active (writes
+// the same red_r[1], red_r[2] terms K3 will write).
+__global__ void __launch_bounds__(256) k_mask_counts(const uint8_t* mask, const Workspace ws, int R) {
+  __shared__ long long sh[33];
+  const int i = blockIdx.x;
+  const int64_t b = ws.seq_off[i], e = ws.seq_off[i + 1];
+  long long cnt = 0;
+  for (int64_t t = b + threadIdx.x; t < e; t += blockDim.x) {
+    const uint8_t m = mask ? (mask[t] != 0) : 1;
+    ws.pmask[t] = m;
+    cnt += m;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) sh[w] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long n = 0;
+    for (int k = 0; k < int(blockDim.x >> 5); ++k) n += sh[k];
+    const bool act = ws.cand[i] && n > 0;
+    ws.red_r[1ll * R + i] = act ? 1.0 : 0.0;
+    ws.red_r[2ll * R + i] = act ? static_cast<double>(n) : 0.0;
+  }
+}
+
+// K0b — {N, T_active} in rollout order (deterministic).
+__global__ void __launch_bounds__(256) k_mask_reduce(const Workspace ws, int R) {
+  __shared__ double sh[2][256];
+  double a = 0.0, n = 0.0;
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    a += ws.red_r[1ll * R + i];
+    n += ws.red_r[2ll * R + i];
+  }
+  sh[0][threadIdx.x] = a;
+  sh[1][threadIdx.x] = n;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sh[0][threadIdx.x] += sh[0][threadIdx.x + s];
+      sh[1][threadIdx.x] += sh[1][threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ws.dpre[0] = sh[0][0];
+    ws.dpre[1] = sh[1][0];
+  }
+}
+
+// K0c — backward scale λ/D from the (all-reduced) counts; same expression as K4b.
+__global__ void k_mask_scale(const Workspace ws, int norm, float logit_scale) {
+  const double D = (norm == ESPO_NORM_SEQ) ? ws.dpre[0] : ws.dpre[1];
+  *ws.bwd_scale = D > 0 ? static_cast<float>(static_cast<double>(logit_scale) / D) : 0.f;
+}
+
+// Single-pass chunk check: both ends of [lo, hi) must be rollout boundaries.
+__global__ void k_check_chunk(const Workspace ws, int64_t lo, int64_t hi, int64_t T) {
+  auto boundary = [&](int64_t r) { return r == T || ws.seq_off[ws.row_seq[r]] == r; };
+  if (!boundary(lo) || !boundary(hi)) set_error(ws.err, ESPO_ERR_INVALID_ARGUMENT);
 }
 
 // K4 — rank-local deterministic reduction of the per-rollout terms (fixed order).

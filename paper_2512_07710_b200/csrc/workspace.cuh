@@ -17,6 +17,7 @@ struct Workspace {
   uint8_t* flag = nullptr;   // 1 = row read (active cand ∧ mask) (K2)
   uint8_t* bucket = nullptr; // stats bucket                      (K3)
   uint8_t* clip = nullptr;   // 1 = gradient clipped              (K3)
+  uint8_t* pmask = nullptr;  // single-pass mode: copy of the batch mask (espo_set_mask)
   void* list = nullptr;      // per-chunk row records (FwdRec / BwdRec), 32 B × T
   int32_t* zlist = nullptr;  // per-chunk zero-fill rows (bwd), 4 B × T
   float* partial = nullptr;  // vocabulary shard: per-row {R, S, W, u_y}, 16 B × T
@@ -34,7 +35,8 @@ struct Workspace {
   double* red_r = nullptr;     // [kRedLen·R] per-rollout reduction terms (K3), SoA
   // ---- scalars ----
   double* red = nullptr;       // [kRedLen] rank-local → all-reduced sums (K4)
-  float* bwd_scale = nullptr;  // [1] λ/D (0 if D == 0)            (K4b)
+  float* bwd_scale = nullptr;  // [1] λ/D (0 if D == 0)            (K4b; K0 in single-pass)
+  double* dpre = nullptr;      // [2] single-pass: {N, T_active} counted from the mask (K0)
   int* err = nullptr;          // sticky device error word
   int* count = nullptr;        // [2] row-list lengths of the current sweep
 };

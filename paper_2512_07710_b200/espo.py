@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = [
     "espo_loss_fwd", "espo_loss_finalize", "espo_loss_bwd", "espo_get_error",
     "espo_status_string", "espo_export_token_stats", "espo_export_rollout_stats",
     "espo_launch_count", "espo_set_option", "espo_loss_fwd_partial", "espo_loss_fwd_combine",
-    "espo_attach_tp", "espo_lmhead_fwd", "espo_lmhead_bwd", "espo_reward_shaping_default",
+    "espo_attach_tp", "espo_lmhead_fwd", "espo_lmhead_bwd", "espo_set_mask", "espo_loss_fwd_bwd", "espo_reward_shaping_default",
     "espo_reshape_rewards",
 ]
 
@@ -121,6 +121,8 @@ def load_library():
         "espo_loss_fwd_combine": (I32, [P, P, I32, I64, I64, P]),
         "espo_attach_tp": (I32, [P, P, I32, I32]),
         "espo_lmhead_fwd": (I32, [P, P, I64, P, I64, I32, P, P, P, I64, I64, P]),
+        "espo_set_mask": (I32, [P, P, P]),
+        "espo_loss_fwd_bwd": (I32, [P, P, I64, P, P, P, I64, P, I64, I64, P]),
         "espo_lmhead_bwd": (I32, [P, P, I64, P, I64, I32, P, I64, I32, P, I64, P, I64, I64, P]),
         "espo_reward_shaping_default": (None, [ctypes.POINTER(RewardShaping), I32]),
         "espo_reshape_rewards": (I32, [P, ctypes.POINTER(RewardShaping), P, P, P, I32, I64, P,
@@ -250,6 +252,23 @@ class Espo:
         _check(self._lib.espo_loss_fwd(self._h, _ptr(logits), int(logits.stride(0)),
                                        _ptr(tokens), _ptr(old_logp), _ptr(mask), int(row_begin),
                                        n, 0, self._stream()), "espo_loss_fwd")
+
+    def set_mask(self, mask=None):
+        """espo_set_mask: single-pass mode; D counted from the batch mask u8[T] (None = ones)."""
+        _check(self._lib.espo_set_mask(self._h, _ptr(mask), self._stream()), "espo_set_mask")
+
+    def loss_fwd_bwd(self, logits, tokens, old_logp, dlogits=None, row_begin=0, grad_loss=None):
+        """espo_loss_fwd_bwd: forward + backward of a chunk of complete rollouts."""
+        if logits.dtype != self.logits_dtype:
+            raise TypeError(f"logits dtype {logits.dtype} != context {self.logits_dtype}")
+        if dlogits is None:
+            dlogits = torch.empty(logits.shape, dtype=self.grad_dtype, device=logits.device)
+        _check(self._lib.espo_loss_fwd_bwd(self._h, _ptr(logits), int(logits.stride(0)),
+                                           _ptr(tokens), _ptr(old_logp), _ptr(dlogits),
+                                           int(dlogits.stride(0)), _ptr(grad_loss),
+                                           int(row_begin), int(logits.shape[0]), self._stream()),
+               "espo_loss_fwd_bwd")
+        return dlogits
 
     def loss_fwd_partial(self, logits, tokens, old_logp, mask=None, row_begin=0, partial=None):
         """espo_loss_fwd_partial: this vocabulary shard's per-row {R, S, W, u_y} (f32[n, 4])."""
