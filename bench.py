@@ -47,10 +47,15 @@ def parse():
     p.add_argument("--bwd-impl", type=int, default=0, help="0/7 = tiled grid, 1 = LDG, 2-6 = TMA rings")
     p.add_argument("--blocks-per-sm", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=1)
-    p.add_argument("--e2e-host-rows", type=int, default=2048)
+    p.add_argument("--e2e-host-rows", type=int, default=8192,
+                   help="host ring rows (≥ the longest rollout; chunks pack whole rollouts)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-tokens", type=int, default=128, help="tokens per rollout")
+    p.add_argument("--single-pass", action="store_true",
+                   help="device leg through espo_set_mask + espo_loss_fwd_bwd (chunks of whole rollouts)")
+    p.add_argument("--e2e-mode", default="single-pass", choices=["single-pass", "two-sweep"],
+                   help="e2e leg: logits chunks cross PCIe once (single-pass) or twice")
     p.add_argument("--zv-mode", default="mask", choices=["mask", "rlzvp"],
                    help="zero-variance groups: eliminated (default) or RL-ZVP advantages")
     p.add_argument("--vocab-shards", type=int, default=1,
@@ -118,7 +123,23 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ workload
-def make_batch(w, seed, dev, buffer_rows, log):
+def rollout_chunks(seq_offsets, max_rows):
+    """Greedy chunks of whole rollouts with ≤ max_rows rows each (single-pass mode needs
+    rollout-aligned chunks); a rollout longer than max_rows is an error."""
+    so = [int(x) for x in seq_offsets]
+    chunks, b = [], 0
+    for i in range(1, len(so)):
+        if so[i] - so[i - 1] > max_rows:
+            raise SystemExit(f"rollout {i - 1} has {so[i] - so[i - 1]} rows > chunk {max_rows}")
+        if so[i] - b > max_rows:
+            chunks.append((b, so[i - 1]))
+            b = so[i - 1]
+    if so[-1] > b:
+        chunks.append((b, so[-1]))
+    return chunks
+
+
+def make_batch(w, seed, dev, buffer_rows, log, single_pass=False):
     """Device-resident synthetic C1 batch: chunk buffer + per-token arrays."""
     import torch
     V = w.V
@@ -136,7 +157,14 @@ def make_batch(w, seed, dev, buffer_rows, log):
         ls = torch.log_softmax(buf[r0:r1].float(), dim=1)
         buf_lp[r0:r1] = ls.gather(1, buf_tok[r0:r1].long().unsqueeze(1)).squeeze(1)
         del ls
-    idx = torch.arange(T, device=dev) % Rc
+    # chunks: fixed R_c tiles (two sweeps) or whole-rollout packs (single pass); batch row t
+    # reads buffer row t − (its chunk's first row)
+    chunks = rollout_chunks(seq_offsets, Rc) if single_pass else \
+        [(b, min(T, b + Rc)) for b in range(0, T, Rc)]
+    idx_np = np.empty(T, dtype=np.int64)
+    for b, e in chunks:
+        idx_np[b:e] = np.arange(e - b)
+    idx = torch.from_numpy(idx_np).to(dev)
     tokens = buf_tok[idx].contiguous()
     lp = buf_lp[idx]
     g = torch.Generator(device=dev)
@@ -148,7 +176,7 @@ def make_batch(w, seed, dev, buffer_rows, log):
     torch.cuda.synchronize(dev)
     log(f"generated batch T={T} buffer={Rc} rows in {time.time() - t0:.1f}s")
     return dict(buf=buf, tokens=tokens, old=old, T=T, Rc=Rc, buf_tok=buf_tok, buf_lp=buf_lp,
-                drift=drift,
+                drift=drift, chunks=chunks,
                 rewards=torch.from_numpy(rewards).to(dev),
                 group_ids=torch.from_numpy(group_ids).to(dev),
                 seq_offsets=torch.from_numpy(seq_offsets).to(dev),
@@ -160,8 +188,7 @@ def run_step(ctx, d, dlog, ev=None):
     import torch
     T, Rc, buf = d["T"], d["Rc"], d["buf"]
     ctx.prepare(d["rewards"], d["group_ids"], d["seq_offsets"], n_tokens=T)
-    for b in range(0, T, Rc):
-        e = min(T, b + Rc)
+    for b, e in d["chunks"]:
         if ev is not None:
             s0 = torch.cuda.Event(enable_timing=True)
             s0.record()
@@ -171,8 +198,7 @@ def run_step(ctx, d, dlog, ev=None):
             s1.record()
             ev["fwd"].append((s0, s1))
     loss, stats = ctx.loss_finalize()
-    for b in range(0, T, Rc):
-        e = min(T, b + Rc)
+    for b, e in d["chunks"]:
         if ev is not None:
             s0 = torch.cuda.Event(enable_timing=True)
             s0.record()
@@ -242,19 +268,44 @@ def run_step_sharded(sh, d, dlog, ev=None):
     return outs[0]
 
 
+def run_step_single(ctx, d, dlog, ev=None):
+    """Single-pass step: prepare → set_mask → fwd_bwd per chunk of whole rollouts → finalize.
+    ev["fwdbwd"] gets one event pair per chunk."""
+    import torch
+    buf = d["buf"]
+    ctx.prepare(d["rewards"], d["group_ids"], d["seq_offsets"], n_tokens=d["T"])
+    ctx.set_mask(None)
+    for b, e in d["chunks"]:
+        if ev is not None:
+            s0 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+        ctx.loss_fwd_bwd(buf[:e - b], d["tokens"][b:e], d["old"][b:e], dlog[:e - b], row_begin=b)
+        if ev is not None:
+            s1 = torch.cuda.Event(enable_timing=True)
+            s1.record()
+            ev["fwdbwd"].append((s0, s1))
+    return ctx.loss_finalize()
+
+
 def run_e2e(ctx, d, dlog, args, dev):
     """End-to-end through the public API with HOST inputs: every step copies its inputs
-    (rewards, group ids, offsets, tokens, old log-probs and every logits chunk, for the fwd
-    and again for the bwd sweep) from pinned host memory and reads the loss back. Logits
-    stream through a pinned host ring of --e2e-host-rows rows; copies run on a side stream
-    double-buffered against the kernels."""
+    (rewards, group ids, offsets, tokens, old log-probs and every logits chunk) from pinned
+    host memory and reads the loss back. Logits stream through a pinned host ring of
+    --e2e-host-rows rows in chunks of whole rollouts; copies run on a side stream,
+    double-buffered against the kernels. single-pass (default): each chunk crosses PCIe once
+    (espo_set_mask + espo_loss_fwd_bwd); two-sweep: once for the forward and again for the
+    backward sweep."""
     import torch
     T, V = d["T"], d["buf"].shape[1]
     Hr = min(args.e2e_host_rows, d["Rc"])
+    chunks = rollout_chunks(d["np"]["seq_offsets"], Hr)
     host = torch.empty((Hr, V), dtype=torch.bfloat16, pin_memory=True)
     host.copy_(d["buf"][:Hr].cpu())
-    # batch row t reads host ring row t mod Hr: tokens / old log-probs follow that row
-    idx = torch.arange(T, device=dev) % Hr
+    # batch row t reads host ring row t − (its chunk's first row): tokens / old follow it
+    idx_np = np.empty(T, dtype=np.int64)
+    for b, e in chunks:
+        idx_np[b:e] = np.arange(e - b)
+    idx = torch.from_numpy(idx_np).to(dev)
     h_tok = d["buf_tok"][idx].cpu().pin_memory()
     h_old = (d["buf_lp"][idx] + d["drift"]).cpu().pin_memory()
     h_rw = d["rewards"].cpu().pin_memory()
@@ -267,6 +318,7 @@ def run_e2e(ctx, d, dlog, args, dev):
     h_loss = torch.empty(1, dtype=torch.float32, pin_memory=True)
     copy_s = torch.cuda.Stream(dev)
     comp = torch.cuda.current_stream(dev)
+    single = args.e2e_mode == "single-pass"
 
     def one_step():
         h2d = 0
@@ -274,13 +326,14 @@ def run_e2e(ctx, d, dlog, args, dev):
             dst.copy_(src, non_blocking=True)
             h2d += src.numel() * src.element_size()
         ctx.prepare(d_rw, d_gid, d_so, n_tokens=T)
+        if single:
+            ctx.set_mask(None)
         done = [torch.cuda.Event() for _ in range(2)]
-        for sweep in ("fwd", "bwd"):
+        for sweep in (("fwdbwd",) if single else ("fwd", "bwd")):
             if sweep == "bwd":
                 loss, _ = ctx.loss_finalize()
             used = [None, None]
-            for k, b in enumerate(range(0, T, Hr)):
-                e = min(T, b + Hr)
+            for k, (b, e) in enumerate(chunks):
                 sb = stage[k % 2]
                 with torch.cuda.stream(copy_s):
                     if used[k % 2] is not None:
@@ -291,11 +344,15 @@ def run_e2e(ctx, d, dlog, args, dev):
                 comp.wait_event(done[k % 2])
                 if sweep == "fwd":
                     ctx.loss_fwd(sb[:e - b], d_tok[b:e], d_old[b:e], None, row_begin=b)
-                else:
+                elif sweep == "bwd":
                     ctx.loss_bwd(sb[:e - b], dlog[:e - b], row_begin=b)
+                else:
+                    ctx.loss_fwd_bwd(sb[:e - b], d_tok[b:e], d_old[b:e], dlog[:e - b], row_begin=b)
                 ev = torch.cuda.Event()
                 ev.record(comp)
                 used[k % 2] = ev
+        if single:
+            loss, _ = ctx.loss_finalize()
         h_loss.copy_(loss, non_blocking=True)
         return h2d, 4
 
@@ -360,7 +417,7 @@ def main_ours(args):
     log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
     w = S.WORKLOADS[args.config]
     seed = S.config_seed(w.index) ^ (rank * 0x9E3779B9)
-    d = make_batch(w, seed, dev, args.buffer_rows, log)
+    d = make_batch(w, seed, dev, args.buffer_rows, log, single_pass=args.single_pass)
     kw = dict(zero_fill_inactive_rows=not args.compact,
               zv_mode=1 if args.zv_mode == "rlzvp" else 0)
     S_ = args.vocab_shards
@@ -382,7 +439,7 @@ def main_ours(args):
         ctx.set_option(OPT_FWD_IMPL, args.fwd_impl)
         ctx.set_option(OPT_BWD_IMPL, args.bwd_impl)
         ctx.set_option(OPT_BLOCKS_PER_SM, args.blocks_per_sm)
-        step_fn = run_step
+        step_fn = run_step_single if args.single_pass else run_step
     dlog = torch.empty((d["Rc"], w.V), dtype=torch.bfloat16, device=dev)
 
     for _ in range(args.warmup):
@@ -393,7 +450,7 @@ def main_ours(args):
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
-    ev = {"fwd": [], "bwd": []}
+    ev = {"fwd": [], "bwd": [], "fwdbwd": []}
     launches0 = ctx.launch_count
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
@@ -423,26 +480,35 @@ def main_ours(args):
     if args.compact:
         bwd_bytes += (n_act - n_clip) * 2 * V      # swept rows are still written
     step_bytes = fwd_bytes + bwd_bytes
-    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["fwd"])
-    bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["bwd"])
-    n_chunks = len(ev["bwd"]) // args.steps
     peak, peak_src = measured_peaks()
-    bwd_gbs = bwd_bytes / n_chunks / (bwd_ms * 1e-3) / 1e9
-    fwd_gbs = fwd_bytes / n_chunks / (fwd_ms * 1e-3) / 1e9
+    if args.single_pass:       # one event pair per fused chunk: report the fused chunk
+        fb_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["fwdbwd"])
+        n_chunks = len(ev["fwdbwd"]) // args.steps
+        fwd_ms = bwd_ms = fb_ms
+        fwd_gbs = bwd_gbs = step_bytes / n_chunks / (fb_ms * 1e-3) / 1e9
+    else:
+        fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["fwd"])
+        bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["bwd"])
+        n_chunks = len(ev["bwd"]) // args.steps
+        bwd_gbs = bwd_bytes / n_chunks / (bwd_ms * 1e-3) / 1e9
+        fwd_gbs = fwd_bytes / n_chunks / (fwd_ms * 1e-3) / 1e9
     step_gbs = step_bytes / (ms_step * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         tr = json.load(open(tpath))
-        traffic = tr.get("bwd_bytes_per_launch")
+        traffic = None if args.single_pass else tr.get("bwd_bytes_per_launch")
 
     e2e = None
     if not args.no_e2e and S_ == 1:
         tps, h2d, d2h, dt = run_e2e(ctx, d, dlog, args, dev)
         e2e = {"value": tps * world, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-               "note": "host-resident inputs incl. every logits chunk (fwd and bwd sweep) over "
-                       "PCIe from a pinned host ring; wall clock"}
+               "mode": args.e2e_mode,
+               "note": "host-resident inputs incl. every logits chunk over PCIe from a pinned "
+                       "host ring (" + ("once per step: espo_set_mask + espo_loss_fwd_bwd on "
+                       "chunks of whole rollouts" if args.e2e_mode == "single-pass" else
+                       "twice per step: fwd and bwd sweeps") + "); wall clock"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(d, w, args.cpu_sample_tokens, log)
@@ -465,7 +531,8 @@ def main_ours(args):
                         f"vocab {V}, bf16 logits/grads" + (", compact dlogits" if args.compact else "")
                         + (", RL-ZVP advantages for zero-variance groups" if args.zv_mode == "rlzvp" else "")
                         + (f", {S_} vocabulary shards back to back on one GPU (TP emulation, "
-                           "partials gathered by device copy)" if S_ > 1 else ""),
+                           "partials gathered by device copy)" if S_ > 1 else "")
+                        + (", single-pass (espo_loss_fwd_bwd per chunk of whole rollouts)" if args.single_pass else ""),
             "global_batch_tokens": T * world, "seq_len": w.L, "parallelism": f"dp{world} (prompt-group sharded)",
             "chunk_rows": d["Rc"], "l2": "inputs larger than L2 (chunk buffer "
                                          f"{d['Rc'] * V * 2 / 1e9:.2f} GB > 126 MB)",
@@ -478,7 +545,8 @@ def main_ours(args):
             "active_tokens": n_act, "clipped_tokens": n_clip,
             "zv_groups": st["n_zv_groups"], "groups": st["n_groups"],
         },
-        "roofline": {"bound": "hbm", "kernel": "espo_loss_bwd sweep (k_bwd_recs + k_dlogits_tile)",
+        "roofline": {"bound": "hbm", "kernel": ("espo_loss_fwd_bwd chunk (K2 + K3 + K5)" if args.single_pass
+                                                else "espo_loss_bwd sweep (k_bwd_recs + k_dlogits_tile)"),
                      "achieved": bwd_gbs, "peak": peak, "unit": "GB/s",
                      "frac": bwd_gbs / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": bwd_bytes / n_chunks},
