@@ -53,7 +53,9 @@ def build(name, dev, seed=None):
     b.old = S.drift_old_logp(lp_u[idx], b.seq_offsets, seed)
     b.logits = Cycled(rows)
     buf = torch.from_numpy(rows).to(dev).to(torch.bfloat16)
-    b.buf = buf.repeat(CHUNK // U_ROWS, 1)            # [CHUNK, V]: buffer row r = distinct r % 1024
+    # [CHUNK + 1024, V]: buffer row r = distinct r % 1024 (the extra 1024 rows let a chunk
+    # starting at any batch row t0 use the view buf[t0 % 1024:])
+    b.buf = buf.repeat(CHUNK // U_ROWS + 1, 1)
     return b
 
 
@@ -71,7 +73,7 @@ def run(b, dev, bwd_rows=None):
         ctx.loss_fwd(b.buf[:c1 - c0], tok[c0:c1], old[c0:c1], None, row_begin=c0)
     loss, stats = ctx.loss_finalize()
     grads = {}
-    dl = torch.empty_like(b.buf)
+    dl = torch.empty((CHUNK, b.V), dtype=torch.bfloat16, device=dev)
     for c0 in range(0, b.T, CHUNK):
         c1 = min(b.T, c0 + CHUNK)
         ctx.loss_bwd(b.buf[:c1 - c0], dl[:c1 - c0], row_begin=c0)
@@ -201,3 +203,74 @@ def test_full_size_sampled_groups(name):
             np.testing.assert_allclose(rol["J"][r0:r1], sub2.J_i, rtol=1e-5,
                                        atol=1e-5 * np.abs(sub2.J_i).max())
     ctx.close()
+
+
+def _rollout_chunks(so, max_rows):
+    chunks, s = [], 0
+    for i in range(1, len(so)):
+        if so[i] - s > max_rows:
+            chunks.append((s, int(so[i - 1])))
+            s = int(so[i - 1])
+    if so[-1] > s:
+        chunks.append((s, int(so[-1])))
+    return chunks
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_full_size_single_pass_is_bitwise_two_sweep(name):
+    """At full size in the bench launch configuration, the single-pass mode (espo_set_mask +
+    espo_loss_fwd_bwd on chunks of whole rollouts) reproduces the two-sweep pass bit for bit:
+    loss, statistics and sampled gradient rows from every chunk."""
+    from paper_2512_07710_b200.espo import Espo, stats_to_dict
+    dev = require_cuda()
+    b = build(name, dev)
+    rng = np.random.default_rng(1)
+    tok = to_dev(b.tokens, torch.int32, dev)
+    old = to_dev(b.old, torch.float32, dev)
+    args = (to_dev(b.rewards, torch.float32, dev), to_dev(b.group_ids, torch.int32, dev),
+            to_dev(b.seq_offsets, torch.int64, dev))
+    dl = torch.empty((CHUNK, b.V), dtype=torch.bfloat16, device=dev)
+
+    def view(c0, c1):
+        o = c0 % U_ROWS
+        return b.buf[o:o + (c1 - c0)]
+
+    def pick(c0, c1):
+        return np.sort(rng.choice(c1 - c0, min(16, c1 - c0), replace=False))
+
+    # two sweeps, chunks of CHUNK rows
+    ctx = Espo(b.V, logits_dtype=torch.bfloat16, device=dev.index)
+    ctx.prepare(*args, n_tokens=b.T)
+    tiles = [(c0, min(b.T, c0 + CHUNK)) for c0 in range(0, b.T, CHUNK)]
+    for c0, c1 in tiles:
+        ctx.loss_fwd(view(c0, c1), tok[c0:c1], old[c0:c1], None, row_begin=c0)
+    loss2, st2 = ctx.loss_finalize()
+    ref_rows = {}
+    single_chunks = _rollout_chunks(b.seq_offsets, CHUNK)
+    want_rows = {c0: c0 + pick(c0, c1) for c0, c1 in single_chunks}
+    flat = np.concatenate(list(want_rows.values()))
+    for c0, c1 in tiles:
+        ctx.loss_bwd(view(c0, c1), dl[:c1 - c0], row_begin=c0)
+        sel = flat[(flat >= c0) & (flat < c1)]
+        if len(sel):
+            got = dl[torch.as_tensor(sel - c0, device=dev)].cpu()
+            for k, t in enumerate(sel):
+                ref_rows[int(t)] = got[k]
+    ctx.get_error()
+    loss2, st2 = float(loss2.item()), stats_to_dict(st2)
+    ctx.close()
+    # single pass, chunks of whole rollouts
+    ctx = Espo(b.V, logits_dtype=torch.bfloat16, device=dev.index)
+    ctx.prepare(*args, n_tokens=b.T)
+    ctx.set_mask(None)
+    for c0, c1 in single_chunks:
+        ctx.loss_fwd_bwd(view(c0, c1), tok[c0:c1], old[c0:c1], dl[:c1 - c0], row_begin=c0)
+        sel = want_rows[c0]
+        got = dl[torch.as_tensor(sel - c0, device=dev)].cpu()
+        for k, t in enumerate(sel):
+            assert torch.equal(got[k], ref_rows[int(t)]), (c0, int(t))
+    loss1, st1 = ctx.loss_finalize()
+    ctx.get_error()
+    ctx.close()
+    assert float(loss1.item()) == loss2
+    assert stats_to_dict(st1) == st2
