@@ -387,7 +387,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   switch (option) {
     case ESPO_OPT_FWD_IMPL:
-      if (value < 0 || value > 7) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 8) return ESPO_ERR_INVALID_ARGUMENT;
       c->fwd_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_BWD_IMPL:

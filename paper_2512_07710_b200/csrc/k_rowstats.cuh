@@ -222,6 +222,42 @@ template <typename Tin, int U, int NPOLY = 0>
 __device__ __forceinline__ void acc_batch(const uint4* v, float lamL, float nref, float& bS,
                                           float& bW) {
   constexpr int EPV = Vec<Tin>::EPV;
+  if constexpr (NPOLY < 0) {
+    // packed variant: the same two (s, w) chains as below, issued as sm_100 f32x2 FFMA2 /
+    // FADD2 pairs (bitwise the same per-lane arithmetic, half the FP32 instructions)
+    const float2 L2 = make_float2(lamL, lamL), N2 = make_float2(nref, nref);
+    float2 s, w;
+    {
+      float x[EPV];
+      Vec<Tin>::unpack(v[0], x);
+      const float2 t = __ffma2_rn(make_float2(x[0], x[1]), L2, N2);
+      const float2 e = make_float2(ex2(t.x), ex2(t.y));
+      s = e;
+      w = __fmul2_rn(e, t);
+#pragma unroll
+      for (int k = 2; k < EPV; k += 2) {
+        const float2 tk = __ffma2_rn(make_float2(x[k], x[k + 1]), L2, N2);
+        const float2 ek = make_float2(ex2(tk.x), ex2(tk.y));
+        s = __fadd2_rn(s, ek);
+        w = __ffma2_rn(ek, tk, w);
+      }
+    }
+#pragma unroll
+    for (int u = 1; u < U; ++u) {
+      float x[EPV];
+      Vec<Tin>::unpack(v[u], x);
+#pragma unroll
+      for (int k = 0; k < EPV; k += 2) {
+        const float2 tk = __ffma2_rn(make_float2(x[k], x[k + 1]), L2, N2);
+        const float2 ek = make_float2(ex2(tk.x), ex2(tk.y));
+        s = __fadd2_rn(s, ek);
+        w = __ffma2_rn(ek, tk, w);
+      }
+    }
+    bS = s.x + s.y;
+    bW = w.x + w.y;
+    return;
+  }
   // two (s, w) chains, seeded by the first vector (no 0 + x instructions)
   float s0, s1, w0, w1;
   {
@@ -463,7 +499,8 @@ inline cudaError_t launch_rowstats_tma(const FwdParams& p, const FwdRec* list, c
     case 5: return ESPO_FWD_CFG(24, 2, 4096, 4, 1);
     case 6: return ESPO_FWD_CFG(16, 3, 4096, 8, 1);
     case 7: return ESPO_FWD_CFG(8, 3, 8192, 8, 1);
-    default: return ESPO_FWD_CFG(16, 3, 4096, 4, 0);  // measured best on C1 (K2)
+    case 8: return ESPO_FWD_CFG(16, 3, 4096, 4, 0);    // the default geometry, scalar FP32
+    default: return ESPO_FWD_CFG(16, 3, 4096, 4, -1);  // measured best on C1: packed f32x2 (K2)
   }
 #undef ESPO_FWD_CFG
 }
