@@ -391,7 +391,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->fwd_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_BWD_IMPL:
-      if (value < 0 || value > 7) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 8) return ESPO_ERR_INVALID_ARGUMENT;
       c->bwd_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_BLOCKS_PER_SM:
@@ -954,7 +954,7 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
   int32_t* zl = c->ws.zlist;
   int* cnt = c->ws.count;
   const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
-  if (c->bwd_impl == 0 || c->bwd_impl == 7) {
+  if (c->bwd_impl == 0 || c->bwd_impl == 7 || c->bwd_impl == 8) {
     // tiled (default): per-row records indexed by row, non-persistent (row, tile) grid
     k_bwd_recs<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, p.zero_fill,
                                         shard_begin(c), p.V, c->ws, list);
@@ -965,7 +965,11 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
     const int ntiles = (nvec + 256 * vpt - 1) / (256 * vpt);
     const int64_t grid = n_rows * int64_t(ntiles);
     if (grid > INT32_MAX) return ESPO_ERR_INVALID_ARGUMENT;
-    if (vpt == 4) {
+    if (c->bwd_impl == 8) {   // the default tiles with scalar FP32 (A/B of the packed f32x2)
+      if (bi && bo) k_dlogits_tile<__nv_bfloat16, __nv_bfloat16, 8, false><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+      else if (bi) k_dlogits_tile<__nv_bfloat16, float, 8, false><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+      else k_dlogits_tile<float, float, 8, false><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+    } else if (vpt == 4) {
       if (bi && bo) k_dlogits_tile<__nv_bfloat16, __nv_bfloat16, 4><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
       else if (bi) k_dlogits_tile<__nv_bfloat16, float, 4><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
       else k_dlogits_tile<float, float, 4><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);

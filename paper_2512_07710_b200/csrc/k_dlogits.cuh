@@ -61,14 +61,27 @@ __device__ __forceinline__ void zero_row(char* orow, int V, int lane) {
 }
 
 // Computes the EPV outputs of one input vector j of a swept row.
-template <typename Tin>
+// P2: the FFMA and FMUL of element pairs issued as sm_100 packed f32x2 (bitwise the same).
+template <typename Tin, bool P2 = true>
 __device__ __forceinline__ void dz_vec(const uint4& v, int j, int vy, int yoff, float lamL,
                                        const BwdRec& rec, float* d) {
   constexpr int EPV = Vec<Tin>::EPV;
   float x[EPV];
   Vec<Tin>::unpack(v, x);
+  if constexpr (P2) {
+    const float2 L2 = make_float2(lamL, lamL), N2 = make_float2(rec.nlseL, rec.nlseL);
+    const float2 G2 = make_float2(rec.ng, rec.ng);
 #pragma unroll
-  for (int e = 0; e < EPV; ++e) d[e] = rec.ng * ex2(fmaf(x[e], lamL, rec.nlseL));
+    for (int e = 0; e < EPV; e += 2) {
+      const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), L2, N2);
+      const float2 o = __fmul2_rn(G2, make_float2(ex2(t.x), ex2(t.y)));
+      d[e] = o.x;
+      d[e + 1] = o.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) d[e] = rec.ng * ex2(fmaf(x[e], lamL, rec.nlseL));
+  }
   if (j == vy) {
 #pragma unroll
     for (int e = 0; e < EPV; ++e)
@@ -216,7 +229,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dlogits_tma(const BwdParams p, c
 // loads in flight, computes and writes it back — the access pattern of the fastest copy
 // measured on this part (tools/bwprobe.cu: 6.9 TB/s vs 6.3 for per-warp rings), and a
 // zero-fill tile is a pure write.
-template <typename Tin, typename Tout, int VPT>
+template <typename Tin, typename Tout, int VPT, bool P2 = true>
 __global__ void __launch_bounds__(256) k_dlogits_tile(const BwdParams p, const BwdRec* rec,
                                                       int ntiles) {
   constexpr int EPV = Vec<Tin>::EPV;
@@ -253,7 +266,7 @@ __global__ void __launch_bounds__(256) k_dlogits_tile(const BwdParams p, const B
     const int j = j0 + 256 * u;
     if (j < nvec) {
       float dd[EPV];
-      dz_vec<Tin>(v[u], j, vy, yoff, lamL, rc, dd);
+      dz_vec<Tin, P2>(v[u], j, vy, yoff, lamL, rc, dd);
       store_out<Tin, Tout>(orow, j, dd, p.V);
     }
   }

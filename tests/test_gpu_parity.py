@@ -189,12 +189,13 @@ def test_rlzvp_mode(dev):
 
 def test_packed_f32x2_variant_is_bitwise_default(dev, c0):
     """The default fwd issues the fast-path chains as sm_100 FFMA2/FADD2 pairs; variant 8 is
-    the same kernel in scalar FP32: the per-lane arithmetic is unchanged, so every statistic
-    and gradient is bitwise equal."""
+    the same kernel in scalar FP32 (likewise K5's tiles: packed default, scalar bwd variant
+    8): the per-lane arithmetic is unchanged, so every statistic and gradient is bitwise
+    equal."""
     inst = tiny_instance(33, V=4104, group_sizes=(4, 4), L=40, dtype="bf16", mask_tail=5)
     for case, kw in ((c0, {}), (inst, {"logits_dtype": torch.bfloat16})):
         a = run_gpu(case, dev, fwd_impl=0, **kw)
-        b = run_gpu(case, dev, fwd_impl=8, **kw)
+        b = run_gpu(case, dev, fwd_impl=8, bwd_impl=8, **kw)
         assert a["loss"] == b["loss"] and a["stats"] == b["stats"]
         assert np.array_equal(a["dlogits"], b["dlogits"])
         for k in ("lse", "lp", "H", "q"):
