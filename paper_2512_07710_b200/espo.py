@@ -17,7 +17,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libespo.so")
+LIB_PATH = os.environ.get("ESPO_LIB") or os.path.join(_HERE, "libespo.so")  # ESPO_LIB: A/B builds
 
 ESPO_MAX_BUCKETS = 4
 F32, BF16 = 0, 1
