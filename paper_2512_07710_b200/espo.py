@@ -157,7 +157,10 @@ def bootstrap_unique_id(rank: int, process_group=None) -> bytes:
         raw = ctypes.create_string_buffer(128)
         _check(load_library().espo_get_unique_id(raw), "espo_get_unique_id")
         buf[0] = raw.raw
-    dist.broadcast_object_list(buf, src=0, group=process_group)
+    if process_group is None:
+        dist.broadcast_object_list(buf, src=0)
+    else:   # `rank` is the rank inside `process_group`; its member 0 draws the id
+        dist.broadcast_object_list(buf, group=process_group, group_src=0)
     return buf[0]
 
 

@@ -71,3 +71,14 @@ def worker_sharded_oracle(rank, world, port, out_q):
     dist.all_gather_object(plans, plan)
     out_q.put((rank, loss, v.numpy().tolist(), toks.tolist(), g.tolist(), plans))
     dist.destroy_process_group()
+
+
+def worker_subgroup_unique_id(rank, world, port, out_q):
+    """bootstrap over a sub-group that does not contain global rank 0 (a TP group)."""
+    dist = _init(rank, world, port)
+    from paper_2512_07710_b200.espo import bootstrap_unique_id
+    sub = dist.new_group(ranks=[1])
+    uid = bootstrap_unique_id(0, sub) if rank == 1 else None
+    full = bootstrap_unique_id(rank)
+    out_q.put((rank, None if uid is None else len(uid), len(full)))
+    dist.destroy_process_group()

@@ -80,3 +80,9 @@ def test_plan_covers_groups_and_balances():
         r, toks, lg, lso = shard_batch(lpt[0], gid, so)
         assert lso[-1] == len(toks) and len(lg) == len(r)
         assert np.all(np.diff(lg) >= 0)
+
+
+def test_unique_id_bootstrap_over_subgroup():
+    out = run_world(mp_workers.worker_subgroup_unique_id)
+    assert out[1][1] == 128 and out[0][1] is None
+    assert all(o[2] == 128 for o in out)
