@@ -324,9 +324,12 @@ uint64_t espo_launch_count(espo_ctx_t ctx);
 /* Kernel-variant switches for A/B measurement. */
 typedef enum {
   ESPO_OPT_FWD_IMPL = 0,       /* 0 = TMA bulk-copy smem ring (default), 1 = LDG.128 warp per
-                                  row, 2..7 = other ring geometries (K2) */
+                                  row, 2..7 = other ring geometries, 8 = default geometry in
+                                  scalar FP32 (K2) */
   ESPO_OPT_BWD_IMPL = 1,       /* 0 = tiled (row, 32 KB tile) grid (default), 1 = LDG.128 warp
-                                  per row, 2..6 = TMA ring geometries, 7 = 16 KB tiles */
+                                  per row, 2..6 = TMA ring geometries, 7 = 16 KB tiles,
+                                  8 = tiles with scalar FP32, 9 = tiles over the compact row
+                                  lists (4 rows per block) */
   ESPO_OPT_BLOCKS_PER_SM = 2,  /* persistent grid = blocks_per_sm × SM count (0 = auto) */
   ESPO_OPT_LMHEAD_PARTS = 3,   /* espo_lmhead_fwd/bwd vocabulary parts per row block (0 = auto) */
   ESPO_OPT_LMHEAD_BWD_ROWS = 4 /* espo_lmhead_bwd rows per dz sub-chunk (multiple of 128;

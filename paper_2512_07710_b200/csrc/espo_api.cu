@@ -391,7 +391,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->fwd_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_BWD_IMPL:
-      if (value < 0 || value > 8) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 11) return ESPO_ERR_INVALID_ARGUMENT;
       c->bwd_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_BLOCKS_PER_SM:
@@ -936,6 +936,10 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
                        cudaStream_t s) {
   const espo_config& cf = c->cfg;
   const bool aliased = logits == dlogits;
+  // default: (row, tile) grid when every row is written; in compact mode (rows without
+  // gradient untouched) tiles over the compact row lists, 8 rows per block (measured on C3)
+  int impl = c->bwd_impl;
+  if (impl == 0 && !cf.zero_fill_inactive_rows) impl = 10;
   BwdParams p;
   p.logits = logits;
   p.ld = ld;
@@ -954,18 +958,18 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
   int32_t* zl = c->ws.zlist;
   int* cnt = c->ws.count;
   const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
-  if (c->bwd_impl == 0 || c->bwd_impl == 7 || c->bwd_impl == 8) {
+  if (impl == 0 || impl == 7 || impl == 8) {
     // tiled (default): per-row records indexed by row, non-persistent (row, tile) grid
     k_bwd_recs<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, p.zero_fill,
                                         shard_begin(c), p.V, c->ws, list);
     ESPO_LAUNCHED(c);
     const int epv = bi ? 8 : 4;
     const int nvec = (p.V + epv - 1) / epv;
-    const int vpt = (c->bwd_impl == 7) ? 4 : 8;  // default 0: 32 KB tiles (measured best)
+    const int vpt = (impl == 7) ? 4 : 8;  // default 0: 32 KB tiles (measured best)
     const int ntiles = (nvec + 256 * vpt - 1) / (256 * vpt);
     const int64_t grid = n_rows * int64_t(ntiles);
     if (grid > INT32_MAX) return ESPO_ERR_INVALID_ARGUMENT;
-    if (c->bwd_impl == 8) {   // the default tiles with scalar FP32 (A/B of the packed f32x2)
+    if (impl == 8) {   // the default tiles with scalar FP32 (A/B of the packed f32x2)
       if (bi && bo) k_dlogits_tile<__nv_bfloat16, __nv_bfloat16, 8, false><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
       else if (bi) k_dlogits_tile<__nv_bfloat16, float, 8, false><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
       else k_dlogits_tile<float, float, 8, false><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
@@ -985,7 +989,22 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
   k_bwd_rows<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, p.zero_fill, shard_begin(c),
                                       p.V, c->ws, list, zl, cnt);
   ESPO_LAUNCHED(c);
-  if (c->bwd_impl == 1) {
+  if (impl >= 9) {   // tiled over the compact lists, RPB rows per block
+    const int rpb = impl == 9 ? 4 : (impl == 10 ? 8 : 16);
+    const int epv = bi ? 8 : 4;
+    const int ntiles = (((p.V + epv - 1) / epv) + 256 * 8 - 1) / (256 * 8);
+    const int64_t grid = (n_rows + rpb - 1) / rpb * int64_t(ntiles);
+    if (grid > INT32_MAX) return ESPO_ERR_INVALID_ARGUMENT;
+#define ESPO_TLIST(RPB)                                                                                    \
+    if (bi && bo) k_dlogits_tlist<__nv_bfloat16, __nv_bfloat16, 8, RPB><<<unsigned(grid), 256, 0, s>>>(p, list, zl, cnt, ntiles); \
+    else if (bi) k_dlogits_tlist<__nv_bfloat16, float, 8, RPB><<<unsigned(grid), 256, 0, s>>>(p, list, zl, cnt, ntiles);         \
+    else k_dlogits_tlist<float, float, 8, RPB><<<unsigned(grid), 256, 0, s>>>(p, list, zl, cnt, ntiles);
+    if (rpb == 4) { ESPO_TLIST(4) } else if (rpb == 8) { ESPO_TLIST(8) } else { ESPO_TLIST(16) }
+#undef ESPO_TLIST
+    ESPO_LAUNCHED(c);
+    return ESPO_OK;
+  }
+  if (impl == 1) {
     if (bi && bo) {
       auto k = k_dlogits_ldg<__nv_bfloat16, __nv_bfloat16, 8>;
       k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, zl, cnt);
@@ -998,7 +1017,7 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
     }
   } else {
     cudaError_t le;
-    const int v = c->bwd_impl;  // 2..5 geometry variants, 6 = 8 warps × 4 × 4 KB
+    const int v = impl;  // 2..5 geometry variants, 6 = 8 warps × 4 × 4 KB
     if (bi && bo) le = launch_dlogits_tma<__nv_bfloat16, __nv_bfloat16>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
     else if (bi) le = launch_dlogits_tma<__nv_bfloat16, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
     else le = launch_dlogits_tma<float, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);

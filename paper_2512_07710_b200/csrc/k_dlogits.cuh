@@ -229,6 +229,59 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dlogits_tma(const BwdParams p, c
 // loads in flight, computes and writes it back — the access pattern of the fastest copy
 // measured on this part (tools/bwprobe.cu: 6.9 TB/s vs 6.3 for per-warp rings), and a
 // zero-fill tile is a pure write.
+// Tiled variant over the compact row lists of k_bwd_rows: block b handles tile b % ntiles of
+// list entries [RPB·(b / ntiles), +RPB) — sweep rows first, then zero-fill rows. Blocks past
+// the lists' end exit at once; with RPB rows per block there are RPB× fewer of them than in
+// the per-row grid (compact mode, where most rows have no gradient and are not written).
+template <typename Tin, typename Tout, int VPT, int RPB>
+__global__ void __launch_bounds__(256) k_dlogits_tlist(const BwdParams p, const BwdRec* list,
+                                                       const int32_t* zlist, const int* count,
+                                                       int ntiles) {
+  constexpr int EPV = Vec<Tin>::EPV;
+  const int g = blockIdx.x / ntiles;
+  const int tile = blockIdx.x - g * ntiles;
+  const int n_sweep = count[0], n_all = n_sweep + count[1];
+  const int nvec = (p.V + EPV - 1) / EPV;
+  const int j0 = tile * (256 * VPT) + threadIdx.x;
+  const float lamL = p.lam_log2e;
+  for (int k = 0; k < RPB; ++k) {
+    const int idx = g * RPB + k;
+    if (idx >= n_all) return;
+    if (idx >= n_sweep) {   // zero-fill row: write only
+      char* orow = static_cast<char*>(p.dlogits) + int64_t(zlist[idx - n_sweep]) * p.ldg * int64_t(sizeof(Tout));
+      float z[EPV];
+#pragma unroll
+      for (int e = 0; e < EPV; ++e) z[e] = 0.f;
+#pragma unroll
+      for (int u = 0; u < VPT; ++u) {
+        const int j = j0 + 256 * u;
+        if (j < nvec) store_out<Tin, Tout>(orow, j, z, p.V);
+      }
+      continue;
+    }
+    const BwdRec rc = list[idx];
+    const char* row = static_cast<const char*>(p.logits) + int64_t(rc.r) * p.ld * int64_t(sizeof(Tin));
+    char* orow = static_cast<char*>(p.dlogits) + int64_t(rc.r) * p.ldg * int64_t(sizeof(Tout));
+    const int vy = rc.yl >= 0 ? rc.yl / EPV : -1, yoff = rc.yl >= 0 ? rc.yl % EPV : 0;
+    uint4 v[VPT];
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int j = j0 + 256 * u;
+      if (j < nvec)
+        v[u] = p.aliased ? ld_stream_coherent(row + int64_t(j) * 16) : ld_stream(row + int64_t(j) * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int j = j0 + 256 * u;
+      if (j < nvec) {
+        float dd[EPV];
+        dz_vec<Tin>(v[u], j, vy, yoff, lamL, rc, dd);
+        store_out<Tin, Tout>(orow, j, dd, p.V);
+      }
+    }
+  }
+}
+
 template <typename Tin, typename Tout, int VPT, bool P2 = true>
 __global__ void __launch_bounds__(256) k_dlogits_tile(const BwdParams p, const BwdRec* rec,
                                                       int ntiles) {

@@ -200,3 +200,19 @@ def test_packed_f32x2_variant_is_bitwise_default(dev, c0):
         assert np.array_equal(a["dlogits"], b["dlogits"])
         for k in ("lse", "lp", "H", "q"):
             assert np.array_equal(a["tok"][k], b["tok"][k], equal_nan=True), k
+
+
+@pytest.mark.parametrize("compact", [False, True], ids=["zero_fill", "compact"])
+def test_tiled_list_bwd_variant_is_bitwise_default(dev, compact):
+    """bwd variant 9 (tiles over the compact row lists) writes exactly the default's gradient
+    (the per-element arithmetic is shared; only the work distribution differs); in compact
+    mode rows without gradient stay untouched."""
+    inst = tiny_instance(34, V=4104, group_sizes=(4, 4, 2), L=40, dtype="bf16", mask_tail=7,
+                         rewards=[1, 0, 1, 1, 1, 1, 1, 1, 0, 1])
+    kw = {"logits_dtype": torch.bfloat16, "cfgkw": {"zero_fill_inactive_rows": not compact}}
+    a = run_gpu(inst, dev, **kw)
+    b = run_gpu(inst, dev, bwd_impl=9, **kw)
+    assert np.array_equal(a["dlogits"], b["dlogits"], equal_nan=True)
+    if compact:
+        untouched = ~(a["tok"]["coef"] != 0)
+        assert np.isnan(b["dlogits"][untouched]).all()
