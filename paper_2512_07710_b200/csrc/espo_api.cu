@@ -387,7 +387,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   switch (option) {
     case ESPO_OPT_FWD_IMPL:
-      if (value < 0 || value > 8) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 11) return ESPO_ERR_INVALID_ARGUMENT;
       c->fwd_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_BWD_IMPL:
@@ -485,6 +485,9 @@ espo_status check_coverage(espo_ctx_t c, int64_t b, int64_t e) {
   return ESPO_OK;
 }
 
+espo_status launch_combine(espo_ctx_t c, const float* partials, int n_shards, int64_t row_begin,
+                           int64_t n_rows, cudaStream_t s);
+
 // K2 (+ its row-list pre-pass) over one chunk; writes statistics, or partials if `partial`.
 espo_status launch_sweep_fwd(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
                              const float* old_logp, const uint8_t* mask, int64_t row_begin,
@@ -514,6 +517,29 @@ espo_status launch_sweep_fwd(espo_ctx_t c, const void* logits, int64_t ld, const
     k_fwd_rows<float><<<pre_grid, 256, 0, s>>>(logits, ld, tokens, old_logp, mask, row_begin, n_rows,
                                                V, v0, p.V, p.lam_log2e, c->ws, list, c->ws.count);
   ESPO_LAUNCHED(c);
+  if (c->fwd_impl >= 9 && partial == nullptr) {
+    // tiled: (listed row, 32 KB tile) blocks → per-tile partials → k_fwd_combine
+    const int epv = bf ? 8 : 4;
+    const int ntiles = (((p.V + epv - 1) / epv) + 256 * 8 - 1) / (256 * 8);
+    const int64_t grid = n_rows * int64_t(ntiles);
+    if (grid > INT32_MAX) return ESPO_ERR_INVALID_ARGUMENT;
+    const size_t need = size_t(ntiles) * size_t(n_rows) * 16;
+    if (need > c->lmh_cap) {
+      if (c->lmh_partial) cudaFree(c->lmh_partial);
+      c->lmh_partial = nullptr;
+      c->lmh_cap = 0;
+      ESPO_CUDA(cudaMalloc(&c->lmh_partial, need));
+      c->lmh_cap = need;
+    }
+    float4* part = reinterpret_cast<float4*>(c->lmh_partial);
+#define ESPO_FTILE(MB)                                                                                        \
+    if (bf) k_rowstats_tile<__nv_bfloat16, 8, MB><<<unsigned(grid), 256, 0, s>>>(p, list, c->ws.count, ntiles, part); \
+    else k_rowstats_tile<float, 8, MB><<<unsigned(grid), 256, 0, s>>>(p, list, c->ws.count, ntiles, part);
+    if (c->fwd_impl == 9) { ESPO_FTILE(4) } else if (c->fwd_impl == 10) { ESPO_FTILE(3) } else { ESPO_FTILE(2) }
+#undef ESPO_FTILE
+    ESPO_LAUNCHED(c);
+    return launch_combine(c, c->lmh_partial, ntiles, row_begin, n_rows, s);
+  }
   if (c->fwd_impl == 1) {
     if (bf) {
       auto k = k_rowstats_ldg<__nv_bfloat16, 8>;

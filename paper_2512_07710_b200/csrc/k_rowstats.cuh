@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(256) k_fwd_combine(const float4* partials, int
 
 // Slow path for one batch: NaN/+inf detection and a max-based reference. Re-unpacks the
 // packed vectors (kept in registers) instead of holding U·EPV floats.
-template <typename Tin, int U>
+template <typename Tin, int U, int STRIDE = 32>   // vector k of the batch is j0 + STRIDE·k
 __device__ __forceinline__ void batch_slow(const uint4* v, int j0, int nvec, int vy, int yoff,
                                            int jrag, int V, float lamL, float& r, float& S,
                                            float& W, float& bS, float& bW, int* err) {
@@ -172,7 +172,7 @@ __device__ __forceinline__ void batch_slow(const uint4* v, int j0, int nvec, int
   bool bad = false;
 #pragma unroll
   for (int k = 0; k < U; ++k) {
-    const int j = j0 + 32 * k;
+    const int j = j0 + STRIDE * k;
     if (j >= nvec) continue;
     float x[EPV];
     Vec<Tin>::unpack(v[k], x);
@@ -198,7 +198,7 @@ __device__ __forceinline__ void batch_slow(const uint4* v, int j0, int nvec, int
   bW = 0.f;
 #pragma unroll
   for (int k = 0; k < U; ++k) {
-    const int j = j0 + 32 * k;
+    const int j = j0 + STRIDE * k;
     if (j >= nvec) continue;
     float x[EPV];
     Vec<Tin>::unpack(v[k], x);
@@ -470,6 +470,80 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
       }
     }
     row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane, p.partial, rec.r);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Variant TILE: a non-persistent grid of (listed row, tile) blocks — the K5 access pattern,
+// which reaches the part's streaming ceiling. Block = 256 threads × VPT 16-byte vectors (32 KB
+// of bf16 at VPT = 8), all loads in flight; each thread reduces its VPT vectors relative to
+// the row's target logit (batch_slow for the target / ragged vector or an overflow), the
+// block merges its threads (max reference, rebase, tree sums) and writes the tile's partial
+// {R, S, W, u_y} to part[tile][row]; k_fwd_combine merges the tiles exactly like vocabulary
+// shards.
+// ---------------------------------------------------------------------------------------
+template <typename Tin, int VPT, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_rowstats_tile(const FwdParams p, const FwdRec* list,
+                                                       const int* count, int ntiles,
+                                                       float4* part) {
+  constexpr int EPV = Vec<Tin>::EPV;
+  __shared__ float sh_r[8], sh_s[8], sh_w[8];
+  const int i = blockIdx.x / ntiles;
+  const int tile = blockIdx.x - i * ntiles;
+  if (i >= *count) return;
+  const FwdRec rec = list[i];
+  const char* row = static_cast<const char*>(p.logits) + int64_t(rec.r) * p.ld * int64_t(sizeof(Tin));
+  const int nvec = (p.V + EPV - 1) / EPV;
+  const int jrag = (p.V % EPV) ? nvec - 1 : -1;
+  const int vy = rec.yl >= 0 ? rec.yl / EPV : -1, yoff = rec.yl >= 0 ? rec.yl % EPV : 0;
+  const float lamL = p.lam_log2e;
+  const int j0 = tile * (256 * VPT) + threadIdx.x;
+  const uint4 ninf = make_uint4(Vec<Tin>::kNegInfWord, Vec<Tin>::kNegInfWord, Vec<Tin>::kNegInfWord,
+                                Vec<Tin>::kNegInfWord);
+  uint4 v[VPT];
+#pragma unroll
+  for (int u = 0; u < VPT; ++u) {
+    const int j = j0 + 256 * u;
+    v[u] = (j < nvec) ? ld_stream(row + int64_t(j) * 16) : ninf;
+  }
+  float ref = rec.yl >= 0 ? rec.uy : -INFINITY, bS, bW;
+  acc_batch<Tin, VPT, -1>(v, lamL, -ref, bS, bW);
+  const unsigned dy = static_cast<unsigned>(vy - j0), dr = static_cast<unsigned>(jrag - j0);
+  const bool special = (vy >= 0 && dy < 256u * VPT && (dy & 255u) == 0) ||
+                       (jrag >= 0 && dr < 256u * VPT && (dr & 255u) == 0);
+  if (special || !(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {
+    float S = 0.f, W = 0.f;
+    batch_slow<Tin, VPT, 256>(v, j0, nvec, vy, yoff, jrag, p.V, lamL, ref, S, W, bS, bW, p.ws.err);
+  }
+  // block merge: max reference, rebase, fixed-order tree sums
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float R = warp_max(ref);
+  if (lane == 0) sh_r[w] = R;
+  __syncthreads();
+  R = sh_r[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) R = fmaxf(R, sh_r[k]);
+  if (R == -INFINITY) {
+    bS = 0.f;
+    bW = 0.f;
+  } else {
+    rebase(ref, R, bS, bW);
+  }
+  bS = warp_sum(bS);
+  bW = warp_sum(bW);
+  if (lane == 0) {
+    sh_s[w] = bS;
+    sh_w[w] = bW;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float S = 0.f, W = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      S += sh_s[k];
+      W += sh_w[k];
+    }
+    part[int64_t(tile) * p.n_rows + rec.r] = make_float4(R, S, W, rec.uy);
   }
 }
 

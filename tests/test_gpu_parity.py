@@ -216,3 +216,29 @@ def test_tiled_list_bwd_variant_is_bitwise_default(dev, compact):
     if compact:
         untouched = ~(a["tok"]["coef"] != 0)
         assert np.isnan(b["dlogits"][untouched]).all()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_tiled_fwd_variant(dev, c0, dtype):
+    """fwd variant 9: (row, 32 KB tile) blocks with per-tile partials merged by the combine
+    kernel — a different summation order, so equal to the default within fp32 summation
+    error, and to the oracle at the parity tolerances."""
+    if dtype == "f32":
+        inst, kw = c0, {}
+    else:
+        inst = tiny_instance(35, V=40000, group_sizes=(4, 4), L=24, dtype="bf16", mask_tail=5)
+        kw = {"logits_dtype": torch.bfloat16, "grad_dtype": torch.float32}
+    a = run_gpu(inst, dev, **kw)
+    b = run_gpu(inst, dev, fwd_impl=9, **kw)
+    assert b["loss"] == pytest.approx(a["loss"], rel=1e-6, abs=1e-9)
+    v = a["tok"]["valid"].astype(bool)
+    for k, tol in (("lse", 2e-6), ("lp", 2e-6), ("H", 1e-5)):
+        x, y = a["tok"][k][v].astype(np.float64), b["tok"][k][v].astype(np.float64)
+        assert np.all(np.abs(x - y) <= tol * np.maximum(1, np.abs(x))), k
+    cfg = oracle_cfg(inst.V)
+    ref = inst.run(cfg)
+    check_exact_fields(b, ref)
+    check_token_stats(b, ref)
+    ref2, _ = decision_aware_reference(b, inst, ref, cfg)
+    check_loss(b, ref2, 1e-5)
+    check_dlogits_f32(b["dlogits"], oracle_dlogits(ref2, inst, cfg, np.arange(inst.T)))
