@@ -332,8 +332,10 @@ typedef enum {
                                   lists (4 rows per block) */
   ESPO_OPT_BLOCKS_PER_SM = 2,  /* persistent grid = blocks_per_sm × SM count (0 = auto) */
   ESPO_OPT_LMHEAD_PARTS = 3,   /* espo_lmhead_fwd/bwd vocabulary parts per row block (0 = auto) */
-  ESPO_OPT_LMHEAD_BWD_ROWS = 4 /* espo_lmhead_bwd rows per dz sub-chunk (multiple of 128;
+  ESPO_OPT_LMHEAD_BWD_ROWS = 4,/* espo_lmhead_bwd rows per dz sub-chunk (multiple of 128;
                                   0 = default 8192) */
+  ESPO_OPT_LMHEAD_2CTA = 5     /* 1: LM-head kernels on CTA pairs (tcgen05 cta_group::2,
+                                  M = 256 per pair); 0: one CTA per 128-row block */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

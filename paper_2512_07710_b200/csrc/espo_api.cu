@@ -14,6 +14,7 @@
 #include "k_rowlist.cuh"
 #include "k_seq.cuh"
 #include "k_lmhead.cuh"
+#include "k_lmhead2.cuh"
 #include "k_reward.cuh"
 #include "workspace.cuh"
 
@@ -123,6 +124,7 @@ struct espo_ctx_s {
   void* rs_scratch = nullptr;    // reward reshaping hash tables, grown on demand
   int64_t rs_cap = 0;
   int lmh_bwd_rows = 8192;       // LM-head backward dz sub-chunk rows
+  int lmh_2cta = 0;              // 1: CTA-pair (cta_group::2) LM-head kernels
   void* lmh_dz = nullptr;        // [lmh_bwd_rows][round_up(V, 256)] bf16, grown on demand
   size_t lmh_dz_cap = 0;
   cublasHandle_t blas = nullptr;
@@ -401,6 +403,10 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
     case ESPO_OPT_LMHEAD_PARTS:
       if (value < 0 || value > 64) return ESPO_ERR_INVALID_ARGUMENT;
       c->lmh_parts = static_cast<int>(value);
+      return ESPO_OK;
+    case ESPO_OPT_LMHEAD_2CTA:
+      if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
+      c->lmh_2cta = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_BWD_ROWS:
       if (value < 0 || value > (1 << 20) || value % kLmBM) return ESPO_ERR_INVALID_ARGUMENT;
@@ -726,13 +732,14 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   }
   CUtensorMap mh, mw;
   if (!make_map_bf16(&mh, hidden, uint64_t(n_rows), uint64_t(d), uint64_t(ldh) * 2, kLmBM) ||
-      !make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, kLmBN))
+      !make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, c->lmh_2cta ? kLmBN / 2 : kLmBN))
     return ESPO_ERR_CUDA;
   const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
   k_lmh_rows<<<pre_grid, 256, 0, s>>>(tokens, old_logp, mask, row_begin, n_rows, V, c->ws);
   ESPO_LAUNCHED(c);
-  static unsigned long long attr_mask = 0;
+  static unsigned long long attr_mask = 0, attr_mask2 = 0;
   ESPO_CUDA(ensure_smem_attr(k_lmhead_fwd, int(kLmSmem), attr_mask));
+  ESPO_CUDA(ensure_smem_attr(k_lmhead2_fwd, int(kL2Smem), attr_mask2));
   LmParams lp;
   lp.n_rows = int(n_rows);
   lp.row_begin = row_begin;
@@ -744,7 +751,10 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   lp.tokens = tokens;
   lp.partial = c->lmh_partial;
   lp.ws = c->ws;
-  k_lmhead_fwd<<<dim3(parts, mblocks), kLmThreads, kLmSmem, s>>>(mh, mw, lp);
+  if (c->lmh_2cta)   // CTA pairs: (2·part + rank, row-block pair), cluster (2, 1, 1)
+    k_lmhead2_fwd<<<dim3(2 * parts, (mblocks + 1) / 2), kLmThreads, kL2Smem, s>>>(mh, mw, lp);
+  else
+    k_lmhead_fwd<<<dim3(parts, mblocks), kLmThreads, kLmSmem, s>>>(mh, mw, lp);
   ESPO_LAUNCHED(c);
   if ((st = launch_combine(c, c->lmh_partial, parts, row_begin, n_rows, s)) != ESPO_OK) return st;
   c->covered[row_begin] = row_begin + n_rows;
@@ -798,10 +808,11 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
   k_bwd_recs<<<pre_grid, 256, 0, s>>>(row_begin, n_rows, grad_loss_dev, 1, 0, V, c->ws, rec);
   ESPO_LAUNCHED(c);
-  static unsigned long long attr_mask = 0;
+  static unsigned long long attr_mask = 0, attr_mask2 = 0;
   ESPO_CUDA(ensure_smem_attr(k_lmhead_dz, int(kLmSmem), attr_mask));
+  ESPO_CUDA(ensure_smem_attr(k_lmhead2_dz, int(kL2Smem), attr_mask2));
   CUtensorMap mw;
-  if (!make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, kLmBN))
+  if (!make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, c->lmh_2cta ? kLmBN / 2 : kLmBN))
     return ESPO_ERR_CUDA;
   const float one = 1.f, zero = 0.f;
   const char* hb = static_cast<const char*>(hidden);
@@ -824,7 +835,10 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
     lp.dz = static_cast<__nv_bfloat16*>(c->lmh_dz);
     lp.ldz = ldz;
     lp.ws = c->ws;
-    k_lmhead_dz<<<dim3(parts, mblocks), kLmThreads, kLmSmem, s>>>(mh, mw, lp);
+    if (c->lmh_2cta)
+      k_lmhead2_dz<<<dim3(2 * parts, (mblocks + 1) / 2), kLmThreads, kL2Smem, s>>>(mh, mw, lp);
+    else
+      k_lmhead_dz<<<dim3(parts, mblocks), kLmThreads, kLmSmem, s>>>(mh, mw, lp);
     ESPO_LAUNCHED(c);
     // z = h·Wᵀ (dz already carries λ, as K5's) ⇒ dh = dz·W and dW = dzᵀ·h
     if (dhidden) {   // column-major view: dhᵀ[d, n] = Wᵀ[d, V] · dzᵀ[V, n]

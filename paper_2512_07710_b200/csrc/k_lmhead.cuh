@@ -137,6 +137,75 @@ __device__ __forceinline__ void lm_store_dz(const float* x, const BwdRec& rc, in
   for (int e = 0; e < 4; ++e) o[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
 }
 
+// One 32-column chunk of a row's logits x (fp32, from TMEM) into the row's base-2 online
+// reduction (R, S, W) with Kahan compensation (cS, cW); captures u_y from the target's chunk.
+__device__ __forceinline__ void lm_row_chunk(float* x, int col0, int y, int V, float lamL,
+                                             float& R, float& S, float& W, float& cS, float& cW,
+                                             float& uy, int* err) {
+  const bool special = (y >= col0 && y < col0 + 32) || (col0 + 32 > V);
+  if (special) {
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const int col = col0 + e;
+      if (col == y) uy = x[e] * lamL;
+      if (col == y || col >= V) x[e] = -INFINITY;
+    }
+  }
+  if (R == -INFINITY) {                      // first chunk: reference = its max
+    float m = x[0];
+#pragma unroll
+    for (int e = 1; e < 32; ++e) m = fmaxf(m, x[e]);
+    R = m * lamL;
+    if (R == -INFINITY) return;
+  }
+  // fast chunk: no clamp, no max (logits are finite; masked columns are −inf and go
+  // through the checked path below via NaN = 0·(−inf))
+  float bS, bW;
+  {
+    const float nR = -R;
+    float s0 = 0.f, s1 = 0.f, w0 = 0.f, w1 = 0.f;
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      const float ta = fmaf(x[e], lamL, nR), tb = fmaf(x[e + 1], lamL, nR);
+      const float ea = ex2(ta), eb = ex2(tb);
+      s0 += ea;
+      s1 += eb;
+      w0 = fmaf(ea, ta, w0);
+      w1 = fmaf(eb, tb, w1);
+    }
+    bS = s0 + s1;
+    bW = w0 + w1;
+  }
+  if (!(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {  // overflow / −inf / NaN: checked
+    S -= cS;
+    W -= cW;
+    cS = cW = 0.f;
+    float m = -INFINITY;
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      bad |= isnan(x[e]) || x[e] == INFINITY;
+      m = fmaxf(m, x[e] * lamL);
+    }
+    if (bad) set_error(err, ESPO_ERR_NONFINITE_INPUT);
+    if (m > R + 60.f) {
+      rebase(R, m, S, W);
+      R = m;
+    }
+    bS = 0.f;
+    bW = 0.f;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const float t = max_nan(fmaf(x[e], lamL, -R), -127.f);
+      const float ex = ex2(t);
+      bS += ex;
+      bW = fmaf(ex, t, bW);
+    }
+  }
+  kahan_add(S, cS, bS);
+  kahan_add(W, cW, bW);
+}
+
 // kDz = false: forward statistics (k_lmhead_fwd); kDz = true: backward recompute writing the
 // bf16 gradient tile dz = ∂(grad·loss)/∂z (k_lmhead_dz). Same TMA/MMA pipeline, same tile
 // order and K order, so the recomputed logits are bitwise the forward's.
@@ -296,68 +365,7 @@ __device__ __forceinline__ void lmhead_body(const CUtensorMap& tmap_h, const CUt
         tmem_ld32(base + uint32_t(c * 32), x);
         const int col0 = tile * kLmBN + c * 32;
         if (!valid) continue;
-        const bool special = (y >= col0 && y < col0 + 32) || (col0 + 32 > p.V);
-        if (special) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int col = col0 + e;
-            if (col == y) uy = x[e] * lamL;
-            if (col == y || col >= p.V) x[e] = -INFINITY;
-          }
-        }
-        if (R == -INFINITY) {                      // first chunk: reference = its max
-          float m = x[0];
-#pragma unroll
-          for (int e = 1; e < 32; ++e) m = fmaxf(m, x[e]);
-          R = m * lamL;
-          if (R == -INFINITY) continue;
-        }
-        // fast chunk: no clamp, no max (logits are finite; masked columns are −inf and go
-        // through the checked path below via NaN = 0·(−inf))
-        float bS, bW;
-        {
-          const float nR = -R;
-          float s0 = 0.f, s1 = 0.f, w0 = 0.f, w1 = 0.f;
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const float ta = fmaf(x[e], lamL, nR), tb = fmaf(x[e + 1], lamL, nR);
-            const float ea = ex2(ta), eb = ex2(tb);
-            s0 += ea;
-            s1 += eb;
-            w0 = fmaf(ea, ta, w0);
-            w1 = fmaf(eb, tb, w1);
-          }
-          bS = s0 + s1;
-          bW = w0 + w1;
-        }
-        if (!(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {  // overflow / −inf / NaN: checked
-          S -= cS;
-          W -= cW;
-          cS = cW = 0.f;
-          float m = -INFINITY;
-          bool bad = false;
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            bad |= isnan(x[e]) || x[e] == INFINITY;
-            m = fmaxf(m, x[e] * lamL);
-          }
-          if (bad) set_error(p.ws.err, ESPO_ERR_NONFINITE_INPUT);
-          if (m > R + 60.f) {
-            rebase(R, m, S, W);
-            R = m;
-          }
-          bS = 0.f;
-          bW = 0.f;
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float t = max_nan(fmaf(x[e], lamL, -R), -127.f);
-            const float ex = ex2(t);
-            bS += ex;
-            bW = fmaf(ex, t, bW);
-          }
-        }
-        kahan_add(S, cS, bS);
-        kahan_add(W, cW, bW);
+        lm_row_chunk(x, col0, y, p.V, lamL, R, S, W, cS, cW, uy, p.ws.err);
       }
       __syncwarp();
       tc_fence_before();

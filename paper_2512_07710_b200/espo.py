@@ -26,6 +26,7 @@ RATIO_GSPO_TOKEN, RATIO_LITERAL_OLD = 0, 1
 NORM_SEQ, NORM_TOKEN = 0, 1
 ZV_MASK, ZV_RLZVP = 0, 1
 OPT_FWD_IMPL, OPT_BWD_IMPL, OPT_BLOCKS_PER_SM, OPT_LMHEAD_PARTS, OPT_LMHEAD_BWD_ROWS = 0, 1, 2, 3, 4
+OPT_LMHEAD_2CTA = 5
 
 STATUS = {
     0: "ESPO_OK", 1: "ESPO_ERR_INVALID_ARGUMENT", 2: "ESPO_ERR_ALIGNMENT",

@@ -40,8 +40,10 @@ def make_case(seed, n_groups, G, L, V, d, zv_group=None):
                 old=old, mask=mask, T=T, R=R)
 
 
-def run_path(case, dev, fused, V):
+def run_path(case, dev, fused, V, two_cta=False):
+    from paper_2512_07710_b200.espo import OPT_LMHEAD_2CTA
     ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
+    ctx.set_option(OPT_LMHEAD_2CTA, int(two_cta))
     tok = to_dev(case["tokens"], torch.int32, dev)
     old = to_dev(case["old"], torch.float32, dev)
     mask = to_dev(case["mask"], torch.uint8, dev)
@@ -66,14 +68,15 @@ def run_path(case, dev, fused, V):
     return out
 
 
+@pytest.mark.parametrize("two_cta", [False, True], ids=["1cta", "2cta"])
 @pytest.mark.parametrize("shape", [(4, 4, 40, 1000, 200), (2, 8, 64, 4099, 512)],
                          ids=["V1000_d200", "V4099_d512"])
-def test_lmhead_fwd_matches_logits_path(shape):
+def test_lmhead_fwd_matches_logits_path(shape, two_cta):
     torch.backends.cuda.matmul.allow_tf32 = False
     dev = require_cuda()
     ng, G, L, V, d = shape
     case = make_case(5, ng, G, L, V, d, zv_group=1)
-    f = run_path(case, dev, True, V)
+    f = run_path(case, dev, True, V, two_cta)
     u = run_path(case, dev, False, V)
     v = u["tok"]["valid"].astype(bool)
     assert np.array_equal(f["tok"]["valid"], u["tok"]["valid"])
@@ -98,15 +101,16 @@ def test_lmhead_fwd_matches_logits_path(shape):
     assert f["stats"]["n_zv_groups"] == ref.stats["n_zv_groups"] == 1
 
 
+@pytest.mark.parametrize("two_cta", [False, True], ids=["1cta", "2cta"])
 @pytest.mark.parametrize("shape,sub,dh_bf16", [((4, 4, 40, 1000, 200), 0, False),
                                                ((2, 8, 64, 4099, 512), 256, True)],
                          ids=["V1000_d200", "V4099_d512_sub256_bf16"])
-def test_lmhead_bwd_matches_oracle(shape, sub, dh_bf16):
+def test_lmhead_bwd_matches_oracle(shape, sub, dh_bf16, two_cta):
     """espo_lmhead_bwd (tcgen05 recompute → bf16 dz → dh = dz·W, dW += dzᵀ·h) against O9 on
     fp64 logits, with the GPU's bucket / clip decisions injected where they flipped. Bound:
     dz is rounded to bf16 (2^-9) after an fp32 recompute whose logit error is ≤ the GEMM
     bound b_t; the contractions accumulate in fp32 over V (resp. n) terms."""
-    from paper_2512_07710_b200.espo import OPT_LMHEAD_BWD_ROWS
+    from paper_2512_07710_b200.espo import OPT_LMHEAD_2CTA, OPT_LMHEAD_BWD_ROWS
     from tests._instances import Instance
     from tests.gpu_common import decision_aware_reference
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -117,6 +121,7 @@ def test_lmhead_bwd_matches_oracle(shape, sub, dh_bf16):
     ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
     if sub:
         ctx.set_option(OPT_LMHEAD_BWD_ROWS, sub)
+    ctx.set_option(OPT_LMHEAD_2CTA, int(two_cta))
     tok = to_dev(case["tokens"], torch.int32, dev)
     old = to_dev(case["old"], torch.float32, dev)
     mask = to_dev(case["mask"], torch.uint8, dev)
@@ -161,3 +166,40 @@ def test_lmhead_bwd_matches_oracle(shape, sub, dh_bf16):
     # rows of the zero-variance group and masked rows carry no gradient
     zrows = ref2.kappa < 0
     assert zrows.any() and np.all(got_dh[zrows] == 0)
+
+
+def test_lmhead_2cta_equals_1cta():
+    """The CTA-pair kernels compute the same dot products in the same K order: statistics and
+    the backward's dh/dW agree with the one-CTA kernels (bitwise where the MMA order is the
+    same; within fp32 rounding otherwise)."""
+    from paper_2512_07710_b200.espo import OPT_LMHEAD_2CTA
+    dev = require_cuda()
+    V, d = 3000, 384
+    case = make_case(9, 3, 4, 48, V, d, zv_group=2)
+    outs = []
+    for two in (0, 1):
+        ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
+        ctx.set_option(OPT_LMHEAD_2CTA, two)
+        tok = to_dev(case["tokens"], torch.int32, dev)
+        ctx.prepare(to_dev(case["rewards"], torch.float32, dev),
+                    to_dev(case["group_ids"], torch.int32, dev), to_dev(case["so"], torch.int64, dev),
+                    n_tokens=case["T"])
+        h = to_dev(case["h"], torch.bfloat16, dev)
+        W = to_dev(case["W"], torch.bfloat16, dev)
+        ctx.lmhead_fwd(h, W, tok, to_dev(case["old"], torch.float32, dev),
+                       to_dev(case["mask"], torch.uint8, dev))
+        loss, _ = ctx.loss_finalize()
+        dW = torch.zeros((V, d), dtype=torch.float32, device=dev)
+        dh, _ = ctx.lmhead_bwd(h, W, None, dW)
+        ctx.get_error()
+        t = {k: v.cpu().numpy() for k, v in ctx.export_token_stats().items()}
+        outs.append((float(loss.item()), t, dh.cpu().numpy(), dW.cpu().numpy()))
+        ctx.close()
+    (l0, t0, h0, w0), (l1, t1, h1, w1) = outs
+    v = t0["valid"].astype(bool)
+    assert np.array_equal(v, t1["valid"].astype(bool))
+    for k in ("lse", "lp", "H"):
+        np.testing.assert_allclose(t1[k][v], t0[k][v], rtol=2e-6, atol=2e-6)
+    assert l1 == pytest.approx(l0, rel=1e-5, abs=1e-8)
+    np.testing.assert_allclose(h1, h0, rtol=1e-3, atol=1e-6 * np.abs(h0).max())
+    np.testing.assert_allclose(w1, w0, rtol=1e-3, atol=1e-6 * np.abs(w0).max())

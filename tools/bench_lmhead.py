@@ -12,7 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_07710_b200.espo import Espo  # noqa: E402
 
 
-def main(d=4096, n=32768, V=151936, iters=5, parts=0):
+def main(d=4096, n=32768, V=151936, iters=5, parts=0, two_cta=0):
     dev = torch.device("cuda", 0)
     torch.manual_seed(0)
     h = (torch.randn(n, d, device=dev) / d ** 0.5 * 3).to(torch.bfloat16)
@@ -25,6 +25,7 @@ def main(d=4096, n=32768, V=151936, iters=5, parts=0):
     so = torch.arange(G + 1, device=dev, dtype=torch.int64) * (n // G)
     ctx = Espo(V, logits_dtype=torch.bfloat16, device=0)
     ctx.set_option(3, parts)
+    ctx.set_option(5, two_cta)
 
     def fused():
         ctx.prepare(rewards, gid, so, n_tokens=n)
@@ -49,10 +50,11 @@ def main(d=4096, n=32768, V=151936, iters=5, parts=0):
         res[name] = {"ms": ms, "TFLOPs": 2.0 * n * V * d / (ms * 1e-3) / 1e12,
                      "tokens_per_s": n / (ms * 1e-3)}
     ctx.get_error()
-    res["config"] = {"n": n, "V": V, "d": d, "parts": parts or "auto"}
+    res["config"] = {"n": n, "V": V, "d": d, "parts": parts or "auto", "two_cta": two_cta}
     print(json.dumps(res))
 
 
 if __name__ == "__main__":
     main(d=int(sys.argv[1]) if len(sys.argv) > 1 else 4096,
-         parts=int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+         parts=int(sys.argv[2]) if len(sys.argv) > 2 else 0,
+         two_cta=int(sys.argv[3]) if len(sys.argv) > 3 else 0)
