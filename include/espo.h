@@ -143,6 +143,10 @@ typedef struct {
   double mean_ratio[ESPO_MAX_BUCKETS];   /* token-weighted mean of the ratio value */
   double mean_eps[ESPO_MAX_BUCKETS];     /* token-weighted mean of ε_τ */
   double tokens_per_bucket[ESPO_MAX_BUCKETS];
+  /* train/inference mismatch of the rollout-engine log-probs (§2.4.4 Router
+   * Replay; Δ_t = log π_θ(y_t) − log π_old(y_t) over active tokens): */
+  double mean_sq_logratio;     /* mean Δ² */
+  double mean_k3;              /* mean (e^Δ − 1 − Δ): k3 estimate of KL(π_old ‖ π_θ) */
 } espo_stats;
 
 /* Fills *cfg with the defaults listed above for the given vocab (bf16 logits and grads). */

@@ -379,6 +379,8 @@ def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
     vsum_k = np.zeros(K)
     esum_k = np.zeros(K)
     sum_abs_lr = 0.0
+    sum_sq_lr = 0.0
+    sum_k3 = 0.0
     sum_H = 0.0
     n_clipped = 0
 
@@ -452,7 +454,12 @@ def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
                 vsum_k[sk] += v
                 esum_k[sk] += eps
                 n_clipped += 0 if kap else 1
-                sum_abs_lr += abs(lp[j] - old[j])
+                d_lr = lp[j] - old[j]
+                sum_abs_lr += abs(d_lr)
+                sum_sq_lr += d_lr * d_lr
+                # k3 estimator of KL(π_old ‖ π_θ) from samples y ~ π_old: r − 1 − log r,
+                # r = π_θ(y)/π_old(y) (train/inference mismatch)
+                sum_k3 += math.expm1(d_lr) - d_lr
                 sum_H += H[j]
         J_i[i] = Ji
 
@@ -475,6 +482,8 @@ def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
         "mean_ratio": [vsum_k[k] / tok_k[k] if tok_k[k] else 0.0 for k in range(K)],
         "mean_eps": [esum_k[k] / tok_k[k] if tok_k[k] else 0.0 for k in range(K)],
         "tokens_per_bucket": tok_k.tolist(),
+        "mean_sq_logratio": sum_sq_lr / t_active if t_active else 0.0,
+        "mean_k3": sum_k3 / t_active if t_active else 0.0,
     }
     return OracleResult(loss=loss, J_sum=J_sum, denom=denom, adv=grp["adv"], zv=grp["zv"],
                         active=active, n_valid=n_valid, J_i=J_i, nb=nb_a, lse=lse_a,

@@ -14,7 +14,7 @@ constexpr int kMaxK = ESPO_MAX_BUCKETS;
 // Number of fp64 values in the per-rank reduction vector (all-reduced with NCCL).
 //  0 ΣJ_i  1 N_active  2 T_active  3 n_zv_groups  4 n_groups  5 n_clipped
 //  6 Σ|lp−old|  7 ΣH  8..11 tokens_k  12..15 clipped_k  16..19 Σv_k  20..23 Σε_k
-constexpr int kRedLen = 24;
+constexpr int kRedLen = 26;
 
 // ----------------------------------------------------------------------------- errors
 __device__ __forceinline__ void set_error(int* err, int code) {

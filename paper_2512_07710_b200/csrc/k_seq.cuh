@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_reduce(const SeqParams p) {
 
   // ---- O5: per-token surrogate, clip decision, coefficient
   const double w_single = (p.norm == ESPO_NORM_SEQ) ? 1.0 / static_cast<double>(n) : 1.0;
-  double Jl = 0.0, abslr = 0.0, hsum = 0.0;
+  double Jl = 0.0, abslr = 0.0, hsum = 0.0, sqlr = 0.0, k3 = 0.0;
   double st_tok[kMaxK] = {0, 0, 0, 0}, st_clip[kMaxK] = {0, 0, 0, 0};
   double st_v[kMaxK] = {0, 0, 0, 0}, st_e[kMaxK] = {0, 0, 0, 0};
   for (int64_t t = b + threadIdx.x; t < e; t += blockDim.x) {
@@ -319,12 +319,17 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_reduce(const SeqParams p) {
         st_tok[k] += 1.0; st_clip[k] += clipped ? 1.0 : 0.0; st_v[k] += v; st_e[k] += eps;
       }
     }
-    abslr += fabs(lp - old);
+    const double dlr = lp - old;
+    abslr += fabs(dlr);
+    sqlr += dlr * dlr;
+    k3 += expm1(dlr) - dlr;   // KL(π_old ‖ π_θ) k3 estimator (train/inference mismatch)
     hsum += h;
   }
   const double J = block_sum<double>(Jl, shd);
   const double al = block_sum<double>(abslr, shd);
   const double hs = block_sum<double>(hsum, shd);
+  const double sq = block_sum<double>(sqlr, shd);
+  const double kk = block_sum<double>(k3, shd);
   double ncl = 0;
   for (int k = 0; k < kMaxK; ++k) {
     const double a = block_sum<double>(st_tok[k], shd);
@@ -346,6 +351,8 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_reduce(const SeqParams p) {
   put(5, ncl);
   put(6, al);
   put(7, hs);
+  put(24, sq);
+  put(25, kk);
 }
 
 // ------------------------------------------------------------------ K0 (single-pass mode)
@@ -456,6 +463,8 @@ __global__ void k_finalize_scalar(const Workspace ws, int norm, float logit_scal
       stats->mean_eps[k] = tk > 0 ? r[20 + k] / tk : 0.0;
       stats->tokens_per_bucket[k] = tk;
     }
+    stats->mean_sq_logratio = r[2] > 0 ? r[24] / r[2] : 0.0;
+    stats->mean_k3 = r[2] > 0 ? r[25] / r[2] : 0.0;
   }
 }
 

@@ -78,7 +78,8 @@ class RewardShaping(ctypes.Structure):
 STATS_FIELDS = ["loss", "n_active_rollouts", "n_active_tokens", "n_zv_groups", "n_groups",
                 "n_clipped_tokens", "mean_abs_logratio", "mean_entropy"]
 STATS_ARRAYS = ["clip_frac", "mean_ratio", "mean_eps", "tokens_per_bucket"]
-STATS_LEN = len(STATS_FIELDS) + ESPO_MAX_BUCKETS * len(STATS_ARRAYS)  # doubles
+STATS_TAIL = ["mean_sq_logratio", "mean_k3"]
+STATS_LEN = len(STATS_FIELDS) + ESPO_MAX_BUCKETS * len(STATS_ARRAYS) + len(STATS_TAIL)  # doubles
 
 
 def stats_to_dict(t: torch.Tensor) -> dict:
@@ -87,6 +88,9 @@ def stats_to_dict(t: torch.Tensor) -> dict:
     o = len(STATS_FIELDS)
     for j, k in enumerate(STATS_ARRAYS):
         d[k] = v[o + j * ESPO_MAX_BUCKETS: o + (j + 1) * ESPO_MAX_BUCKETS]
+    o += ESPO_MAX_BUCKETS * len(STATS_ARRAYS)
+    for j, k in enumerate(STATS_TAIL):
+        d[k] = v[o + j]
     return d
 
 

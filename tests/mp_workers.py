@@ -17,10 +17,10 @@ def _init(rank, world, port):
 
 
 def partial_vector(res):
-    """The 24 rank-local fp64 terms libespo all-reduces (layout of kRedLen in common.cuh)."""
+    """The 26 rank-local fp64 terms libespo all-reduces (layout of kRedLen in common.cuh)."""
     st = res.stats
     tok = np.array(st["tokens_per_bucket"])
-    v = np.zeros(24)
+    v = np.zeros(26)
     v[0] = res.J_sum
     v[1] = st["n_active_rollouts"]
     v[2] = st["n_active_tokens"]
@@ -33,6 +33,8 @@ def partial_vector(res):
     v[12:16] = np.array(st["clip_frac"]) * tok
     v[16:20] = np.array(st["mean_ratio"]) * tok
     v[20:24] = np.array(st["mean_eps"]) * tok
+    v[24] = st["mean_sq_logratio"] * st["n_active_tokens"]
+    v[25] = st["mean_k3"] * st["n_active_tokens"]
     return v
 
 

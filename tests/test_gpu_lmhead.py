@@ -203,3 +203,38 @@ def test_lmhead_2cta_equals_1cta():
     assert l1 == pytest.approx(l0, rel=1e-5, abs=1e-8)
     np.testing.assert_allclose(h1, h0, rtol=1e-3, atol=1e-6 * np.abs(h0).max())
     np.testing.assert_allclose(w1, w0, rtol=1e-3, atol=1e-6 * np.abs(w0).max())
+
+
+def test_lmhead_errors_and_state():
+    """espo_lmhead_bwd before finalize → BAD_STATE; fused LM head on a vocabulary-sharded
+    context → UNSUPPORTED; misaligned hidden pitch → ALIGNMENT."""
+    from paper_2512_07710_b200.espo import EspoError
+    dev = require_cuda()
+    V, d, T = 512, 64, 32
+    h = torch.zeros((T, d), dtype=torch.bfloat16, device=dev)
+    W = torch.zeros((V, d), dtype=torch.bfloat16, device=dev)
+    tok = torch.zeros(T, dtype=torch.int32, device=dev)
+    old = torch.zeros(T, dtype=torch.float32, device=dev)
+    args = (torch.tensor([1.0, 0.0], device=dev), torch.zeros(2, dtype=torch.int32, device=dev),
+            torch.tensor([0, 16, 32], dtype=torch.int64, device=dev))
+    ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
+    ctx.prepare(*args, n_tokens=T)
+    with pytest.raises(EspoError) as e:
+        ctx.lmhead_bwd(h, W)
+    assert e.value.code == "ESPO_ERR_BAD_STATE"
+    hp = torch.zeros((T, d + 3), dtype=torch.bfloat16, device=dev)[:, :d]   # 134-byte pitch
+    with pytest.raises(EspoError) as e:
+        ctx.lmhead_fwd(hp, W, tok, old)
+    assert e.value.code == "ESPO_ERR_ALIGNMENT"
+    ctx.lmhead_fwd(h, W, tok, old)
+    ctx.loss_finalize()
+    dh, _ = ctx.lmhead_bwd(h, W)
+    ctx.get_error()
+    assert torch.isfinite(dh).all()
+    ctx.close()
+    sh = Espo(V, logits_dtype=torch.float32, device=dev.index, vocab_shard=(0, 256))
+    sh.prepare(*args, n_tokens=T)
+    with pytest.raises(EspoError) as e:
+        sh.lmhead_fwd(h, W[:256], tok, old)
+    assert e.value.code == "ESPO_ERR_UNSUPPORTED"
+    sh.close()

@@ -48,6 +48,12 @@ def test_c0_full_parity(dev, c0, fwd_impl, bwd_impl):
     assert s["n_zv_groups"] == 1
     for k in ("mean_entropy", "mean_abs_logratio"):
         assert s[k] == pytest.approx(ref.stats[k], rel=1e-5)
+    # Δ = lp − old carries lp's fp32 error (≤ 2e-6·max(1,|lp|)): bound the means by it
+    lim = 2e-6 * max(1.0, float(np.nanmax(np.abs(ref.lp))))
+    assert abs(s["mean_sq_logratio"] - ref.stats["mean_sq_logratio"]) <= 2 * lim * (
+        ref.stats["mean_abs_logratio"] + lim) + 1e-12
+    assert abs(s["mean_k3"] - ref.stats["mean_k3"]) <= 2 * lim * (
+        ref.stats["mean_abs_logratio"] + lim) + 1e-12
     assert s["n_clipped_tokens"] == ref.stats["n_clipped_tokens"]
     for k in range(4):
         assert s["clip_frac"][k] == pytest.approx(ref.stats["clip_frac"][k], abs=1e-12)

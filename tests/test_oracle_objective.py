@@ -481,3 +481,21 @@ def test_lmhead_grads_match_finite_differences():
         Wp[v, j] += eps
         Wm[v, j] -= eps
         assert (F(h, Wp) - F(h, Wm)) / (2 * eps) == pytest.approx(dW[v, j], rel=1e-5, abs=1e-9)
+
+
+def test_mismatch_statistics_closed_forms():
+    """Train/inference mismatch stats: with old = lp − c on every token,
+    mean|Δ| = |c|, mean Δ² = c² and the k3 KL estimate = e^c − 1 − c (up to the f32 rounding
+    of old_logp); on-policy all three vanish; k3 ≥ 0 always."""
+    inst = _full_groups_instance(2)
+    res0 = inst.run(O.OracleConfig(vocab=inst.V))
+    for c in (0.0, 0.03, -0.2, 0.7):
+        inst.old_logp = (res0.lp - c).astype(np.float32)
+        st = inst.run(O.OracleConfig(vocab=inst.V)).stats
+        assert st["mean_abs_logratio"] == pytest.approx(abs(c), abs=2e-6)
+        assert st["mean_sq_logratio"] == pytest.approx(c * c, abs=4e-6)
+        assert st["mean_k3"] == pytest.approx(math.expm1(c) - c, abs=4e-6)
+    rng = np.random.default_rng(0)
+    inst.old_logp = (res0.lp + rng.normal(0, 0.5, size=len(res0.lp))).astype(np.float32)
+    st = inst.run(O.OracleConfig(vocab=inst.V)).stats
+    assert st["mean_k3"] > 0 and st["mean_sq_logratio"] >= st["mean_abs_logratio"] ** 2
