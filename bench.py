@@ -386,11 +386,13 @@ def cpu_baseline(d, w, n_tok_per_rollout, log):
     gid = np.zeros(G, np.int32)
     so_s = np.arange(G + 1, dtype=np.int64) * L
     cfg = O.OracleConfig(vocab=V, alpha=float(np.float32(0.4)), eps_min=float(np.float32(0.01)))
-    t0 = time.perf_counter()
-    res = O.espo_loss(z, tok, old, None, rw, gid, so_s, cfg)
-    for t in range(len(rows)):
-        O.dlogits_row(res, t, z[t], int(tok[t]), cfg)
-    dt = time.perf_counter() - t0
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):          # the oracle as it stands, on one core
+        t0 = time.perf_counter()
+        res = O.espo_loss(z, tok, old, None, rw, gid, so_s, cfg)
+        for t in range(len(rows)):
+            O.dlogits_row(res, t, z[t], int(tok[t]), cfg)
+        dt = time.perf_counter() - t0
     n = len(rows)
     log(f"cpu oracle: {n} tokens in {dt:.1f}s")
     return {"value": n / dt, "unit": "tokens/s", "cores": 1, "kind": "oracle",
@@ -591,12 +593,14 @@ def main_reference(args):
             O.dlogits_row(res, t, rows[t], int(tok[t]), cfg)
 
     samples = [sample(i) for i in range(args.warmup + args.steps)]
-    for i in range(args.warmup):
-        step(samples[i])
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        step(samples[args.warmup + i])
-    dt = (time.perf_counter() - t0) / args.steps
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):          # one core, as "cores" reports
+        for i in range(args.warmup):
+            step(samples[i])
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            step(samples[args.warmup + i])
+        dt = (time.perf_counter() - t0) / args.steps
     n = G * L
     out = {
         "impl": "reference",
