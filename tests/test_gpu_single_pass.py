@@ -121,3 +121,27 @@ def test_single_pass_rejects_misaligned_chunks_and_mixed_calls():
         ctx.get_error()
     assert e.value.code == "ESPO_ERR_INVALID_ARGUMENT"
     ctx.close()
+
+
+@pytest.mark.parametrize("cfgkw,dtype", [
+    ({"zero_fill_inactive_rows": False}, "bf16"),
+    ({"zv_mode": O.ZV_RLZVP, "norm": O.NORM_TOKEN}, "bf16"),
+    ({"partition": O.PARTITION_SINGLETON,
+      "ratio_mode": O.RATIO_LITERAL_OLD}, "f32"),
+    ({"n_buckets": 3, "logit_scale": 1.3}, "f32"),
+], ids=["compact_bf16", "rlzvp_token_bf16", "singleton_literal_f32", "k3_lambda_f32"])
+def test_single_pass_config_matrix(cfgkw, dtype):
+    """Single-pass ≡ two sweeps, bitwise, across modes (compact output, RL-ZVP + TOKEN
+    normalisation, singleton partition with the literal ratio, K = 3 with a temperature)."""
+    dev = require_cuda()
+    inst = tiny_instance(71, V=2056, group_sizes=(4, 3, 4), L=21, mask_tail=4,
+                         dtype=dtype, rewards=[1, 0, 1, 1, 1, 1, 1, 0, 0, 1, 0],
+                         logit_scale=cfgkw.get("logit_scale", 1.0))
+    kw = dict(cfgkw=cfgkw)
+    if dtype == "bf16":
+        kw.update(logits_dtype=torch.bfloat16, grad_dtype=torch.bfloat16)
+    chunks = [(7, 11), (0, 2), (2, 7)]
+    g = run_single(inst, dev, chunks, grad_loss=1.7, **kw)
+    two = run_gpu(inst, dev, grad_loss=1.7, **kw)
+    assert g["loss"] == two["loss"]
+    assert np.array_equal(g["dlogits"], two["dlogits"], equal_nan=True)
