@@ -139,10 +139,11 @@ def test_c1_full_size():
         check_dlogits_bf16(grads[c0], want)
 
 
-@pytest.mark.parametrize("name", ["C3", "C2"])
+@pytest.mark.parametrize("name", ["C3", "C2", "C4"])
 def test_full_size_sampled_groups(name):
-    """C3 (variable lengths, 60 % eliminated groups, chunks splitting sequences) and C2
-    (32 × 16 × 32,768 long-CoT sequences, each spanning a whole 32,768-row chunk)."""
+    """C3 (variable lengths, 60 % eliminated groups, chunks splitting sequences), C2
+    (32 × 16 × 32,768 long-CoT sequences, each spanning a whole 32,768-row chunk) and C4
+    (512 × 16 × 16,384 = 134 M tokens: the largest configuration, on one GPU)."""
     dev = require_cuda()
     b = build(name, dev)
     ctx, loss, st, _ = run(b, dev)
@@ -164,7 +165,7 @@ def test_full_size_sampled_groups(name):
     zv_g = [g for g in range(b.w.n_prompts) if rol["zv"][g * G]]
     cfg = oracle_cfg(b.V)
     picks = [active_groups[0], active_groups[len(active_groups) // 2]] + zv_g[:1]
-    if name == "C2":
+    if name in ("C2", "C4"):
         picks = picks[:1] + zv_g[:1]     # one 16 × 32k group is 524k tokens for the oracle
     for g in picks:
         r0, r1 = g * G, (g + 1) * G
