@@ -58,6 +58,9 @@ def parse():
                    help="e2e leg: logits chunks cross PCIe once (single-pass) or twice")
     p.add_argument("--zv-mode", default="mask", choices=["mask", "rlzvp"],
                    help="zero-variance groups: eliminated (default) or RL-ZVP advantages")
+    p.add_argument("--tp-p2p", action="store_true",
+                   help="with --vocab-shards: exchange partials through the fused peer-memory "
+                        "path (espo_tp_p2p_*) instead of partial + device-copy gather + combine")
     p.add_argument("--vocab-shards", type=int, default=1,
                    help="S > 1: vocabulary-parallel leg, S shard contexts back to back on this "
                         "GPU (partials gathered by a device copy)")
@@ -216,10 +219,15 @@ class ShardedStep:
     sweeps → gathered partials (one device tensor) → S combines; after finalize, S backward
     sweeps each writing its columns of the dlogits buffer."""
 
-    def __init__(self, ctxs, shards, Rc, dev):
+    def __init__(self, ctxs, shards, Rc, dev, p2p=False):
         import torch
-        self.ctxs, self.shards = ctxs, shards
+        self.ctxs, self.shards, self.p2p = ctxs, shards, p2p
         self.part = torch.empty((len(ctxs), Rc, 4), dtype=torch.float32, device=dev)
+        if p2p:
+            for c in ctxs:
+                c.tp_p2p_buffer(Rc, len(ctxs))
+            for k, c in enumerate(ctxs):
+                c.tp_p2p_connect_local(ctxs, k)
 
     @property
     def launch_count(self):
@@ -244,11 +252,18 @@ def run_step_sharded(sh, d, dlog, ev=None):
         if ev is not None:
             s0 = torch.cuda.Event(enable_timing=True)
             s0.record()
-        for k, (c, (v0, w)) in enumerate(zip(sh.ctxs, sh.shards)):
-            c.loss_fwd_partial(buf[:e - b, v0:v0 + w], d["tokens"][b:e], d["old"][b:e], None,
-                               row_begin=b, partial=sh.part[k, :e - b])
-        for c in sh.ctxs:
-            c.loss_fwd_combine(sh.part[:, :e - b], row_begin=b)
+        if sh.p2p:     # fused: each sweep stores its partials into every rank's buffer
+            for c, (v0, w) in zip(sh.ctxs, sh.shards):
+                c.loss_fwd_p2p_send(buf[:e - b, v0:v0 + w], d["tokens"][b:e], d["old"][b:e],
+                                    None, row_begin=b)
+            for c in sh.ctxs:
+                c.loss_fwd_p2p_recv(b, e - b)
+        else:
+            for k, (c, (v0, w)) in enumerate(zip(sh.ctxs, sh.shards)):
+                c.loss_fwd_partial(buf[:e - b, v0:v0 + w], d["tokens"][b:e], d["old"][b:e], None,
+                                   row_begin=b, partial=sh.part[k, :e - b])
+            for c in sh.ctxs:
+                c.loss_fwd_combine(sh.part[:, :e - b], row_begin=b)
         if ev is not None:
             s1 = torch.cuda.Event(enable_timing=True)
             s1.record()
@@ -434,7 +449,7 @@ def main_ours(args):
         for c in ctxs:
             c.set_option(OPT_FWD_IMPL, args.fwd_impl)
             c.set_option(OPT_BWD_IMPL, args.bwd_impl)
-        ctx = ShardedStep(ctxs, shards, d["Rc"], dev)
+        ctx = ShardedStep(ctxs, shards, d["Rc"], dev, p2p=args.tp_p2p)
         step_fn = run_step_sharded
     else:
         ctx = Espo(w.V, logits_dtype=torch.bfloat16, device=local, rank=rank, world=world, **kw)
@@ -533,7 +548,8 @@ def main_ours(args):
                         f"vocab {V}, bf16 logits/grads" + (", compact dlogits" if args.compact else "")
                         + (", RL-ZVP advantages for zero-variance groups" if args.zv_mode == "rlzvp" else "")
                         + (f", {S_} vocabulary shards back to back on one GPU (TP emulation, "
-                           "partials gathered by device copy)" if S_ > 1 else "")
+                           + ("partials exchanged by the fused peer-memory path)" if args.tp_p2p
+                              else "partials gathered by device copy)") if S_ > 1 else "")
                         + (", single-pass (espo_loss_fwd_bwd per chunk of whole rollouts)" if args.single_pass else ""),
             "global_batch_tokens": T * world, "seq_len": w.L, "parallelism": f"dp{world} (prompt-group sharded)",
             "chunk_rows": d["Rc"], "l2": "inputs larger than L2 (chunk buffer "

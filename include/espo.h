@@ -74,7 +74,8 @@ typedef enum {
   ESPO_ERR_CUDA = 8,
   ESPO_ERR_NCCL = 9,
   ESPO_ERR_UNSUPPORTED = 10,
-  ESPO_ERR_BLAS = 11                 /* libcublas missing or a cuBLAS call failed */
+  ESPO_ERR_BLAS = 11,                /* libcublas missing or a cuBLAS call failed */
+  ESPO_ERR_PEER_TIMEOUT = 12         /* a TP peer never signalled its partials (peer-memory mode) */
 } espo_status;
 
 typedef enum { ESPO_F32 = 0, ESPO_BF16 = 1 } espo_dtype;
@@ -242,6 +243,39 @@ espo_status espo_loss_fwd_combine(espo_ctx_t ctx, const float* partials, int32_t
  * communicator given to espo_create. */
 espo_status espo_attach_tp(espo_ctx_t ctx, const void* tp_unique_id, int32_t tp_rank,
                            int32_t tp_world);
+
+/* ---- vocabulary-parallel partial exchange over peer memory (NVLink / NVSwitch) ----
+ * The alternative to espo_attach_tp: instead of partial sweep → ncclAllGather → combine, the
+ * forward sweep's own epilogue stores each row's 16-byte partial {R, S, W, u_y} into the
+ * exchange buffer of EVERY TP rank (peer pointers from CUDA IPC), then releases a flag per
+ * rank; the combine acquires all ranks' flags for the chunk and merges (PAPER.md:129 Megatron
+ * vocab-parallel layout). Two slots alternate between chunks; a slot is
+ * rewritten only after every rank posted that it consumed it. Waits are bounded: a missing
+ * peer gives ESPO_ERR_PEER_TIMEOUT (sticky, via espo_get_error), not a hang.
+ *
+ * espo_tp_p2p_buffer: allocates this rank's exchange buffer for chunks of ≤ max_rows rows
+ *   (4 KB flags + 2·tp_world·max_rows·16 B) and writes its cudaIpcMemHandle_t
+ *   (ESPO_IPC_HANDLE_BYTES, nullable) — the caller all-gathers the handles over its TP group.
+ * espo_tp_p2p_open: maps the peers' buffers (handles laid out [tp_world][64], own ignored).
+ * espo_tp_p2p_connect_local: same-device variant for tests and single-GPU emulation: `ranks`
+ *   are the tp_world contexts (one per shard) on this device, each with its buffer allocated.
+ * espo_loss_fwd_p2p_send / _recv: the two halves of a chunk's forward (send: wait until the
+ *   slot is free, fused sweep + stores, signal; recv: wait for all ranks, combine, post
+ *   consumed; records coverage). espo_loss_fwd on a connected context runs both. Every rank
+ *   must process the same chunks in the same order. */
+#define ESPO_IPC_HANDLE_BYTES 64
+espo_status espo_tp_p2p_buffer(espo_ctx_t ctx, int64_t max_rows, int32_t tp_world,
+                               void* ipc_handle_out);
+espo_status espo_tp_p2p_open(espo_ctx_t ctx, const void* ipc_handles, int32_t tp_rank,
+                             int32_t tp_world);
+espo_status espo_tp_p2p_connect_local(espo_ctx_t ctx, const espo_ctx_t* ranks, int32_t tp_rank,
+                                      int32_t tp_world);
+espo_status espo_loss_fwd_p2p_send(espo_ctx_t ctx, const void* logits, int64_t ld,
+                                   const int32_t* tokens, const float* old_logp,
+                                   const uint8_t* mask, int64_t row_begin, int64_t n_rows,
+                                   espo_stream_t stream);
+espo_status espo_loss_fwd_p2p_recv(espo_ctx_t ctx, int64_t row_begin, int64_t n_rows,
+                                   espo_stream_t stream);
 
 /* ---- single-pass mode: forward and backward of a chunk in one call ----
  * The loss normaliser D (N active rollouts; T_active in TOKEN mode) depends only on the

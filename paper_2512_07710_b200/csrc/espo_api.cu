@@ -7,6 +7,7 @@
 #include <cstring>
 #include <map>
 #include <new>
+#include <vector>
 
 #include "common.cuh"
 #include "k_dlogits.cuh"
@@ -16,6 +17,7 @@
 #include "k_lmhead.cuh"
 #include "k_lmhead2.cuh"
 #include "k_reward.cuh"
+#include "k_tpx.cuh"
 #include "workspace.cuh"
 
 #include <cublas_v2.h>
@@ -129,6 +131,16 @@ struct espo_ctx_s {
   size_t lmh_dz_cap = 0;
   cublasHandle_t blas = nullptr;
   void* blas_ws = nullptr;
+  // vocabulary-parallel exchange over peer memory (k_tpx.cuh)
+  void* x_buf = nullptr;              // this rank's exchange buffer
+  int64_t x_cap = 0;                  // rows per (slot, rank) block
+  int x_world = 0;                    // tp_world the buffer was sized for
+  bool tp_p2p = false;                // connected
+  int tp_rank = 0;
+  uint8_t** d_xpeer = nullptr;        // device [tp_world]: exchange bases of all ranks
+  float4** d_xgath = nullptr;         // device [tp_world]: their partial regions
+  std::vector<void*> x_opened;        // IPC-mapped peer buffers (closed at destroy)
+  uint32_t x_send_epoch = 0, x_recv_epoch = 0;
 };
 
 namespace {
@@ -304,6 +316,7 @@ const char* espo_status_string(espo_status s) {
     case ESPO_ERR_NCCL: return "ESPO_ERR_NCCL";
     case ESPO_ERR_UNSUPPORTED: return "ESPO_ERR_UNSUPPORTED";
     case ESPO_ERR_BLAS: return "ESPO_ERR_BLAS";
+    case ESPO_ERR_PEER_TIMEOUT: return "ESPO_ERR_PEER_TIMEOUT";
   }
   return "ESPO_ERR_UNKNOWN";
 }
@@ -380,6 +393,9 @@ espo_status espo_destroy(espo_ctx_t c) {
     if (c->lmh_dz) cudaFree(c->lmh_dz);
     if (c->blas) g_blas.destroy(c->blas);
     if (c->blas_ws) cudaFree(c->blas_ws);
+    for (void* q : c->x_opened) cudaIpcCloseMemHandle(q);
+    if (c->d_xpeer) cudaFree(c->d_xpeer);
+    if (c->x_buf) cudaFree(c->x_buf);
   }
   delete c;
   return ESPO_OK;
@@ -497,8 +513,12 @@ espo_status launch_combine(espo_ctx_t c, const float* partials, int n_shards, in
 // K2 (+ its row-list pre-pass) over one chunk; writes statistics, or partials if `partial`.
 espo_status launch_sweep_fwd(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
                              const float* old_logp, const uint8_t* mask, int64_t row_begin,
-                             int64_t n_rows, float* partial, cudaStream_t s) {
+                             int64_t n_rows, float* partial, cudaStream_t s,
+                             float4* const* xbase = nullptr, int nx = 0, int64_t xoff = 0) {
   FwdParams p;
+  p.xbase = xbase;
+  p.nx = nx;
+  p.xoff = xoff;
   p.logits = logits;
   p.ld = ld;
   p.tokens = tokens;
@@ -523,7 +543,7 @@ espo_status launch_sweep_fwd(espo_ctx_t c, const void* logits, int64_t ld, const
     k_fwd_rows<float><<<pre_grid, 256, 0, s>>>(logits, ld, tokens, old_logp, mask, row_begin, n_rows,
                                                V, v0, p.V, p.lam_log2e, c->ws, list, c->ws.count);
   ESPO_LAUNCHED(c);
-  if (c->fwd_impl >= 9 && partial == nullptr) {
+  if (c->fwd_impl >= 9 && partial == nullptr && nx == 0) {
     // tiled: (listed row, 32 KB tile) blocks → per-tile partials → k_fwd_combine
     const int epv = bf ? 8 : 4;
     const int ntiles = (((p.V + epv - 1) / epv) + 256 * 8 - 1) / (256 * 8);
@@ -572,13 +592,56 @@ espo_status launch_combine(espo_ctx_t c, const float* partials, int n_shards, in
   return ESPO_OK;
 }
 
+TpxParams tpx_params(espo_ctx_t c, uint32_t epoch) {
+  TpxParams x;
+  x.peer = c->d_xpeer;
+  x.local = static_cast<uint8_t*>(c->x_buf);
+  x.tp_rank = c->tp_rank;
+  x.tp_world = c->x_world;
+  x.cap = c->x_cap;
+  x.epoch = epoch;
+  x.slot = int(epoch & 1u);
+  return x;
+}
+
+// peer-memory TP, first half: slot free → fused sweep (partials stored to every rank) → signal
+espo_status p2p_send(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
+                     const float* old_logp, const uint8_t* mask, int64_t row_begin,
+                     int64_t n_rows, cudaStream_t s) {
+  const TpxParams x = tpx_params(c, ++c->x_send_epoch);
+  k_tpx_wait_consumed<<<1, 32, 0, s>>>(x, c->ws.err);
+  ESPO_LAUNCHED(c);
+  const int64_t xoff = (int64_t(x.slot) * x.tp_world + x.tp_rank) * x.cap;
+  espo_status st = launch_sweep_fwd(c, logits, ld, tokens, old_logp, mask, row_begin, n_rows,
+                                    nullptr, s, c->d_xgath, x.tp_world, xoff);
+  if (st != ESPO_OK) return st;
+  k_tpx_signal<<<1, 32 * ((x.tp_world + 31) / 32), 0, s>>>(x);
+  ESPO_LAUNCHED(c);
+  return ESPO_OK;
+}
+
+// second half: wait for every rank's partials → combine → post consumed
+espo_status p2p_recv(espo_ctx_t c, int64_t row_begin, int64_t n_rows, cudaStream_t s) {
+  const TpxParams x = tpx_params(c, ++c->x_recv_epoch);
+  const int grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  k_tpx_combine<<<grid, 256, 0, s>>>(x, row_begin, n_rows, c->ws);
+  ESPO_LAUNCHED(c);
+  k_tpx_post<<<1, 32 * ((x.tp_world + 31) / 32), 0, s>>>(x);
+  ESPO_LAUNCHED(c);
+  return ESPO_OK;
+}
+
 // Forward of one chunk (arguments and coverage already checked); records the coverage.
 espo_status fwd_chunk(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
                       const float* old_logp, const uint8_t* mask, int64_t row_begin,
                       int64_t n_rows, cudaStream_t s) {
   espo_status st;
   const bool sharded = c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab;
-  if (sharded) {
+  if (sharded && c->tp_p2p) {
+    if (n_rows > c->x_cap) return ESPO_ERR_INVALID_ARGUMENT;
+    if ((st = p2p_send(c, logits, ld, tokens, old_logp, mask, row_begin, n_rows, s)) != ESPO_OK) return st;
+    if ((st = p2p_recv(c, row_begin, n_rows, s)) != ESPO_OK) return st;
+  } else if (sharded) {
     // vocabulary-parallel: partial → all-gather over the TP group → combine
     float* part = c->ws.partial;
     float* gath = c->ws.gathered;
@@ -628,7 +691,7 @@ espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const in
   espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
   if (st != ESPO_OK || n_rows == 0) return st;
   const bool sharded = c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab;
-  if (sharded && !c->tp_comm) return ESPO_ERR_BAD_STATE;  // use partial + combine
+  if (sharded && !c->tp_comm && !c->tp_p2p) return ESPO_ERR_BAD_STATE;  // use partial + combine
   if (c->single_pass) return ESPO_ERR_BAD_STATE;           // use espo_loss_fwd_bwd
   if ((st = check_coverage(c, row_begin, row_begin + n_rows)) != ESPO_OK) return st;
   DevGuard g(c->device);
@@ -928,6 +991,114 @@ espo_status espo_attach_tp(espo_ctx_t c, const void* tp_unique_id, int32_t tp_ra
   return ESPO_OK;
 }
 
+espo_status espo_tp_p2p_buffer(espo_ctx_t c, int64_t max_rows, int32_t tp_world,
+                               void* ipc_handle_out) {
+  if (!c || max_rows < 1 || max_rows > INT32_MAX || tp_world < 1 || tp_world > 1024)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->cfg.vocab_local <= 0 || c->tp_p2p || c->x_buf) return ESPO_ERR_BAD_STATE;
+  DevGuard g(c->device);
+  const size_t bytes = kTpxFlagBytes + size_t(2) * tp_world * size_t(max_rows) * 16;
+  ESPO_CUDA(cudaMalloc(&c->x_buf, bytes));
+  ESPO_CUDA(cudaMemset(c->x_buf, 0, bytes));
+  c->x_cap = max_rows;
+  c->x_world = tp_world;
+  if (ipc_handle_out) {
+    cudaIpcMemHandle_t h;
+    ESPO_CUDA(cudaIpcGetMemHandle(&h, c->x_buf));
+    std::memcpy(ipc_handle_out, &h, sizeof(h));
+  }
+  return ESPO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+espo_status tpx_finish_connect(espo_ctx_t c, const std::vector<uint8_t*>& bases, int32_t tp_rank) {
+  const int w = int(bases.size());
+  std::vector<void*> host(2 * w);
+  for (int k = 0; k < w; ++k) {
+    host[k] = bases[k];
+    host[w + k] = bases[k] + kTpxFlagBytes;
+  }
+  ESPO_CUDA(cudaMalloc(&c->d_xpeer, host.size() * sizeof(void*)));
+  ESPO_CUDA(cudaMemcpy(c->d_xpeer, host.data(), host.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  c->d_xgath = reinterpret_cast<float4**>(c->d_xpeer + w);
+  c->tp_rank = tp_rank;
+  c->tp_p2p = true;
+  c->x_send_epoch = c->x_recv_epoch = 0;
+  return ESPO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+espo_status espo_tp_p2p_open(espo_ctx_t c, const void* ipc_handles, int32_t tp_rank,
+                             int32_t tp_world) {
+  if (!c || !ipc_handles || tp_rank < 0 || tp_rank >= tp_world) return ESPO_ERR_INVALID_ARGUMENT;
+  if (!c->x_buf || c->x_world != tp_world || c->tp_p2p) return ESPO_ERR_BAD_STATE;
+  DevGuard g(c->device);
+  std::vector<uint8_t*> bases(tp_world);
+  for (int k = 0; k < tp_world; ++k) {
+    if (k == tp_rank) {
+      bases[k] = static_cast<uint8_t*>(c->x_buf);
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(ipc_handles) + size_t(k) * ESPO_IPC_HANDLE_BYTES, sizeof(h));
+    void* q = nullptr;
+    ESPO_CUDA(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+    c->x_opened.push_back(q);
+    bases[k] = static_cast<uint8_t*>(q);
+  }
+  return tpx_finish_connect(c, bases, tp_rank);
+}
+
+espo_status espo_tp_p2p_connect_local(espo_ctx_t c, const espo_ctx_t* ranks, int32_t tp_rank,
+                                      int32_t tp_world) {
+  if (!c || !ranks || tp_rank < 0 || tp_rank >= tp_world || ranks[tp_rank] != c)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (!c->x_buf || c->x_world != tp_world || c->tp_p2p) return ESPO_ERR_BAD_STATE;
+  std::vector<uint8_t*> bases(tp_world);
+  for (int k = 0; k < tp_world; ++k) {
+    if (!ranks[k] || !ranks[k]->x_buf || ranks[k]->device != c->device ||
+        ranks[k]->x_cap != c->x_cap || ranks[k]->x_world != tp_world)
+      return ESPO_ERR_INVALID_ARGUMENT;
+    bases[k] = static_cast<uint8_t*>(ranks[k]->x_buf);
+  }
+  DevGuard g(c->device);
+  return tpx_finish_connect(c, bases, tp_rank);
+}
+
+espo_status espo_loss_fwd_p2p_send(espo_ctx_t c, const void* logits, int64_t ld,
+                                   const int32_t* tokens, const float* old_logp,
+                                   const uint8_t* mask, int64_t row_begin, int64_t n_rows,
+                                   espo_stream_t stream) {
+  espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
+  if (st != ESPO_OK || n_rows == 0) return st;
+  if (!c->tp_p2p || c->single_pass) return ESPO_ERR_BAD_STATE;
+  if (n_rows > c->x_cap) return ESPO_ERR_INVALID_ARGUMENT;
+  if ((st = check_coverage(c, row_begin, row_begin + n_rows)) != ESPO_OK) return st;
+  DevGuard g(c->device);
+  return p2p_send(c, logits, ld, tokens, old_logp, mask, row_begin, n_rows, S(stream));
+}
+
+espo_status espo_loss_fwd_p2p_recv(espo_ctx_t c, int64_t row_begin, int64_t n_rows,
+                                   espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Prepared || !c->tp_p2p || c->single_pass) return ESPO_ERR_BAD_STATE;
+  if (n_rows < 0 || n_rows > c->x_cap || row_begin < 0 || row_begin + n_rows > c->T)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rows == 0) return ESPO_OK;
+  espo_status st = check_coverage(c, row_begin, row_begin + n_rows);
+  if (st != ESPO_OK) return st;
+  if (c->x_recv_epoch >= c->x_send_epoch) return ESPO_ERR_BAD_STATE;   // recv before its send
+  DevGuard g(c->device);
+  if ((st = p2p_recv(c, row_begin, n_rows, S(stream))) != ESPO_OK) return st;
+  c->covered[row_begin] = row_begin + n_rows;
+  c->n_covered += n_rows;
+  return ESPO_OK;
+}
+
 espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_dev,
                                espo_stream_t stream) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
@@ -1117,7 +1288,7 @@ espo_status espo_loss_fwd_bwd(espo_ctx_t c, const void* logits, int64_t ld, cons
   if (!c->single_pass) return ESPO_ERR_BAD_STATE;
   if (n_rows == 0) return ESPO_OK;
   const bool sharded = c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab;
-  if (sharded && !c->tp_comm) return ESPO_ERR_BAD_STATE;
+  if (sharded && !c->tp_comm && !c->tp_p2p) return ESPO_ERR_BAD_STATE;
   if ((st = check_bwd_args(c, logits, ld, dlogits, ldg)) != ESPO_OK) return st;
   if ((st = check_coverage(c, row_begin, row_begin + n_rows)) != ESPO_OK) return st;
   DevGuard g(c->device);

@@ -26,6 +26,11 @@ struct FwdParams {
   int V;                // columns of a logits row held here (the shard width if sharded)
   float lam_log2e;      // λ·log2(e)
   float* partial;       // vocabulary-parallel: per-row {R, S, W, u_y} instead of statistics
+  // vocabulary-parallel over peer memory: the partial of chunk row r goes straight to
+  // xbase[k][xoff + r] for every TP rank k (NVLink stores into the peers' exchange buffers)
+  float4* const* xbase = nullptr;
+  int nx = 0;
+  int64_t xoff = 0;
   Workspace ws;
 };
 
@@ -114,7 +119,8 @@ __device__ __forceinline__ void rebase(float r, float R, float& S, float& W) {
 // statistics — or, for a vocabulary shard, the row's partial {R, S, W, u_y}.
 __device__ __forceinline__ void row_finish(float r, float S, float W, float uy, const Workspace& ws,
                                            int64_t t, int lane, float* partial = nullptr,
-                                           int64_t pr = 0) {
+                                           int64_t pr = 0, float4* const* xbase = nullptr,
+                                           int nx = 0, int64_t xoff = 0) {
   const float R = warp_max(r);
   if (R == -INFINITY) {
     S = 0.f;
@@ -125,7 +131,10 @@ __device__ __forceinline__ void row_finish(float r, float S, float W, float uy, 
   S = warp_sum(S);
   W = warp_sum(W);
   if (lane == 0) {
-    if (partial) {
+    if (nx > 0) {            // fused exchange: the partial goes to every TP rank's buffer
+      const float4 v = make_float4(R, S, W, uy);
+      for (int k = 0; k < nx; ++k) xbase[k][xoff + pr] = v;
+    } else if (partial) {
       reinterpret_cast<float4*>(partial)[pr] = make_float4(R, S, W, uy);
     } else {
       finish_stats(R, S, W, uy, ws, t);
@@ -335,8 +344,12 @@ __global__ void __launch_bounds__(256) k_rowstats_ldg(const FwdParams p, const F
       kahan_add(S, cS, bS);
       kahan_add(W, cW, bW);
     }
-    row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane, p.partial, rec.r);
+    row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane, p.partial, rec.r,
+               p.xbase, p.nx, p.xoff);
   }
+  // peer-memory exchange: lane 0 issued this warp's partial stores; one system-scope fence
+  // orders them before k_tpx_signal's release of the ready flags
+  if (p.nx > 0 && lane == 0) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -469,8 +482,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
         kahan_add(W, cW, bW);
       }
     }
-    row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane, p.partial, rec.r);
+    row_finish(ref, S - cS, W - cW, rec.uy, p.ws, p.row_begin + rec.r, lane, p.partial, rec.r,
+               p.xbase, p.nx, p.xoff);
   }
+  // peer-memory exchange: lane 0 issued this warp's partial stores; one system-scope fence
+  // orders them before k_tpx_signal's release of the ready flags
+  if (p.nx > 0 && lane == 0) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------------------

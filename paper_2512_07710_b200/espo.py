@@ -34,14 +34,15 @@ STATUS = {
     5: "ESPO_ERR_NONFINITE_INPUT", 6: "ESPO_ERR_TOKEN_OUT_OF_RANGE",
     7: "ESPO_ERR_OUT_OF_MEMORY", 8: "ESPO_ERR_CUDA", 9: "ESPO_ERR_NCCL",
     10: "ESPO_ERR_UNSUPPORTED",
-    11: "ESPO_ERR_BLAS",
+    11: "ESPO_ERR_BLAS", 12: "ESPO_ERR_PEER_TIMEOUT",
 }
 EXPORTED_SYMBOLS = [
     "espo_config_default", "espo_get_unique_id", "espo_create", "espo_destroy", "espo_prepare",
     "espo_loss_fwd", "espo_loss_finalize", "espo_loss_bwd", "espo_get_error",
     "espo_status_string", "espo_export_token_stats", "espo_export_rollout_stats",
     "espo_launch_count", "espo_set_option", "espo_loss_fwd_partial", "espo_loss_fwd_combine",
-    "espo_attach_tp", "espo_lmhead_fwd", "espo_lmhead_bwd", "espo_set_mask", "espo_loss_fwd_bwd", "espo_reward_shaping_default",
+    "espo_attach_tp", "espo_lmhead_fwd", "espo_lmhead_bwd", "espo_set_mask", "espo_loss_fwd_bwd", "espo_tp_p2p_buffer", "espo_tp_p2p_open",
+    "espo_tp_p2p_connect_local", "espo_loss_fwd_p2p_send", "espo_loss_fwd_p2p_recv", "espo_reward_shaping_default",
     "espo_reshape_rewards",
 ]
 
@@ -127,6 +128,11 @@ def load_library():
         "espo_attach_tp": (I32, [P, P, I32, I32]),
         "espo_lmhead_fwd": (I32, [P, P, I64, P, I64, I32, P, P, P, I64, I64, P]),
         "espo_set_mask": (I32, [P, P, P]),
+        "espo_tp_p2p_buffer": (I32, [P, I64, I32, P]),
+        "espo_tp_p2p_open": (I32, [P, P, I32, I32]),
+        "espo_tp_p2p_connect_local": (I32, [P, P, I32, I32]),
+        "espo_loss_fwd_p2p_send": (I32, [P, P, I64, P, P, P, I64, I64, P]),
+        "espo_loss_fwd_p2p_recv": (I32, [P, I64, I64, P]),
         "espo_loss_fwd_bwd": (I32, [P, P, I64, P, P, P, I64, P, I64, I64, P]),
         "espo_lmhead_bwd": (I32, [P, P, I64, P, I64, I32, P, I64, I32, P, I64, P, I64, I64, P]),
         "espo_reward_shaping_default": (None, [ctypes.POINTER(RewardShaping), I32]),
@@ -261,6 +267,36 @@ class Espo:
                                        _ptr(tokens), _ptr(old_logp), _ptr(mask), int(row_begin),
                                        n, 0, self._stream()), "espo_loss_fwd")
 
+    # -- vocabulary-parallel exchange over peer memory -----------------------------------
+    def tp_p2p_buffer(self, max_rows: int, tp_world: int) -> bytes:
+        """espo_tp_p2p_buffer: allocate this rank's exchange buffer; returns its IPC handle."""
+        h = ctypes.create_string_buffer(64)
+        _check(self._lib.espo_tp_p2p_buffer(self._h, int(max_rows), int(tp_world), h),
+               "espo_tp_p2p_buffer")
+        return h.raw
+
+    def tp_p2p_open(self, handles: bytes, tp_rank: int, tp_world: int):
+        """espo_tp_p2p_open: map the peers' buffers (handles concatenated in TP-rank order)."""
+        buf = ctypes.create_string_buffer(bytes(handles), len(handles))
+        _check(self._lib.espo_tp_p2p_open(self._h, buf, int(tp_rank), int(tp_world)),
+               "espo_tp_p2p_open")
+
+    def tp_p2p_connect_local(self, ranks, tp_rank: int):
+        """espo_tp_p2p_connect_local: same-device TP group (tests / emulation)."""
+        arr = (ctypes.c_void_p * len(ranks))(*[r._h.value for r in ranks])
+        _check(self._lib.espo_tp_p2p_connect_local(self._h, arr, int(tp_rank), len(ranks)),
+               "espo_tp_p2p_connect_local")
+
+    def loss_fwd_p2p_send(self, logits, tokens, old_logp, mask=None, row_begin=0):
+        _check(self._lib.espo_loss_fwd_p2p_send(self._h, _ptr(logits), int(logits.stride(0)),
+                                                _ptr(tokens), _ptr(old_logp), _ptr(mask),
+                                                int(row_begin), int(logits.shape[0]),
+                                                self._stream()), "espo_loss_fwd_p2p_send")
+
+    def loss_fwd_p2p_recv(self, row_begin, n_rows):
+        _check(self._lib.espo_loss_fwd_p2p_recv(self._h, int(row_begin), int(n_rows),
+                                                self._stream()), "espo_loss_fwd_p2p_recv")
+
     def set_mask(self, mask=None):
         """espo_set_mask: single-pass mode; D counted from the batch mask u8[T] (None = ones)."""
         _check(self._lib.espo_set_mask(self._h, _ptr(mask), self._stream()), "espo_set_mask")
@@ -390,6 +426,16 @@ class Espo:
             self._stream()), "espo_export_rollout_stats")
         out["theta"] = out["theta"].view(R, ESPO_MAX_BUCKETS - 1)
         return out
+
+
+def attach_tp_p2p(ctx: "Espo", max_rows: int, tp_rank: int, tp_world: int, group=None):
+    """Connects a vocabulary-sharded context to its TP group over peer memory: allocate the
+    exchange buffer, all-gather the IPC handles over `group` (torch.distributed), map them."""
+    import torch.distributed as dist
+    h = ctx.tp_p2p_buffer(max_rows, tp_world)
+    handles = [None] * tp_world
+    dist.all_gather_object(handles, h, group=group)
+    ctx.tp_p2p_open(b"".join(handles), tp_rank, tp_world)
 
 
 def espo_loss(ctx: Espo, logits, tokens, old_logp, rewards, group_ids, seq_offsets, mask=None,

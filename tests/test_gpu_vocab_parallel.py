@@ -104,3 +104,99 @@ def test_sharded_context_requires_partial_path():
         ctx.loss_fwd(z, to_dev(inst.tokens, torch.int32, dev), to_dev(inst.old_logp, torch.float32, dev))
     assert e.value.code == "ESPO_ERR_BAD_STATE"
     ctx.close()
+
+
+def run_p2p(inst, dev, shards, chunks, logits_dtype=torch.float32, cfgkw=None, single_pass=False):
+    """Peer-memory TP on one device: one context per shard connected with
+    espo_tp_p2p_connect_local; per chunk every rank sends (fused sweep stores its partials into
+    every rank's exchange buffer, then signals) before any rank receives (waits, combines) —
+    so no kernel waits on a kernel launched after it."""
+    from paper_2512_07710_b200.espo import stats_to_dict
+    T = inst.T
+    align = 8 if logits_dtype == torch.bfloat16 else 4
+    zfull = to_dev(inst.logits, torch.float32, dev)
+    tok = to_dev(inst.tokens, torch.int32, dev)
+    old = to_dev(inst.old_logp, torch.float32, dev)
+    mask = to_dev(inst.mask, torch.uint8, dev)
+    args = (to_dev(inst.rewards, torch.float32, dev), to_dev(inst.group_ids, torch.int32, dev),
+            to_dev(inst.seq_offsets, torch.int64, dev))
+    ctxs, zs = [], []
+    max_rows = max(e - b for b, e in chunks)
+    for v0, w in shards:
+        ctx = Espo(inst.V, logits_dtype=logits_dtype, device=dev.index, vocab_shard=(v0, w),
+                   **(cfgkw or {}))
+        ctx.tp_p2p_buffer(max_rows, len(shards))
+        ld = (w + align - 1) // align * align
+        z = torch.zeros((T, ld), dtype=logits_dtype, device=dev)
+        z[:, :w] = zfull[:, v0:v0 + w].to(logits_dtype)
+        ctxs.append(ctx)
+        zs.append(z)
+    for k, c in enumerate(ctxs):
+        c.tp_p2p_connect_local(ctxs, k)
+    for step in range(2):                        # two steps: epochs keep running across them
+        for c in ctxs:
+            c.prepare(*args, n_tokens=T)
+        for b, e in chunks:
+            for c, z in zip(ctxs, zs):
+                c.loss_fwd_p2p_send(z[b:e], tok[b:e], old[b:e], mask[b:e], row_begin=b)
+            for c in ctxs:
+                c.loss_fwd_p2p_recv(b, e - b)
+        out = []
+        for (v0, w), c, z in zip(shards, ctxs, zs):
+            loss, stats = c.loss_finalize()
+            dz = c.loss_bwd(z)
+            c.get_error()
+            out.append((float(loss.item()), stats_to_dict(stats), dz[:, :w].float().cpu().numpy()))
+    tokst = {k: v.cpu().numpy() for k, v in ctxs[0].export_token_stats().items()}
+    rol = {k: v.cpu().numpy() for k, v in ctxs[0].export_rollout_stats().items()}
+    for c in ctxs:
+        c.close()
+    return dict(loss=out[0][0], stats=out[0][1], losses=[o[0] for o in out],
+                dlogits=np.concatenate([o[2] for o in out], axis=1), tok=tokst, rol=rol,
+                zv_out=rol["zv"])
+
+
+def test_vocab_parallel_peer_memory_exchange():
+    """Fused exchange over peer memory ≡ the device-copy all-gather path, bitwise (the same
+    partials are merged in the same order), and ≡ the oracle at fp32 tolerances; chunks split
+    sequences, arrive out of order, and reuse both exchange slots over two steps."""
+    dev = require_cuda()
+    inst = workload_instance("C0")
+    shards = [(0, 300), (300, 400), (700, 324)]
+    chunks = [(700, inst.T), (0, 130), (130, 700)]
+    g = run_p2p(inst, dev, shards, chunks)
+    ref_path = run_sharded(inst, dev, shards)
+    assert len(set(g["losses"])) == 1
+    assert g["loss"] == ref_path["loss"]
+    assert np.array_equal(g["dlogits"], ref_path["dlogits"])
+    cfg = oracle_cfg(inst.V)
+    ref = inst.run(cfg)
+    check_exact_fields(g, ref)
+    check_token_stats(g, ref)
+    ref2, _ = decision_aware_reference(g, inst, ref, cfg)
+    check_loss(g, ref2, 1e-5)
+    check_dlogits_f32(g["dlogits"], oracle_dlogits(ref2, inst, cfg, np.arange(inst.T)))
+
+
+def test_peer_memory_recv_without_peer_times_out():
+    """A rank whose peer never sends reports ESPO_ERR_PEER_TIMEOUT instead of hanging."""
+    from paper_2512_07710_b200.espo import EspoError
+    dev = require_cuda()
+    inst = tiny_instance(19, V=256, group_sizes=(2,), L=4)
+    ctxs = [Espo(256, logits_dtype=torch.float32, device=dev.index, vocab_shard=(128 * k, 128))
+            for k in range(2)]
+    for c in ctxs:
+        c.tp_p2p_buffer(16, 2)
+    for k, c in enumerate(ctxs):
+        c.tp_p2p_connect_local(ctxs, k)
+    z = torch.zeros((inst.T, 128), dtype=torch.float32, device=dev)
+    c = ctxs[0]
+    c.prepare(to_dev(inst.rewards, torch.float32, dev), to_dev(inst.group_ids, torch.int32, dev),
+              to_dev(inst.seq_offsets, torch.int64, dev), n_tokens=inst.T)
+    c.loss_fwd_p2p_send(z, to_dev(inst.tokens, torch.int32, dev), to_dev(inst.old_logp, torch.float32, dev))
+    c.loss_fwd_p2p_recv(0, inst.T)               # rank 1 never sends
+    with pytest.raises(EspoError) as e:
+        c.get_error()
+    assert e.value.code == "ESPO_ERR_PEER_TIMEOUT"
+    for x in ctxs:
+        x.close()
