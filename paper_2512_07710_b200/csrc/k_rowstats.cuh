@@ -216,6 +216,27 @@ __device__ __forceinline__ void batch_slow(const uint4* v, int j0, int nvec, int
   }
 }
 
+// Special batch (holds the target vector, the ragged vocabulary end or vectors past the row
+// end): one pass with the target / out-of-range elements set to −inf and the SAFE form
+// (t clamped at −127: −inf contributes exactly 0 under ftz), relative to the current
+// reference. The caller falls back to batch_slow if the sums overflow or carry NaN/+inf.
+template <typename Tin, int U, int STRIDE = 32>
+__device__ __forceinline__ void batch_safe(const uint4* v, int j0, int nvec, int vy, int yoff,
+                                           int V, float lamL, float r, float& bS, float& bW) {
+  constexpr int EPV = Vec<Tin>::EPV;
+  bS = 0.f;
+  bW = 0.f;
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const int j = j0 + STRIDE * k;
+    if (j >= nvec) continue;
+    float x[EPV];
+    Vec<Tin>::unpack(v[k], x);
+    fix_special<EPV>(x, j, vy, yoff, V);
+    acc_vec<EPV, true>(x, lamL, -r, bS, bW);
+  }
+}
+
 // Fast path: U vectors into the batch sums with no per-vector checks. The batch that
 // holds the target element or the ragged end of the row (at most two per lane and row)
 // is routed to batch_slow instead (see `special`).
@@ -471,8 +492,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
         }
         const int j0 = c * VPC + h * 32 * SUB + lane;
         float bS, bW;
-        acc_batch<Tin, SUB>(v, lamL, -ref, bS, bW);
-        if (special_batch<SUB>(j0, vy, jrag) || !(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {
+        if (special_batch<SUB>(j0, vy, jrag) || j0 + 32 * (SUB - 1) >= nvec)
+          batch_safe<Tin, SUB>(v, j0, nvec, vy, yoff, p.V, lamL, ref, bS, bW);
+        else
+          acc_batch<Tin, SUB, NPOLY>(v, lamL, -ref, bS, bW);
+        if (!(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {
           S -= cS;
           W -= cW;
           cS = cW = 0.f;
