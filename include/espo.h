@@ -277,6 +277,25 @@ espo_status espo_loss_fwd_p2p_send(espo_ctx_t ctx, const void* logits, int64_t l
 espo_status espo_loss_fwd_p2p_recv(espo_ctx_t ctx, int64_t row_begin, int64_t n_rows,
                                    espo_stream_t stream);
 
+/* ---- context parallelism (long-CoT rollouts split across ranks by token blocks) ----
+ * SURVEY §8(f) row 3's sibling: CP rank k owns the packed token rows [k·Tb, min(T,(k+1)·Tb)),
+ * Tb = ⌈T / cp_world⌉ (sequences are cut anywhere). Each rank sweeps only its rows (fwd and
+ * bwd calls outside the block → ESPO_ERR_INVALID_ARGUMENT). At espo_loss_finalize the per-token
+ * values the per-rollout reduction reads — lp, H, old_logp (f32) and the valid flag (u8):
+ * 13 B/token, negligible next to the 2V-byte logits rows — are all-gathered in place over the
+ * CP communicator, and every CP rank runs the same per-rollout partition / Eq. 2 / Eq. 3 /
+ * surrogate (the entropy split needs all of a rollout's entropies), so each rank holds the
+ * coefficients of its own rows and the same loss. Combine with DP through espo_create's
+ * communicator (the DP group spans different data; the CP ranks of one group hold the same
+ * rollouts). Not with single-pass mode.
+ * espo_attach_cp: right after espo_create; cp_unique_id = NCCL id of the CP group, or NULL for
+ *   same-device emulation, where espo_cp_gather_local must run (after every rank's forward)
+ *   in place of the all-gather: it copies the other ranks' blocks from their contexts. */
+espo_status espo_attach_cp(espo_ctx_t ctx, const void* cp_unique_id, int32_t cp_rank,
+                           int32_t cp_world);
+espo_status espo_cp_gather_local(espo_ctx_t ctx, const espo_ctx_t* ranks, int32_t cp_world,
+                                 espo_stream_t stream);
+
 /* ---- single-pass mode: forward and backward of a chunk in one call ----
  * The loss normaliser D (N active rollouts; T_active in TOKEN mode) depends only on the
  * zero-variance filter and the mask (readings Q10, Q11), and every other

@@ -38,6 +38,7 @@ typedef int (*fn_destroy)(nccl_comm);
 typedef int (*fn_allgather)(const void*, void*, size_t, int, nccl_comm, cudaStream_t);
 constexpr int kNcclFloat64 = 8;  // ncclFloat64
 constexpr int kNcclFloat32 = 7;  // ncclFloat32
+constexpr int kNcclUint8 = 1;    // ncclUint8
 constexpr int kNcclSum = 0;      // ncclSum
 
 struct NcclApi {
@@ -141,6 +142,10 @@ struct espo_ctx_s {
   float4** d_xgath = nullptr;         // device [tp_world]: their partial regions
   std::vector<void*> x_opened;        // IPC-mapped peer buffers (closed at destroy)
   uint32_t x_send_epoch = 0, x_recv_epoch = 0;
+  // context parallelism (rollouts split across CP ranks by token blocks)
+  int cp_rank = 0, cp_world = 1;
+  nccl_comm cp_comm = nullptr;        // nullptr with cp_world > 1: same-device emulation
+  bool cp_gathered = false;           // espo_cp_gather_local ran for this step
 };
 
 namespace {
@@ -385,6 +390,7 @@ espo_status espo_destroy(espo_ctx_t c) {
     cudaDeviceSynchronize();
     if (c->comm) g_nccl.destroy(c->comm);
     if (c->tp_comm) g_nccl.destroy(c->tp_comm);
+    if (c->cp_comm) g_nccl.destroy(c->cp_comm);
     if (c->blocks_tok) cudaFree(c->blocks_tok);
     if (c->blocks_roll) cudaFree(c->blocks_roll);
     if (c->blocks_scalar) cudaFree(c->blocks_scalar);
@@ -441,7 +447,9 @@ espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* grou
   if (n_rollouts < 0 || n_tokens < 0 || n_tokens > (int64_t(1) << 40))
     return ESPO_ERR_INVALID_ARGUMENT;
   DevGuard g(c->device);
-  espo_status st = ensure_workspace(c, n_rollouts, n_tokens);
+  // CP: the per-token arrays hold cp_world equal blocks (in-place all-gather at finalize)
+  const int64_t tb = (n_tokens + c->cp_world - 1) / c->cp_world;
+  espo_status st = ensure_workspace(c, n_rollouts, std::max<int64_t>(n_tokens, tb * c->cp_world));
   if (st != ESPO_OK) return st;
   cudaStream_t s = S(stream);
   ESPO_CUDA(cudaMemsetAsync(c->ws.err, 0, sizeof(int), s));
@@ -450,6 +458,7 @@ espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* grou
   c->covered.clear();
   c->n_covered = 0;
   c->single_pass = false;
+  c->cp_gathered = false;
   PrepParams p;
   p.rewards = rewards;
   p.group_ids = group_ids;
@@ -497,7 +506,13 @@ espo_status check_fwd_args(espo_ctx_t c, const void* logits, int64_t ld, const i
   return ESPO_OK;
 }
 
+// context parallelism: CP rank k owns token rows [k·Tb, min(T, (k+1)·Tb)), Tb = ⌈T / cp⌉
+inline int64_t cp_block(const espo_ctx_s* c) { return (c->T + c->cp_world - 1) / c->cp_world; }
+inline int64_t cp_lo(const espo_ctx_s* c) { return std::min(c->T, c->cp_rank * cp_block(c)); }
+inline int64_t cp_hi(const espo_ctx_s* c) { return std::min(c->T, (c->cp_rank + 1) * cp_block(c)); }
+
 espo_status check_coverage(espo_ctx_t c, int64_t b, int64_t e) {
+  if (c->cp_world > 1 && (b < cp_lo(c) || e > cp_hi(c))) return ESPO_ERR_INVALID_ARGUMENT;
   auto it = c->covered.upper_bound(b);
   if (it != c->covered.begin()) {
     auto pv = std::prev(it);
@@ -842,6 +857,8 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       (dweight && (!aligned16(dweight) || (lddw * 4) % 16)))
     return ESPO_ERR_ALIGNMENT;
   if (c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab) return ESPO_ERR_UNSUPPORTED;
+  if (c->cp_world > 1 && (row_begin < cp_lo(c) || row_begin + n_rows > cp_hi(c)))
+    return ESPO_ERR_INVALID_ARGUMENT;
   DevGuard g(c->device);
   cudaStream_t s = S(stream);
   const int V = c->cfg.vocab;
@@ -1099,13 +1116,69 @@ espo_status espo_loss_fwd_p2p_recv(espo_ctx_t c, int64_t row_begin, int64_t n_ro
   return ESPO_OK;
 }
 
+espo_status espo_attach_cp(espo_ctx_t c, const void* cp_unique_id, int32_t cp_rank,
+                           int32_t cp_world) {
+  if (!c || cp_world < 1 || cp_rank < 0 || cp_rank >= cp_world) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->cp_world > 1 || c->state != State::Created) return ESPO_ERR_BAD_STATE;
+  if (cp_world > 1 && cp_unique_id) {
+    if (!g_nccl.load()) return ESPO_ERR_NCCL;
+    DevGuard g(c->device);
+    nccl_uid id;
+    std::memcpy(&id, cp_unique_id, sizeof(id));
+    if (g_nccl.init_rank(&c->cp_comm, cp_world, id, cp_rank) != 0) {
+      c->cp_comm = nullptr;
+      return ESPO_ERR_NCCL;
+    }
+  }
+  c->cp_rank = cp_rank;
+  c->cp_world = cp_world;
+  return ESPO_OK;
+}
+
+espo_status espo_cp_gather_local(espo_ctx_t c, const espo_ctx_t* ranks, int32_t cp_world,
+                                 espo_stream_t stream) {
+  if (!c || !ranks || cp_world != c->cp_world || cp_world < 2 || ranks[c->cp_rank] != c)
+    return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->cp_comm || c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
+  for (int k = 0; k < cp_world; ++k)
+    if (!ranks[k] || ranks[k]->device != c->device || ranks[k]->T != c->T ||
+        ranks[k]->cp_rank != k || ranks[k]->state != State::Prepared)
+      return ESPO_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  const int64_t tb = cp_block(c);
+  for (int k = 0; k < cp_world; ++k) {
+    if (k == c->cp_rank) continue;
+    const int64_t lo = std::min(c->T, k * tb), n = std::min(c->T, (k + 1) * tb) - lo;
+    if (n <= 0) continue;
+    const Workspace& w = ranks[k]->ws;
+    ESPO_CUDA(cudaMemcpyAsync(c->ws.lp + lo, w.lp + lo, n * 4, cudaMemcpyDeviceToDevice, s));
+    ESPO_CUDA(cudaMemcpyAsync(c->ws.H + lo, w.H + lo, n * 4, cudaMemcpyDeviceToDevice, s));
+    ESPO_CUDA(cudaMemcpyAsync(c->ws.old + lo, w.old + lo, n * 4, cudaMemcpyDeviceToDevice, s));
+    ESPO_CUDA(cudaMemcpyAsync(c->ws.flag + lo, w.flag + lo, n, cudaMemcpyDeviceToDevice, s));
+  }
+  c->cp_gathered = true;
+  return ESPO_OK;
+}
+
 espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_dev,
                                espo_stream_t stream) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
-  if (c->state != State::Prepared || c->n_covered != c->T) return ESPO_ERR_BAD_STATE;
+  const int64_t need = c->cp_world > 1 ? cp_hi(c) - cp_lo(c) : c->T;
+  if (c->state != State::Prepared || c->n_covered != need) return ESPO_ERR_BAD_STATE;
+  if (c->cp_world > 1 && !c->cp_comm && !c->cp_gathered) return ESPO_ERR_BAD_STATE;
   DevGuard g(c->device);
   cudaStream_t s = S(stream);
   const espo_config& cf = c->cfg;
+  if (c->cp_world > 1 && c->cp_comm && c->T > 0) {
+    // context parallelism: in-place all-gather of the per-token values K3 reads (13 B/token)
+    const size_t tb = size_t(cp_block(c)), off = size_t(c->cp_rank) * tb;
+    float* f32s[3] = {c->ws.lp, c->ws.H, c->ws.old};
+    for (float* f : f32s)
+      if (g_nccl.allgather(f + off, f, tb, kNcclFloat32, c->cp_comm, s) != 0) return ESPO_ERR_NCCL;
+    if (g_nccl.allgather(c->ws.flag + off, c->ws.flag, tb, kNcclUint8, c->cp_comm, s) != 0)
+      return ESPO_ERR_NCCL;
+  }
   if (c->R > 0) {
     if (!c->single_pass || c->T == 0) {   // single-pass chunks ran K3 already
       k_seq_reduce<<<c->R, kSeqThreads, 0, s>>>(seq_params(c, 0, c->T));
@@ -1249,6 +1322,8 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
   if (c->state != State::Finalized || c->single_pass) return ESPO_ERR_BAD_STATE;
   if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T)
     return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->cp_world > 1 && n_rows > 0 && (row_begin < cp_lo(c) || row_begin + n_rows > cp_hi(c)))
+    return ESPO_ERR_INVALID_ARGUMENT;   // a CP rank owns only its token block
   if (n_rows == 0) return ESPO_OK;
   espo_status st = check_bwd_args(c, logits, ld, dlogits, ldg);
   if (st != ESPO_OK) return st;
@@ -1258,7 +1333,7 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
 
 espo_status espo_set_mask(espo_ctx_t c, const uint8_t* mask, espo_stream_t stream) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
-  if (c->state != State::Prepared || c->n_covered != 0) return ESPO_ERR_BAD_STATE;
+  if (c->state != State::Prepared || c->n_covered != 0 || c->cp_world > 1) return ESPO_ERR_BAD_STATE;
   DevGuard g(c->device);
   cudaStream_t s = S(stream);
   if (c->R > 0) {

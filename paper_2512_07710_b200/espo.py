@@ -42,7 +42,8 @@ EXPORTED_SYMBOLS = [
     "espo_status_string", "espo_export_token_stats", "espo_export_rollout_stats",
     "espo_launch_count", "espo_set_option", "espo_loss_fwd_partial", "espo_loss_fwd_combine",
     "espo_attach_tp", "espo_lmhead_fwd", "espo_lmhead_bwd", "espo_set_mask", "espo_loss_fwd_bwd", "espo_tp_p2p_buffer", "espo_tp_p2p_open",
-    "espo_tp_p2p_connect_local", "espo_loss_fwd_p2p_send", "espo_loss_fwd_p2p_recv", "espo_reward_shaping_default",
+    "espo_tp_p2p_connect_local", "espo_loss_fwd_p2p_send", "espo_loss_fwd_p2p_recv",
+    "espo_attach_cp", "espo_cp_gather_local", "espo_reward_shaping_default",
     "espo_reshape_rewards",
 ]
 
@@ -128,6 +129,8 @@ def load_library():
         "espo_attach_tp": (I32, [P, P, I32, I32]),
         "espo_lmhead_fwd": (I32, [P, P, I64, P, I64, I32, P, P, P, I64, I64, P]),
         "espo_set_mask": (I32, [P, P, P]),
+        "espo_attach_cp": (I32, [P, P, I32, I32]),
+        "espo_cp_gather_local": (I32, [P, P, I32, P]),
         "espo_tp_p2p_buffer": (I32, [P, I64, I32, P]),
         "espo_tp_p2p_open": (I32, [P, P, I32, I32]),
         "espo_tp_p2p_connect_local": (I32, [P, P, I32, I32]),
@@ -220,6 +223,7 @@ class Espo:
         self._h = h
         self.n_tokens = 0
         self.n_rollouts = 0
+        self.cp_rank, self.cp_world = 0, 1
         if tp_world > 1:
             tuid = ctypes.create_string_buffer(bootstrap_unique_id(tp_rank, tp_group), 128)
             _check(lib.espo_attach_tp(self._h, tuid, int(tp_rank), int(tp_world)),
@@ -266,6 +270,28 @@ class Espo:
         _check(self._lib.espo_loss_fwd(self._h, _ptr(logits), int(logits.stride(0)),
                                        _ptr(tokens), _ptr(old_logp), _ptr(mask), int(row_begin),
                                        n, 0, self._stream()), "espo_loss_fwd")
+
+    # -- context parallelism ------------------------------------------------------------------
+    def attach_cp(self, cp_rank: int, cp_world: int, group=None, local=False):
+        """espo_attach_cp: this context is CP rank cp_rank of cp_world (token blocks). With
+        local=True (same-device emulation) no communicator is created; call cp_gather_local
+        before loss_finalize. Otherwise the NCCL id is broadcast over `group`."""
+        uid = None
+        if cp_world > 1 and not local:
+            uid = ctypes.create_string_buffer(bootstrap_unique_id(cp_rank, group), 128)
+        _check(self._lib.espo_attach_cp(self._h, uid, int(cp_rank), int(cp_world)),
+               "espo_attach_cp")
+        self.cp_rank, self.cp_world = int(cp_rank), int(cp_world)
+
+    def cp_block(self):
+        """(first, end) token rows this CP rank owns for the prepared batch."""
+        tb = -(-self.n_tokens // self.cp_world)
+        return min(self.n_tokens, self.cp_rank * tb), min(self.n_tokens, (self.cp_rank + 1) * tb)
+
+    def cp_gather_local(self, ranks):
+        arr = (ctypes.c_void_p * len(ranks))(*[r._h.value for r in ranks])
+        _check(self._lib.espo_cp_gather_local(self._h, arr, len(ranks), self._stream()),
+               "espo_cp_gather_local")
 
     # -- vocabulary-parallel exchange over peer memory -----------------------------------
     def tp_p2p_buffer(self, max_rows: int, tp_world: int) -> bytes:
