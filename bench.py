@@ -519,6 +519,10 @@ def main_ours(args):
     e2e = None
     if not args.no_e2e and S_ == 1:
         tps, h2d, d2h, dt = run_e2e(ctx, d, dlog, args, dev)
+        if world > 1:       # whole-job rate: every rank's tokens over the slowest rank's time
+            t_e2e = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+            tps = d["T"] / float(t_e2e.item())
         e2e = {"value": tps * world, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "mode": args.e2e_mode,
