@@ -523,8 +523,8 @@ def main_ours(args):
             t_e2e = torch.tensor([dt], dtype=torch.float64, device=dev)
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
             tps = d["T"] / float(t_e2e.item())
-        e2e = {"value": tps * world, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+        e2e = {"value": tps * world, "unit": "tokens/s", "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": d2h * world, "steps": args.e2e_steps,
                "mode": args.e2e_mode,
                "note": "host-resident inputs incl. every logits chunk over PCIe from a pinned "
                        "host ring (" + ("once per step: espo_set_mask + espo_loss_fwd_bwd on "
