@@ -85,3 +85,49 @@ def test_graph_capture_and_replay():
     ref2, _ = decision_aware_reference(got, b, ref, cfg)
     check_loss(got, ref2, 1e-5)
     check_dlogits_f32(got["dlogits"], oracle_dlogits(ref2, b, cfg, np.arange(T)))
+
+
+def test_graph_capture_single_pass():
+    """The single-pass mode captures too: prepare → set_mask → fwd_bwd per rollout chunk →
+    finalize, replayed on new data equals an eager run on that data, bitwise."""
+    from paper_2512_07710_b200.espo import STATS_LEN, Espo
+    dev = require_cuda()
+    a = workload_instance("C0")
+    b = workload_instance("C0", seed=777)
+    T, V = a.T, a.V
+    buf = _inputs(a, dev)
+    ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    stats = torch.empty(STATS_LEN, dtype=torch.float64, device=dev)
+    dz = torch.empty((T, V), dtype=torch.float32, device=dev)
+    so = a.seq_offsets
+    chunks = [(int(so[i]), int(so[j])) for i, j in ((0, 5), (5, 9), (9, 16))]
+
+    def step():
+        ctx.prepare(buf["rew"], buf["gid"], buf["off"], n_tokens=T)
+        ctx.set_mask(buf["mask"])
+        for lo, hi in chunks:
+            ctx.loss_fwd_bwd(buf["z"][lo:hi], buf["tok"][lo:hi], buf["old"][lo:hi], dz[lo:hi],
+                             row_begin=lo)
+        ctx.loss_finalize(loss, stats)
+
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream(dev).wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    nb = _inputs(b, dev)
+    for k in buf:
+        buf[k].copy_(nb[k])
+    g.replay()
+    torch.cuda.synchronize(dev)
+    ctx.get_error()
+    got_loss, got_dz = loss.clone(), dz.clone()
+    step()                                       # eager on the same (new) data
+    torch.cuda.synchronize(dev)
+    ctx.get_error()
+    assert torch.equal(got_loss, loss) and torch.equal(got_dz, dz)
+    ctx.close()

@@ -14,7 +14,7 @@ from tests.gpu_common import oracle_cfg, require_cuda, to_dev
 pytestmark = pytest.mark.gpu
 
 
-def make_case(seed, n_groups, G, L, V, d, zv_group=None):
+def make_case(seed, n_groups, G, L, V, d, zv_group=None, lam=1.0):
     rng = np.random.default_rng(seed)
     R = n_groups * G
     T = R * L
@@ -23,7 +23,7 @@ def make_case(seed, n_groups, G, L, V, d, zv_group=None):
     W[rng.integers(0, V, size=V // 50)] *= 3.0                  # a few strong tokens
     h, W = S.round_to_bf16(h), S.round_to_bf16(W)
     z64 = h.astype(np.float64) @ W.astype(np.float64).T
-    tokens = S.sample_tokens_gumbel(z64.astype(np.float32), seed)
+    tokens = S.sample_tokens_gumbel(z64.astype(np.float32), seed, logit_scale=lam)
     group_ids = np.repeat(np.arange(n_groups, dtype=np.int32), G)
     so = np.arange(R + 1, dtype=np.int64) * L
     rewards = (rng.uniform(size=R) < 0.5).astype(np.float32)
@@ -32,7 +32,7 @@ def make_case(seed, n_groups, G, L, V, d, zv_group=None):
         rewards[g * G + 1] = 0.0
     if zv_group is not None:
         rewards[zv_group * G:(zv_group + 1) * G] = 1.0
-    lp = np.array([O.row_stats(z64[t], int(tokens[t]))[1] for t in range(T)])
+    lp = np.array([O.row_stats(z64[t], int(tokens[t]), lam)[1] for t in range(T)])
     old = S.drift_old_logp(lp, so, seed)
     mask = np.ones(T, np.uint8)
     mask[L - 5:L] = 0
@@ -102,10 +102,11 @@ def test_lmhead_fwd_matches_logits_path(shape, two_cta):
 
 
 @pytest.mark.parametrize("two_cta", [False, True], ids=["1cta", "2cta"])
-@pytest.mark.parametrize("shape,sub,dh_bf16", [((4, 4, 40, 1000, 200), 0, False),
-                                               ((2, 8, 64, 4099, 512), 256, True)],
-                         ids=["V1000_d200", "V4099_d512_sub256_bf16"])
-def test_lmhead_bwd_matches_oracle(shape, sub, dh_bf16, two_cta):
+@pytest.mark.parametrize("shape,sub,dh_bf16,lam", [((4, 4, 40, 1000, 200), 0, False, 1.0),
+                                                   ((2, 8, 64, 4099, 512), 256, True, 1.0),
+                                                   ((3, 4, 32, 2000, 128), 128, False, 0.8)],
+                         ids=["V1000_d200", "V4099_d512_sub256_bf16", "V2000_d128_lambda0.8"])
+def test_lmhead_bwd_matches_oracle(shape, sub, dh_bf16, two_cta, lam):
     """espo_lmhead_bwd (tcgen05 recompute → bf16 dz → dh = dz·W, dW += dzᵀ·h) against O9 on
     fp64 logits, with the GPU's bucket / clip decisions injected where they flipped. Bound:
     dz is rounded to bf16 (2^-9) after an fp32 recompute whose logit error is ≤ the GEMM
@@ -116,9 +117,9 @@ def test_lmhead_bwd_matches_oracle(shape, sub, dh_bf16, two_cta):
     torch.backends.cuda.matmul.allow_tf32 = False
     dev = require_cuda()
     ng, G, L, V, d = shape
-    case = make_case(7, ng, G, L, V, d, zv_group=0)
+    case = make_case(7, ng, G, L, V, d, zv_group=0, lam=lam)
     T = case["T"]
-    ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
+    ctx = Espo(V, logits_dtype=torch.float32, device=dev.index, logit_scale=lam)
     if sub:
         ctx.set_option(OPT_LMHEAD_BWD_ROWS, sub)
     ctx.set_option(OPT_LMHEAD_2CTA, int(two_cta))
@@ -143,7 +144,7 @@ def test_lmhead_bwd_matches_oracle(shape, sub, dh_bf16, two_cta):
     ctx.close()
     inst = Instance(case["z64"], case["tokens"], case["old"], case["mask"], case["rewards"],
                     case["group_ids"], case["so"], V)
-    cfg = oracle_cfg(V)
+    cfg = oracle_cfg(V, logit_scale=lam)
     ref = inst.run(cfg)
     ref2, _ = decision_aware_reference(g, inst, ref, cfg)
     dz, dh_ref, dW_ref = O.lmhead_grads(ref2, case["h"], case["W"], case["tokens"], cfg, 0.75)
