@@ -558,7 +558,7 @@ def main_ours(args):
             "global_batch_tokens": T * world, "seq_len": w.L, "parallelism": f"dp{world} (prompt-group sharded)",
             "chunk_rows": d["Rc"], "l2": "inputs larger than L2 (chunk buffer "
                                          f"{d['Rc'] * V * 2 / 1e9:.2f} GB > 126 MB)",
-            "fwd_impl": ["tma16x3x4k_s4_f32x2", "ldg", "tma16x3x4k_s8_f32x2", "tma8x3x8k_s4_f32x2", "tma20x2x4k_s4_f32x2", "tma24x2x4k_s4_f32x2", "tma16x3x4k_s4_poly1", "tma8x3x4k_s4_f32x2", "tma16x3x4k_s4_scalar", "tile32k_b4", "tile32k_b3", "tile32k_b2"][args.fwd_impl],
+            "fwd_impl": ["tma16x2x6k_s4_f32x2 (rows >= 64 KB; 16x3x4k below)", "ldg", "tma16x2x7k_s2_f32x2", "tma14x2x7k_s2_f32x2", "tma20x2x5k_s2_f32x2", "tma16x3x4k_s4_f32x2", "tma16x2x6k_s4_poly1", "tma18x2x6k_s4_f32x2", "tma16x2x6k_s4_scalar", "tile32k_b4", "tile32k_b3", "tile32k_b2"][args.fwd_impl],
             "bwd_impl": ["tile32k_f32x2", "ldg", "tma16x3x4k", "tma16x2x4k", "tma12x4x4k", "tma8x6x4k", "tma8x4x4k", "tile16k", "tile32k_scalar", "tlist32k_r4", "tlist32k_r8", "tlist32k_r16"][args.bwd_impl],
             "achieved_hbm_gbs_step": step_gbs, "frac_of_8TBs_step": step_gbs / NOMINAL_HBM_GBS,
             "frac_of_measured_step": step_gbs / peak,

@@ -608,14 +608,18 @@ inline cudaError_t launch_rowstats_tma(const FwdParams& p, const FwdRec* list, c
 #define ESPO_FWD_CFG(NW, ST, CH, SB, NP) \
   launch_rowstats_tma_cfg<Tin, NW, ST, CH, SB, NP>(p, list, count, num_sms, blocks_per_sm, s)
   switch (variant) {
-    case 2: return ESPO_FWD_CFG(16, 3, 4096, 8, -1);
-    case 3: return ESPO_FWD_CFG(8, 3, 8192, 4, -1);
-    case 4: return ESPO_FWD_CFG(20, 2, 4096, 4, -1);
-    case 5: return ESPO_FWD_CFG(24, 2, 4096, 4, -1);
-    case 6: return ESPO_FWD_CFG(16, 3, 4096, 4, 1);    // 1 element in 8 by polynomial exp2
-    case 7: return ESPO_FWD_CFG(8, 3, 4096, 4, -1);    // half-size CTA (2 per SM with blocks_per_sm 2)
-    case 8: return ESPO_FWD_CFG(16, 3, 4096, 4, 0);    // the default geometry, scalar FP32
-    default: return ESPO_FWD_CFG(16, 3, 4096, 4, -1);  // measured best on C1: packed f32x2 (K2)
+    case 2: return ESPO_FWD_CFG(16, 2, 7168, 2, -1);
+    case 3: return ESPO_FWD_CFG(14, 2, 7168, 2, -1);
+    case 4: return ESPO_FWD_CFG(20, 2, 5120, 2, -1);
+    case 5: return ESPO_FWD_CFG(16, 3, 4096, 4, -1);   // the previous default (3 × 4 KB ring)
+    case 6: return ESPO_FWD_CFG(16, 2, 6144, 4, 1);    // 1 element in 8 by polynomial exp2
+    case 7: return ESPO_FWD_CFG(18, 2, 6144, 4, -1);
+    case 8:    // the default geometries, scalar FP32
+      if (int64_t(p.V) * int64_t(sizeof(Tin)) >= 65536) return ESPO_FWD_CFG(16, 2, 6144, 4, 0);
+      return ESPO_FWD_CFG(16, 3, 4096, 4, 0);
+    default:   // packed f32x2; ring geometry by row width (measured: C1 / C3 vs 1/8-vocab shards)
+      if (int64_t(p.V) * int64_t(sizeof(Tin)) >= 65536) return ESPO_FWD_CFG(16, 2, 6144, 4, -1);
+      return ESPO_FWD_CFG(16, 3, 4096, 4, -1);
   }
 #undef ESPO_FWD_CFG
 }
