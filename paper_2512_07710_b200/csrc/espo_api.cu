@@ -340,7 +340,9 @@ espo_status espo_create(const espo_config* cfg, const void* nccl_unique_id, int3
   if (!cfg || !out) return ESPO_ERR_INVALID_ARGUMENT;
   *out = nullptr;
   if (world < 1 || rank < 0 || rank >= world) return ESPO_ERR_INVALID_ARGUMENT;
-  if ((world == 1) != (nccl_unique_id == nullptr)) return ESPO_ERR_INVALID_ARGUMENT;
+  // world > 1 needs the NCCL id; world == 1 may pass one too (a one-rank communicator: the
+  // collective code path runs, e.g. to validate the NCCL plumbing on a single GPU)
+  if (world > 1 && nccl_unique_id == nullptr) return ESPO_ERR_INVALID_ARGUMENT;
   espo_status st = validate_config(*cfg);
   if (st != ESPO_OK) return st;
   int ndev = 0;
@@ -366,7 +368,7 @@ espo_status espo_create(const espo_config* cfg, const void* nccl_unique_id, int3
   c->ws.err = reinterpret_cast<int*>(p + 768);
   c->ws.count = reinterpret_cast<int*>(p + 896);
   cudaMemset(c->blocks_scalar, 0, 1024);
-  if (world > 1) {
+  if (nccl_unique_id) {
     if (!g_nccl.load()) {
       espo_destroy(c);
       return ESPO_ERR_NCCL;
@@ -992,7 +994,7 @@ espo_status espo_reshape_rewards(espo_ctx_t c, const espo_reward_shaping* prm,
 
 espo_status espo_attach_tp(espo_ctx_t c, const void* tp_unique_id, int32_t tp_rank,
                            int32_t tp_world) {
-  if (!c || !tp_unique_id || tp_world < 2 || tp_rank < 0 || tp_rank >= tp_world)
+  if (!c || !tp_unique_id || tp_world < 1 || tp_rank < 0 || tp_rank >= tp_world)
     return ESPO_ERR_INVALID_ARGUMENT;
   if (c->cfg.vocab_local <= 0 || c->tp_comm) return ESPO_ERR_BAD_STATE;
   if (!g_nccl.load()) return ESPO_ERR_NCCL;
@@ -1120,7 +1122,7 @@ espo_status espo_attach_cp(espo_ctx_t c, const void* cp_unique_id, int32_t cp_ra
                            int32_t cp_world) {
   if (!c || cp_world < 1 || cp_rank < 0 || cp_rank >= cp_world) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->cp_world > 1 || c->state != State::Created) return ESPO_ERR_BAD_STATE;
-  if (cp_world > 1 && cp_unique_id) {
+  if (cp_unique_id) {
     if (!g_nccl.load()) return ESPO_ERR_NCCL;
     DevGuard g(c->device);
     nccl_uid id;
@@ -1170,7 +1172,7 @@ espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_
   DevGuard g(c->device);
   cudaStream_t s = S(stream);
   const espo_config& cf = c->cfg;
-  if (c->cp_world > 1 && c->cp_comm && c->T > 0) {
+  if (c->cp_comm && c->T > 0) {
     // context parallelism: in-place all-gather of the per-token values K3 reads (13 B/token)
     const size_t tb = size_t(cp_block(c)), off = size_t(c->cp_rank) * tb;
     float* f32s[3] = {c->ws.lp, c->ws.H, c->ws.old};
@@ -1189,7 +1191,7 @@ espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_
   } else {
     ESPO_CUDA(cudaMemsetAsync(c->ws.red, 0, kRedLen * sizeof(double), s));
   }
-  if (c->world > 1) {
+  if (c->comm) {
     if (g_nccl.allreduce(c->ws.red, c->ws.red, kRedLen, kNcclFloat64, kNcclSum, c->comm, s) != 0)
       return ESPO_ERR_NCCL;
   }
@@ -1344,7 +1346,7 @@ espo_status espo_set_mask(espo_ctx_t c, const uint8_t* mask, espo_stream_t strea
   } else {
     ESPO_CUDA(cudaMemsetAsync(c->ws.dpre, 0, 2 * sizeof(double), s));
   }
-  if (c->world > 1) {
+  if (c->comm) {
     if (g_nccl.allreduce(c->ws.dpre, c->ws.dpre, 2, kNcclFloat64, kNcclSum, c->comm, s) != 0)
       return ESPO_ERR_NCCL;
   }

@@ -162,6 +162,13 @@ def _check(status, where):
 _DT = {torch.float32: F32, torch.bfloat16: BF16}
 
 
+def new_unique_id() -> bytes:
+    """A fresh NCCL unique id (espo_get_unique_id), e.g. for a one-rank communicator."""
+    raw = ctypes.create_string_buffer(128)
+    _check(load_library().espo_get_unique_id(raw), "espo_get_unique_id")
+    return raw.raw
+
+
 def bootstrap_unique_id(rank: int, process_group=None) -> bytes:
     """Rank 0 draws the NCCL unique id through libespo (espo_get_unique_id) and broadcasts
     its 128 bytes over the caller's torch.distributed process group (gloo or nccl)."""
@@ -187,7 +194,7 @@ class Espo:
                  log_ratio_clamp=20.0, logits_dtype=torch.bfloat16, grad_dtype=None,
                  zero_fill_inactive_rows=True, zv_mode=ZV_MASK, zvp_beta=0.05,
                  zvp_threshold=0.5, vocab_shard=None, device=None, rank=0, world=1,
-                 process_group=None, tp_rank=0, tp_world=1, tp_group=None):
+                 process_group=None, tp_rank=0, tp_world=1, tp_group=None, nccl_id=None):
         lib = load_library()
         self._lib = lib
         cfg = Config()
@@ -214,7 +221,9 @@ class Espo:
         self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
         self.rank, self.world = int(rank), int(world)
         uid = None
-        if self.world > 1:
+        if nccl_id is not None:          # explicit id (any world, including a 1-rank group)
+            uid = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        elif self.world > 1:
             uid = ctypes.create_string_buffer(
                 bootstrap_unique_id(self.rank, process_group), 128)
         h = ctypes.c_void_p()
@@ -272,12 +281,19 @@ class Espo:
                                        n, 0, self._stream()), "espo_loss_fwd")
 
     # -- context parallelism ------------------------------------------------------------------
-    def attach_cp(self, cp_rank: int, cp_world: int, group=None, local=False):
+    def attach_tp_id(self, nccl_id: bytes, tp_rank: int, tp_world: int):
+        """espo_attach_tp with an explicit NCCL id (the TP group's id, already shared)."""
+        _check(self._lib.espo_attach_tp(self._h, ctypes.create_string_buffer(bytes(nccl_id), 128),
+                                        int(tp_rank), int(tp_world)), "espo_attach_tp")
+
+    def attach_cp(self, cp_rank: int, cp_world: int, group=None, local=False, nccl_id=None):
         """espo_attach_cp: this context is CP rank cp_rank of cp_world (token blocks). With
         local=True (same-device emulation) no communicator is created; call cp_gather_local
         before loss_finalize. Otherwise the NCCL id is broadcast over `group`."""
         uid = None
-        if cp_world > 1 and not local:
+        if nccl_id is not None:
+            uid = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        elif cp_world > 1 and not local:
             uid = ctypes.create_string_buffer(bootstrap_unique_id(cp_rank, group), 128)
         _check(self._lib.espo_attach_cp(self._h, uid, int(cp_rank), int(cp_world)),
                "espo_attach_cp")
