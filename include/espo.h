@@ -270,6 +270,9 @@ espo_status espo_tp_p2p_open(espo_ctx_t ctx, const void* ipc_handles, int32_t tp
                              int32_t tp_world);
 espo_status espo_tp_p2p_connect_local(espo_ctx_t ctx, const espo_ctx_t* ranks, int32_t tp_rank,
                                       int32_t tp_world);
+/* Disconnects: unmaps the peers' buffers (call on every rank, then synchronise the ranks,
+ * before any rank destroys its context — an exporter must outlive the mappings of it). */
+espo_status espo_tp_p2p_unmap(espo_ctx_t ctx);
 espo_status espo_loss_fwd_p2p_send(espo_ctx_t ctx, const void* logits, int64_t ld,
                                    const int32_t* tokens, const float* old_logp,
                                    const uint8_t* mask, int64_t row_begin, int64_t n_rows,

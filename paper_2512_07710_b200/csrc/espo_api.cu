@@ -1088,6 +1088,19 @@ espo_status espo_tp_p2p_connect_local(espo_ctx_t c, const espo_ctx_t* ranks, int
   return tpx_finish_connect(c, bases, tp_rank);
 }
 
+espo_status espo_tp_p2p_unmap(espo_ctx_t c) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  cudaDeviceSynchronize();
+  for (void* q : c->x_opened) cudaIpcCloseMemHandle(q);
+  c->x_opened.clear();
+  if (c->d_xpeer) cudaFree(c->d_xpeer);
+  c->d_xpeer = nullptr;
+  c->d_xgath = nullptr;
+  c->tp_p2p = false;
+  return ESPO_OK;
+}
+
 espo_status espo_loss_fwd_p2p_send(espo_ctx_t c, const void* logits, int64_t ld,
                                    const int32_t* tokens, const float* old_logp,
                                    const uint8_t* mask, int64_t row_begin, int64_t n_rows,

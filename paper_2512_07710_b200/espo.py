@@ -42,7 +42,7 @@ EXPORTED_SYMBOLS = [
     "espo_status_string", "espo_export_token_stats", "espo_export_rollout_stats",
     "espo_launch_count", "espo_set_option", "espo_loss_fwd_partial", "espo_loss_fwd_combine",
     "espo_attach_tp", "espo_lmhead_fwd", "espo_lmhead_bwd", "espo_set_mask", "espo_loss_fwd_bwd", "espo_tp_p2p_buffer", "espo_tp_p2p_open",
-    "espo_tp_p2p_connect_local", "espo_loss_fwd_p2p_send", "espo_loss_fwd_p2p_recv",
+    "espo_tp_p2p_connect_local", "espo_tp_p2p_unmap", "espo_loss_fwd_p2p_send", "espo_loss_fwd_p2p_recv",
     "espo_attach_cp", "espo_cp_gather_local", "espo_reward_shaping_default",
     "espo_reshape_rewards",
 ]
@@ -134,6 +134,7 @@ def load_library():
         "espo_tp_p2p_buffer": (I32, [P, I64, I32, P]),
         "espo_tp_p2p_open": (I32, [P, P, I32, I32]),
         "espo_tp_p2p_connect_local": (I32, [P, P, I32, I32]),
+        "espo_tp_p2p_unmap": (I32, [P]),
         "espo_loss_fwd_p2p_send": (I32, [P, P, I64, P, P, P, I64, I64, P]),
         "espo_loss_fwd_p2p_recv": (I32, [P, I64, I64, P]),
         "espo_loss_fwd_bwd": (I32, [P, P, I64, P, P, P, I64, P, I64, I64, P]),
@@ -328,6 +329,9 @@ class Espo:
         arr = (ctypes.c_void_p * len(ranks))(*[r._h.value for r in ranks])
         _check(self._lib.espo_tp_p2p_connect_local(self._h, arr, int(tp_rank), len(ranks)),
                "espo_tp_p2p_connect_local")
+
+    def tp_p2p_unmap(self):
+        _check(self._lib.espo_tp_p2p_unmap(self._h), "espo_tp_p2p_unmap")
 
     def loss_fwd_p2p_send(self, logits, tokens, old_logp, mask=None, row_begin=0):
         _check(self._lib.espo_loss_fwd_p2p_send(self._h, _ptr(logits), int(logits.stride(0)),

@@ -200,3 +200,33 @@ def test_peer_memory_recv_without_peer_times_out():
     assert e.value.code == "ESPO_ERR_PEER_TIMEOUT"
     for x in ctxs:
         x.close()
+
+
+def test_peer_memory_exchange_over_cuda_ipc_two_processes():
+    """The multi-process path of the peer-memory exchange (IPC handles all-gathered over a
+    process group, cudaIpcOpenMemHandle, NVLink-style stores into the other process's buffer)
+    with two processes sharing the one GPU; phases ordered by the host so no kernel waits on a
+    running kernel of the other process. Loss and gradient equal the single-process run."""
+    import multiprocessing as mp
+    import socket
+    from tests import ipc_workers
+    dev = require_cuda()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    ps = [ctxm.Process(target=ipc_workers.worker_p2p_ipc, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in ps], key=lambda x: x[0])
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    inst = workload_instance("C0")
+    u = run_gpu(inst, dev)
+    assert out[0][1] == out[1][1]
+    assert out[0][1] == pytest.approx(u["loss"], rel=1e-6)
+    dl = np.concatenate([out[0][2], out[1][2]], axis=1)
+    np.testing.assert_allclose(dl, u["dlogits"], rtol=1e-5, atol=1e-7 * np.abs(u["dlogits"]).max())
