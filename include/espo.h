@@ -117,7 +117,7 @@ typedef struct {
   float logit_scale;           /* λ = 1/temperature applied to logits (Q15), default 1 */
   float log_ratio_clamp;       /* clamp of the Eq. 2 mean log-ratio (Q14), default 20; 0=off */
   int32_t logits_dtype;        /* espo_dtype of logits */
-  int32_t grad_dtype;          /* espo_dtype of dlogits (bf16 logits may emit f32 grads) */
+  int32_t grad_dtype;          /* espo_dtype of dlogits: any of f32 / bf16 for either logits dtype */
   int32_t zero_fill_inactive_rows; /* 1 (default): bwd writes 0 to rows of masked tokens,
                                       ZV groups and clipped tokens; 0: leaves them as-is */
   int32_t zv_mode;             /* espo_zv_mode, default MASK */

@@ -35,6 +35,9 @@ __device__ __forceinline__ uint4 ld_stream_coherent(const void* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+__device__ __forceinline__ void st_stream2(void* p, uint32_t x, uint32_t y) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" :: "l"(p), "r"(x), "r"(y) : "memory");
+}
 __device__ __forceinline__ void st_stream(void* p, uint4 v) {
   asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};"
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");

@@ -186,7 +186,6 @@ espo_status validate_config(const espo_config& c) {
   if ((c.logits_dtype != ESPO_F32 && c.logits_dtype != ESPO_BF16) ||
       (c.grad_dtype != ESPO_F32 && c.grad_dtype != ESPO_BF16))
     return ESPO_ERR_INVALID_ARGUMENT;
-  if (c.logits_dtype == ESPO_F32 && c.grad_dtype == ESPO_BF16) return ESPO_ERR_UNSUPPORTED;
   if (c.vocab_local < 0 || (c.vocab_local > 0 && (c.vocab_begin < 0 ||
                                                    int64_t(c.vocab_begin) + c.vocab_local > c.vocab)))
     return ESPO_ERR_INVALID_ARGUMENT;
@@ -1271,14 +1270,17 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
     if (impl == 8) {   // the default tiles with scalar FP32 (A/B of the packed f32x2)
       if (bi && bo) k_dlogits_tile<__nv_bfloat16, __nv_bfloat16, 8, false><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
       else if (bi) k_dlogits_tile<__nv_bfloat16, float, 8, false><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+      else if (bo) k_dlogits_tile<float, __nv_bfloat16, 8, false><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
       else k_dlogits_tile<float, float, 8, false><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
     } else if (vpt == 4) {
       if (bi && bo) k_dlogits_tile<__nv_bfloat16, __nv_bfloat16, 4><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
       else if (bi) k_dlogits_tile<__nv_bfloat16, float, 4><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+      else if (bo) k_dlogits_tile<float, __nv_bfloat16, 4><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
       else k_dlogits_tile<float, float, 4><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
     } else {
       if (bi && bo) k_dlogits_tile<__nv_bfloat16, __nv_bfloat16, 8><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
       else if (bi) k_dlogits_tile<__nv_bfloat16, float, 8><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
+      else if (bo) k_dlogits_tile<float, __nv_bfloat16, 8><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
       else k_dlogits_tile<float, float, 8><<<unsigned(grid), 256, 0, s>>>(p, list, ntiles);
     }
     ESPO_LAUNCHED(c);
@@ -1297,6 +1299,7 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
 #define ESPO_TLIST(RPB)                                                                                    \
     if (bi && bo) k_dlogits_tlist<__nv_bfloat16, __nv_bfloat16, 8, RPB><<<unsigned(grid), 256, 0, s>>>(p, list, zl, cnt, ntiles); \
     else if (bi) k_dlogits_tlist<__nv_bfloat16, float, 8, RPB><<<unsigned(grid), 256, 0, s>>>(p, list, zl, cnt, ntiles);         \
+    else if (bo) k_dlogits_tlist<float, __nv_bfloat16, 8, RPB><<<unsigned(grid), 256, 0, s>>>(p, list, zl, cnt, ntiles); \
     else k_dlogits_tlist<float, float, 8, RPB><<<unsigned(grid), 256, 0, s>>>(p, list, zl, cnt, ntiles);
     if (rpb == 4) { ESPO_TLIST(4) } else if (rpb == 8) { ESPO_TLIST(8) } else { ESPO_TLIST(16) }
 #undef ESPO_TLIST
@@ -1310,6 +1313,9 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
     } else if (bi) {
       auto k = k_dlogits_ldg<__nv_bfloat16, float, 8>;
       k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, zl, cnt);
+    } else if (bo) {
+      auto k = k_dlogits_ldg<float, __nv_bfloat16, 4>;
+      k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, zl, cnt);
     } else {
       auto k = k_dlogits_ldg<float, float, 4>;
       k<<<grid_for(c, (const void*)k, 256), 256, 0, s>>>(p, list, zl, cnt);
@@ -1319,6 +1325,7 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
     const int v = impl;  // 2..5 geometry variants, 6 = 8 warps × 4 × 4 KB
     if (bi && bo) le = launch_dlogits_tma<__nv_bfloat16, __nv_bfloat16>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
     else if (bi) le = launch_dlogits_tma<__nv_bfloat16, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
+    else if (bo) le = launch_dlogits_tma<float, __nv_bfloat16>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
     else le = launch_dlogits_tma<float, float>(p, list, zl, cnt, c->num_sms, c->blocks_per_sm, v, s);
     if (le != cudaSuccess) return cuda_status(le);
   }

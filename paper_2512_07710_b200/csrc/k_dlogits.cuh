@@ -33,9 +33,14 @@ __device__ __forceinline__ void store_out(char* orow, int j, const float* d, int
   constexpr int EPI = Vec<Tin>::EPV;
   constexpr int EPO = Out<Tout>::EPV;
   if ((j + 1) * EPI <= V) {
+    if constexpr (EPI < EPO) {   // f32 in → bf16 out: 4 values → one 8-byte store
+      st_stream2(orow + int64_t(j) * EPI * sizeof(Tout), pack_bf16x2(d[0], d[1]),
+                 pack_bf16x2(d[2], d[3]));
+    } else {
 #pragma unroll
-    for (int h = 0; h < EPI / EPO; ++h)
-      st_stream(orow + (int64_t(j) * EPI + h * EPO) * sizeof(Tout), Out<Tout>::pack(d + h * EPO));
+      for (int h = 0; h < EPI / EPO; ++h)
+        st_stream(orow + (int64_t(j) * EPI + h * EPO) * sizeof(Tout), Out<Tout>::pack(d + h * EPO));
+    }
   } else {
 #pragma unroll
     for (int e = 0; e < EPI; ++e) {

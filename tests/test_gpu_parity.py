@@ -248,3 +248,17 @@ def test_tiled_fwd_variant(dev, c0, dtype):
     ref2, _ = decision_aware_reference(b, inst, ref, cfg)
     check_loss(b, ref2, 1e-5)
     check_dlogits_f32(b["dlogits"], oracle_dlogits(ref2, inst, cfg, np.arange(inst.T)))
+
+
+@pytest.mark.parametrize("impl", [0, 1, 2, 9], ids=["tile", "ldg", "tma", "tlist"])
+def test_f32_logits_bf16_grads(dev, c0, impl):
+    """fp32 logits with bf16 gradients (8-byte packed stores): every bwd variant within one
+    bf16 rounding of the oracle, and equal to rounding the fp32-gradient run."""
+    g = run_gpu(c0, dev, grad_dtype=torch.bfloat16, bwd_impl=impl)
+    f = run_gpu(c0, dev, bwd_impl=impl)
+    cfg = oracle_cfg(c0.V)
+    ref = c0.run(cfg)
+    ref2, _ = decision_aware_reference(g, c0, ref, cfg)
+    check_dlogits_bf16(g["dlogits"], oracle_dlogits(ref2, c0, cfg, np.arange(c0.T)))
+    want = torch.from_numpy(f["dlogits"]).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(g["dlogits"], want)
