@@ -23,6 +23,10 @@
  * Every call is asynchronous on the given CUDA stream; the only host↔device
  * synchronisation is espo_get_error. With world > 1, espo_loss_finalize issues the one
  * NCCL all-reduce of the pass (global active-rollout / token counts and loss terms).
+ * Other modes (declared below): single pass (espo_set_mask + espo_loss_fwd_bwd on chunks of
+ * whole rollouts), the fused LM head (espo_lmhead_fwd / espo_lmhead_bwd: logits never
+ * materialised), vocabulary parallelism (partial + combine, NCCL all-gather, or the fused
+ * peer-memory exchange), context parallelism (espo_attach_cp) and reward reshaping.
  *
  * Layout: token rows are packed (cu_seqlens): rollout i owns rows
  * [seq_offsets[i], seq_offsets[i+1]). Logits row t is the distribution that produced
@@ -33,7 +37,7 @@
  * Ownership: all pointer arguments are caller-owned; "device" pointers must be CUDA
  * device memory of the context's device, "host" pointers host memory. Inputs of a chunk
  * call are read before the call's work completes on the stream; the context keeps what
- * it needs (per-token workspace ≈ 30 B/token, per-rollout arrays) until the next prepare.
+ * it needs (per-token workspace ≈ 72 B/token, per-rollout arrays) until the next prepare.
  *
  * Errors: host-detectable problems (NULL, sizes, alignment, call order, chunk overlap)
  * return a status immediately and enqueue nothing. Data problems found on the device
