@@ -494,9 +494,11 @@ inline int shard_width(espo_ctx_t c) {
 }
 
 espo_status check_fwd_args(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
-                           const float* old_logp, int64_t row_begin, int64_t n_rows) {
+                           const float* old_logp, int64_t row_begin, int64_t n_rows,
+                           bool single_pass_call = false) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
-  if (c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
+  // single-pass mode admits only espo_loss_fwd_bwd; the other modes never admit it
+  if (c->state != State::Prepared || c->single_pass != single_pass_call) return ESPO_ERR_BAD_STATE;
   if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T)
     return ESPO_ERR_INVALID_ARGUMENT;
   if (n_rows == 0) return ESPO_OK;
@@ -728,7 +730,7 @@ espo_status espo_loss_fwd_partial(espo_ctx_t c, const void* logits, int64_t ld,
 espo_status espo_loss_fwd_combine(espo_ctx_t c, const float* partials, int32_t n_shards,
                                   int64_t row_begin, int64_t n_rows, espo_stream_t stream) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
-  if (c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
+  if (c->state != State::Prepared || c->single_pass) return ESPO_ERR_BAD_STATE;
   if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T ||
       n_shards < 1 || n_shards > 1024)
     return ESPO_ERR_INVALID_ARGUMENT;
@@ -785,7 +787,7 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
                             const uint8_t* mask, int64_t row_begin, int64_t n_rows,
                             espo_stream_t stream) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
-  if (c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
+  if (c->state != State::Prepared || c->single_pass) return ESPO_ERR_BAD_STATE;
   if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T || d < 1)
     return ESPO_ERR_INVALID_ARGUMENT;
   if (n_rows == 0) return ESPO_OK;
@@ -1380,9 +1382,8 @@ espo_status espo_loss_fwd_bwd(espo_ctx_t c, const void* logits, int64_t ld, cons
                               const float* old_logp, void* dlogits, int64_t ldg,
                               const float* grad_loss_dev, int64_t row_begin, int64_t n_rows,
                               espo_stream_t stream) {
-  espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
+  espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows, true);
   if (st != ESPO_OK) return st;
-  if (!c->single_pass) return ESPO_ERR_BAD_STATE;
   if (n_rows == 0) return ESPO_OK;
   const bool sharded = c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab;
   if (sharded && !c->tp_comm && !c->tp_p2p) return ESPO_ERR_BAD_STATE;

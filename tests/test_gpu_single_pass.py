@@ -107,6 +107,14 @@ def test_single_pass_rejects_misaligned_chunks_and_mixed_calls():
     with pytest.raises(EspoError) as e:
         ctx.loss_fwd(z, tok, old)
     assert e.value.code == "ESPO_ERR_BAD_STATE"
+    with pytest.raises(EspoError) as e:
+        ctx.loss_fwd_partial(z, tok, old)
+    assert e.value.code == "ESPO_ERR_BAD_STATE"
+    hb = torch.zeros((T, 64), dtype=torch.bfloat16, device=dev)
+    Wb = torch.zeros((V, 64), dtype=torch.bfloat16, device=dev)
+    with pytest.raises(EspoError) as e:
+        ctx.lmhead_fwd(hb, Wb, tok, old)
+    assert e.value.code == "ESPO_ERR_BAD_STATE"
     ctx.loss_fwd_bwd(z, tok, old)
     ctx.loss_finalize()
     with pytest.raises(EspoError) as e:
