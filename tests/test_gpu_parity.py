@@ -262,3 +262,15 @@ def test_f32_logits_bf16_grads(dev, c0, impl):
     check_dlogits_bf16(g["dlogits"], oracle_dlogits(ref2, c0, cfg, np.arange(c0.T)))
     want = torch.from_numpy(f["dlogits"]).to(torch.bfloat16).float().numpy()
     assert np.array_equal(g["dlogits"], want)
+
+
+def test_group_permutation_invariance_gpu(dev, c0):
+    """Reordering prompt groups (with their rollouts and token rows) permutes the gradient
+    rows bit for bit and leaves the loss unchanged up to the fp64 order of the rollout sum —
+    the per-row / per-rollout work is independent of where a group sits in the batch."""
+    from tests.test_oracle_properties import _permute_groups
+    a = run_gpu(c0, dev)
+    p, rows = _permute_groups(c0, [3, 1, 0, 2])
+    b = run_gpu(p, dev)
+    assert b["loss"] == pytest.approx(a["loss"], rel=1e-12)
+    assert np.array_equal(b["dlogits"], a["dlogits"][rows])
