@@ -54,6 +54,10 @@ def parse():
     p.add_argument("--cpu-sample-tokens", type=int, default=128, help="tokens per rollout")
     p.add_argument("--single-pass", action="store_true",
                    help="device leg through espo_set_mask + espo_loss_fwd_bwd (chunks of whole rollouts)")
+    p.add_argument("--factored", action="store_true",
+                   help="factored-gradient leg: espo_loss_fwd_factored (one sweep per row writes "
+                        "G = onehot - p) + espo_loss_row_scale")
+    p.add_argument("--factored-impl", type=int, default=0, help="ESPO_OPT_FACTORED_IMPL (0 = default)")
     p.add_argument("--e2e-mode", default="single-pass", choices=["single-pass", "two-sweep"],
                    help="e2e leg: logits chunks cross PCIe once (single-pass) or twice")
     p.add_argument("--zv-mode", default="mask", choices=["mask", "rlzvp"],
@@ -302,6 +306,30 @@ def run_step_single(ctx, d, dlog, ev=None):
     return ctx.loss_finalize()
 
 
+def run_step_factored(ctx, d, dlog, ev=None):
+    """Factored-gradient step: prepare → espo_loss_fwd_factored per chunk (statistics + the
+    row factor G = onehot − p into dlog, one sweep) → finalize → espo_loss_row_scale (the
+    per-row scale a consumer applies in its GEMM). ev["fwdbwd"] gets one pair per chunk."""
+    import torch
+    buf = d["buf"]
+    ctx.prepare(d["rewards"], d["group_ids"], d["seq_offsets"], n_tokens=d["T"])
+    for b, e in d["chunks"]:
+        if ev is not None:
+            s0 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+        ctx.loss_fwd_factored(buf[:e - b], d["tokens"][b:e], d["old"][b:e], None,
+                              grad=dlog[:e - b], row_begin=b)
+        if ev is not None:
+            s1 = torch.cuda.Event(enable_timing=True)
+            s1.record()
+            ev["fwdbwd"].append((s0, s1))
+    out = ctx.loss_finalize()
+    if "scale" not in d:
+        d["scale"] = torch.empty(d["T"], dtype=torch.float32, device=buf.device)
+    ctx.loss_row_scale(out=d["scale"])
+    return out
+
+
 def run_e2e(ctx, d, dlog, args, dev):
     """End-to-end through the public API with HOST inputs: every step copies its inputs
     (rewards, group ids, offsets, tokens, old log-probs and every logits chunk) from pinned
@@ -422,8 +450,8 @@ def cpu_baseline(d, w, n_tok_per_rollout, log):
 def main_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_2512_07710_b200.espo import (Espo, OPT_BLOCKS_PER_SM, OPT_BWD_IMPL, OPT_FWD_IMPL,
-                                            stats_to_dict)
+    from paper_2512_07710_b200.espo import (Espo, OPT_BLOCKS_PER_SM, OPT_BWD_IMPL,
+                                            OPT_FACTORED_IMPL, OPT_FWD_IMPL, stats_to_dict)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -456,7 +484,9 @@ def main_ours(args):
         ctx.set_option(OPT_FWD_IMPL, args.fwd_impl)
         ctx.set_option(OPT_BWD_IMPL, args.bwd_impl)
         ctx.set_option(OPT_BLOCKS_PER_SM, args.blocks_per_sm)
-        step_fn = run_step_single if args.single_pass else run_step
+        ctx.set_option(OPT_FACTORED_IMPL, args.factored_impl)
+        step_fn = (run_step_factored if args.factored else
+                   run_step_single if args.single_pass else run_step)
     dlog = torch.empty((d["Rc"], w.V), dtype=torch.bfloat16, device=dev)
 
     for _ in range(args.warmup):
@@ -497,8 +527,13 @@ def main_ours(args):
     if args.compact:
         bwd_bytes += (n_act - n_clip) * 2 * V      # swept rows are still written
     step_bytes = fwd_bytes + bwd_bytes
+    if args.factored:          # one sweep: read valid rows once, write G (or zeros) per row
+        step_bytes = n_act * (2 * V + 4 + 4 + 16) + T * (4 + 4 + 1 + 8 + 9) + \
+            (n_act if args.compact else T) * 2 * V
+        bwd_bytes = step_bytes
+    fused = args.single_pass or args.factored
     peak, peak_src = measured_peaks()
-    if args.single_pass:       # one event pair per fused chunk: report the fused chunk
+    if fused:                  # one event pair per fused chunk: report the fused chunk
         fb_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["fwdbwd"])
         n_chunks = len(ev["fwdbwd"]) // args.steps
         fwd_ms = bwd_ms = fb_ms
@@ -514,7 +549,8 @@ def main_ours(args):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         tr = json.load(open(tpath))
-        traffic = None if args.single_pass else tr.get("bwd_bytes_per_launch")
+        traffic = tr.get("factored_bytes_per_launch") if args.factored else \
+            None if args.single_pass else tr.get("bwd_bytes_per_launch")
 
     e2e = None
     if not args.no_e2e and S_ == 1:
@@ -554,7 +590,9 @@ def main_ours(args):
                         + (f", {S_} vocabulary shards back to back on one GPU (TP emulation, "
                            + ("partials exchanged by the fused peer-memory path)" if args.tp_p2p
                               else "partials gathered by device copy)") if S_ > 1 else "")
-                        + (", single-pass (espo_loss_fwd_bwd per chunk of whole rollouts)" if args.single_pass else ""),
+                        + (", single-pass (espo_loss_fwd_bwd per chunk of whole rollouts)" if args.single_pass else "")
+                        + (", factored gradient (espo_loss_fwd_factored: one sweep writes G = onehot - p; "
+                           "dlogits = row_scale * G applied by the consumer)" if args.factored else ""),
             "global_batch_tokens": T * world, "seq_len": w.L, "parallelism": f"dp{world} (prompt-group sharded)",
             "chunk_rows": d["Rc"], "l2": "inputs larger than L2 (chunk buffer "
                                          f"{d['Rc'] * V * 2 / 1e9:.2f} GB > 126 MB)",
@@ -567,7 +605,8 @@ def main_ours(args):
             "active_tokens": n_act, "clipped_tokens": n_clip,
             "zv_groups": st["n_zv_groups"], "groups": st["n_groups"],
         },
-        "roofline": {"bound": "hbm", "kernel": ("espo_loss_fwd_bwd chunk (K2 + K3 + K5)" if args.single_pass
+        "roofline": {"bound": "hbm", "kernel": ("espo_loss_fwd_factored chunk (k_fwd_rows + k_fwd_grad)" if args.factored
+                                                else "espo_loss_fwd_bwd chunk (K2 + K3 + K5)" if args.single_pass
                                                 else "espo_loss_bwd sweep (k_bwd_recs + k_dlogits_tile)"),
                      "achieved": bwd_gbs, "peak": peak, "unit": "GB/s",
                      "frac": bwd_gbs / peak, "traffic": traffic, "peak_source": peak_src,
@@ -578,6 +617,10 @@ def main_ours(args):
         "clocks": clk,
         "loss": st["loss"],
     }
+    if args.factored:
+        out["config"]["factored_impl"] = ["ring 20+1 warps x 5 x 40 KB", "cta1024 L2 re-read",
+                                          "ring 16+1 x 6 x 32 KB", "ring 24+1 x 4 x 48 KB",
+                                          "ring 24+1 x 5 x 36 KB", "ring 28+1 x 6 x 28 KB"][args.factored_impl]
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()

@@ -327,6 +327,33 @@ espo_status espo_loss_fwd_bwd(espo_ctx_t ctx, const void* logits, int64_t ld,
                               int64_t ldg, const float* grad_loss_dev, int64_t row_begin,
                               int64_t n_rows, espo_stream_t stream);
 
+/* ---- factored gradient (one sweep per row: statistics + the row-local gradient factor) ----
+ * The gradient of the loss w.r.t. logits row t factors as
+ *   d loss/d z_t = scale_t · G_t,  G_t = onehot(y_t) − softmax(λ z_t),  scale_t = λ·g_t
+ * (only the Eq. 1 numerator log π_θ(y_t) carries gradient; g_t = −grad·c_t/D
+ * from Eqs. 1-3). G_t needs only the row, scale_t the rollout-level
+ * reduction, so a consumer that applies scale_t in its own GEMM (dh = diag(scale)·G·W,
+ * dW = Gᵀ·(diag(scale)·h)) reads each logits row once: 2V read + one G row written.
+ * espo_loss_fwd_factored: espo_loss_fwd for rows [row_begin, row_begin + n_rows) (same
+ * arguments, checks, coverage and errors) that also writes G_t into grad (device,
+ * [n_rows, ldg ≥ vocab] of grad_dtype, 16-byte aligned; may alias logits when ldg == ld and
+ * the dtypes are equal — the rows' logits are then overwritten). The target entry is
+ * q_t = 1 − p_y (no cancellation); rows without gradient (masked, eliminated group, inactive
+ * rollout) are zero-filled without being read when zero_fill_inactive_rows, else untouched;
+ * clipped rows get their G_t (their scale is 0). Unsharded contexts, not in single-pass mode
+ * (ESPO_ERR_BAD_STATE). Statistics agree with espo_loss_fwd's within fp32 rounding (a
+ * different summation order), not bitwise.
+ * espo_loss_row_scale (after espo_loss_finalize): scale_out[r] = scale_t for rows
+ * [row_begin, row_begin + n_rows) (device f32 [n_rows]), 0 for rows without gradient;
+ * grad_loss_dev as in espo_loss_bwd. scale_t·G_t equals espo_loss_bwd's row up to the bf16
+ * rounding of G_t instead of the product. */
+espo_status espo_loss_fwd_factored(espo_ctx_t ctx, const void* logits, int64_t ld,
+                                   const int32_t* tokens, const float* old_logp,
+                                   const uint8_t* mask, void* grad, int64_t ldg, int64_t row_begin,
+                                   int64_t n_rows, espo_stream_t stream);
+espo_status espo_loss_row_scale(espo_ctx_t ctx, const float* grad_loss_dev, float* scale_out,
+                                int64_t row_begin, int64_t n_rows, espo_stream_t stream);
+
 /* ---- fused LM head + forward statistics (tcgen05) ----
  * Computes the same row statistics as espo_loss_fwd for logits z = hidden · weightᵀ (softmax
  * of λ·z as there) without writing the logits: hidden bf16 [n_rows, ldh ≥ d] (row row_begin of the chunk first),
@@ -398,8 +425,11 @@ typedef enum {
   ESPO_OPT_LMHEAD_PARTS = 3,   /* espo_lmhead_fwd/bwd vocabulary parts per row block (0 = auto) */
   ESPO_OPT_LMHEAD_BWD_ROWS = 4,/* espo_lmhead_bwd rows per dz sub-chunk (multiple of 128;
                                   0 = default 8192) */
-  ESPO_OPT_LMHEAD_2CTA = 5     /* 1: LM-head kernels on CTA pairs (tcgen05 cta_group::2,
+  ESPO_OPT_LMHEAD_2CTA = 5,    /* 1: LM-head kernels on CTA pairs (tcgen05 cta_group::2,
                                   M = 256 per pair); 0: one CTA per 128-row block */
+  ESPO_OPT_FACTORED_IMPL = 6   /* espo_loss_fwd_factored: 0 = TMA ring (1 producer + 20 consumer
+                                  warps, 5 × 40 KB slots, default), 1 = 1024-thread CTA per row
+                                  with plain loads, 2-5 = other ring geometries (A/B only) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

@@ -18,6 +18,7 @@
 #include "k_lmhead2.cuh"
 #include "k_reward.cuh"
 #include "k_tpx.cuh"
+#include "k_fwdgrad.cuh"
 #include "workspace.cuh"
 
 #include <cublas_v2.h>
@@ -119,6 +120,7 @@ struct espo_ctx_s {
   int fwd_impl = 0, bwd_impl = 0;
   int blocks_per_sm = 0;
   int lmh_parts = 0;  // 0 = auto
+  int factored_impl = 0;       // espo_loss_fwd_factored kernel geometry
   void* blocks_tok = nullptr;  // one allocation for all per-token arrays
   void* blocks_roll = nullptr; // one allocation for all per-rollout arrays
   void* blocks_scalar = nullptr;
@@ -430,6 +432,10 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
     case ESPO_OPT_LMHEAD_2CTA:
       if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
       c->lmh_2cta = static_cast<int>(value);
+      return ESPO_OK;
+    case ESPO_OPT_FACTORED_IMPL:
+      if (value < 0 || value > 5) return ESPO_ERR_INVALID_ARGUMENT;
+      c->factored_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_BWD_ROWS:
       if (value < 0 || value > (1 << 20) || value % kLmBM) return ESPO_ERR_INVALID_ARGUMENT;
@@ -1438,6 +1444,99 @@ espo_status espo_export_rollout_stats(espo_ctx_t c, double* adv, uint8_t* zv, ui
   DevGuard g(c->device);
   k_export_rollouts<<<(c->R + 255) / 256, 256, 0, S(stream)>>>(c->ws, c->R, adv, zv, active, J_i,
                                                                  nb, theta);
+  ESPO_LAUNCHED(c);
+  return ESPO_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+espo_status espo_loss_fwd_factored(espo_ctx_t c, const void* logits, int64_t ld,
+                                   const int32_t* tokens, const float* old_logp,
+                                   const uint8_t* mask, void* grad, int64_t ldg, int64_t row_begin,
+                                   int64_t n_rows, espo_stream_t stream) {
+  espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
+  if (st != ESPO_OK || n_rows == 0) return st;
+  if (c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab) return ESPO_ERR_BAD_STATE;
+  if ((st = check_bwd_args(c, logits, ld, grad, ldg)) != ESPO_OK) return st;
+  if ((st = check_coverage(c, row_begin, row_begin + n_rows)) != ESPO_OK) return st;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  const espo_config& cf = c->cfg;
+  FwdParams p;
+  p.logits = logits;
+  p.ld = ld;
+  p.tokens = tokens;
+  p.old_logp = old_logp;
+  p.mask = mask;
+  p.row_begin = row_begin;
+  p.n_rows = n_rows;
+  p.V = cf.vocab;
+  p.lam_log2e = cf.logit_scale * kLog2e;
+  p.partial = nullptr;
+  p.ws = c->ws;
+  const bool bi = cf.logits_dtype == ESPO_BF16, bo = cf.grad_dtype == ESPO_BF16;
+  FwdRec* list = static_cast<FwdRec*>(c->ws.list);
+  int32_t* zl = cf.zero_fill_inactive_rows ? c->ws.zlist : nullptr;
+  ESPO_CUDA(cudaMemsetAsync(c->ws.count, 0, 3 * sizeof(int), s));
+  const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  if (bi)
+    k_fwd_rows<__nv_bfloat16><<<pre_grid, 256, 0, s>>>(logits, ld, tokens, old_logp, mask, row_begin,
+                                                       n_rows, cf.vocab, 0, cf.vocab, p.lam_log2e,
+                                                       c->ws, list, c->ws.count, zl);
+  else
+    k_fwd_rows<float><<<pre_grid, 256, 0, s>>>(logits, ld, tokens, old_logp, mask, row_begin, n_rows,
+                                               cf.vocab, 0, cf.vocab, p.lam_log2e, c->ws, list,
+                                               c->ws.count, zl);
+  ESPO_LAUNCHED(c);
+  const int al = logits == grad ? 1 : 0;
+  // geometry (ESPO_OPT_FACTORED_IMPL): 0 = TMA ring, 20 consumer warps + 1 producer warp,
+  // 5 × 40 KB slots (measured best); 1 = CTA of 1024 threads re-reading each row
+  // through L2 with plain loads; 2-5 = other ring geometries
+#define ESPO_FG(NT, U)                                                                     \
+  {                                                                                            \
+    const int grid = c->num_sms * (1024 / NT);                                                  \
+    if (bi && bo) k_fwd_grad<__nv_bfloat16, __nv_bfloat16, NT, U><<<grid, NT, 0, s>>>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al); \
+    else if (bi) k_fwd_grad<__nv_bfloat16, float, NT, U><<<grid, NT, 0, s>>>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al);         \
+    else if (bo) k_fwd_grad<float, __nv_bfloat16, NT, U><<<grid, NT, 0, s>>>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al);         \
+    else k_fwd_grad<float, float, NT, U><<<grid, NT, 0, s>>>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al);                         \
+  }
+#define ESPO_FGR(NC, ST, CH)                                                           \
+  {                                                                                            \
+    cudaError_t le;                                                                            \
+    if (bi && bo) le = launch_fwd_grad_ring<__nv_bfloat16, __nv_bfloat16, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s); \
+    else if (bi) le = launch_fwd_grad_ring<__nv_bfloat16, float, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s);         \
+    else if (bo) le = launch_fwd_grad_ring<float, __nv_bfloat16, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s);         \
+    else le = launch_fwd_grad_ring<float, float, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s);                         \
+    if (le != cudaSuccess) return cuda_status(le);                                             \
+  }
+  switch (c->factored_impl) {
+    case 1: ESPO_FG(1024, 4) break;
+    case 2: ESPO_FGR(16, 6, 32768) break;
+    case 3: ESPO_FGR(24, 4, 49152) break;
+    case 4: ESPO_FGR(24, 5, 36864) break;
+    case 5: ESPO_FGR(28, 6, 28672) break;
+    default: ESPO_FGR(20, 5, 40960) break;
+  }
+#undef ESPO_FG
+#undef ESPO_FGR
+  ESPO_LAUNCHED(c);
+  c->covered[row_begin] = row_begin + n_rows;
+  c->n_covered += n_rows;
+  return ESPO_OK;
+}
+
+espo_status espo_loss_row_scale(espo_ctx_t c, const float* grad_loss_dev, float* scale_out,
+                                int64_t row_begin, int64_t n_rows, espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Finalized) return ESPO_ERR_BAD_STATE;
+  if (n_rows < 0 || row_begin < 0 || row_begin + n_rows > c->T) return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rows == 0) return ESPO_OK;
+  if (!scale_out) return ESPO_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  const int grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  k_row_scale<<<grid, 256, 0, S(stream)>>>(row_begin, n_rows, grad_loss_dev, c->ws, scale_out);
   ESPO_LAUNCHED(c);
   return ESPO_OK;
 }

@@ -115,10 +115,13 @@ __device__ __forceinline__ void lm_store_dz(const float* x, const BwdRec& rc, in
   uint32_t w[16];
   if (rc.ng != 0.f) {
     const bool special = (rc.y >= col0 && rc.y < col0 + 32) || (col0 + 32 > V);
+    const float2 L2 = make_float2(lamL, lamL), N2 = make_float2(rc.nlseL, rc.nlseL),
+                 G2 = make_float2(rc.ng, rc.ng);
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
-      float a = rc.ng * ex2(fmaf(x[e], lamL, rc.nlseL));
-      float b = rc.ng * ex2(fmaf(x[e + 1], lamL, rc.nlseL));
+      const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), L2, N2);
+      const float2 o = __fmul2_rn(G2, make_float2(ex2(t.x), ex2(t.y)));
+      float a = o.x, b = o.y;
       if (special) {
         if (col0 + e == rc.y) a = rc.gq;
         if (col0 + e + 1 == rc.y) b = rc.gq;
@@ -162,19 +165,18 @@ __device__ __forceinline__ void lm_row_chunk(float* x, int col0, int y, int V, f
   // through the checked path below via NaN = 0·(−inf))
   float bS, bW;
   {
-    const float nR = -R;
-    float s0 = 0.f, s1 = 0.f, w0 = 0.f, w1 = 0.f;
+    // two even/odd chains as packed FFMA2/FADD2 (bitwise the scalar arithmetic, as in K2)
+    const float2 L2 = make_float2(lamL, lamL), N2 = make_float2(-R, -R);
+    float2 s = make_float2(0.f, 0.f), w = make_float2(0.f, 0.f);
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
-      const float ta = fmaf(x[e], lamL, nR), tb = fmaf(x[e + 1], lamL, nR);
-      const float ea = ex2(ta), eb = ex2(tb);
-      s0 += ea;
-      s1 += eb;
-      w0 = fmaf(ea, ta, w0);
-      w1 = fmaf(eb, tb, w1);
+      const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), L2, N2);
+      const float2 ex = make_float2(ex2(t.x), ex2(t.y));
+      s = __fadd2_rn(s, ex);
+      w = __ffma2_rn(ex, t, w);
     }
-    bS = s0 + s1;
-    bW = w0 + w1;
+    bS = s.x + s.y;
+    bW = w.x + w.y;
   }
   if (!(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {  // overflow / −inf / NaN: checked
     S -= cS;

@@ -38,14 +38,14 @@ __device__ __forceinline__ int warp_append(bool take, int* count) {
 }
 
 // Forward: copies tokens/old_logp into the workspace, sets flag[t], lists valid rows of
-// active rollouts. Errors: token ∉ [0,V) and a non-finite target logit.
+// active rollouts (and, given zlist, the other rows at count[1]). Errors: token ∉ [0,V) and a non-finite target logit.
 template <typename Tin>
 __global__ void __launch_bounds__(256) k_fwd_rows(const void* logits, int64_t ld,
                                                   const int32_t* tokens, const float* old_logp,
                                                   const uint8_t* mask, int64_t row_begin,
                                                   int64_t n_rows, int V, int v0, int Vl,
                                                   float lamL, Workspace ws, FwdRec* list,
-                                                  int* count) {
+                                                  int* count, int32_t* zlist = nullptr) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const int64_t n_round = (n_rows + 31) / 32 * 32;  // whole warps stay converged
   for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_round; r += stride) {
@@ -77,6 +77,11 @@ __global__ void __launch_bounds__(256) k_fwd_rows(const void* logits, int64_t ld
         }
       }
       ws.flag[t] = valid ? 1 : 0;
+    }
+    if (zlist) {   // factored-gradient sweep: rows without gradient are zero-filled
+      const bool zero = r < n_rows && !valid;
+      const int pz = warp_append(zero, count + 1);
+      if (zero) zlist[pz] = static_cast<int32_t>(r);
     }
     const int pos = warp_append(valid, count);
     if (valid) {

@@ -27,6 +27,7 @@ NORM_SEQ, NORM_TOKEN = 0, 1
 ZV_MASK, ZV_RLZVP = 0, 1
 OPT_FWD_IMPL, OPT_BWD_IMPL, OPT_BLOCKS_PER_SM, OPT_LMHEAD_PARTS, OPT_LMHEAD_BWD_ROWS = 0, 1, 2, 3, 4
 OPT_LMHEAD_2CTA = 5
+OPT_FACTORED_IMPL = 6
 
 STATUS = {
     0: "ESPO_OK", 1: "ESPO_ERR_INVALID_ARGUMENT", 2: "ESPO_ERR_ALIGNMENT",
@@ -44,7 +45,7 @@ EXPORTED_SYMBOLS = [
     "espo_attach_tp", "espo_lmhead_fwd", "espo_lmhead_bwd", "espo_set_mask", "espo_loss_fwd_bwd", "espo_tp_p2p_buffer", "espo_tp_p2p_open",
     "espo_tp_p2p_connect_local", "espo_tp_p2p_unmap", "espo_loss_fwd_p2p_send", "espo_loss_fwd_p2p_recv",
     "espo_attach_cp", "espo_cp_gather_local", "espo_reward_shaping_default",
-    "espo_reshape_rewards",
+    "espo_reshape_rewards", "espo_loss_fwd_factored", "espo_loss_row_scale",
 ]
 
 
@@ -138,6 +139,8 @@ def load_library():
         "espo_loss_fwd_p2p_send": (I32, [P, P, I64, P, P, P, I64, I64, P]),
         "espo_loss_fwd_p2p_recv": (I32, [P, I64, I64, P]),
         "espo_loss_fwd_bwd": (I32, [P, P, I64, P, P, P, I64, P, I64, I64, P]),
+        "espo_loss_fwd_factored": (I32, [P, P, I64, P, P, P, P, I64, I64, I64, P]),
+        "espo_loss_row_scale": (I32, [P, P, P, I64, I64, P]),
         "espo_lmhead_bwd": (I32, [P, P, I64, P, I64, I32, P, I64, I32, P, I64, P, I64, I64, P]),
         "espo_reward_shaping_default": (None, [ctypes.POINTER(RewardShaping), I32]),
         "espo_reshape_rewards": (I32, [P, ctypes.POINTER(RewardShaping), P, P, P, I32, I64, P,
@@ -359,6 +362,29 @@ class Espo:
                                            int(row_begin), int(logits.shape[0]), self._stream()),
                "espo_loss_fwd_bwd")
         return dlogits
+
+    def loss_fwd_factored(self, logits, tokens, old_logp, mask=None, grad=None, row_begin=0):
+        """espo_loss_fwd_factored: the forward of these rows plus G = onehot(y) − softmax(λz)
+        written to `grad` (allocated if None; may be `logits` itself). Returns grad."""
+        if logits.dtype != self.logits_dtype:
+            raise TypeError(f"logits dtype {logits.dtype} != context {self.logits_dtype}")
+        if grad is None:
+            grad = torch.empty(logits.shape, dtype=self.grad_dtype, device=logits.device)
+        _check(self._lib.espo_loss_fwd_factored(
+            self._h, _ptr(logits), int(logits.stride(0)), _ptr(tokens), _ptr(old_logp), _ptr(mask),
+            _ptr(grad), int(grad.stride(0)), int(row_begin), int(logits.shape[0]), self._stream()),
+            "espo_loss_fwd_factored")
+        return grad
+
+    def loss_row_scale(self, row_begin=0, n_rows=None, grad_loss=None, out=None):
+        """espo_loss_row_scale: per-row scale_t with dlogits_t = scale_t · G_t."""
+        if n_rows is None:
+            n_rows = self.n_tokens - row_begin
+        if out is None:
+            out = torch.empty(n_rows, dtype=torch.float32, device=self.device)
+        _check(self._lib.espo_loss_row_scale(self._h, _ptr(grad_loss), _ptr(out), int(row_begin),
+                                             int(n_rows), self._stream()), "espo_loss_row_scale")
+        return out
 
     def loss_fwd_partial(self, logits, tokens, old_logp, mask=None, row_begin=0, partial=None):
         """espo_loss_fwd_partial: this vocabulary shard's per-row {R, S, W, u_y} (f32[n, 4])."""

@@ -38,14 +38,18 @@ def to_dev(a, dtype, dev):
 
 
 def run_gpu(inst, dev, cfgkw=None, logits_dtype=torch.float32, grad_dtype=None, chunks=None,
-            fwd_impl=0, bwd_impl=0, ld_pad=0, in_place=False, grad_loss=None):
-    """Full pass on the GPU. chunks: list of (begin, end) for fwd (bwd uses the same)."""
-    from paper_2512_07710_b200.espo import Espo, OPT_FWD_IMPL, OPT_BWD_IMPL, stats_to_dict
+            fwd_impl=0, bwd_impl=0, ld_pad=0, in_place=False, grad_loss=None, factored=False, factored_impl=0):
+    """Full pass on the GPU. chunks: list of (begin, end) for fwd (bwd uses the same).
+    factored: espo_loss_fwd_factored per chunk + espo_loss_row_scale; "dlogits" is then
+    scale_t · G_t formed in fp64 here (no second rounding), "G"/"scale" are returned too."""
+    from paper_2512_07710_b200.espo import (Espo, OPT_BWD_IMPL, OPT_FACTORED_IMPL, OPT_FWD_IMPL,
+                                            stats_to_dict)
     cfgkw = dict(cfgkw or {})
     V, T = inst.V, inst.T
     ctx = Espo(V, logits_dtype=logits_dtype, grad_dtype=grad_dtype, device=dev.index, **cfgkw)
     ctx.set_option(OPT_FWD_IMPL, fwd_impl)
     ctx.set_option(OPT_BWD_IMPL, bwd_impl)
+    ctx.set_option(OPT_FACTORED_IMPL, factored_impl)
     ld = V + ld_pad
     zfull = torch.zeros((T, ld), dtype=logits_dtype, device=dev)
     zfull[:, :V] = to_dev(inst.logits, torch.float32, dev).to(logits_dtype)
@@ -59,11 +63,31 @@ def run_gpu(inst, dev, cfgkw=None, logits_dtype=torch.float32, grad_dtype=None, 
                 to_dev(inst.seq_offsets, torch.int64, dev), n_tokens=T, adv_out=adv_out,
                 zv_out=zv_out)
     chunks = chunks or [(0, T)]
+    gl = None if grad_loss is None else torch.tensor([grad_loss], dtype=torch.float32, device=dev)
+    if factored:
+        G = z if in_place else torch.full((T, ld), float("nan"), dtype=ctx.grad_dtype, device=dev)
+        for b, e in chunks:
+            ctx.loss_fwd_factored(z[b:e], tokens[b:e], old[b:e],
+                                  None if mask is None else mask[b:e], grad=G[b:e], row_begin=b)
+        loss, stats = ctx.loss_finalize()
+        scale = ctx.loss_row_scale(grad_loss=gl)
+        ctx.get_error()
+        Gn = G[:, :V].double().cpu().numpy()
+        sc = scale.double().cpu().numpy()
+        with np.errstate(invalid="ignore"):
+            dl = sc[:, None] * Gn
+        dl[sc == 0] = 0.0          # rows without gradient (G untouched in compact mode)
+        tok = {k: v.cpu().numpy() for k, v in ctx.export_token_stats().items()}
+        rol = {k: v.cpu().numpy() for k, v in ctx.export_rollout_stats().items()}
+        out = dict(loss=float(loss.item()), stats=stats_to_dict(stats), dlogits=dl, G=Gn,
+                   scale=sc, tok=tok, rol=rol, adv_out=adv_out.cpu().numpy(),
+                   zv_out=zv_out.cpu().numpy(), launches=ctx.launch_count)
+        ctx.close()
+        return out
     for b, e in chunks:
         ctx.loss_fwd(z[b:e], tokens[b:e], old[b:e], None if mask is None else mask[b:e],
                      row_begin=b)
     loss, stats = ctx.loss_finalize()
-    gl = None if grad_loss is None else torch.tensor([grad_loss], dtype=torch.float32, device=dev)
     if in_place:
         dz = z
     else:
