@@ -195,11 +195,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_fwd_grad(const FwdParams p, c
     const float uy = rec.uy;
 
     // ---- pass 1: S, W relative to R = u_y (HBM read)
+    // fp32 sums per batch (two chains of ≤ 4·EPV/2 terms), accumulated in fp64 across batches:
+    // rows with a low-probability target (lp ≈ −14) lose ~44× in H = ln S − ln2·W/S, so a
+    // plain fp32 running sum over a thread's ~250 terms is not enough for 1e-5 on H
     float R = uy;
-    float2 s2 = make_float2(0.f, 0.f), w2 = make_float2(0.f, 0.f);
+    double S = 0.0, W = 0.0;
     {
       const float2 L2 = make_float2(lamL, lamL), N2 = make_float2(-R, -R);
       for (int j0 = tid; j0 < nvec; j0 += NT * U) {
+        float2 s2 = make_float2(0.f, 0.f), w2 = make_float2(0.f, 0.f);
         uint4 v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -229,9 +233,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_fwd_grad(const FwdParams p, c
             }
           }
         }
+        S += double(s2.x) + double(s2.y);
+        W += double(w2.x) + double(w2.y);
       }
     }
-    double S = double(s2.x) + double(s2.y), W = double(w2.x) + double(w2.y);
     block_sum2<NT>(S, W, s_red);
     if (!(S < 0x1p100) || !(fabs(W) < 0x1p110)) {
       // rare: overflow against u_y (lp < −69), −inf logits (0·−inf) or NaN/+inf input —
@@ -409,13 +414,14 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_ring(const FwdPar
     const int vy = rec.y / EPV, yoff = rec.y % EPV;
     const float uy = rec.uy;
 
-    // ---- pass 1
+    // ---- pass 1 (fp32 sums per chunk, fp64 across chunks: see k_fwd_grad)
     float R = uy;
-    float2 s2 = make_float2(0.f, 0.f), w2 = make_float2(0.f, 0.f);
+    double S = 0.0, W = 0.0;
     {
       const float2 L2 = make_float2(lamL, lamL), N2 = make_float2(-R, -R);
       for (int c = 0; c < nch; ++c) {
         if (c > 0) take(slot);
+        float2 s2 = make_float2(0.f, 0.f), w2 = make_float2(0.f, 0.f);
         uint4 v[VPT];
 #pragma unroll
         for (int u = 0; u < VPT; ++u)
@@ -443,9 +449,10 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_ring(const FwdPar
             }
           }
         }
+        S += double(s2.x) + double(s2.y);
+        W += double(w2.x) + double(w2.y);
       }
     }
-    double S = double(s2.x) + double(s2.y), W = double(w2.x) + double(w2.y);
     block_sum2_named<NTC>(S, W, s_red);
     if (!(S < 0x1p100) || !(fabs(W) < 0x1p110)) {
       // rare (see k_fwd_grad): redo from global memory with the row maximum as reference

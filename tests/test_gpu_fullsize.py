@@ -59,15 +59,31 @@ def build(name, dev, seed=None):
     return b
 
 
-def run(b, dev, bwd_rows=None, cfgkw=None):
+def run(b, dev, bwd_rows=None, cfgkw=None, factored=False):
     """prepare → fwd chunks → finalize → bwd chunks (32,768 rows, as bench.py). Returns the
-    loss/stats and, for each (chunk_start, rows-in-chunk) in bwd_rows, the gradient rows."""
+    loss/stats and, for each (chunk_start, rows-in-chunk) in bwd_rows, the gradient rows.
+    factored: espo_loss_fwd_factored chunks (G into one reused buffer, as bench.py --factored)
+    and the gradient rows as espo_loss_row_scale · G in fp64."""
     from paper_2512_07710_b200.espo import Espo, stats_to_dict
     ctx = Espo(b.V, logits_dtype=torch.bfloat16, device=dev.index, **(cfgkw or {}))
     tok = to_dev(b.tokens, torch.int32, dev)
     old = to_dev(b.old, torch.float32, dev)
     ctx.prepare(to_dev(b.rewards, torch.float32, dev), to_dev(b.group_ids, torch.int32, dev),
                 to_dev(b.seq_offsets, torch.int64, dev), n_tokens=b.T)
+    if factored:
+        dl = torch.empty((CHUNK, b.V), dtype=torch.bfloat16, device=dev)
+        Gs = {}
+        for c0 in range(0, b.T, CHUNK):
+            c1 = min(b.T, c0 + CHUNK)
+            ctx.loss_fwd_factored(b.buf[:c1 - c0], tok[c0:c1], old[c0:c1], None, grad=dl[:c1 - c0],
+                                  row_begin=c0)
+            if bwd_rows and c0 in bwd_rows:
+                Gs[c0] = dl[torch.as_tensor(bwd_rows[c0], device=dev)].double().cpu().numpy()
+        loss, stats = ctx.loss_finalize()
+        scale = ctx.loss_row_scale().double().cpu().numpy()
+        ctx.get_error()
+        grads = {c0: scale[c0 + np.asarray(bwd_rows[c0])][:, None] * G for c0, G in Gs.items()}
+        return ctx, float(loss.item()), stats_to_dict(stats), grads
     for c0 in range(0, b.T, CHUNK):
         c1 = min(b.T, c0 + CHUNK)
         ctx.loss_fwd(b.buf[:c1 - c0], tok[c0:c1], old[c0:c1], None, row_begin=c0)
@@ -84,13 +100,14 @@ def run(b, dev, bwd_rows=None, cfgkw=None):
     return ctx, float(loss.item()), stats_to_dict(stats), grads
 
 
-def test_c1_full_size():
+@pytest.mark.parametrize("factored", [False, True], ids=["two_sweep", "factored"])
+def test_c1_full_size(factored):
     dev = require_cuda()
     b = build("C1", dev)
     rng = np.random.default_rng(0)
     chunks = [0, 5 * CHUNK, b.T - CHUNK]
     bwd_rows = {c: np.sort(rng.choice(CHUNK, 48, replace=False)) for c in chunks}
-    ctx, loss, st, grads = run(b, dev, bwd_rows)
+    ctx, loss, st, grads = run(b, dev, bwd_rows, factored=factored)
     tok = {k: v.cpu().numpy() for k, v in ctx.export_token_stats().items()}
     rol = {k: v.cpu().numpy() for k, v in ctx.export_rollout_stats().items()}
     ctx.close()

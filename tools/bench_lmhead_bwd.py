@@ -1,7 +1,9 @@
 """Fused LM head + ESPO forward AND backward (espo_lmhead_fwd → finalize → espo_lmhead_bwd:
 tcgen05 recompute with the bf16 dz epilogue, then dh = dz·W and dW += dzᵀ·h) vs the unfused
 pipeline on the same data (torch.matmul logits in bf16 → espo_loss_fwd/bwd in place →
-torch.matmul dh and dW). One chunk of n rows, V = 151,936. Prints one JSON line."""
+torch.matmul dh and dW) vs the factored pipeline (torch.matmul logits → espo_loss_fwd_factored
+in place, G = onehot − p → espo_loss_row_scale s → dh = diag(s)·(G·W), dW += Gᵀ·(diag(s)·h):
+each logits row is read once). One chunk of n rows, V = 151,936. Prints one JSON line."""
 import json
 import os
 import sys
@@ -18,15 +20,22 @@ def main(d=4096, n=16384, V=151936, iters=3):
     h = (torch.randn(n, d, device=dev) / d ** 0.5 * 3).to(torch.bfloat16)
     W = torch.randn(V, d, device=dev).to(torch.bfloat16)
     tokens = torch.randint(0, V, (n,), device=dev, dtype=torch.int32)
-    old = torch.full((n,), -1.0, device=dev)
     G = 8
     rewards = torch.tensor([1.0, 0.0] * (G // 2), device=dev)
     gid = torch.zeros(G, dtype=torch.int32, device=dev)
     so = torch.arange(G + 1, device=dev, dtype=torch.int64) * (n // G)
     fctx = Espo(V, logits_dtype=torch.bfloat16, device=0)
     uctx = Espo(V, logits_dtype=torch.bfloat16, grad_dtype=torch.bfloat16, device=0)
+    # rollout log-probs near the current policy's (untimed): old = lp + N(0, 0.02²), so the
+    # clip fraction is realistic (a constant old_logp would clip nearly every token)
+    uctx.prepare(rewards, gid, so, n_tokens=n)
+    uctx.loss_fwd(torch.matmul(h, W.T), tokens, torch.zeros(n, device=dev))
+    uctx.loss_finalize()
+    old = (uctx.export_token_stats()["lp"] + 0.02 * torch.randn(n, device=dev)).contiguous()
+    xctx = Espo(V, logits_dtype=torch.bfloat16, grad_dtype=torch.bfloat16, device=0)
     dh = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
     dW = torch.zeros((V, d), dtype=torch.float32, device=dev)
+    sc = torch.empty(n, dtype=torch.float32, device=dev)
 
     def fused():
         fctx.prepare(rewards, gid, so, n_tokens=n)
@@ -43,8 +52,32 @@ def main(d=4096, n=16384, V=151936, iters=3):
         torch.matmul(z, W, out=dh)
         dW.add_(torch.matmul(z.T, h))             # bf16 GEMM, fp32 accumulate into dW
 
+    def factored():
+        xctx.prepare(rewards, gid, so, n_tokens=n)
+        z = torch.matmul(h, W.T)
+        xctx.loss_fwd_factored(z, tokens, old, grad=z)   # in place: z becomes G (bf16)
+        xctx.loss_finalize()
+        xctx.loss_row_scale(out=sc)
+        torch.matmul(z, W, out=dh)
+        dh.mul_(sc[:, None])                              # dh = diag(s)·(G·W)
+        dW.add_(torch.matmul(z.T, h * sc[:, None].to(h.dtype)))   # dW += Gᵀ·(diag(s)·h)
+
+    # agreement of the three backward results on one pass (dW from zero)
+    outs = {}
+    for name, fn in (("fused", fused), ("unfused", unfused), ("factored", factored)):
+        dW.zero_()
+        fn()
+        torch.cuda.synchronize()
+        outs[name] = (dh.float().clone(), dW.clone())
+    agree = {}
+    for name in ("fused", "factored"):
+        a, b = outs[name], outs["unfused"]
+        agree[name] = {"dh_rel_err": float((a[0] - b[0]).norm() / b[0].norm()),
+                       "dW_rel_err": float((a[1] - b[1]).norm() / b[1].norm())}
+    del outs
+
     res = {}
-    for name, fn in (("fused", fused), ("unfused", unfused)):
+    for name, fn in (("fused", fused), ("unfused", unfused), ("factored", factored)):
         for _ in range(2):
             fn()
         torch.cuda.synchronize()
@@ -59,6 +92,8 @@ def main(d=4096, n=16384, V=151936, iters=3):
                      "model_TFLOPs": 6.0 * n * V * d / (ms * 1e-3) / 1e12}
     fctx.get_error()
     uctx.get_error()
+    xctx.get_error()
+    res["agreement_vs_unfused"] = agree
     # fused backward alone (recompute + dz + 2 GEMMs)
     fctx.prepare(rewards, gid, so, n_tokens=n)
     fctx.lmhead_fwd(h, W, tokens, old)
@@ -72,6 +107,11 @@ def main(d=4096, n=16384, V=151936, iters=3):
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / iters
     res["fused_bwd_only"] = {"ms": ms, "TFLOPs_3gemm": 6.0 * n * V * d / (ms * 1e-3) / 1e12}
+    uctx.prepare(rewards, gid, so, n_tokens=n)
+    uctx.loss_fwd(torch.matmul(h, W.T), tokens, old)
+    from paper_2512_07710_b200.espo import stats_to_dict
+    st = stats_to_dict(uctx.loss_finalize()[1])
+    res["clipped_fraction"] = st["n_clipped_tokens"] / max(st["n_active_tokens"], 1)
     res["config"] = {"n": n, "V": V, "d": d,
                      "model_flops": "6·n·V·d (fwd logits GEMM + dh + dW GEMMs)"}
     print(json.dumps(res))
