@@ -96,6 +96,10 @@ def main(tag, out_dir="gpurun_out"):
     if os.path.exists(tr):
         t = traffic(tr)
         t["source"] = f"profiles/{tag}/traffic.csv (ncu dram__bytes_read/write over one step)"
+        jp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(jp):    # keep the factored-mode entries (written from their own capture)
+            old = json.load(open(jp))
+            t.update({k: v for k, v in old.items() if k.startswith("factored")})
         shutil.copy(tr, os.path.join(dst, "traffic.csv"))
         json.dump(t, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
         open(os.path.join(dst, "traffic.md"), "w").write(
