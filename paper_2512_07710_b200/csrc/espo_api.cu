@@ -1493,7 +1493,8 @@ espo_status espo_loss_fwd_factored(espo_ctx_t c, const void* logits, int64_t ld,
   const int al = logits == grad ? 1 : 0;
   // geometry (ESPO_OPT_FACTORED_IMPL): 0 = TMA ring, 20 consumer warps + 1 producer warp,
   // 5 × 40 KB slots (measured best); 1 = CTA of 1024 threads re-reading each row
-  // through L2 with plain loads; 2-5 = other ring geometries
+  // through L2 with plain loads; 2 = 16 warps × 6 × 32 KB; 3 = the default with the TMEM
+  // stash of pass 1's exponentials; 4, 5 = two CTAs per SM (thrash the L2)
 #define ESPO_FG(NT, U)                                                                     \
   {                                                                                            \
     const int grid = c->num_sms * (1024 / NT);                                                  \
@@ -1502,22 +1503,22 @@ espo_status espo_loss_fwd_factored(espo_ctx_t c, const void* logits, int64_t ld,
     else if (bo) k_fwd_grad<float, __nv_bfloat16, NT, U><<<grid, NT, 0, s>>>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al);         \
     else k_fwd_grad<float, float, NT, U><<<grid, NT, 0, s>>>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al);                         \
   }
-#define ESPO_FGR(NC, ST, CH)                                                           \
+#define ESPO_FGR(NC, ST, CH, TM, CPS)                                                           \
   {                                                                                            \
     cudaError_t le;                                                                            \
-    if (bi && bo) le = launch_fwd_grad_ring<__nv_bfloat16, __nv_bfloat16, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s); \
-    else if (bi) le = launch_fwd_grad_ring<__nv_bfloat16, float, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s);         \
-    else if (bo) le = launch_fwd_grad_ring<float, __nv_bfloat16, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s);         \
-    else le = launch_fwd_grad_ring<float, float, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s);                         \
+    if (bi && bo) le = launch_fwd_grad_ring<__nv_bfloat16, __nv_bfloat16, NC, ST, CH, TM>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s, CPS); \
+    else if (bi) le = launch_fwd_grad_ring<__nv_bfloat16, float, NC, ST, CH, TM>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s, CPS);         \
+    else if (bo) le = launch_fwd_grad_ring<float, __nv_bfloat16, NC, ST, CH, TM>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s, CPS);         \
+    else le = launch_fwd_grad_ring<float, float, NC, ST, CH, TM>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s, CPS);                         \
     if (le != cudaSuccess) return cuda_status(le);                                             \
   }
   switch (c->factored_impl) {
     case 1: ESPO_FG(1024, 4) break;
-    case 2: ESPO_FGR(16, 6, 32768) break;
-    case 3: ESPO_FGR(24, 4, 49152) break;
-    case 4: ESPO_FGR(24, 5, 36864) break;
-    case 5: ESPO_FGR(28, 6, 28672) break;
-    default: ESPO_FGR(20, 5, 40960) break;
+    case 2: ESPO_FGR(16, 6, 32768, 0, 1) break;
+    case 3: ESPO_FGR(20, 5, 40960, 1, 1) break;
+    case 4: ESPO_FGR(10, 5, 20480, 0, 2) break;
+    case 5: ESPO_FGR(12, 4, 24576, 0, 2) break;
+    default: ESPO_FGR(20, 5, 40960, 0, 1) break;
   }
 #undef ESPO_FG
 #undef ESPO_FGR

@@ -298,6 +298,33 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_fwd_grad(const FwdParams p, c
   }
 }
 
+
+// TMEM stash helpers: one warp stores / loads N consecutive 32-bit columns of its 32 lanes.
+template <int N>
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  if constexpr (N == 8)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+                 "r"(r[6]), "r"(r[7]) : "memory");
+  else
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+                 ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[N];
+  if constexpr (N == 8)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7]) : "r"(taddr));
+  else
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // TMA-ring variant: one producer warp streams every row through a CTA-wide shared-memory
 // ring twice — pass 1 from HBM, pass 2 again (an L2 hit) — so up to STAGES × CH bytes are in
 // flight per SM independent of the consumers' registers, and the next row's pass-1 chunks
@@ -306,7 +333,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_fwd_grad(const FwdParams p, c
 // consumer thread i takes vectors i, i + 32·NC, … of it. The producer claims rows (count[2]),
 // publishes each slot's row in slot_row[] before its arrive (mbarrier release/acquire); a
 // zero-fill row is one slot without data, the end one slot with k = INT_MAX.
-template <typename Tin, typename Tout, int NC, int STAGES, int CH>
+template <typename Tin, typename Tout, int NC, int STAGES, int CH, int TM = 0>
 __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_ring(const FwdParams p,
                                                                    const FwdRec* list,
                                                                    const int32_t* zlist,
@@ -317,12 +344,19 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_ring(const FwdPar
   constexpr int NTC = NC * 32;                 // consumer threads
   static_assert(VPC % NTC == 0, "chunk must hold whole vectors per consumer thread");
   constexpr int VPT = VPC / NTC;               // vectors per consumer thread per chunk
+  // TM: pass 1 keeps its 2^(u − u_y) of the first CT chunks of a row in TMEM (each warp owns
+  // COLS columns of its lane quarter) and pass 2 turns them into p = 2^(u − u_y)·p_y with one
+  // FMUL instead of a second MUFU exponential
+  constexpr int WPQ = (NC + 3) / 4;            // consumer warps per TMEM lane quarter
+  constexpr int COLS = (512 / WPQ) / (VPT * EPV) * (VPT * EPV);
+  constexpr int CT = TM ? COLS / (VPT * EPV) : 0;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * CH);
   uint64_t* empty = full + STAGES;
   int* slot_row = reinterpret_cast<int*>(empty + STAGES);
   double* s_red = reinterpret_cast<double*>(slot_row + STAGES + (STAGES & 1));  // 8-B aligned
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_red + 2 * NC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int k = 0; k < STAGES; ++k) {
@@ -331,7 +365,14 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_ring(const FwdPar
     }
     fence_mbar_init();
   }
+  if (TM && warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (TM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int n = count[0], nz = count[1];
   const int V = p.V;
   const int nvec = (V + EPV - 1) / EPV;
@@ -391,12 +432,15 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_ring(const FwdPar
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
   };
+  // this warp's TMEM columns: lanes 32·(warp % 4) …, columns (warp / 4)·COLS …
+  const uint32_t tcol = TM ? *tmem_slot + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * COLS) : 0u;
+  const bool stash_ok = TM && nch > CT;        // the first CT chunks of every row are full
   for (;;) {
     int slot;
     const int k = take(slot);
     if (k >= n) {
       release(slot);
-      if (k == INT_MAX) return;
+      if (k == INT_MAX) break;
       char* orow = static_cast<char*>(grad) + int64_t(zlist[k - n]) * gpitch;
       constexpr int EPO = Out<Tout>::EPV;
       const int nfull = V / EPO;
@@ -427,6 +471,34 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_ring(const FwdPar
         for (int u = 0; u < VPT; ++u)
           v[u] = lds128(ring + size_t(slot) * CH + size_t(u * NTC + tid) * 16);
         release(slot);
+        if (TM && stash_ok && c < CT) {          // full chunk: every lane has VPT vectors
+#pragma unroll
+          for (int u = 0; u < VPT; ++u) {
+            const int j = c * VPC + u * NTC + tid;
+            float x[EPV];
+            Vec<Tin>::unpack(v[u], x);
+            const bool spec = j == vy || j == jrag;
+            if (spec) fix_special<EPV>(x, j, vy, yoff, V);
+            uint32_t ev[EPV];
+#pragma unroll
+            for (int e = 0; e < EPV; e += 2) {
+              float2 tt = __ffma2_rn(make_float2(x[e], x[e + 1]), L2, N2);
+              if (spec) {
+                tt.x = max_nan(tt.x, -127.f);
+                tt.y = max_nan(tt.y, -127.f);
+              }
+              const float2 ex = make_float2(ex2(tt.x), ex2(tt.y));
+              s2 = __fadd2_rn(s2, ex);
+              w2 = __ffma2_rn(ex, tt, w2);
+              ev[e] = __float_as_uint(ex.x);
+              ev[e + 1] = __float_as_uint(ex.y);
+            }
+            tmem_st8<EPV>(tcol + uint32_t((c * VPT + u) * EPV), ev);
+          }
+          S += double(s2.x) + double(s2.y);
+          W += double(w2.x) + double(w2.y);
+          continue;
+        }
 #pragma unroll
         for (int u = 0; u < VPT; ++u) {
           const int j = c * VPC + u * NTC + tid;
@@ -453,6 +525,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_ring(const FwdPar
         W += double(w2.x) + double(w2.y);
       }
     }
+    if (TM && stash_ok) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     block_sum2_named<NTC>(S, W, s_red);
     if (!(S < 0x1p100) || !(fabs(W) < 0x1p110)) {
       // rare (see k_fwd_grad): redo from global memory with the row maximum as reference
@@ -490,8 +563,36 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_ring(const FwdPar
     g.ng = -1.f;
     g.nlseL = nlseL;
     g.gq = qv;
+    // the stash holds 2^(u − u_y); p = that · 2^(u_y − lse) (= p_y ≤ 1). Not after the slow
+    // path (its reference moved off u_y and the stash may hold overflowed values).
+    const bool use_stash = TM && stash_ok && R == uy;
+    const float py2 = ex2(uy + nlseL);
     for (int c = 0; c < nch; ++c) {
       take(slot);
+      if (TM && use_stash && c < CT) {
+        release(slot);                          // the logits are not needed: p from TMEM
+#pragma unroll
+        for (int u = 0; u < VPT; ++u) {
+          const int j = c * VPC + u * NTC + tid;
+          float e[EPV];
+          tmem_ld8<EPV>(tcol + uint32_t((c * VPT + u) * EPV), e);
+          float d[EPV];
+          const float2 P2 = make_float2(-py2, -py2);
+#pragma unroll
+          for (int q2 = 0; q2 < EPV; q2 += 2) {
+            const float2 o = __fmul2_rn(P2, make_float2(e[q2], e[q2 + 1]));
+            d[q2] = o.x;
+            d[q2 + 1] = o.y;
+          }
+          if (j == vy) {
+#pragma unroll
+            for (int q2 = 0; q2 < EPV; ++q2)
+              if (q2 == yoff) d[q2] = qv;
+          }
+          store_out<Tin, Tout>(orow, j, d, V);
+        }
+        continue;
+      }
       uint4 v[VPT];
 #pragma unroll
       for (int u = 0; u < VPT; ++u)
@@ -507,19 +608,28 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_ring(const FwdPar
       }
     }
   }
+  if (TM) {                                    // all consumer warps are done with TMEM
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    bar_consumers(NTC);
+    if (warp == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512)
+                   : "memory");
+    }
+  }
 }
 
-template <typename Tin, typename Tout, int NC, int STAGES, int CH>
+template <typename Tin, typename Tout, int NC, int STAGES, int CH, int TM = 0>
 cudaError_t launch_fwd_grad_ring(const FwdParams& p, const FwdRec* list, const int32_t* zlist,
                                  const int* count, void* grad, int64_t ldg, int aliased,
-                                 int num_sms, cudaStream_t s) {
+                                 int num_sms, cudaStream_t s, int ctas_per_sm = 1) {
   static unsigned long long attr_mask = 0;
-  auto k = k_fwd_grad_ring<Tin, Tout, NC, STAGES, CH>;
+  auto k = k_fwd_grad_ring<Tin, Tout, NC, STAGES, CH, TM>;
   constexpr size_t smem = size_t(STAGES) * CH + size_t(STAGES) * 16 + size_t(STAGES + 1) * 4 + 8 +
                           size_t(NC) * 16 + 64;
   cudaError_t e = ensure_smem_attr(k, int(smem), attr_mask);
   if (e != cudaSuccess) return e;
-  k<<<num_sms, (NC + 1) * 32, smem, s>>>(p, list, zlist, count, grad, ldg, aliased);
+  k<<<num_sms * ctas_per_sm, (NC + 1) * 32, smem, s>>>(p, list, zlist, count, grad, ldg, aliased);
   return cudaGetLastError();
 }
 

@@ -43,7 +43,7 @@ def full_check(g, inst, cfg, rtol=1e-5, grad="f32", grad_loss=1.0):
     return ref2
 
 
-IMPLS = pytest.mark.parametrize("impl", [0, 1, 2, 4], ids=["ring20w", "cta1024", "ring16w", "ring24w"])
+IMPLS = pytest.mark.parametrize("impl", [0, 1, 2, 3], ids=["ring20w", "cta1024", "ring16w", "ring20w_tmem"])
 
 
 @IMPLS
@@ -204,20 +204,31 @@ def test_factored_errors_and_call_order(dev):
     ctx.close()
 
 
-@pytest.mark.parametrize("impl", [0, 1], ids=["ring20w", "cta1024"])
-def test_factored_full_vocab_low_probability_targets(dev, impl):
+@pytest.mark.parametrize("dt", ["bf16_f32", "f32_f32", "bf16_bf16"])
+@pytest.mark.parametrize("impl", [0, 1, 3, 4], ids=["ring20w", "cta1024", "ring20w_tmem", "ring10w_2cta"])
+def test_factored_full_vocab_low_probability_targets(dev, impl, dt):
     """V = 151,936 with targets ~14 nats below the row maximum: H = ln S − ln2·W/S cancels
-    ~40×, so the row sums must be accurate to ~1e-7 (fp32 per chunk, fp64 across chunks)."""
-    inst = tiny_instance(21, V=151936, group_sizes=(4, 4), L=6, dtype="bf16")
+    ~40×, so the row sums must be accurate to ~1e-7 (fp32 per chunk, fp64 across chunks).
+    Full-width rows also exercise the TMEM stash (geometry 3: pass 2 forms p from pass 1's
+    2^(u − u_y) for the first chunks of a row) and, with lp ≈ −90 rows, its slow-path
+    fallback; geometry 4 runs two CTAs per SM."""
+    inst = tiny_instance(21, V=151936, group_sizes=(4, 4), L=6, dtype="f32" if dt == "f32_f32" else "bf16")
     rng = np.random.default_rng(5)
     for t in range(inst.T):
         if t % 2 == 0:          # a background column: z ≈ −14 against a dominant entry
-            c = int(rng.integers(0, inst.V))
-            inst.tokens[t] = c
+            inst.tokens[t] = int(rng.integers(0, inst.V))
+    for t in (3, 17, 30):       # lp ≈ −90: the u_y-referenced sums overflow
+        inst.logits[t, inst.tokens[t]] = np.max(inst.logits[t]) - 90.0
     import espo_synth as S
+    if dt != "f32_f32":
+        inst.logits = S.round_to_bf16(inst.logits)
     lp = exact_lp(inst.logits, inst.tokens)
-    assert lp.min() < -10
+    assert lp.min() < -85
     inst.old_logp = S.drift_old_logp(lp, inst.seq_offsets, 21)
-    g = run_gpu(inst, dev, logits_dtype=torch.bfloat16, grad_dtype=torch.float32, factored=True,
-                factored_impl=impl)
-    full_check(g, inst, oracle_cfg(inst.V))
+    ldt = torch.float32 if dt == "f32_f32" else torch.bfloat16
+    gdt = torch.bfloat16 if dt == "bf16_bf16" else torch.float32
+    g = run_gpu(inst, dev, logits_dtype=ldt, grad_dtype=gdt, factored=True, factored_impl=impl)
+    if dt == "bf16_bf16":
+        full_check(g, inst, oracle_cfg(inst.V), rtol=2e-3, grad="bf16")
+    else:
+        full_check(g, inst, oracle_cfg(inst.V))
