@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--factored", action="store_true",
                    help="factored-gradient leg: espo_loss_fwd_factored (one sweep per row writes "
                         "G = onehot - p) + espo_loss_row_scale")
+    p.add_argument("--no-factored-leg", action="store_true",
+                   help="skip the factored-gradient leg reported beside the headline")
     p.add_argument("--factored-impl", type=int, default=0, help="ESPO_OPT_FACTORED_IMPL (0 = default)")
     p.add_argument("--e2e-mode", default="single-pass", choices=["single-pass", "two-sweep"],
                    help="e2e leg: logits chunks cross PCIe once (single-pass) or twice")
@@ -552,6 +554,34 @@ def main_ours(args):
         traffic = tr.get("factored_bytes_per_launch") if args.factored else \
             None if args.single_pass else tr.get("bwd_bytes_per_launch")
 
+    # the same workload through the factored-gradient API (one sweep per row; the consumer
+    # applies the row scale), reported beside the headline — not in place of it
+    factored = None
+    if not (args.factored or args.single_pass or args.no_factored_leg) and S_ == 1:
+        for _ in range(2):
+            run_step_factored(ctx, d, dlog)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            run_step_factored(ctx, d, dlog)
+        f1.record()
+        torch.cuda.synchronize(dev)
+        ctx.get_error()
+        t_f = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_f, op=dist.ReduceOp.MAX)
+        f_ms = float(t_f.item()) / args.steps
+        f_bytes = n_act * (2 * V + 4 + 4 + 16) + T * (4 + 4 + 1 + 8 + 9) + \
+            (n_act if args.compact else T) * 2 * V
+        factored = {"value": T * world / (f_ms * 1e-3), "unit": "tokens/s", "ms_per_step": f_ms,
+                    "achieved_hbm_gbs_step": f_bytes / (f_ms * 1e-3) / 1e9,
+                    "api": "espo_loss_fwd_factored + espo_loss_row_scale (dlogits = scale_t * G_t, "
+                           "G = onehot - softmax written by the statistics sweep; the consumer "
+                           "applies scale_t)"}
+
     e2e = None
     if not args.no_e2e and S_ == 1:
         tps, h2d, d2h, dt = run_e2e(ctx, d, dlog, args, dev)
@@ -614,6 +644,7 @@ def main_ours(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
+        "factored_gradient": factored,
         "clocks": clk,
         "loss": st["loss"],
     }
