@@ -633,6 +633,245 @@ cudaError_t launch_fwd_grad_ring(const FwdParams& p, const FwdRec* list, const i
   return cudaGetLastError();
 }
 
+// Rolling variant: the producer interleaves pass 2 of the previous row with pass 1 of the
+// current one chunk by chunk — P2(k−1, 0), P1(k, 0), P2(k−1, 1), P1(k, 1), … — so each SM
+// keeps HBM reads (the new row) and writes (the old row's G) in flight together all the time,
+// including while the consumers reduce a finished row, and the L2 holds about one row per SM
+// (the old row's chunks retire as the new row's arrive). Slot headers carry (row, pass,
+// chunk); the consumers follow them.
+template <typename Tin, typename Tout, int NC, int STAGES, int CH>
+__global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_roll(const FwdParams p,
+                                                                   const FwdRec* list,
+                                                                   const int32_t* zlist,
+                                                                   const int* count, void* grad,
+                                                                   int64_t ldg, int aliased) {
+  constexpr int EPV = Vec<Tin>::EPV;
+  constexpr int VPC = CH / 16;
+  constexpr int NTC = NC * 32;
+  static_assert(VPC % NTC == 0, "chunk must hold whole vectors per consumer thread");
+  constexpr int VPT = VPC / NTC;
+  constexpr int kZero = -1;                    // slot_meta of a zero-fill row
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * CH);
+  uint64_t* empty = full + STAGES;
+  int* slot_row = reinterpret_cast<int*>(empty + STAGES);
+  int* slot_meta = slot_row + STAGES;
+  double* s_red = reinterpret_cast<double*>(slot_meta + STAGES);   // 2·STAGES ints: 8-B aligned
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < STAGES; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], NC);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int n = count[0], nz = count[1];
+  const int V = p.V;
+  const int nvec = (V + EPV - 1) / EPV;
+  const uint32_t rowbytes = uint32_t(nvec) * 16u;
+  const int nch = static_cast<int>((rowbytes + CH - 1) / CH);
+  const int64_t pitch = p.ld * int64_t(sizeof(Tin));
+
+  if (warp == NC) {                            // ---------------- producer
+    if (lane != 0) return;
+    int* claim = const_cast<int*>(count) + 2;
+    const char* base = static_cast<const char*>(p.logits);
+    const uint64_t pol1 = policy_evict_normal(), pol2 = policy_evict_first();
+    uint32_t q = 0;
+    auto next_slot = [&]() {
+      const int slot = q % STAGES;
+      if (q >= STAGES) mbar_wait(&empty[slot], ((q / STAGES) - 1) & 1u);
+      ++q;
+      return slot;
+    };
+    auto emit = [&](int k, const char* row, int pass, int c) {
+      const int slot = next_slot();
+      const uint32_t off = uint32_t(c) * CH;
+      const uint32_t bytes = min(uint32_t(CH), rowbytes - off);
+      slot_row[slot] = k;
+      slot_meta[slot] = pass | (c << 1);
+      mbar_arrive_tx(&full[slot], bytes);
+      bulk_g2s(ring + size_t(slot) * CH, row + off, bytes, &full[slot], pass ? pol2 : pol1);
+    };
+    int prevk = -1;
+    const char* prow = nullptr;
+    for (;;) {
+      const int k = atomicAdd(claim, 1);
+      if (k >= n) {
+        if (k < n + nz) {                      // zero-fill row: a slot without data
+          const int slot = next_slot();
+          slot_row[slot] = k;
+          slot_meta[slot] = kZero;
+          mbar_arrive(&full[slot]);
+          continue;
+        }
+        if (prevk >= 0)
+          for (int c = 0; c < nch; ++c) emit(prevk, prow, 1, c);
+        const int slot = next_slot();          // the end
+        slot_row[slot] = INT_MAX;
+        slot_meta[slot] = kZero;
+        mbar_arrive(&full[slot]);
+        return;
+      }
+      const char* row = base + int64_t(list[k].r) * pitch;
+      for (int c = 0; c < nch; ++c) {
+        if (prevk >= 0) emit(prevk, prow, 1, c);
+        emit(k, row, 0, c);
+      }
+      prevk = k;
+      prow = row;
+    }
+  }
+
+  // ------------------------------------------------------------------ consumers
+  const int tid = threadIdx.x;
+  const int jrag = (V % EPV) ? nvec - 1 : -1;
+  const float lamL = p.lam_log2e;
+  const int64_t gpitch = ldg * int64_t(sizeof(Tout));
+  const bool coh = aliased != 0;
+  const float2 L2 = make_float2(lamL, lamL);
+  uint32_t q = 0;
+  // current row (pass 1 in progress) and previous row (pass 2 pending)
+  int cvy = 0, cyoff = 0, cr = 0;
+  float cuy = 0.f;
+  double S = 0.0, W = 0.0;
+  int pvy = 0, pyoff = 0;
+  char* porow = nullptr;
+  BwdRec g;
+  g.ng = -1.f;
+  for (;;) {
+    const int slot = q % STAGES;
+    mbar_wait(&full[slot], (q / STAGES) & 1u);
+    ++q;
+    const int k = slot_row[slot], meta = slot_meta[slot];
+    if (meta == kZero) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (k == INT_MAX) return;
+      char* orow = static_cast<char*>(grad) + int64_t(zlist[k - n]) * gpitch;
+      constexpr int EPO = Out<Tout>::EPV;
+      const int nfull = V / EPO;
+      const uint4 z = make_uint4(0, 0, 0, 0);
+      for (int j = tid; j < nfull; j += NTC) st_stream(orow + int64_t(j) * 16, z);
+      for (int c = nfull * EPO + tid; c < V; c += NTC) {
+        if (sizeof(Tout) == 4) reinterpret_cast<float*>(orow)[c] = 0.f;
+        else reinterpret_cast<uint16_t*>(orow)[c] = 0;
+      }
+      continue;
+    }
+    const int pass = meta & 1, c = meta >> 1;
+    uint4 v[VPT];
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) v[u] = lds128(ring + size_t(slot) * CH + size_t(u * NTC + tid) * 16);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (pass == 1) {                           // ---- G of the previous row
+#pragma unroll
+      for (int u = 0; u < VPT; ++u) {
+        const int j = c * VPC + u * NTC + tid;
+        if (j >= nvec) continue;
+        float d[EPV];
+        dz_vec<Tin>(v[u], j, pvy, pyoff, lamL, g, d);
+        store_out<Tin, Tout>(porow, j, d, V);
+      }
+      continue;
+    }
+    // ---- pass 1 of the current row
+    if (c == 0) {
+      const FwdRec rec = list[k];
+      cr = rec.r;
+      cvy = rec.y / EPV;
+      cyoff = rec.y % EPV;
+      cuy = rec.uy;
+      S = 0.0;
+      W = 0.0;
+    }
+    {
+      const float2 N2 = make_float2(-cuy, -cuy);
+      float2 s2 = make_float2(0.f, 0.f), w2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < VPT; ++u) {
+        const int j = c * VPC + u * NTC + tid;
+        if (j >= nvec) continue;
+        float x[EPV];
+        Vec<Tin>::unpack(v[u], x);
+        if (j == cvy || j == jrag) {
+          fix_special<EPV>(x, j, cvy, cyoff, V);
+          float s = 0.f, w = 0.f;
+          acc_vec<EPV, true>(x, lamL, -cuy, s, w);
+          s2.x += s;
+          w2.x += w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < EPV; e += 2) {
+            const float2 tt = __ffma2_rn(make_float2(x[e], x[e + 1]), L2, N2);
+            const float2 ex = make_float2(ex2(tt.x), ex2(tt.y));
+            s2 = __fadd2_rn(s2, ex);
+            w2 = __ffma2_rn(ex, tt, w2);
+          }
+        }
+      }
+      S += double(s2.x) + double(s2.y);
+      W += double(w2.x) + double(w2.y);
+    }
+    if (c != nch - 1) continue;
+    // ---- the row's last chunk: reduce, statistics, it becomes the pass-2 row
+    const char* grow = static_cast<const char*>(p.logits) + int64_t(cr) * pitch;
+    block_sum2_named<NTC>(S, W, s_red);
+    float R = cuy;
+    if (!(S < 0x1p100) || !(fabs(W) < 0x1p110)) {   // rare: see k_fwd_grad
+      float m = -INFINITY;
+      bool bad = false;
+      for (int j = tid; j < nvec; j += NTC) {
+        float x[EPV];
+        Vec<Tin>::unpack(coh ? ld_stream_coherent(grow + int64_t(j) * 16) : ld_stream(grow + int64_t(j) * 16), x);
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) {
+          if (j * EPV + e >= V) continue;
+          bad |= isnan(x[e]) || x[e] == INFINITY;
+          m = fmaxf(m, x[e] * lamL);
+        }
+      }
+      if (bad) set_error(p.ws.err, ESPO_ERR_NONFINITE_INPUT);
+      R = block_max_named<NTC>(m, reinterpret_cast<float*>(s_red));
+      if (R == -INFINITY || !(R < INFINITY)) R = cuy;
+      float sa = 0.f, wa = 0.f;
+      for (int j = tid; j < nvec; j += NTC) {
+        float x[EPV];
+        Vec<Tin>::unpack(coh ? ld_stream_coherent(grow + int64_t(j) * 16) : ld_stream(grow + int64_t(j) * 16), x);
+        fix_special<EPV>(x, j, cvy, cyoff, V);
+        acc_vec<EPV, true>(x, lamL, -R, sa, wa);
+      }
+      S = sa;
+      W = wa;
+      block_sum2_named<NTC>(S, W, s_red);
+    }
+    float nlseL, qv;
+    fg_stats(R, float(S), float(W), cuy, p.ws, p.row_begin + cr, tid == 0, nlseL, qv);
+    g.nlseL = nlseL;
+    g.gq = qv;
+    pvy = cvy;
+    pyoff = cyoff;
+    porow = static_cast<char*>(grad) + int64_t(cr) * gpitch;
+  }
+}
+
+template <typename Tin, typename Tout, int NC, int STAGES, int CH>
+cudaError_t launch_fwd_grad_roll(const FwdParams& p, const FwdRec* list, const int32_t* zlist,
+                                 const int* count, void* grad, int64_t ldg, int aliased,
+                                 int num_sms, cudaStream_t s) {
+  static unsigned long long attr_mask = 0;
+  auto k = k_fwd_grad_roll<Tin, Tout, NC, STAGES, CH>;
+  constexpr size_t smem = size_t(STAGES) * CH + size_t(STAGES) * 16 + size_t(STAGES) * 8 +
+                          size_t(NC) * 16 + 64;
+  cudaError_t e = ensure_smem_attr(k, int(smem), attr_mask);
+  if (e != cudaSuccess) return e;
+  k<<<num_sms, (NC + 1) * 32, smem, s>>>(p, list, zlist, count, grad, ldg, aliased);
+  return cudaGetLastError();
+}
+
 // scale_t = λ·g_t = −grad·(λ/D)·c_t for valid rows, 0 otherwise (dlogits_t = scale_t·G_t).
 __global__ void __launch_bounds__(256) k_row_scale(int64_t row_begin, int64_t n_rows,
                                                    const float* grad_loss, Workspace ws,
