@@ -16,7 +16,9 @@ from tests.gpu_common import (check_dlogits_f32, check_exact_fields, check_loss,
 pytestmark = pytest.mark.gpu
 
 
-def run_cp(inst, dev, cp, cfgkw=None, logits_dtype=torch.float32, sub_chunks=2):
+def run_cp(inst, dev, cp, cfgkw=None, logits_dtype=torch.float32, sub_chunks=2, factored=False):
+    """factored: each CP rank runs espo_loss_fwd_factored on its block (G into one buffer) and
+    the gradient rows are espo_loss_row_scale · G (fp64 here)."""
     from paper_2512_07710_b200.espo import Espo, stats_to_dict
     T, V = inst.T, inst.V
     z = to_dev(inst.logits, torch.float32, dev).to(logits_dtype)
@@ -31,25 +33,37 @@ def run_cp(inst, dev, cp, cfgkw=None, logits_dtype=torch.float32, sub_chunks=2):
         c.attach_cp(k, cp, local=True)
         c.prepare(*args, n_tokens=T)
         ctxs.append(c)
+    G = torch.full((T, V), float("nan"), dtype=ctxs[0].grad_dtype, device=dev)
     for c in ctxs:                                   # each rank sweeps its own block
         lo, hi = c.cp_block()
         cuts = np.linspace(lo, hi, sub_chunks + 1).astype(int)
         for b, e in zip(cuts[:-1], cuts[1:]):
             if e > b:
-                c.loss_fwd(z[b:e], tok[b:e], old[b:e], mask[b:e], row_begin=int(b))
+                if factored:
+                    c.loss_fwd_factored(z[b:e], tok[b:e], old[b:e], mask[b:e], grad=G[b:e],
+                                        row_begin=int(b))
+                else:
+                    c.loss_fwd(z[b:e], tok[b:e], old[b:e], mask[b:e], row_begin=int(b))
     for c in ctxs:
         c.cp_gather_local(ctxs)
     dz = torch.full((T, V), float("nan"), dtype=ctxs[0].grad_dtype, device=dev)
+    dzf = np.full((T, V), np.nan)
     out = []
     for c in ctxs:
         loss, stats = c.loss_finalize()
         lo, hi = c.cp_block()
-        if hi > lo:
+        if hi > lo and factored:
+            sc = c.loss_row_scale(lo, hi - lo).double().cpu().numpy()
+            Gb = G[lo:hi].double().cpu().numpy()
+            with np.errstate(invalid="ignore"):
+                dzf[lo:hi] = sc[:, None] * Gb
+            dzf[lo:hi][sc == 0] = 0.0
+        elif hi > lo:
             c.loss_bwd(z[lo:hi], dz[lo:hi], row_begin=lo)
         c.get_error()
         out.append((float(loss.item()), stats_to_dict(stats)))
     res = dict(losses=[o[0] for o in out], loss=out[0][0], stats=out[0][1],
-               dlogits=dz.float().cpu().numpy(),
+               dlogits=dzf if factored else dz.float().cpu().numpy(),
                tok={k: v.cpu().numpy() for k, v in ctxs[0].export_token_stats().items()},
                rol={k: v.cpu().numpy() for k, v in ctxs[0].export_rollout_stats().items()})
     res["zv_out"] = res["rol"]["zv"]
@@ -107,3 +121,22 @@ def test_context_parallel_rejects_rows_outside_block():
         c.loss_finalize()
     assert e.value.code == "ESPO_ERR_BAD_STATE"
     c.close()
+
+
+@pytest.mark.parametrize("cp", [2, 3])
+def test_context_parallel_factored_equals_unsharded_factored(cp):
+    """CP ranks running the factored sweep on their token blocks: loss, statistics and every
+    scale·G row bitwise those of the unsharded factored run (rows are independent of the
+    block cut; K3 sees the same gathered values), hence at parity with the oracle."""
+    dev = require_cuda()
+    inst = workload_instance("C0")
+    g = run_cp(inst, dev, cp, factored=True)
+    u = run_gpu(inst, dev, factored=True)
+    assert all(l == u["loss"] for l in g["losses"])
+    assert g["stats"] == u["stats"]
+    assert np.array_equal(g["dlogits"], u["dlogits"])
+    cfg = oracle_cfg(inst.V)
+    ref = inst.run(cfg)
+    ref2, _ = decision_aware_reference(g, inst, ref, cfg)
+    check_loss(g, ref2, 1e-5)
+    check_dlogits_f32(g["dlogits"], oracle_dlogits(ref2, inst, cfg, np.arange(inst.T)))

@@ -232,3 +232,27 @@ def test_factored_full_vocab_low_probability_targets(dev, impl, dt):
         full_check(g, inst, oracle_cfg(inst.V), rtol=2e-3, grad="bf16")
     else:
         full_check(g, inst, oracle_cfg(inst.V))
+
+
+def test_factored_rlzvp_mode(dev):
+    """RL-ZVP: zero-variance rollouts are read by the factored sweep too; their
+    token advantages are entropy differences (absolute fp32 error ≈ β·1e-6/log V), so their
+    gradient rows are compared at that scale, the rest at 1e-5 (as test_rlzvp_mode)."""
+    from tests.gpu_common import check_exact_fields, check_token_stats
+    inst = workload_instance("C0")
+    kw = dict(zv_mode=O.ZV_RLZVP, zvp_beta=0.2)
+    g = run_gpu(inst, dev, cfgkw=kw, factored=True)
+    cfg = oracle_cfg(inst.V, **kw)
+    ref = inst.run(cfg)
+    check_exact_fields(g, ref)
+    check_token_stats(g, ref)
+    ref2, _ = decision_aware_reference(g, inst, ref, cfg)
+    check_loss(g, ref2, 1e-5)
+    zv_rows = np.zeros(inst.T, bool)
+    for i in range(inst.R):
+        if ref.zv[i]:
+            zv_rows[inst.seq_offsets[i]:inst.seq_offsets[i + 1]] = True
+    assert zv_rows.any()
+    want = oracle_dlogits(ref2, inst, cfg, np.arange(inst.T))
+    check_dlogits_f32(g["dlogits"][~zv_rows], want[~zv_rows])
+    assert np.abs(g["dlogits"][zv_rows] - want[zv_rows]).max() <= 1e-4 * np.abs(want[zv_rows]).max()
