@@ -84,7 +84,7 @@ def main(tag, out_dir="gpurun_out"):
             launch_summary.main(ll)
         open(os.path.join(dst, "launches.md"), "w").write(
             "# ncu launch list (gpu__time_duration.sum, --clock-control none)\n\n"
-            "Command: `python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline` "
+            "Command: `python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-factored-leg` "
             "(cold-cache serialised per-launch times: compare shares, not absolutes).\n\n"
             + buf.getvalue())
     for name in ("fwd", "bwd"):
@@ -105,6 +105,42 @@ def main(tag, out_dir="gpurun_out"):
         open(os.path.join(dst, "traffic.md"), "w").write(
             "# DRAM traffic per sweep launch (one step, ncu)\n\n```\n" + json.dumps(t, indent=1)
             + "\n```\n")
+    fl = os.path.join(src, "launches_factored.csv")
+    if os.path.exists(fl):      # factored-gradient mode: launch shares + DRAM bytes per sweep
+        shutil.copy(fl, os.path.join(dst, "launches_factored.csv"))
+        import io
+        import contextlib
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            launch_summary.main(fl)
+        open(os.path.join(dst, "launches_factored.md"), "w").write(
+            "# ncu launch list, factored-gradient mode (gpu__time_duration.sum, --clock-control none)\n\n"
+            "Command: `python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --factored` "
+            "(cold-cache serialised per-launch times: compare shares, not absolutes).\n\n"
+            + buf.getvalue())
+        with open(fl) as f:
+            lines = [l for l in f if l.startswith('"')]
+        per = {}
+        for r in csv.DictReader(lines):
+            if "k_fwd_grad" not in r["Kernel Name"]:
+                continue
+            u = r["Metric Unit"].lower()
+            sc = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "ns": 1, "usecond": 1e3,
+                  "msecond": 1e6}.get(u, 1)
+            per.setdefault(int(r["ID"]), {})[r["Metric Name"]] = float(r["Metric Value"].replace(",", "")) * sc
+        ids = sorted(per)
+        last = ids[-64:] if len(ids) >= 64 else ids
+        jp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        t = json.load(open(jp)) if os.path.exists(jp) else {}
+        t["factored_bytes_per_launch"] = sum(per[i].get("dram__bytes_read.sum", 0) + per[i].get("dram__bytes_write.sum", 0) for i in last) / max(len(last), 1)
+        t["factored_launches"] = len(last)
+        t["factored_ms_total"] = sum(per[i].get("gpu__time_duration.sum", 0) for i in last) / 1e6
+        t["factored_source"] = f"profiles/{tag}/launches_factored.csv (ncu dram__bytes_read/write of k_fwd_grad* over the last step of bench.py --factored --steps 1)"
+        json.dump(t, open(jp, "w"), indent=1)
+    rep = os.path.join(src, "prof_factored.ncu-rep")
+    if os.path.exists(rep):
+        open(os.path.join(dst, "ncu_factored.md"), "w").write(
+            full_capture_md(rep, "k_fwd_grad_ring (factored-gradient sweep, default geometry)"))
     for f in ("bench_full.json", "bench_full.err"):
         p = os.path.join(src, f)
         if os.path.exists(p):
