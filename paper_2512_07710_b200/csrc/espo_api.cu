@@ -434,7 +434,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->lmh_2cta = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_FACTORED_IMPL:
-      if (value < 0 || value > 11) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 8) return ESPO_ERR_INVALID_ARGUMENT;
       c->factored_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_BWD_ROWS:
@@ -1495,8 +1495,7 @@ espo_status espo_loss_fwd_factored(espo_ctx_t c, const void* logits, int64_t ld,
   // 5 × 40 KB slots (measured best); 1 = CTA of 1024 threads re-reading each row
   // through L2 with plain loads; 2 = 16 warps × 6 × 32 KB; 3 = the default with the TMEM
   // stash of pass 1's exponentials; 4, 5 = two CTAs per SM (thrash the L2); 6-8 = rolling
-  // interleave of pass 2 (row k−1) with pass 1 (row k) (longer L2 reuse distance: slower);
-  // 9-11 = rows split over a 2-CTA cluster, halves' sums exchanged through DSMEM
+  // interleave of pass 2 (row k−1) with pass 1 (row k) (longer L2 reuse distance: slower)
 #define ESPO_FG(NT, U)                                                                     \
   {                                                                                            \
     const int grid = c->num_sms * (1024 / NT);                                                  \
@@ -1523,19 +1522,7 @@ espo_status espo_loss_fwd_factored(espo_ctx_t c, const void* logits, int64_t ld,
     else le = launch_fwd_grad_roll<float, float, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s);                         \
     if (le != cudaSuccess) return cuda_status(le);                                             \
   }
-#define ESPO_FGC(NC, ST, CH)                                                                   \
-  {                                                                                            \
-    cudaError_t le;                                                                            \
-    if (bi && bo) le = launch_fwd_grad_cl<__nv_bfloat16, __nv_bfloat16, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s); \
-    else if (bi) le = launch_fwd_grad_cl<__nv_bfloat16, float, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s);         \
-    else if (bo) le = launch_fwd_grad_cl<float, __nv_bfloat16, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s);         \
-    else le = launch_fwd_grad_cl<float, float, NC, ST, CH>(p, list, c->ws.zlist, c->ws.count, grad, ldg, al, c->num_sms, s);                         \
-    if (le != cudaSuccess) return cuda_status(le);                                             \
-  }
   switch (c->factored_impl) {
-    case 9: ESPO_FGC(10, 5, 20480) break;
-    case 10: ESPO_FGC(12, 4, 24576) break;
-    case 11: ESPO_FGC(8, 6, 16384) break;
     case 6: ESPO_FGL(20, 5, 40960) break;
     case 7: ESPO_FGL(16, 6, 32768) break;
     case 8: ESPO_FGL(16, 12, 16384) break;
@@ -1549,7 +1536,6 @@ espo_status espo_loss_fwd_factored(espo_ctx_t c, const void* logits, int64_t ld,
 #undef ESPO_FG
 #undef ESPO_FGR
 #undef ESPO_FGL
-#undef ESPO_FGC
   ESPO_LAUNCHED(c);
   c->covered[row_begin] = row_begin + n_rows;
   c->n_covered += n_rows;

@@ -23,7 +23,6 @@
 #include "k_rowlist.cuh"
 #include "k_rowstats.cuh"
 #include "k_dlogits.cuh"
-#include "k_lmhead2.cuh"   // cluster helpers (mapa_rank, bounded_wait, arrive_remote)
 
 namespace espo {
 
@@ -870,226 +869,6 @@ cudaError_t launch_fwd_grad_roll(const FwdParams& p, const FwdRec* list, const i
   cudaError_t e = ensure_smem_attr(k, int(smem), attr_mask);
   if (e != cudaSuccess) return e;
   k<<<num_sms, (NC + 1) * 32, smem, s>>>(p, list, zlist, count, grad, ldg, aliased);
-  return cudaGetLastError();
-}
-
-// Cluster variant: a row is split between the two CTAs of a cluster (thread-block cluster of
-// 2, both halves streamed through each CTA's own TMA ring twice). The halves' (S, W) partials
-// meet over distributed shared memory (a remote st.shared::cluster + a remote mbarrier arrive,
-// one exchange per row), so each SM keeps only half a row live per CTA and can host two CTAs
-// — two independent row pipelines per SM, whose reduction bubbles overlap — with the same
-// ~1 row per SM in L2 as the one-CTA ring. Rows are assigned statically (cluster c takes rows
-// c, c + #clusters, …; uniform work), zero-fill rows after them.
-template <typename Tin, typename Tout, int NC, int STAGES, int CH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NC + 1) * 32, 1)
-    k_fwd_grad_cl(const FwdParams p, const FwdRec* list, const int32_t* zlist, const int* count,
-                  void* grad, int64_t ldg, int aliased) {
-  constexpr int EPV = Vec<Tin>::EPV;
-  constexpr int VPC = CH / 16;
-  constexpr int NTC = NC * 32;
-  static_assert(VPC % NTC == 0, "chunk must hold whole vectors per consumer thread");
-  constexpr int VPT = VPC / NTC;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * CH);
-  uint64_t* empty = full + STAGES;
-  uint64_t* xbar = empty + STAGES;             // [2] the peer's partial has arrived
-  double* xbuf = reinterpret_cast<double*>(xbar + 2);   // [2][2] the peer's (S, W)
-  double* s_red = xbuf + 4;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < STAGES; ++k) {
-      mbar_init(&full[k], 1);
-      mbar_init(&empty[k], NC);
-    }
-    mbar_init(&xbar[0], 1);
-    mbar_init(&xbar[1], 1);
-    fence_mbar_init();
-  }
-  cluster_sync_all();                          // both CTAs' barriers exist before any remote use
-  const int n = count[0], nz = count[1];
-  const int V = p.V;
-  const int nvec = (V + EPV - 1) / EPV;
-  const int h = (nvec + 1) / 2;                // rank 0: vectors [0, h), rank 1: [h, nvec)
-  const int v_lo = rank ? h : 0, v_hi = rank ? nvec : h;
-  const uint32_t hbytes = uint32_t(v_hi - v_lo) * 16u;
-  const int nch = static_cast<int>((hbytes + CH - 1) / CH);
-  const int64_t pitch = p.ld * int64_t(sizeof(Tin));
-  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-
-  if (warp == NC) {                            // ---------------- producer
-    if (lane != 0) return;
-    const char* base = static_cast<const char*>(p.logits);
-    const uint64_t pol1 = policy_evict_normal(), pol2 = policy_evict_first();
-    uint32_t q = 0;
-    for (int k = cid; k < n; k += ncl) {
-      const char* src = base + int64_t(list[k].r) * pitch + int64_t(v_lo) * 16;
-      for (int pass = 0; pass < 2; ++pass)
-        for (int c = 0; c < nch; ++c) {
-          const int slot = q % STAGES;
-          if (q >= STAGES) mbar_wait(&empty[slot], ((q / STAGES) - 1) & 1u);
-          ++q;
-          const uint32_t off = uint32_t(c) * CH;
-          const uint32_t bytes = min(uint32_t(CH), hbytes - off);
-          mbar_arrive_tx(&full[slot], bytes);
-          bulk_g2s(ring + size_t(slot) * CH, src + off, bytes, &full[slot], pass ? pol2 : pol1);
-        }
-    }
-    return;
-  }
-
-  // ------------------------------------------------------------------ consumers
-  const int tid = threadIdx.x;
-  const int jrag = (V % EPV) ? nvec - 1 : -1;
-  const float lamL = p.lam_log2e;
-  const int64_t gpitch = ldg * int64_t(sizeof(Tout));
-  const bool coh = aliased != 0;
-  const float2 L2 = make_float2(lamL, lamL);
-  const uint32_t xbuf_peer = mapa_rank(smem_u32(xbuf), peer);
-  const uint32_t xbar_peer = mapa_rank(smem_u32(xbar), peer);
-  uint32_t q = 0;
-  int it = 0;                                  // rows done by this cluster
-  for (int k = cid; k < n; k += ncl, ++it) {
-    const FwdRec rec = list[k];
-    const char* grow = static_cast<const char*>(p.logits) + int64_t(rec.r) * pitch;
-    char* orow = static_cast<char*>(grad) + int64_t(rec.r) * gpitch;
-    const int vy = rec.y / EPV, yoff = rec.y % EPV;
-    const float uy = rec.uy;
-    // ---- pass 1 over this CTA's half
-    double S = 0.0, W = 0.0;
-    {
-      const float2 N2 = make_float2(-uy, -uy);
-      for (int c = 0; c < nch; ++c) {
-        const int slot = q % STAGES;
-        mbar_wait(&full[slot], (q / STAGES) & 1u);
-        ++q;
-        uint4 v[VPT];
-#pragma unroll
-        for (int u = 0; u < VPT; ++u) v[u] = lds128(ring + size_t(slot) * CH + size_t(u * NTC + tid) * 16);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        float2 s2 = make_float2(0.f, 0.f), w2 = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int u = 0; u < VPT; ++u) {
-          const int j = v_lo + c * VPC + u * NTC + tid;
-          if (j >= v_hi) continue;
-          float x[EPV];
-          Vec<Tin>::unpack(v[u], x);
-          if (j == vy || j == jrag) {
-            fix_special<EPV>(x, j, vy, yoff, V);
-            float sa = 0.f, wa = 0.f;
-            acc_vec<EPV, true>(x, lamL, -uy, sa, wa);
-            s2.x += sa;
-            w2.x += wa;
-          } else {
-#pragma unroll
-            for (int e = 0; e < EPV; e += 2) {
-              const float2 tt = __ffma2_rn(make_float2(x[e], x[e + 1]), L2, N2);
-              const float2 ex = make_float2(ex2(tt.x), ex2(tt.y));
-              s2 = __fadd2_rn(s2, ex);
-              w2 = __ffma2_rn(ex, tt, w2);
-            }
-          }
-        }
-        S += double(s2.x) + double(s2.y);
-        W += double(w2.x) + double(w2.y);
-      }
-    }
-    block_sum2_named<NTC>(S, W, s_red);
-    // ---- exchange the halves' partials (fixed order: rank 0's half first on both CTAs)
-    const int par = it & 1;
-    if (tid == 0) {
-      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(xbuf_peer + uint32_t(par * 16)), "d"(S) : "memory");
-      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(xbuf_peer + uint32_t(par * 16 + 8)), "d"(W) : "memory");
-      arrive_remote(xbar_peer + uint32_t(par * 8));
-    }
-    bounded_wait(smem_u32(&xbar[par]), uint32_t((it >> 1) & 1));
-    const double Sp = xbuf[par * 2], Wp = xbuf[par * 2 + 1];
-    S = rank ? Sp + S : S + Sp;
-    W = rank ? Wp + W : W + Wp;
-    float R = uy;
-    if (!(S < 0x1p100) || !(fabs(W) < 0x1p110)) {
-      // rare (see k_fwd_grad): both CTAs recompute the whole row from global memory with the
-      // row maximum as reference — same data, same order, so the same statistics
-      float m = -INFINITY;
-      bool bad = false;
-      for (int j = tid; j < nvec; j += NTC) {
-        float x[EPV];
-        Vec<Tin>::unpack(coh ? ld_stream_coherent(grow + int64_t(j) * 16) : ld_stream(grow + int64_t(j) * 16), x);
-#pragma unroll
-        for (int e = 0; e < EPV; ++e) {
-          if (j * EPV + e >= V) continue;
-          bad |= isnan(x[e]) || x[e] == INFINITY;
-          m = fmaxf(m, x[e] * lamL);
-        }
-      }
-      if (bad) set_error(p.ws.err, ESPO_ERR_NONFINITE_INPUT);
-      R = block_max_named<NTC>(m, reinterpret_cast<float*>(s_red));
-      if (R == -INFINITY || !(R < INFINITY)) R = uy;
-      float sa = 0.f, wa = 0.f;
-      for (int j = tid; j < nvec; j += NTC) {
-        float x[EPV];
-        Vec<Tin>::unpack(coh ? ld_stream_coherent(grow + int64_t(j) * 16) : ld_stream(grow + int64_t(j) * 16), x);
-        fix_special<EPV>(x, j, vy, yoff, V);
-        acc_vec<EPV, true>(x, lamL, -R, sa, wa);
-      }
-      S = sa;
-      W = wa;
-      block_sum2_named<NTC>(S, W, s_red);
-    }
-    float nlseL, qv;
-    fg_stats(R, float(S), float(W), uy, p.ws, p.row_begin + rec.r, rank == 0 && tid == 0, nlseL, qv);
-    // ---- pass 2 over this CTA's half
-    BwdRec g;
-    g.ng = -1.f;
-    g.nlseL = nlseL;
-    g.gq = qv;
-    for (int c = 0; c < nch; ++c) {
-      const int slot = q % STAGES;
-      mbar_wait(&full[slot], (q / STAGES) & 1u);
-      ++q;
-      uint4 v[VPT];
-#pragma unroll
-      for (int u = 0; u < VPT; ++u) v[u] = lds128(ring + size_t(slot) * CH + size_t(u * NTC + tid) * 16);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-#pragma unroll
-      for (int u = 0; u < VPT; ++u) {
-        const int j = v_lo + c * VPC + u * NTC + tid;
-        if (j >= v_hi) continue;
-        float d[EPV];
-        dz_vec<Tin>(v[u], j, vy, yoff, lamL, g, d);
-        store_out<Tin, Tout>(orow, j, d, V);
-      }
-    }
-  }
-  // ---- zero-fill rows (no data): each CTA writes its half
-  constexpr int EPO = Out<Tout>::EPV;
-  const int o_lo = v_lo * EPV, o_hi = min(V, v_hi * EPV);   // this CTA's columns
-  for (int k = cid; k < nz; k += ncl) {
-    char* orow = static_cast<char*>(grad) + int64_t(zlist[k]) * gpitch;
-    const int f_lo = (o_lo + EPO - 1) / EPO, f_hi = o_hi / EPO;   // whole 16-byte vectors
-    const uint4 z = make_uint4(0, 0, 0, 0);
-    for (int j = f_lo + tid; j < f_hi; j += NTC) st_stream(orow + int64_t(j) * 16, z);
-    for (int c = o_lo + tid; c < o_hi; c += NTC) {
-      if (c >= f_lo * EPO && c < f_hi * EPO) continue;
-      if (sizeof(Tout) == 4) reinterpret_cast<float*>(orow)[c] = 0.f;
-      else reinterpret_cast<uint16_t*>(orow)[c] = 0;
-    }
-  }
-}
-
-template <typename Tin, typename Tout, int NC, int STAGES, int CH>
-cudaError_t launch_fwd_grad_cl(const FwdParams& p, const FwdRec* list, const int32_t* zlist,
-                               const int* count, void* grad, int64_t ldg, int aliased,
-                               int num_sms, cudaStream_t s) {
-  static unsigned long long attr_mask = 0;
-  auto k = k_fwd_grad_cl<Tin, Tout, NC, STAGES, CH>;
-  constexpr size_t smem = size_t(STAGES) * CH + size_t(STAGES) * 16 + 16 + 32 + size_t(NC) * 16 + 64;
-  cudaError_t e = ensure_smem_attr(k, int(smem), attr_mask);
-  if (e != cudaSuccess) return e;
-  k<<<num_sms * 2, (NC + 1) * 32, smem, s>>>(p, list, zlist, count, grad, ldg, aliased);
   return cudaGetLastError();
 }
 

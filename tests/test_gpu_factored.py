@@ -43,7 +43,7 @@ def full_check(g, inst, cfg, rtol=1e-5, grad="f32", grad_loss=1.0):
     return ref2
 
 
-IMPLS = pytest.mark.parametrize("impl", [0, 1, 3, 9], ids=["ring20w", "cta1024", "ring20w_tmem", "cluster2"])
+IMPLS = pytest.mark.parametrize("impl", [0, 1, 3, 6], ids=["ring20w", "cta1024", "ring20w_tmem", "roll20w"])
 
 
 @IMPLS
@@ -205,7 +205,7 @@ def test_factored_errors_and_call_order(dev):
 
 
 @pytest.mark.parametrize("dt", ["bf16_f32", "f32_f32", "bf16_bf16"])
-@pytest.mark.parametrize("impl", [0, 1, 3, 4, 6, 9, 10], ids=["ring20w", "cta1024", "ring20w_tmem", "ring10w_2cta", "roll20w", "cluster2", "cluster2_12w"])
+@pytest.mark.parametrize("impl", [0, 1, 3, 4, 6], ids=["ring20w", "cta1024", "ring20w_tmem", "ring10w_2cta", "roll20w"])
 def test_factored_full_vocab_low_probability_targets(dev, impl, dt):
     """V = 151,936 with targets ~14 nats below the row maximum: H = ln S − ln2·W/S cancels
     ~40×, so the row sums must be accurate to ~1e-7 (fp32 per chunk, fp64 across chunks).

@@ -12,3 +12,6 @@ $Q > gpurun_out/plain_q2.log 2>&1 && ncu --set full --clock-control none --impor
 F="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --factored"
 $F > gpurun_out/plain_fll.log 2>&1 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_factored.csv $F > gpurun_out/ncu_fll.log 2>&1; echo "factored launch list exit=$?"
 $Q --factored > gpurun_out/plain_fq.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_fwd_grad" -s 10 -c 1 -o gpurun_out/prof_factored $Q --factored > gpurun_out/ncu_fact.log 2>&1; echo "ncu factored exit=$?"
+# summarise on the box (ncu reports are large): the profiles/ tree comes back under gpurun_out/
+python tools/make_profiles.py r1 > gpurun_out/make_profiles.log 2>&1; echo "make_profiles exit=$?"
+rm -rf gpurun_out/profiles_new && cp -r profiles gpurun_out/profiles_new && rm -f gpurun_out/*.ncu-rep
