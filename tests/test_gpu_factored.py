@@ -256,3 +256,17 @@ def test_factored_rlzvp_mode(dev):
     want = oracle_dlogits(ref2, inst, cfg, np.arange(inst.T))
     check_dlogits_f32(g["dlogits"][~zv_rows], want[~zv_rows])
     assert np.abs(g["dlogits"][zv_rows] - want[zv_rows]).max() <= 1e-4 * np.abs(want[zv_rows]).max()
+
+
+@pytest.mark.parametrize("impl", [0, 1], ids=["ring20w", "cta1024"])
+def test_factored_f32_logits_bf16_G(dev, c0, impl):
+    """fp32 logits, bf16 G (4 inputs → one 8-byte store per vector): the bf16 bound."""
+    g = run_gpu(c0, dev, grad_dtype=torch.bfloat16, factored=True, factored_impl=impl)
+    full_check(g, c0, oracle_cfg(c0.V), rtol=2e-3, grad="bf16")
+
+
+def test_factored_few_rows(dev):
+    """Fewer rows than CTAs (most CTAs claim nothing) and a chunk of one row."""
+    inst = tiny_instance(31, V=3000, group_sizes=(2, 2), L=3, mask_tail=1)
+    g = run_gpu(inst, dev, factored=True, chunks=[(0, 1), (1, inst.T)])
+    full_check(g, inst, oracle_cfg(inst.V))
