@@ -636,9 +636,9 @@ cudaError_t launch_fwd_grad_ring(const FwdParams& p, const FwdRec* list, const i
 // Rolling variant: the producer interleaves pass 2 of the previous row with pass 1 of the
 // current one chunk by chunk — P2(k−1, 0), P1(k, 0), P2(k−1, 1), P1(k, 1), … — so each SM
 // keeps HBM reads (the new row) and writes (the old row's G) in flight together all the time,
-// including while the consumers reduce a finished row, and the L2 holds about one row per SM
-// (the old row's chunks retire as the new row's arrive). Slot headers carry (row, pass,
-// chunk); the consumers follow them.
+// including while the consumers reduce a finished row. Slot headers carry (row, pass, chunk);
+// the consumers follow them. Measured slower than k_fwd_grad_ring (A/B option only): a
+// chunk's L2 reuse distance grows to ~2 row-volumes and the re-reads start missing.
 template <typename Tin, typename Tout, int NC, int STAGES, int CH>
 __global__ void __launch_bounds__((NC + 1) * 32, 1) k_fwd_grad_roll(const FwdParams p,
                                                                    const FwdRec* list,
