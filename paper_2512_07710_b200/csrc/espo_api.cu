@@ -121,6 +121,14 @@ struct espo_ctx_s {
   int blocks_per_sm = 0;
   int lmh_parts = 0;  // 0 = auto
   int factored_impl = 0;       // espo_loss_fwd_factored kernel geometry
+  // compact mode: a host copy of the rollout layout and the eliminated-group flags, taken
+  // asynchronously at prepare, bounds the backward grid by the rows that can carry gradient
+  // (when the copy has landed; otherwise the grid covers the whole chunk)
+  int64_t* h_so = nullptr;     // pinned [R+1]
+  uint8_t* h_cand = nullptr;   // pinned [R]
+  int h_cap = 0;
+  cudaEvent_t prep_ev = nullptr;
+  bool prep_ev_set = false;
   void* blocks_tok = nullptr;  // one allocation for all per-token arrays
   void* blocks_roll = nullptr; // one allocation for all per-rollout arrays
   void* blocks_scalar = nullptr;
@@ -405,6 +413,9 @@ espo_status espo_destroy(espo_ctx_t c) {
     for (void* q : c->x_opened) cudaIpcCloseMemHandle(q);
     if (c->d_xpeer) cudaFree(c->d_xpeer);
     if (c->x_buf) cudaFree(c->x_buf);
+    if (c->h_so) cudaFreeHost(c->h_so);
+    if (c->h_cand) cudaFreeHost(c->h_cand);
+    if (c->prep_ev) cudaEventDestroy(c->prep_ev);
   }
   delete c;
   return ESPO_OK;
@@ -485,6 +496,25 @@ espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* grou
   if (n_rollouts > 0) {
     k_row_seq<<<n_rollouts, 256, 0, s>>>(c->ws, n_rollouts);
     ESPO_LAUNCHED(c);
+  }
+  c->prep_ev_set = false;
+  if (!c->cfg.zero_fill_inactive_rows && n_rollouts > 0) {
+    if (n_rollouts > c->h_cap) {
+      if (c->h_so) cudaFreeHost(c->h_so);
+      if (c->h_cand) cudaFreeHost(c->h_cand);
+      c->h_so = nullptr;
+      c->h_cand = nullptr;
+      c->h_cap = 0;
+      ESPO_CUDA(cudaMallocHost(&c->h_so, size_t(n_rollouts + 1) * sizeof(int64_t)));
+      ESPO_CUDA(cudaMallocHost(&c->h_cand, size_t(n_rollouts)));
+      c->h_cap = n_rollouts;
+    }
+    if (!c->prep_ev) ESPO_CUDA(cudaEventCreateWithFlags(&c->prep_ev, cudaEventDisableTiming));
+    ESPO_CUDA(cudaMemcpyAsync(c->h_so, seq_offsets, size_t(n_rollouts + 1) * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, s));
+    ESPO_CUDA(cudaMemcpyAsync(c->h_cand, c->ws.cand, size_t(n_rollouts), cudaMemcpyDeviceToHost, s));
+    ESPO_CUDA(cudaEventRecord(c->prep_ev, s));
+    c->prep_ev_set = true;
   }
   c->state = State::Prepared;
   return ESPO_OK;
@@ -1236,6 +1266,19 @@ espo_status check_bwd_args(espo_ctx_t c, const void* logits, int64_t ld, const v
   return ESPO_OK;
 }
 
+// Rows of [b, e) that belong to rollouts whose group is not eliminated (an upper bound on the
+// rows with gradient), from the host copy taken at prepare — or e − b if it has not landed.
+int64_t candidate_rows(espo_ctx_t c, int64_t b, int64_t e) {
+  if (!c->prep_ev_set || cudaEventQuery(c->prep_ev) != cudaSuccess) return e - b;
+  const int64_t* so = c->h_so;
+  const int R = c->R;
+  int i = static_cast<int>(std::upper_bound(so, so + R + 1, b) - so) - 1;   // rollout holding row b
+  int64_t n = 0;
+  for (i = std::max(i, 0); i < R && so[i] < e; ++i)
+    if (c->h_cand[i]) n += std::max<int64_t>(0, std::min(e, so[i + 1]) - std::max(b, so[i]));
+  return n;
+}
+
 // K5 over one chunk (arguments checked).
 espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogits, int64_t ldg,
                        const float* grad_loss_dev, int64_t row_begin, int64_t n_rows,
@@ -1302,7 +1345,11 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
     const int rpb = impl == 9 ? 4 : (impl == 10 ? 8 : 16);
     const int epv = bi ? 8 : 4;
     const int ntiles = (((p.V + epv - 1) / epv) + 256 * 8 - 1) / (256 * 8);
-    const int64_t grid = (n_rows + rpb - 1) / rpb * int64_t(ntiles);
+    // compact mode writes only rows with gradient: bound the grid by the candidate rows so
+    // the blocks past the lists' end are not launched just to exit
+    const int64_t bound = p.zero_fill ? n_rows : candidate_rows(c, row_begin, row_begin + n_rows);
+    if (bound == 0) return ESPO_OK;
+    const int64_t grid = (bound + rpb - 1) / rpb * int64_t(ntiles);
     if (grid > INT32_MAX) return ESPO_ERR_INVALID_ARGUMENT;
 #define ESPO_TLIST(RPB)                                                                                    \
     if (bi && bo) k_dlogits_tlist<__nv_bfloat16, __nv_bfloat16, 8, RPB><<<unsigned(grid), 256, 0, s>>>(p, list, zl, cnt, ntiles); \
