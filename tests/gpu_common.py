@@ -38,7 +38,7 @@ def to_dev(a, dtype, dev):
 
 
 def run_gpu(inst, dev, cfgkw=None, logits_dtype=torch.float32, grad_dtype=None, chunks=None,
-            fwd_impl=0, bwd_impl=0, ld_pad=0, in_place=False, grad_loss=None, factored=False, factored_impl=0):
+            fwd_impl=0, bwd_impl=0, ld_pad=0, in_place=False, grad_loss=None, factored=False, factored_impl=0, sync_after_prepare=False):
     """Full pass on the GPU. chunks: list of (begin, end) for fwd (bwd uses the same).
     factored: espo_loss_fwd_factored per chunk + espo_loss_row_scale; "dlogits" is then
     scale_t · G_t formed in fp64 here (no second rounding), "G"/"scale" are returned too."""
@@ -62,6 +62,8 @@ def run_gpu(inst, dev, cfgkw=None, logits_dtype=torch.float32, grad_dtype=None, 
     ctx.prepare(to_dev(inst.rewards, torch.float32, dev), to_dev(inst.group_ids, torch.int32, dev),
                 to_dev(inst.seq_offsets, torch.int64, dev), n_tokens=T, adv_out=adv_out,
                 zv_out=zv_out)
+    if sync_after_prepare:     # lets host-side copies taken at prepare land before the sweeps
+        torch.cuda.synchronize(dev)
     chunks = chunks or [(0, T)]
     gl = None if grad_loss is None else torch.tensor([grad_loss], dtype=torch.float32, device=dev)
     if factored:

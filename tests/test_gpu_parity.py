@@ -274,3 +274,23 @@ def test_group_permutation_invariance_gpu(dev, c0):
     b = run_gpu(p, dev)
     assert b["loss"] == pytest.approx(a["loss"], rel=1e-12)
     assert np.array_equal(b["dlogits"], a["dlogits"][rows])
+
+
+def test_compact_grid_bound_variable_lengths(dev):
+    """Compact mode bounds the backward grid by the rows of non-eliminated rollouts, counted
+    on the host from the layout copied at prepare: with variable lengths, empty rollouts, an
+    eliminated group and chunks cutting rollouts, every row with gradient must still be
+    written exactly as in full-size mode and every other row left untouched."""
+    inst = tiny_instance(35, V=3000, group_sizes=(3, 4, 2, 3), dtype="bf16", mask_tail=3,
+                         lengths=[17, 0, 40, 9, 9, 9, 9, 33, 1, 0, 25, 12],
+                         rewards=[1, 0, 1, 1, 1, 1, 1, 0, 1, 1, 0, 0])
+    chunks = [(0, 20), (20, 55), (55, 120), (120, inst.T)]
+    kw = dict(logits_dtype=torch.bfloat16, chunks=chunks)
+    full = run_gpu(inst, dev, **kw)
+    # synchronised after prepare, so the grid bound (not the whole-chunk fallback) is used
+    comp = run_gpu(inst, dev, cfgkw={"zero_fill_inactive_rows": 0}, sync_after_prepare=True, **kw)
+    has_grad = full["tok"]["coef"] != 0
+    assert has_grad.any() and (~has_grad).any()
+    assert np.array_equal(comp["dlogits"][has_grad], full["dlogits"][has_grad])
+    assert np.isnan(comp["dlogits"][~has_grad]).all()
+    assert comp["loss"] == full["loss"]
