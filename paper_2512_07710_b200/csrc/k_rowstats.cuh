@@ -499,6 +499,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
       const int vlim = min(VPC, nvec - c * VPC);
 #pragma unroll
       for (int h = 0; h < NSUB; ++h) {
+        if (h * 32 * SUB >= vlim) {            // past the row's end for every lane: nothing
+          if (h == NSUB - 1) {                 // to add (warp-uniform), just refill the slot
+            __syncwarp();
+            if (pk < n) issue_one(slot);
+          }
+          continue;
+        }
         uint4 v[SUB];
 #pragma unroll
         for (int u = 0; u < SUB; ++u) {
