@@ -707,8 +707,7 @@ def main_ours(args):
                                           "ring 16+1 x 6 x 32 KB", "ring 20+1 x 5 x 40 KB + TMEM stash",
                                           "ring 10+1 x 5 x 20 KB, 2 CTAs/SM",
                                           "ring 12+1 x 4 x 24 KB, 2 CTAs/SM",
-                                          "rolling 20+1 x 5 x 40 KB", "rolling 16+1 x 6 x 32 KB",
-                                          "rolling 16+1 x 12 x 16 KB"][args.factored_impl]
+                                          "rolling 20+1 x 5 x 40 KB"][args.factored_impl]
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()

@@ -431,7 +431,7 @@ typedef enum {
                                   warps, 5 × 40 KB slots, default), 1 = 1024-thread CTA per row
                                   with plain loads, 2 = 16 warps × 6 × 32 KB, 3 = default + TMEM
                                   stash of pass-1 exponentials, 4-5 = two CTAs per SM,
-                                  6-8 = rolling pass-2/pass-1 interleave (A/B) */
+                                  6 = rolling pass-2/pass-1 interleave (A/B) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

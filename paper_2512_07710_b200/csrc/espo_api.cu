@@ -445,7 +445,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->lmh_2cta = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_FACTORED_IMPL:
-      if (value < 0 || value > 8) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 6) return ESPO_ERR_INVALID_ARGUMENT;
       c->factored_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_BWD_ROWS:
@@ -1541,7 +1541,7 @@ espo_status espo_loss_fwd_factored(espo_ctx_t c, const void* logits, int64_t ld,
   // geometry (ESPO_OPT_FACTORED_IMPL): 0 = TMA ring, 20 consumer warps + 1 producer warp,
   // 5 × 40 KB slots (measured best); 1 = CTA of 1024 threads re-reading each row
   // through L2 with plain loads; 2 = 16 warps × 6 × 32 KB; 3 = the default with the TMEM
-  // stash of pass 1's exponentials; 4, 5 = two CTAs per SM (thrash the L2); 6-8 = rolling
+  // stash of pass 1's exponentials; 4, 5 = two CTAs per SM (thrash the L2); 6 = rolling
   // interleave of pass 2 (row k−1) with pass 1 (row k) (longer L2 reuse distance: slower)
 #define ESPO_FG(NT, U)                                                                     \
   {                                                                                            \
@@ -1571,8 +1571,6 @@ espo_status espo_loss_fwd_factored(espo_ctx_t c, const void* logits, int64_t ld,
   }
   switch (c->factored_impl) {
     case 6: ESPO_FGL(20, 5, 40960) break;
-    case 7: ESPO_FGL(16, 6, 32768) break;
-    case 8: ESPO_FGL(16, 12, 16384) break;
     case 1: ESPO_FG(1024, 4) break;
     case 2: ESPO_FGR(16, 6, 32768, 0, 1) break;
     case 3: ESPO_FGR(20, 5, 40960, 1, 1) break;
