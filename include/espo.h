@@ -173,7 +173,10 @@ espo_status espo_destroy(espo_ctx_t ctx);
  * seq_offsets[0] = 0, non-decreasing, seq_offsets[R] = n_tokens. Outputs (device,
  * nullable): adv_out f32[R] (0 for ZV groups), zv_out u8[R] (1 = eliminated group).
  * Resets the sticky error word and the chunk coverage; may grow the workspace
- * (the only call that allocates). */
+ * (the only call that allocates). With zero_fill_inactive_rows = 0 (compact mode) it also
+ * enqueues an asynchronous copy of seq_offsets and the eliminated-group flags into pinned
+ * host memory owned by the context (8·(R+1) + R bytes, grown on demand); espo_loss_bwd uses
+ * it, once it has landed, only to size its grid (results do not depend on it). */
 espo_status espo_prepare(espo_ctx_t ctx, const float* rewards, const int32_t* group_ids,
                          const int64_t* seq_offsets, int32_t n_rollouts, int64_t n_tokens,
                          float* adv_out, uint8_t* zv_out, espo_stream_t stream);
