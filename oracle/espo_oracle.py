@@ -19,6 +19,8 @@ order the paper states the method; citations are ``PAPER.md:<line> (<section/eq>
                          PAPER.md:119 (Eq. 3 entropy-adaptive ε_τ)
   O5  token_surrogate    PAPER.md:105 (J_ESPO min/clip surrogate) and PAPER.md:111-113
                          (Eq. 1 with stop-gradient)
+  O3-5 rollout_objective one rollout's J_i and ∂J_i/∂lp: O3 → O4 per bucket → O5, with the
+                         1/|τ|·1/|y_τ| normalisers (PAPER.md:105-121)
   O6  espo_loss          PAPER.md:105 (expectation, 1/G, 1/|τ|, 1/|y_τ| normalisers)
   O7  dlogits            chain rule through log-softmax of the Eq. 1 numerator; every
                          sg[·] term is constant (PAPER.md:113)
@@ -306,6 +308,67 @@ def token_surrogate(v: float, A: float, eps: float):
 
 
 # ----------------------------------------------------------------------------------------
+# O3-O5 composed — one rollout's ESPO objective J_i
+# ----------------------------------------------------------------------------------------
+def rollout_objective(lp, old, H, A_t, cfg: OracleConfig, inject_bucket=None,
+                      inject_kappa=None) -> dict:
+    """One active rollout i with valid tokens t = 0..n−1 (index order), PAPER.md:105-121:
+
+      J_i = (1/|τ|) Σ_τ (1/|y_τ|) Σ_{t∈y_τ} min(v_t·Â_t, clip(v_t, 1−ε_τ, 1+ε_τ)·Â_t)
+
+    with the buckets τ of O3 (|τ| = nb, the number of non-empty buckets, reading Q2),
+    s_τ from Eq. 2 and ε_τ from Eq. 3 evaluated over the bucket's own tokens (O4), and
+    v_t = s_τ (reading R2: sg[s_τ]·π_θ/sg[π_θ]) or v_t = s_τ·π_θ/π_old
+    (R1, the literal sg[π_old] denominator). NORM_TOKEN replaces 1/(nb·|y_τ|) by 1.
+
+    ∂J_i/∂lp_t: every sg[·] is constant, so only the Eq. 1 numerator
+    π_θ(y_t) varies and ∂v_t/∂lp_t = v_t; the min picks the clipped branch (slope 0) when
+    it is strictly smaller (O5's κ): ∂J_i/∂lp_t = κ_t·Â_t·v_t·w_t, w_t = 1/(nb·|y_τ|).
+
+    Inputs: lp, old, H, A_t — arrays over the rollout's valid tokens. ``inject_*`` replace
+    the bucket / clip decisions (P11 decision-aware protocol). Returns per-token arrays
+    (bucket, kappa, v, s, eps, w, ell, dJ_dlp) and J, nb, theta."""
+    lp = np.asarray(lp, dtype=np.float64)
+    old = np.asarray(old, dtype=np.float64)
+    H = np.asarray(H, dtype=np.float64)
+    A_t = np.asarray(A_t, dtype=np.float64)
+    n = len(lp)
+    b, nb = partition(H, cfg)
+    theta = None
+    if cfg.partition == PARTITION_QUANTILE and cfg.n_buckets > 1 and n > 0:
+        srt = sorted(H.tolist())
+        theta = [srt[rk - 1] for rk in split_ranks(n, cfg)]
+    if inject_bucket is not None and cfg.partition == PARTITION_QUANTILE:
+        b = np.asarray(inject_bucket).astype(np.int64)
+        nb = len(set(b.tolist()))
+    out = {k: np.zeros(n) for k in ("v", "s", "eps", "w", "ell", "dJ_dlp")}
+    out["bucket"] = np.zeros(n, dtype=np.int64)
+    out["kappa"] = np.zeros(n, dtype=bool)
+    Ji = 0.0
+    for k in sorted(set(b.tolist())):
+        sel = np.nonzero(b == k)[0]
+        size = len(sel)
+        s, eps = bucket_ratio_clip(lp[sel], old[sel], H[sel], cfg)
+        w = 1.0 / (nb * size) if cfg.norm == NORM_SEQ else 1.0
+        for j in sel.tolist():
+            if cfg.ratio_mode == RATIO_GSPO_TOKEN:
+                v = s                     # sg[s_τ]·π_θ/sg[π_θ]: value s_τ
+            else:
+                v = s * math.exp(lp[j] - old[j])
+            At = float(A_t[j])
+            ell, kap = token_surrogate(v, At, eps)
+            if inject_kappa is not None:
+                kap = bool(np.asarray(inject_kappa)[j])
+            Ji += w * ell
+            out["dJ_dlp"][j] = At * v * w if kap else 0.0
+            out["bucket"][j] = 0 if cfg.partition != PARTITION_QUANTILE else k
+            out["kappa"][j] = kap
+            out["v"][j], out["s"][j], out["eps"][j], out["w"][j], out["ell"][j] = v, s, eps, w, ell
+    out.update(J=Ji, nb=nb, theta=theta)
+    return out
+
+
+# ----------------------------------------------------------------------------------------
 # O6/O7 — the whole pass
 # ----------------------------------------------------------------------------------------
 @dataclass
@@ -416,52 +479,33 @@ def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
         A_t = zvp_token_advantages(H, float(rewards32[i]), cfg) if zvp else np.full(n, A)
         adv_tok[valid] = A_t
 
-        # O3 partition
-        b, nb = partition(H, cfg)
-        if cfg.partition == PARTITION_QUANTILE and cfg.n_buckets > 1:
-            srt = sorted(H.tolist())
-            theta[i] = [srt[rk - 1] for rk in split_ranks(n, cfg)]
-        if inject_bucket is not None and cfg.partition == PARTITION_QUANTILE:
-            b = np.asarray(inject_bucket)[valid].astype(np.int64)
-            nb = len(set(b.tolist()))
-        nb_a[i] = nb
-
-        # O4 per bucket, O5 per token
-        Ji = 0.0
-        for k in sorted(set(b.tolist())):
-            sel = np.nonzero(b == k)[0]
-            size = len(sel)
-            s, eps = bucket_ratio_clip(lp[sel], old[sel], H[sel], cfg)
-            w = 1.0 / (nb * size) if cfg.norm == NORM_SEQ else 1.0
-            for j in sel.tolist():
-                t = int(valid[j])
-                if cfg.ratio_mode == RATIO_GSPO_TOKEN:
-                    v = s                     # sg[s_τ]·π_θ/sg[π_θ]: value s_τ
-                else:
-                    v = s * math.exp(lp[j] - old[j])
-                At = float(A_t[j])
-                ell, kap = token_surrogate(v, At, eps)
-                if inject_kappa is not None:
-                    kap = bool(np.asarray(inject_kappa)[t])
-                Ji += w * ell
-                coef_a[t] = At * v * w if kap else 0.0
-                sk = 0 if cfg.partition != PARTITION_QUANTILE else k
-                bucket_a[t] = sk
-                kappa_a[t] = 1 if kap else 0
-                v_a[t], eps_a[t], s_a[t], w_a[t] = v, eps, s, w
-                tok_k[sk] += 1
-                clip_k[sk] += 0 if kap else 1
-                vsum_k[sk] += v
-                esum_k[sk] += eps
-                n_clipped += 0 if kap else 1
-                d_lr = lp[j] - old[j]
-                sum_abs_lr += abs(d_lr)
-                sum_sq_lr += d_lr * d_lr
-                # k3 estimator of KL(π_old ‖ π_θ) from samples y ~ π_old: r − 1 − log r,
-                # r = π_θ(y)/π_old(y) (train/inference mismatch)
-                sum_k3 += math.expm1(d_lr) - d_lr
-                sum_H += H[j]
-        J_i[i] = Ji
+        # O3-O5 for this rollout
+        inj_b = None if inject_bucket is None else np.asarray(inject_bucket)[valid]
+        inj_k = None if inject_kappa is None else np.asarray(inject_kappa)[valid]
+        ro = rollout_objective(lp, old, H, A_t, cfg, inject_bucket=inj_b, inject_kappa=inj_k)
+        if ro["theta"] is not None:
+            theta[i] = ro["theta"]
+        nb_a[i] = ro["nb"]
+        for j, t in enumerate(valid.tolist()):
+            kap = bool(ro["kappa"][j])
+            sk = int(ro["bucket"][j])
+            coef_a[t] = ro["dJ_dlp"][j]
+            bucket_a[t] = sk
+            kappa_a[t] = 1 if kap else 0
+            v_a[t], eps_a[t], s_a[t], w_a[t] = ro["v"][j], ro["eps"][j], ro["s"][j], ro["w"][j]
+            tok_k[sk] += 1
+            clip_k[sk] += 0 if kap else 1
+            vsum_k[sk] += ro["v"][j]
+            esum_k[sk] += ro["eps"][j]
+            n_clipped += 0 if kap else 1
+            d_lr = lp[j] - old[j]
+            sum_abs_lr += abs(d_lr)
+            sum_sq_lr += d_lr * d_lr
+            # k3 estimator of KL(π_old ‖ π_θ) from samples y ~ π_old: r − 1 − log r,
+            # r = π_θ(y)/π_old(y) (train/inference mismatch)
+            sum_k3 += math.expm1(d_lr) - d_lr
+            sum_H += H[j]
+        J_i[i] = ro["J"]
 
     n_active = int(active.sum())
     t_active = int(n_valid[active].sum())
