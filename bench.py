@@ -2,16 +2,31 @@
 """ESPO loss fwd+bwd benchmark (BASELINE.json metric) — one JSON line on rank 0.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--scaling weak|strong] [--config C1..C4] [--verify]
 
 A step = one whole ESPO pass (espo_prepare → espo_loss_fwd over every chunk →
-espo_loss_finalize → espo_loss_bwd over every chunk) over one synthetic batch of the
-BASELINE configuration C1 (64 prompts × 8 rollouts × 4096 tokens, vocab 151,936, bf16
-logits) per GPU (weak scaling: each rank owns its own C1 batch; the one NCCL all-reduce of
-the pass normalises the loss over all ranks). Logits do not fit in HBM (637 GB per batch),
-so they stream through a device chunk buffer of --buffer-rows rows (9.96 GB at 32,768 rows,
-well above the 126 MB L2): batch row t reads buffer row t mod R_c. Timing: CUDA events on
-the launching stream, W warm-up steps, barrier + synchronize around exactly K steps, max
-over ranks. `--impl reference` times the CPU oracle (oracle/) on bounded samples.
+espo_loss_finalize → espo_loss_bwd over every chunk) over one synthetic batch.
+
+--gpus N: one process per GPU. Under torchrun (WORLD_SIZE set) N must equal WORLD_SIZE;
+without it and N > 1 this script re-executes itself under
+`python -m torch.distributed.run --nproc-per-node N` (127.0.0.1 rendezvous). Fewer visible
+GPUs than N is an error (exit 2): a world is never silently shrunk.
+
+--scaling weak (default): each rank owns its own batch of the configuration (C1 =
+64 prompts × 8 rollouts × 4096 tokens, vocab 151,936, bf16 logits); the one NCCL all-reduce of
+the pass normalises the loss over all ranks. --scaling strong (north_star's C4 scaling
+config): one fixed global batch, identical on every rank, whose prompt groups are split over
+the ranks by sharding.plan_shards (LPT on expected sweep cost, PAPER.md:244's length
+balancing); each rank sweeps only its groups. --verify adds an untimed pass that hashes every
+dlogits row with its global row id (order-independent, summed over ranks): in strong mode the
+digest and the loss must not depend on N.
+
+Logits do not fit in HBM (637 GB per C1 batch), so they stream through a device chunk buffer
+of --buffer-rows rows (9.96 GB at 32,768 rows, well above the 126 MB L2): a row at offset o
+inside its chunk reads buffer row o (chunks are fixed R_c slabs of the batch in weak mode, and
+R_c slabs of each prompt group in strong mode, so a row's data never depends on N). Timing:
+CUDA events on the launching stream, W warm-up steps, barrier + synchronize around exactly K
+steps, max over ranks. `--impl reference` times the CPU oracle (oracle/) on bounded samples.
 """
 from __future__ import annotations
 
@@ -35,7 +50,17 @@ NOMINAL_HBM_GBS = 8000.0
 
 def parse():
     p = argparse.ArgumentParser()
-    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--gpus", type=int, default=None,
+                   help="GPUs = ranks (default: WORLD_SIZE under torchrun, else 1)")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: a batch of --config per rank; strong: one global batch split "
+                        "over the ranks by prompt group (LPT)")
+    p.add_argument("--verify", action="store_true",
+                   help="untimed extra pass: order-independent digest of every dlogits row")
+    p.add_argument("--drift-seq", type=float, default=0.04,
+                   help="std of the per-rollout log-prob drift of the rollout engine")
+    p.add_argument("--drift-tok", type=float, default=0.02,
+                   help="std of the per-token log-prob drift")
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -71,6 +96,41 @@ def parse():
                    help="S > 1: vocabulary-parallel leg, S shard contexts back to back on this "
                         "GPU (partials gathered by a device copy)")
     return p.parse_args()
+
+
+# ------------------------------------------------------------------------------ launch
+def resolve_world(args):
+    """--gpus vs the torchrun environment. Returns the world size this process runs in, or
+    re-executes the script under torchrun (never returns) when N > 1 ranks are requested
+    from a plain `python bench.py --gpus N`."""
+    env = os.environ.get("WORLD_SIZE")
+    if env is not None:
+        world = int(env)
+        if args.gpus is not None and args.gpus != world:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} != WORLD_SIZE {world}")
+        args.gpus = world
+        return world
+    n = 1 if args.gpus is None else args.gpus
+    if n < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    args.gpus = n
+    if n == 1:
+        return 1
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            print(f"bench.py: --gpus {n} but only {have} CUDA device(s) visible", file=sys.stderr)
+            raise SystemExit(2)
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
 
 
 # ------------------------------------------------------------------------------ helpers
@@ -148,15 +208,52 @@ def rollout_chunks(seq_offsets, max_rows):
     return chunks
 
 
-def make_batch(w, seed, dev, buffer_rows, log, single_pass=False):
-    """Device-resident synthetic C1 batch: chunk buffer + per-token arrays."""
-    import torch
-    V = w.V
+def strong_plan(w, seed, world):
+    """Strong scaling: the global layout/rewards (identical on every rank) and the LPT plan."""
+    from paper_2512_07710_b200.sharding import plan_shards
     group_ids, seq_offsets = S.make_layout(w, seed)
     rewards = S.make_rewards(w, seed)
-    T = int(seq_offsets[-1])
-    Rc = min(buffer_rows, T)
+    plan = plan_shards(group_ids, seq_offsets, world, rewards=rewards)
+    return group_ids, seq_offsets, rewards, plan
+
+
+def group_chunks(local_so, local_gid, Rc):
+    """Chunks of ≤ Rc rows that never cross a prompt group and start at multiples of Rc
+    inside their group: a row at offset o in its group reads buffer row o mod Rc, whatever
+    other groups the rank holds."""
+    from paper_2512_07710_b200.sharding import group_spans
+    chunks = []
+    for a, b in group_spans(local_gid):
+        g0, g1 = int(local_so[a]), int(local_so[b])
+        chunks += [(x, min(g1, x + Rc)) for x in range(g0, g1, Rc)]
+    return chunks
+
+
+def make_batch(w, seed, dev, buffer_rows, log, single_pass=False, shard=None,
+               drift=(0.04, 0.02)):
+    """Device-resident synthetic batch: chunk buffer + per-token arrays. shard = (world,
+    rank): strong scaling, this rank's groups of the global batch (seed shared by all ranks)."""
+    import torch
+    V = w.V
     t0 = time.time()
+    if shard is None:
+        group_ids, seq_offsets = S.make_layout(w, seed)
+        rewards = S.make_rewards(w, seed)
+        g_so, rows_global = seq_offsets, None
+    else:
+        world, rank = shard
+        from paper_2512_07710_b200.sharding import shard_batch
+        g_gid, g_so, g_rw, plan = strong_plan(w, seed, world)
+        rollouts, _, group_ids, seq_offsets = shard_batch(plan[rank], g_gid, g_so)
+        rewards = g_rw[rollouts]
+        # global row of each local rollout's first row (for the per-token drift and digest)
+        rows_global = (rollouts, g_so)
+    T = int(seq_offsets[-1])
+    if shard is None:
+        Rc = max(1, min(buffer_rows, T))
+    else:                       # the same buffer for every N: bounded by the largest group
+        from paper_2512_07710_b200.sharding import group_spans
+        Rc = max(1, min(buffer_rows, max(int(g_so[b] - g_so[a]) for a, b in group_spans(g_gid))))
     buf = S.make_logit_rows_torch(Rc, V, seed, dev, torch.bfloat16)
     buf_tok = S.sample_tokens_gumbel_torch(buf, seed)
     # bench setup only (untimed): rollout-engine log-probs = log_softmax + drift
@@ -166,30 +263,84 @@ def make_batch(w, seed, dev, buffer_rows, log, single_pass=False):
         ls = torch.log_softmax(buf[r0:r1].float(), dim=1)
         buf_lp[r0:r1] = ls.gather(1, buf_tok[r0:r1].long().unsqueeze(1)).squeeze(1)
         del ls
-    # chunks: fixed R_c tiles (two sweeps) or whole-rollout packs (single pass); batch row t
-    # reads buffer row t − (its chunk's first row)
-    chunks = rollout_chunks(seq_offsets, Rc) if single_pass else \
-        [(b, min(T, b + Rc)) for b in range(0, T, Rc)]
+    # chunks: fixed R_c tiles (two sweeps), R_c tiles of each group (strong scaling) or
+    # whole-rollout packs (single pass); batch row t reads buffer row t − (its chunk's first row)
+    if single_pass:
+        chunks = rollout_chunks(seq_offsets, Rc)
+    elif shard is not None:
+        chunks = group_chunks(seq_offsets, group_ids, Rc)
+    else:
+        chunks = [(b, min(T, b + Rc)) for b in range(0, T, Rc)]
     idx_np = np.empty(T, dtype=np.int64)
     for b, e in chunks:
         idx_np[b:e] = np.arange(e - b)
     idx = torch.from_numpy(idx_np).to(dev)
     tokens = buf_tok[idx].contiguous()
     lp = buf_lp[idx]
+    # drift: per-rollout b_i and per-token noise, drawn over the GLOBAL batch (the same on
+    # every rank and for every N in strong mode), then this rank's rows gathered
     g = torch.Generator(device=dev)
     g.manual_seed(seed & ((1 << 62) - 1))
-    lengths = torch.from_numpy(np.diff(seq_offsets)).to(dev)
-    b = torch.repeat_interleave(torch.randn(w.R, generator=g, device=dev) * 0.04, lengths)
-    drift = b + 0.02 * torch.randn(T, generator=g, device=dev)
-    old = (lp + drift).contiguous()
-    torch.cuda.synchronize(dev)
-    log(f"generated batch T={T} buffer={Rc} rows in {time.time() - t0:.1f}s")
+    Tg = int(g_so[-1]) if shard is not None else T
+    Rg = len(g_so) - 1
+    lengths = torch.from_numpy(np.diff(g_so)).to(dev)
+    b = torch.repeat_interleave(torch.randn(Rg, generator=g, device=dev) * drift[0], lengths)
+    drift_g = b + drift[1] * torch.randn(Tg, generator=g, device=dev)
+    if shard is not None:
+        rl, gso = rows_global
+        starts = torch.from_numpy(gso[rl]).to(dev)
+        lens = torch.from_numpy(gso[rl + 1] - gso[rl]).to(dev)
+        first_local = torch.from_numpy(seq_offsets[:-1]).to(dev)
+        roll = torch.repeat_interleave(torch.arange(len(rl), device=dev), lens)
+        grow = starts[roll] + (torch.arange(T, device=dev) - first_local[roll])
+        drift_l = drift_g[grow]
+        del drift_g
+    else:
+        grow = None
+        drift_l = drift_g
+    old = (lp + drift_l).contiguous()
+    if dev.type == "cuda":
+        torch.cuda.synchronize(dev)
+    log(f"generated batch T={T} buffer={Rc} rows, {len(chunks)} chunks in {time.time() - t0:.1f}s")
     return dict(buf=buf, tokens=tokens, old=old, T=T, Rc=Rc, buf_tok=buf_tok, buf_lp=buf_lp,
-                drift=drift, chunks=chunks,
+                drift=drift_l, chunks=chunks, global_row=grow,
                 rewards=torch.from_numpy(rewards).to(dev),
                 group_ids=torch.from_numpy(group_ids).to(dev),
                 seq_offsets=torch.from_numpy(seq_offsets).to(dev),
-                np=dict(rewards=rewards, group_ids=group_ids, seq_offsets=seq_offsets))
+                np=dict(rewards=rewards, group_ids=group_ids, seq_offsets=seq_offsets,
+                        chunk_of_row=None))
+
+
+def dlogits_digest(ctx, d, dlog, log):
+    """Untimed verification pass (--verify): one more full step; after each backward chunk,
+    per-row sums of the dlogits bits (all elements, and every 7th 32-bit word) are mixed with
+    the row's GLOBAL id and summed mod 2^64. The sum is order-independent, so rank digests
+    add up (all-reduce) to the digest one GPU would print for the same global batch."""
+    import torch
+    T, Rc, buf = d["T"], d["Rc"], d["buf"]
+    M = np.uint64(0xFFFFFFFFFFFFFFFF)
+    ctx.prepare(d["rewards"], d["group_ids"], d["seq_offsets"], n_tokens=T)
+    for b, e in d["chunks"]:
+        ctx.loss_fwd(buf[:e - b], d["tokens"][b:e], d["old"][b:e], None, row_begin=b)
+    loss, stats = ctx.loss_finalize()
+    acc = np.uint64(0)
+    grow = d["global_row"]
+    with np.errstate(over="ignore"):
+        for b, e in d["chunks"]:
+            ctx.loss_bwd(buf[:e - b], dlog[:e - b], row_begin=b)
+            w32 = dlog[:e - b].view(torch.int32)
+            s1 = w32.sum(1, dtype=torch.int64).cpu().numpy().astype(np.uint64)
+            s2 = w32[:, ::7].sum(1, dtype=torch.int64).cpu().numpy().astype(np.uint64)
+            gid = (np.arange(b, e, dtype=np.uint64) if grow is None else
+                   grow[b:e].cpu().numpy().astype(np.uint64))
+            x = gid * np.uint64(0x9E3779B97F4A7C15) ^ s1 * np.uint64(0xBF58476D1CE4E5B9) ^ \
+                s2 * np.uint64(0x94D049BB133111EB)
+            x ^= x >> np.uint64(31)
+            x *= np.uint64(0xD6E8FEB86659FD93)
+            x ^= x >> np.uint64(32)
+            acc = (acc + (x.sum(dtype=np.uint64) & M)) & M
+    ctx.get_error()
+    return int(acc), loss, stats
 
 
 def run_step(ctx, d, dlog, ev=None):
@@ -505,14 +656,25 @@ def main_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.device_count() <= local:
+        print(f"bench.py: rank {rank} needs cuda:{local}, {torch.cuda.device_count()} visible",
+              file=sys.stderr)
+        raise SystemExit(2)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # NCCL logs "nranks N" at init
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
     w = S.WORKLOADS[args.config]
-    seed = S.config_seed(w.index) ^ (rank * 0x9E3779B9)
-    d = make_batch(w, seed, dev, args.buffer_rows, log, single_pass=args.single_pass)
+    strong = args.scaling == "strong"
+    if strong and (args.single_pass or args.vocab_shards > 1):
+        raise SystemExit("--scaling strong runs the two-sweep (or --factored) path")
+    # weak: every rank draws its own batch; strong: one global batch, the same seed everywhere
+    seed = S.config_seed(w.index) ^ (0 if strong else rank * 0x9E3779B9)
+    d = make_batch(w, seed, dev, args.buffer_rows, log, single_pass=args.single_pass,
+                   shard=(world, rank) if strong else None, drift=(args.drift_seq, args.drift_tok))
     kw = dict(zero_fill_inactive_rows=not args.compact,
               zv_mode=1 if args.zv_mode == "rlzvp" else 0)
     S_ = args.vocab_shards
@@ -531,6 +693,10 @@ def main_ours(args):
         step_fn = run_step_sharded
     else:
         ctx = Espo(w.V, logits_dtype=torch.bfloat16, device=local, rank=rank, world=world, **kw)
+        nranks = ctx.comm_size
+        log(f"DP communicator: nranks={nranks} (world {world}, rank {rank}, cuda:{local})")
+        if nranks != world:
+            raise SystemExit(f"bench.py: NCCL communicator has {nranks} ranks, world is {world}")
         ctx.set_option(OPT_FWD_IMPL, args.fwd_impl)
         ctx.set_option(OPT_BWD_IMPL, args.bwd_impl)
         ctx.set_option(OPT_BLOCKS_PER_SM, args.blocks_per_sm)
@@ -567,10 +733,14 @@ def main_ours(args):
     if world > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms_step = float(t_ms.item()) / args.steps
+    t_all = torch.tensor([d["T"]], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_all)
+    T_total = int(t_all.item())             # tokens all ranks processed per step
 
     # algorithmic bytes (per rank, per step); SURVEY §8(d) per-row figures
     V, T = w.V, d["T"]
-    n_act = st["n_active_tokens"] / world      # stats are global (all-reduced)
+    n_act = st["n_active_tokens"] / world      # stats are global (all-reduced): per-rank mean
     n_clip = st["n_clipped_tokens"] / world
     fwd_bytes = n_act * (2 * V + 4 + 4 + 16) + T * (4 + 4 + 1 + 8)
     bwd_bytes = (n_act - n_clip) * 2 * V + (0 if args.compact else T) * 2 * V + T * 12
@@ -624,7 +794,7 @@ def main_ours(args):
         f_ms = float(t_f.item()) / args.steps
         f_bytes = n_act * (2 * V + 4 + 4 + 16) + T * (4 + 4 + 1 + 8 + 9) + \
             (n_act if args.compact else T) * 2 * V
-        factored = {"value": T * world / (f_ms * 1e-3), "unit": "tokens/s", "ms_per_step": f_ms,
+        factored = {"value": T_total / (f_ms * 1e-3), "unit": "tokens/s", "ms_per_step": f_ms,
                     "achieved_hbm_gbs_step": f_bytes / (f_ms * 1e-3) / 1e9,
                     "api": "espo_loss_fwd_factored + espo_loss_row_scale (dlogits = scale_t * G_t, "
                            "G = onehot - softmax written by the statistics sweep; the consumer "
@@ -634,16 +804,22 @@ def main_ours(args):
     if not args.no_e2e and S_ == 1:
         tps, h2d, d2h, dt = run_e2e(ctx, d, dlog, args, dev)
         if world > 1:       # whole-job rate: every rank's tokens over the slowest rank's time
-            t_e2e = torch.tensor([dt], dtype=torch.float64, device=dev)
+            t_e2e = torch.tensor([dt, h2d, d2h], dtype=torch.float64, device=dev)
+            red = t_e2e.clone()
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-            tps = d["T"] / float(t_e2e.item())
-        e2e = {"value": tps * world, "unit": "tokens/s", "h2d_bytes_per_step": h2d * world,
-               "d2h_bytes_per_step": d2h * world, "steps": args.e2e_steps,
+            dist.all_reduce(red)
+            dt, h2d, d2h = float(t_e2e[0].item()), int(red[1].item()), int(red[2].item())
+        tps = T_total / dt
+        e2e = {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "mode": args.e2e_mode,
                "note": "host-resident inputs incl. every logits chunk over PCIe from a pinned "
                        "host ring (" + ("once per step: espo_set_mask + espo_loss_fwd_bwd on "
                        "chunks of whole rollouts" if args.e2e_mode == "single-pass" else
-                       "twice per step: fwd and bwd sweeps") + "); wall clock"}
+                       "twice per step: fwd and bwd sweeps") + "); wall clock over "
+                       f"{args.e2e_steps} step(s) after one warm-up; dlogits stay on the device "
+                       "(a trainer consumes them there: they are the input of the LM-head "
+                       "backward), d2h is the loss"}
     cpu = cpu_par = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(d, w, args.cpu_sample_tokens, log)
@@ -654,21 +830,35 @@ def main_ours(args):
         except Exception as e:          # the single-core baseline above stands on its own
             cpu_par = {"unavailable": f"{type(e).__name__}: {e}"}
 
+    digest = None
+    if args.verify:
+        dg, vloss, vstats = dlogits_digest(ctx, d, dlog, log)
+        dgt = torch.tensor([dg - (1 << 64) if dg >= (1 << 63) else dg], dtype=torch.int64,
+                           device=dev)
+        if world > 1:
+            dist.all_reduce(dgt)            # int64 sum wraps mod 2^64, like the digest
+        digest = {"dlogits_digest": "%016x" % (int(dgt.item()) & ((1 << 64) - 1)),
+                  "loss_f64": stats_to_dict(vstats)["loss"],
+                  "note": "order-independent hash of every dlogits row (bits) with its global "
+                          "row id, summed over ranks; strong scaling: must not depend on N"}
+
+    gname = (f"{w.name} global batch: {w.n_prompts} prompts x {w.G} rollouts x {w.L} tokens "
+             f"split over {world} GPU(s) by prompt group (LPT plan)") if strong else \
+        f"{w.name}: {w.n_prompts} prompts x {w.G} rollouts x {w.L} tokens per GPU"
     out = {
         "metric": "ESPO loss fwd+bwd tokens/sec (achieved HBM GB/s vs 8 TB/s in config)",
-        "value": T * world / (ms_step * 1e-3),
+        "value": T_total / (ms_step * 1e-3),
         "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (espo_synth recipe: 80/20 entropy logits, Gumbel-sampled tokens, "
                 "Bernoulli rewards, drifted old log-probs)",
         "config": {
-            "workload": f"{w.name}: {w.n_prompts} prompts x {w.G} rollouts x {w.L} tokens per GPU, "
-                        f"vocab {V}, bf16 logits/grads" + (", compact dlogits" if args.compact else "")
+            "workload": gname + f", vocab {V}, bf16 logits/grads" + (", compact dlogits" if args.compact else "")
                         + (", RL-ZVP advantages for zero-variance groups" if args.zv_mode == "rlzvp" else "")
                         + (f", {S_} vocabulary shards back to back on one GPU (TP emulation, "
                            + ("partials exchanged by the fused peer-memory path)" if args.tp_p2p
@@ -676,7 +866,13 @@ def main_ours(args):
                         + (", single-pass (espo_loss_fwd_bwd per chunk of whole rollouts)" if args.single_pass else "")
                         + (", factored gradient (espo_loss_fwd_factored: one sweep writes G = onehot - p; "
                            "dlogits = row_scale * G applied by the consumer)" if args.factored else ""),
-            "global_batch_tokens": T * world, "seq_len": w.L, "parallelism": f"dp{world} (prompt-group sharded)",
+            "global_batch_tokens": T_total, "seq_len": w.L,
+            "parallelism": f"dp{world} (prompt-group sharded" + (", LPT plan)" if strong else ")"),
+            "nccl_nranks": ctx.comm_size if S_ == 1 else 1,
+            "drift": {"seq_sigma": args.drift_seq, "tok_sigma": args.drift_tok,
+                      "clip_frac": n_clip / n_act if n_act else 0.0,
+                      "note": "old_logp = lp + b_i + tok_sigma*n_t, b_i ~ N(0, seq_sigma); clipped "
+                              "tokens need no logits read in the backward (c_t = 0)"},
             "chunk_rows": d["Rc"], "l2": "inputs larger than L2 (chunk buffer "
                                          f"{d['Rc'] * V * 2 / 1e9:.2f} GB > 126 MB)",
             "fwd_impl": ["tma16x2x6k_s4_f32x2 (rows >= 64 KB; 16x3x4k below)", "ldg", "tma16x2x7k_s2_f32x2", "tma14x2x7k_s2_f32x2", "tma20x2x5k_s2_f32x2", "tma16x3x4k_s4_f32x2", "tma16x2x6k_s4_poly1", "tma18x2x6k_s4_f32x2", "tma16x2x6k_s4_scalar", "tile32k_b4", "tile32k_b3", "tile32k_b2"][args.fwd_impl],
@@ -699,6 +895,7 @@ def main_ours(args):
         "e2e": e2e,
         "gpu_launches": launches,
         "factored_gradient": factored,
+        "verify": digest,
         "clocks": clk,
         "loss": st["loss"],
     }
@@ -755,9 +952,9 @@ def main_reference(args):
     out = {
         "impl": "reference",
         "metric": "ESPO loss fwd+bwd tokens/sec (achieved HBM GB/s vs 8 TB/s in config)",
-        "value": n / dt, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+        "value": n / dt, "unit": "tokens/s", "n_gpus": args.gpus or 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{w.name}: bounded sample per step: one prompt group "
                                f"({G} rollouts) x {L} tokens, vocab {V}"},
         "cpu_baseline": {"value": n / dt, "unit": "tokens/s", "cores": 1, "kind": "oracle",
@@ -771,6 +968,7 @@ def main_reference(args):
 
 if __name__ == "__main__":
     a = parse()
+    resolve_world(a)
     if a.impl == "reference":
         main_reference(a)
     else:

@@ -168,7 +168,14 @@ espo_status espo_create(const espo_config* cfg, const void* nccl_unique_id, int3
                         int32_t world, int32_t cuda_device, espo_ctx_t* out);
 espo_status espo_destroy(espo_ctx_t ctx);
 
-/* Step begin (K1 kernels). Device inputs: rewards f32[R], group_ids i32[R] (each prompt
+/* Step begin (K1 kernels) — §2.4.1 zero-variance elimination and §2.4.2's advantage.
+ * Operation: prompt groups are the maximal runs of equal group_ids (the G rollouts
+ * {y_i} ~ π_old of one prompt); a group whose rewards all compare equal (or
+ * G = 1) has zero variance and is eliminated ("identical rewards … zero
+ * advantage", masked out per PAPER.md:91 / north_star; reading Q8); every other rollout gets
+ * the GRPO advantage Â_i = (r_i − μ_g)/(σ_g + adv_eps) ("normalized
+ * token-level advantage", formula SPEC.md:335; population std, reading Q7), in fp64.
+ * Device inputs: rewards f32[R], group_ids i32[R] (each prompt
  * group is one run of equal ids; ids must be non-decreasing), seq_offsets i64[R+1] with
  * seq_offsets[0] = 0, non-decreasing, seq_offsets[R] = n_tokens. Outputs (device,
  * nullable): adv_out f32[R] (0 for ZV groups), zv_out u8[R] (1 = eliminated group).
@@ -176,30 +183,71 @@ espo_status espo_destroy(espo_ctx_t ctx);
  * (the only call that allocates). With zero_fill_inactive_rows = 0 (compact mode) it also
  * enqueues an asynchronous copy of seq_offsets and the eliminated-group flags into pinned
  * host memory owned by the context (8·(R+1) + R bytes, grown on demand); espo_loss_bwd uses
- * it, once it has landed, only to size its grid (results do not depend on it). */
+ * it, once it has landed, only to size its grid (results do not depend on it). Under CUDA
+ * stream capture the copy is skipped (the backward grid then covers whole chunks).
+ * Errors: NULL input / negative sizes → ESPO_ERR_INVALID_ARGUMENT (nothing enqueued);
+ * non-finite reward, decreasing group_ids, inconsistent seq_offsets → sticky device error. */
 espo_status espo_prepare(espo_ctx_t ctx, const float* rewards, const int32_t* group_ids,
                          const int64_t* seq_offsets, int32_t n_rollouts, int64_t n_tokens,
                          float* adv_out, uint8_t* zv_out, espo_stream_t stream);
 
-/* Forward sweep over token rows [row_begin, row_begin + n_rows) (K2). Device inputs,
+/* Forward sweep over token rows [row_begin, row_begin + n_rows) (K2).
+ * Operation: for each row t of an active rollout with mask = 1, one pass over the vocabulary
+ * gives lse_t = log Σ_v e^{λz_v}, the log-prob of the sampled token lp_t = λz_{y_t} − lse_t
+ * (the Eq. 1 numerator log π_θ(y_t|x, y_<t)), the token entropy
+ * e_t = −Σ_v p_v log p_v (Eq. 3's e_t) and q_t = 1 − p_{y_t}; rows of
+ * eliminated groups and masked rows are not read. Device inputs,
  * each pointing at row row_begin: logits (dtype cfg.logits_dtype, 16-byte aligned,
  * ld·sizeof(dtype) % 16 == 0, ld ≥ vocab), tokens i32, old_logp f32 (rollout-engine
- * log π_old, nats), mask u8 (nullable = all valid). flags must be 0. */
+ * log π_old, nats), mask u8 (nullable = all valid). flags must be 0. Chunks may come in any
+ * order and may split a rollout; every row exactly once before espo_loss_finalize.
+ * Errors: NULL / misaligned / overlapping chunk → immediate status (nothing enqueued);
+ * NaN/+inf logit, −inf target logit, token ∉ [0, vocab) in a read row → sticky device error. */
 espo_status espo_loss_fwd(espo_ctx_t ctx, const void* logits, int64_t ld,
                           const int32_t* tokens, const float* old_logp, const uint8_t* mask,
                           int64_t row_begin, int64_t n_rows, uint32_t flags,
                           espo_stream_t stream);
 
-/* After all rows are covered (K3 per-sequence reduction, K4 reduction + NCCL all-reduce
- * when world > 1). Device outputs, nullable: loss_dev f32[1] (= −J; 0 when no rollout is
- * active; NaN after a device-detected data error), stats_dev espo_stats. */
+/* After all rows are covered: K3 per sequence, K4 reduction, NCCL all-reduce when world > 1.
+ * Operation (§2.4.2): within each rollout the valid tokens are grouped by
+ * entropy (K = 2 split at the 80/20 order statistic of PAPER.md:95, reading Q3);
+ * per bucket τ, s_τ = exp(mean_{t∈τ}(lp_t − old_t)) (Eq. 2) and
+ * ε_τ = max(ε_min, α·mean_{t∈τ} e_t / log|V|) (Eq. 3); per token the clipped
+ * surrogate ℓ_t = min(v_t·Â, clip(v_t, 1 ± ε_τ)·Â) with v_t = s_τ (Eq. 1, reading R2);
+ * J_i = (1/|τ|)·Σ_τ (1/|y_τ|)·Σ_{t∈τ} ℓ_t and loss = −(1/N)·Σ_i J_i over the N active
+ * rollouts (J_ESPO; readings Q2, Q10, Q13). The N and Σ J_i terms (26 fp64) are
+ * summed over the DP ranks by one ncclAllReduce. Device outputs, nullable: loss_dev f32[1]
+ * (= −J; 0 when no rollout is active; NaN after a device-detected data error), stats_dev
+ * espo_stats. Errors: rows not covered / wrong call order → ESPO_ERR_BAD_STATE; NCCL failure
+ * → ESPO_ERR_NCCL. */
 espo_status espo_loss_finalize(espo_ctx_t ctx, float* loss_dev, espo_stats* stats_dev,
                                espo_stream_t stream);
 
+/* espo_loss_finalize in two halves, for a caller-owned collective (torch.distributed, MPI,
+ * a different NCCL communicator) or none. espo_loss_reduce_local runs K3 and the fixed-order
+ * K4 reduction and copies this rank's ESPO_REDUCE_LEN fp64 terms to partial_out (device);
+ * the caller sums those vectors element-wise over its ranks and passes the sum to
+ * espo_loss_finalize_reduced (device, ESPO_REDUCE_LEN fp64), which writes loss/stats like
+ * espo_loss_finalize and fixes the backward scale −grad·c_t/N. With the sum of every rank's
+ * vector, each rank's dlogits rows are bitwise those of a single context holding all ranks'
+ * rollouts (N is an integer count; only the fp64 loss sum depends on the reduction order).
+ * The context's own communicator (world > 1) is not used by this pair. States: Prepared with
+ * all rows covered → reduce_local → finalize_reduced → bwd; otherwise ESPO_ERR_BAD_STATE. */
+#define ESPO_REDUCE_LEN 26
+espo_status espo_loss_reduce_local(espo_ctx_t ctx, double* partial_out, espo_stream_t stream);
+espo_status espo_loss_finalize_reduced(espo_ctx_t ctx, const double* reduced, float* loss_dev,
+                                       espo_stats* stats_dev, espo_stream_t stream);
+
 /* Backward sweep (K5): dlogits = d(grad_loss · loss)/d logits for rows
- * [row_begin, row_begin+n_rows). logits as in espo_loss_fwd (the same values);
+ * [row_begin, row_begin+n_rows). Operation: only the Eq. 1 numerator π_θ(y_t) carries
+ * gradient — every sg[·] is a constant — so row t gets
+ * λ·g_t·(onehot(y_t) − softmax(λz_t)) with g_t = −grad_loss·c_t/N, c_t = ∂J_i/∂lp_t =
+ * κ_t·Â·v_t/(|τ|·|y_τ|) (κ_t = 0 where the clipped branch of the min is strictly active);
+ * rows with c_t = 0 (clipped, masked, eliminated) are written as zeros without being read
+ * (or left untouched in compact mode). logits as in espo_loss_fwd (the same values);
  * dlogits (device, cfg.grad_dtype, 16-byte aligned, ldg ≥ vocab) may alias logits when
- * ldg == ld and the dtypes match. grad_loss_dev: device f32[1], nullable = 1.0. */
+ * ldg == ld and the dtypes match. grad_loss_dev: device f32[1], nullable = 1.0.
+ * Errors: before finalize → ESPO_ERR_BAD_STATE; NULL / misaligned → immediate status. */
 espo_status espo_loss_bwd(espo_ctx_t ctx, const void* logits, int64_t ld, void* dlogits,
                           int64_t ldg, const float* grad_loss_dev, int64_t row_begin,
                           int64_t n_rows, espo_stream_t stream);
@@ -257,8 +305,9 @@ espo_status espo_attach_tp(espo_ctx_t ctx, const void* tp_unique_id, int32_t tp_
  * exchange buffer of EVERY TP rank (peer pointers from CUDA IPC), then releases a flag per
  * rank; the combine acquires all ranks' flags for the chunk and merges (PAPER.md:129 Megatron
  * vocab-parallel layout). Two slots alternate between chunks; a slot is
- * rewritten only after every rank posted that it consumed it. Waits are bounded: a missing
- * peer gives ESPO_ERR_PEER_TIMEOUT (sticky, via espo_get_error), not a hang.
+ * rewritten only after every rank posted that it consumed it. Waits are bounded in wall time
+ * (ESPO_OPT_PEER_TIMEOUT_MS, default 120 s): a missing peer gives ESPO_ERR_PEER_TIMEOUT
+ * (sticky, via espo_get_error) and an invalid step, not a hang.
  *
  * espo_tp_p2p_buffer: allocates this rank's exchange buffer for chunks of ≤ max_rows rows
  *   (4 KB flags + 2·tp_world·max_rows·16 B) and writes its cudaIpcMemHandle_t
@@ -343,7 +392,10 @@ espo_status espo_loss_fwd_bwd(espo_ctx_t ctx, const void* logits, int64_t ld,
  * the dtypes are equal — the rows' logits are then overwritten). The target entry is
  * q_t = 1 − p_y (no cancellation); rows without gradient (masked, eliminated group, inactive
  * rollout) are zero-filled without being read when zero_fill_inactive_rows, else untouched;
- * clipped rows get their G_t (their scale is 0). Unsharded contexts, not in single-pass mode
+ * clipped rows get their G_t (their scale is 0). In compact mode the untouched rows keep
+ * whatever grad held (the Python binding zero-initialises a grad it allocates): a consumer
+ * forming diag(scale)·G must either start from a zeroed grad or skip rows whose scale is 0
+ * (0·NaN = NaN would otherwise poison dh/dW). Unsharded contexts, not in single-pass mode
  * (ESPO_ERR_BAD_STATE). Statistics agree with espo_loss_fwd's within fp32 rounding (a
  * different summation order), not bitwise.
  * espo_loss_row_scale (after espo_loss_finalize): scale_out[r] = scale_t for rows
@@ -415,6 +467,10 @@ espo_status espo_export_rollout_stats(espo_ctx_t ctx, double* adv, uint8_t* zv,
 /* Number of kernels this context has launched so far. */
 uint64_t espo_launch_count(espo_ctx_t ctx);
 
+/* Ranks in the data-parallel communicator of espo_create (ncclCommCount): 1 for world == 1,
+ * −1 on error. */
+int32_t espo_comm_size(espo_ctx_t ctx);
+
 /* Kernel-variant switches for A/B measurement. */
 typedef enum {
   ESPO_OPT_FWD_IMPL = 0,       /* 0 = TMA bulk-copy smem ring (default), 1 = LDG.128 warp per
@@ -430,11 +486,15 @@ typedef enum {
                                   0 = default 8192) */
   ESPO_OPT_LMHEAD_2CTA = 5,    /* 1: LM-head kernels on CTA pairs (tcgen05 cta_group::2,
                                   M = 256 per pair); 0: one CTA per 128-row block */
-  ESPO_OPT_FACTORED_IMPL = 6   /* espo_loss_fwd_factored: 0 = TMA ring (1 producer + 20 consumer
+  ESPO_OPT_FACTORED_IMPL = 6,  /* espo_loss_fwd_factored: 0 = TMA ring (1 producer + 20 consumer
                                   warps, 5 × 40 KB slots, default), 1 = 1024-thread CTA per row
                                   with plain loads, 2 = 16 warps × 6 × 32 KB, 3 = default + TMEM
                                   stash of pass-1 exponentials, 4-5 = two CTAs per SM,
                                   6 = rolling pass-2/pass-1 interleave (A/B) */
+  ESPO_OPT_PEER_TIMEOUT_MS = 7 /* bound on every peer-memory wait of the TP exchange, in ms of
+                                  device wall time (default 120000); a timeout sets the sticky
+                                  ESPO_ERR_PEER_TIMEOUT and invalidates the step (the chunk's
+                                  row statistics are not written) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

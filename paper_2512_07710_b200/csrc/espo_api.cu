@@ -37,6 +37,7 @@ typedef int (*fn_init_rank)(nccl_comm*, int, nccl_uid, int);
 typedef int (*fn_allreduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t);
 typedef int (*fn_destroy)(nccl_comm);
 typedef int (*fn_allgather)(const void*, void*, size_t, int, nccl_comm, cudaStream_t);
+typedef int (*fn_count)(nccl_comm, int*);
 constexpr int kNcclFloat64 = 8;  // ncclFloat64
 constexpr int kNcclFloat32 = 7;  // ncclFloat32
 constexpr int kNcclUint8 = 1;    // ncclUint8
@@ -49,6 +50,7 @@ struct NcclApi {
   fn_allreduce allreduce = nullptr;
   fn_destroy destroy = nullptr;
   fn_allgather allgather = nullptr;
+  fn_count count = nullptr;
   bool load() {
     if (lib) return true;
     lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -58,6 +60,7 @@ struct NcclApi {
     allreduce = reinterpret_cast<fn_allreduce>(dlsym(lib, "ncclAllReduce"));
     destroy = reinterpret_cast<fn_destroy>(dlsym(lib, "ncclCommDestroy"));
     allgather = reinterpret_cast<fn_allgather>(dlsym(lib, "ncclAllGather"));
+    count = reinterpret_cast<fn_count>(dlsym(lib, "ncclCommCount"));
     return get_uid && init_rank && allreduce && destroy && allgather;
   }
 };
@@ -97,7 +100,8 @@ struct BlasApi {
 BlasApi g_blas;
 constexpr size_t kBlasWorkspace = size_t(32) << 20;
 
-enum class State { Created, Prepared, Finalized };
+static_assert(kRedLen == ESPO_REDUCE_LEN, "reduction vector length is part of the ABI");
+enum class State { Created, Prepared, Reduced, Finalized };
 }  // namespace
 
 struct espo_ctx_s {
@@ -152,6 +156,7 @@ struct espo_ctx_s {
   float4** d_xgath = nullptr;         // device [tp_world]: their partial regions
   std::vector<void*> x_opened;        // IPC-mapped peer buffers (closed at destroy)
   uint32_t x_send_epoch = 0, x_recv_epoch = 0;
+  int64_t peer_timeout_ms = 120000;   // bound on every peer-memory wait (ESPO_OPT_PEER_TIMEOUT_MS)
   // context parallelism (rollouts split across CP ranks by token blocks)
   int cp_rank = 0, cp_world = 1;
   nccl_comm cp_comm = nullptr;        // nullptr with cp_world > 1: same-device emulation
@@ -448,6 +453,10 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       if (value < 0 || value > 6) return ESPO_ERR_INVALID_ARGUMENT;
       c->factored_impl = static_cast<int>(value);
       return ESPO_OK;
+    case ESPO_OPT_PEER_TIMEOUT_MS:
+      if (value < 1 || value > int64_t(24) * 3600 * 1000) return ESPO_ERR_INVALID_ARGUMENT;
+      c->peer_timeout_ms = value;
+      return ESPO_OK;
     case ESPO_OPT_LMHEAD_BWD_ROWS:
       if (value < 0 || value > (1 << 20) || value % kLmBM) return ESPO_ERR_INVALID_ARGUMENT;
       c->lmh_bwd_rows = value ? static_cast<int>(value) : 8192;
@@ -457,6 +466,14 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
 }
 
 uint64_t espo_launch_count(espo_ctx_t c) { return c ? c->launches : 0; }
+
+int32_t espo_comm_size(espo_ctx_t c) {
+  if (!c) return -1;
+  if (!c->comm) return 1;
+  int n = -1;
+  if (!g_nccl.count || g_nccl.count(c->comm, &n) != 0) return -1;
+  return n;
+}
 
 espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* group_ids,
                          const int64_t* seq_offsets, int32_t n_rollouts, int64_t n_tokens,
@@ -498,7 +515,11 @@ espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* grou
     ESPO_LAUNCHED(c);
   }
   c->prep_ev_set = false;
-  if (!c->cfg.zero_fill_inactive_rows && n_rollouts > 0) {
+  // under stream capture the host copy would become a graph node whose landing the host
+  // cannot observe at capture time: skip it (the backward grid then covers whole chunks)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  ESPO_CUDA(cudaStreamIsCapturing(s, &cap));
+  if (!c->cfg.zero_fill_inactive_rows && n_rollouts > 0 && cap == cudaStreamCaptureStatusNone) {
     if (n_rollouts > c->h_cap) {
       if (c->h_so) cudaFreeHost(c->h_so);
       if (c->h_cand) cudaFreeHost(c->h_cand);
@@ -655,6 +676,7 @@ TpxParams tpx_params(espo_ctx_t c, uint32_t epoch) {
   x.cap = c->x_cap;
   x.epoch = epoch;
   x.slot = int(epoch & 1u);
+  x.timeout_ns = uint64_t(c->peer_timeout_ms) * 1000000ull;
   return x;
 }
 
@@ -1213,15 +1235,10 @@ espo_status espo_cp_gather_local(espo_ctx_t c, const espo_ctx_t* ranks, int32_t 
   return ESPO_OK;
 }
 
-espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_dev,
-                               espo_stream_t stream) {
-  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
-  const int64_t need = c->cp_world > 1 ? cp_hi(c) - cp_lo(c) : c->T;
-  if (c->state != State::Prepared || c->n_covered != need) return ESPO_ERR_BAD_STATE;
-  if (c->cp_world > 1 && !c->cp_comm && !c->cp_gathered) return ESPO_ERR_BAD_STATE;
-  DevGuard g(c->device);
-  cudaStream_t s = S(stream);
-  const espo_config& cf = c->cfg;
+namespace {
+// K3 + the fixed-order K4 reduction into ws.red (the rank-local kRedLen fp64 terms); the CP
+// all-gather of the per-token values K3 reads comes first.
+espo_status reduce_local(espo_ctx_t c, cudaStream_t s) {
   if (c->cp_comm && c->T > 0) {
     // context parallelism: in-place all-gather of the per-token values K3 reads (13 B/token)
     const size_t tb = size_t(cp_block(c)), off = size_t(c->cp_rank) * tb;
@@ -1241,11 +1258,58 @@ espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_
   } else {
     ESPO_CUDA(cudaMemsetAsync(c->ws.red, 0, kRedLen * sizeof(double), s));
   }
+  return ESPO_OK;
+}
+
+espo_status finalize_check(espo_ctx_t c) {
+  const int64_t need = c->cp_world > 1 ? cp_hi(c) - cp_lo(c) : c->T;
+  if (c->state != State::Prepared || c->n_covered != need) return ESPO_ERR_BAD_STATE;
+  if (c->cp_world > 1 && !c->cp_comm && !c->cp_gathered) return ESPO_ERR_BAD_STATE;
+  return ESPO_OK;
+}
+}  // namespace
+
+espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_dev,
+                               espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  espo_status st = finalize_check(c);
+  if (st != ESPO_OK) return st;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  const espo_config& cf = c->cfg;
+  if ((st = reduce_local(c, s)) != ESPO_OK) return st;
   if (c->comm) {
     if (g_nccl.allreduce(c->ws.red, c->ws.red, kRedLen, kNcclFloat64, kNcclSum, c->comm, s) != 0)
       return ESPO_ERR_NCCL;
   }
   k_finalize_scalar<<<1, 1, 0, s>>>(c->ws, cf.norm, cf.logit_scale, loss_dev, stats_dev);
+  ESPO_LAUNCHED(c);
+  c->state = State::Finalized;
+  return ESPO_OK;
+}
+
+espo_status espo_loss_reduce_local(espo_ctx_t c, double* partial_out, espo_stream_t stream) {
+  if (!c || !partial_out) return ESPO_ERR_INVALID_ARGUMENT;
+  espo_status st = finalize_check(c);
+  if (st != ESPO_OK) return st;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  if ((st = reduce_local(c, s)) != ESPO_OK) return st;
+  ESPO_CUDA(cudaMemcpyAsync(partial_out, c->ws.red, kRedLen * sizeof(double),
+                            cudaMemcpyDeviceToDevice, s));
+  c->state = State::Reduced;
+  return ESPO_OK;
+}
+
+espo_status espo_loss_finalize_reduced(espo_ctx_t c, const double* reduced, float* loss_dev,
+                                       espo_stats* stats_dev, espo_stream_t stream) {
+  if (!c || !reduced) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Reduced) return ESPO_ERR_BAD_STATE;
+  DevGuard g(c->device);
+  cudaStream_t s = S(stream);
+  ESPO_CUDA(cudaMemcpyAsync(c->ws.red, reduced, kRedLen * sizeof(double),
+                            cudaMemcpyDeviceToDevice, s));
+  k_finalize_scalar<<<1, 1, 0, s>>>(c->ws, c->cfg.norm, c->cfg.logit_scale, loss_dev, stats_dev);
   ESPO_LAUNCHED(c);
   c->state = State::Finalized;
   return ESPO_OK;
@@ -1268,8 +1332,18 @@ espo_status check_bwd_args(espo_ctx_t c, const void* logits, int64_t ld, const v
 
 // Rows of [b, e) that belong to rollouts whose group is not eliminated (an upper bound on the
 // rows with gradient), from the host copy taken at prepare — or e − b if it has not landed.
-int64_t candidate_rows(espo_ctx_t c, int64_t b, int64_t e) {
-  if (!c->prep_ev_set || cudaEventQuery(c->prep_ev) != cudaSuccess) return e - b;
+int64_t candidate_rows(espo_ctx_t c, int64_t b, int64_t e, cudaStream_t s) {
+  if (!c->prep_ev_set) return e - b;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();          // a capture-related query error must not leak into the
+    return e - b;                // ESPO_LAUNCHED check of the launch that follows
+  }
+  const cudaError_t q = cudaEventQuery(c->prep_ev);
+  if (q != cudaSuccess) {
+    if (q != cudaErrorNotReady) cudaGetLastError();   // anything else: treat as not landed
+    return e - b;
+  }
   const int64_t* so = c->h_so;
   const int R = c->R;
   int i = static_cast<int>(std::upper_bound(so, so + R + 1, b) - so) - 1;   // rollout holding row b
@@ -1347,7 +1421,7 @@ espo_status launch_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogi
     const int ntiles = (((p.V + epv - 1) / epv) + 256 * 8 - 1) / (256 * 8);
     // compact mode writes only rows with gradient: bound the grid by the candidate rows so
     // the blocks past the lists' end are not launched just to exit
-    const int64_t bound = p.zero_fill ? n_rows : candidate_rows(c, row_begin, row_begin + n_rows);
+    const int64_t bound = p.zero_fill ? n_rows : candidate_rows(c, row_begin, row_begin + n_rows, s);
     if (bound == 0) return ESPO_OK;
     const int64_t grid = (bound + rpb - 1) / rpb * int64_t(ntiles);
     if (grid > INT32_MAX) return ESPO_ERR_INVALID_ARGUMENT;

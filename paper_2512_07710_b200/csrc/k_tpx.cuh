@@ -14,8 +14,9 @@
 //   recv: k_tpx_combine — acquire-wait until ready[slot][k] == e for all k, then the exact
 //         merge of k_fwd_combine from the local buffer; k_tpx_post — consumed[j] = e on every
 //         rank (the slot may be rewritten at epoch e + 2).
-// Waits are bounded (≈ seconds): a peer that never arrives sets ESPO_ERR_PEER_TIMEOUT instead
-// of hanging the GPU.
+// Waits are bounded in wall time (ESPO_OPT_PEER_TIMEOUT_MS, default 120 s): a peer that never
+// arrives sets ESPO_ERR_PEER_TIMEOUT instead of hanging the GPU; the step is then invalid
+// (k_tpx_combine leaves the chunk's row statistics unwritten).
 #pragma once
 #include "common.cuh"
 #include "k_rowstats.cuh"
@@ -35,14 +36,24 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Bounded spin: true when pred() held; false after ~2^22 polls with back-off.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Bounded spin: true when pred() held; false once timeout_ns of wall time (the device's
+// global timer) passed without it. The bound is ESPO_OPT_PEER_TIMEOUT_MS (default 120 s):
+// generous enough for normal rank skew (host-side data work, GC), finite so a dead peer
+// becomes ESPO_ERR_PEER_TIMEOUT instead of a hung GPU.
 template <typename F>
-__device__ __forceinline__ bool spin_until(F pred) {
-  for (uint32_t it = 0; it < (1u << 22); ++it) {
+__device__ __forceinline__ bool spin_until(F pred, uint64_t timeout_ns) {
+  const uint64_t t0 = globaltimer_ns();
+  for (uint32_t it = 0;; ++it) {
     if (pred()) return true;
+    if ((it & 63) == 63 && globaltimer_ns() - t0 > timeout_ns) return pred();
     __nanosleep(it < 64 ? 32 : 256);
   }
-  return false;
 }
 
 struct TpxParams {
@@ -52,6 +63,7 @@ struct TpxParams {
   int64_t cap;            // rows per (slot, rank) block
   uint32_t epoch;
   int slot;
+  uint64_t timeout_ns;    // bound on every wait (ESPO_OPT_PEER_TIMEOUT_MS)
 };
 
 // wait until every rank consumed epoch − 2 (the last user of this slot)
@@ -60,7 +72,7 @@ __global__ void k_tpx_wait_consumed(const TpxParams x, int* err) {
   const uint32_t* consumed = reinterpret_cast<const uint32_t*>(x.local + kTpxConsumedOff);
   const uint32_t need = x.epoch - 2;
   for (int k = 0; k < x.tp_world; ++k)
-    if (!spin_until([&] { return ld_acquire_sys(consumed + k) >= need; })) {
+    if (!spin_until([&] { return ld_acquire_sys(consumed + k) >= need; }, x.timeout_ns)) {
       set_error(err, ESPO_ERR_PEER_TIMEOUT);
       return;
     }
@@ -83,7 +95,7 @@ __global__ void __launch_bounds__(256) k_tpx_combine(const TpxParams x, int64_t 
     const uint32_t* ready = reinterpret_cast<const uint32_t*>(x.local) + x.slot * x.tp_world;
     ok = 1;
     for (int k = 0; k < x.tp_world && ok; ++k)
-      if (!spin_until([&] { return ld_acquire_sys(ready + k) == x.epoch; })) ok = 0;
+      if (!spin_until([&] { return ld_acquire_sys(ready + k) == x.epoch; }, x.timeout_ns)) ok = 0;
     if (!ok) set_error(ws.err, ESPO_ERR_PEER_TIMEOUT);
   }
   __syncthreads();

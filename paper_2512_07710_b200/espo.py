@@ -28,6 +28,8 @@ ZV_MASK, ZV_RLZVP = 0, 1
 OPT_FWD_IMPL, OPT_BWD_IMPL, OPT_BLOCKS_PER_SM, OPT_LMHEAD_PARTS, OPT_LMHEAD_BWD_ROWS = 0, 1, 2, 3, 4
 OPT_LMHEAD_2CTA = 5
 OPT_FACTORED_IMPL = 6
+OPT_PEER_TIMEOUT_MS = 7
+REDUCE_LEN = 26          # ESPO_REDUCE_LEN: fp64 terms of espo_loss_reduce_local
 
 STATUS = {
     0: "ESPO_OK", 1: "ESPO_ERR_INVALID_ARGUMENT", 2: "ESPO_ERR_ALIGNMENT",
@@ -46,6 +48,7 @@ EXPORTED_SYMBOLS = [
     "espo_tp_p2p_connect_local", "espo_tp_p2p_unmap", "espo_loss_fwd_p2p_send", "espo_loss_fwd_p2p_recv",
     "espo_attach_cp", "espo_cp_gather_local", "espo_reward_shaping_default",
     "espo_reshape_rewards", "espo_loss_fwd_factored", "espo_loss_row_scale",
+    "espo_loss_reduce_local", "espo_loss_finalize_reduced", "espo_comm_size",
 ]
 
 
@@ -124,6 +127,7 @@ def load_library():
         "espo_export_token_stats": (I32, [P, I64, I64, P, P, P, P, P, P, P, P, P]),
         "espo_export_rollout_stats": (I32, [P, P, P, P, P, P, P, P]),
         "espo_launch_count": (ctypes.c_uint64, [P]),
+        "espo_comm_size": (I32, [P]),
         "espo_set_option": (I32, [P, I32, I64]),
         "espo_loss_fwd_partial": (I32, [P, P, I64, P, P, P, I64, I64, P, P]),
         "espo_loss_fwd_combine": (I32, [P, P, I32, I64, I64, P]),
@@ -139,6 +143,8 @@ def load_library():
         "espo_loss_fwd_p2p_send": (I32, [P, P, I64, P, P, P, I64, I64, P]),
         "espo_loss_fwd_p2p_recv": (I32, [P, I64, I64, P]),
         "espo_loss_fwd_bwd": (I32, [P, P, I64, P, P, P, I64, P, I64, I64, P]),
+        "espo_loss_reduce_local": (I32, [P, P, P]),
+        "espo_loss_finalize_reduced": (I32, [P, P, P, P, P]),
         "espo_loss_fwd_factored": (I32, [P, P, I64, P, P, P, P, I64, I64, I64, P]),
         "espo_loss_row_scale": (I32, [P, P, P, I64, I64, P]),
         "espo_lmhead_bwd": (I32, [P, P, I64, P, I64, I32, P, I64, I32, P, I64, P, I64, I64, P]),
@@ -164,6 +170,38 @@ def _check(status, where):
 
 
 _DT = {torch.float32: F32, torch.bfloat16: BF16}
+
+
+def check_tensor(t, name, dtype, device, rows=None, width=None, optional=False):
+    """Argument check before a pointer crosses the C ABI (which only sees addresses and
+    pitches): dtype, device, unit inner stride, and the row count / row width the call will
+    touch. Raises TypeError (dtype) or ValueError (everything else); None passes only when
+    `optional`. A 1-D tensor must be contiguous with ≥ rows elements; a 2-D tensor needs
+    stride(-1) == 1, ≥ rows rows and ≥ width columns."""
+    if t is None:
+        if optional:
+            return
+        raise ValueError(f"{name} is required")
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor, got {type(t).__name__}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} dtype {t.dtype} != {dtype}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, the context on {device}")
+    if t.dim() == 1:
+        if t.numel() > 1 and t.stride(0) != 1:
+            raise ValueError(f"{name} must be contiguous")
+        if rows is not None and t.shape[0] < rows:
+            raise ValueError(f"{name} has {t.shape[0]} elements < {rows}")
+    elif t.dim() == 2:
+        if t.shape[1] > 1 and t.stride(1) != 1:
+            raise ValueError(f"{name} inner stride {t.stride(1)} != 1")
+        if rows is not None and t.shape[0] < rows:
+            raise ValueError(f"{name} has {t.shape[0]} rows < {rows}")
+        if width is not None and t.shape[1] < width:
+            raise ValueError(f"{name} has {t.shape[1]} columns < {width}")
+    else:
+        raise ValueError(f"{name} must be 1-D or 2-D, got {t.dim()}-D")
 
 
 def new_unique_id() -> bytes:
@@ -264,10 +302,43 @@ class Espo:
     def launch_count(self) -> int:
         return int(self._lib.espo_launch_count(self._h))
 
+    @property
+    def comm_size(self) -> int:
+        """espo_comm_size: ranks of the DP communicator (ncclCommCount; 1 at world 1)."""
+        return int(self._lib.espo_comm_size(self._h))
+
+    @property
+    def width(self) -> int:
+        """Columns a logits chunk of this context holds (the shard width when sharded)."""
+        return int(self.cfg.vocab_local) if self.cfg.vocab_local > 0 else self.vocab
+
+    def _check_fwd(self, logits, tokens, old_logp, mask):
+        check_tensor(logits, "logits", self.logits_dtype, self.device, width=self.width)
+        if logits.dim() != 2:
+            raise ValueError("logits must be 2-D [rows, >= vocab]")
+        n = int(logits.shape[0])
+        check_tensor(tokens, "tokens", torch.int32, self.device, n)
+        check_tensor(old_logp, "old_logp", torch.float32, self.device, n)
+        check_tensor(mask, "mask", torch.uint8, self.device, n, optional=True)
+        return n
+
+    def _check_grad(self, t, name, n, optional=False):
+        check_tensor(t, name, self.grad_dtype, self.device, n, self.width, optional=optional)
+        if t is not None and t.dim() != 2:
+            raise ValueError(f"{name} must be 2-D [rows, >= vocab]")
+
+    def _check_scalar(self, grad_loss):
+        check_tensor(grad_loss, "grad_loss", torch.float32, self.device, 1, optional=True)
+
     # -- the pass ---------------------------------------------------------------------------
     def prepare(self, rewards, group_ids, seq_offsets, n_tokens=None, adv_out=None, zv_out=None):
         """espo_prepare: rewards f32[R], group_ids i32[R], seq_offsets i64[R+1] (device)."""
         R = int(rewards.shape[0])
+        check_tensor(rewards, "rewards", torch.float32, self.device, R)
+        check_tensor(group_ids, "group_ids", torch.int32, self.device, R)
+        check_tensor(seq_offsets, "seq_offsets", torch.int64, self.device, R + 1)
+        check_tensor(adv_out, "adv_out", torch.float32, self.device, R, optional=True)
+        check_tensor(zv_out, "zv_out", torch.uint8, self.device, R, optional=True)
         if n_tokens is None:
             n_tokens = int(seq_offsets[-1].item())
         self.n_tokens, self.n_rollouts = int(n_tokens), R
@@ -277,9 +348,7 @@ class Espo:
 
     def loss_fwd(self, logits, tokens, old_logp, mask=None, row_begin=0):
         """espo_loss_fwd over rows [row_begin, row_begin + logits.shape[0])."""
-        if logits.dtype != self.logits_dtype:
-            raise TypeError(f"logits dtype {logits.dtype} != context {self.logits_dtype}")
-        n = int(logits.shape[0])
+        n = self._check_fwd(logits, tokens, old_logp, mask)
         _check(self._lib.espo_loss_fwd(self._h, _ptr(logits), int(logits.stride(0)),
                                        _ptr(tokens), _ptr(old_logp), _ptr(mask), int(row_begin),
                                        n, 0, self._stream()), "espo_loss_fwd")
@@ -337,6 +406,7 @@ class Espo:
         _check(self._lib.espo_tp_p2p_unmap(self._h), "espo_tp_p2p_unmap")
 
     def loss_fwd_p2p_send(self, logits, tokens, old_logp, mask=None, row_begin=0):
+        self._check_fwd(logits, tokens, old_logp, mask)
         _check(self._lib.espo_loss_fwd_p2p_send(self._h, _ptr(logits), int(logits.stride(0)),
                                                 _ptr(tokens), _ptr(old_logp), _ptr(mask),
                                                 int(row_begin), int(logits.shape[0]),
@@ -348,14 +418,16 @@ class Espo:
 
     def set_mask(self, mask=None):
         """espo_set_mask: single-pass mode; D counted from the batch mask u8[T] (None = ones)."""
+        check_tensor(mask, "mask", torch.uint8, self.device, self.n_tokens, optional=True)
         _check(self._lib.espo_set_mask(self._h, _ptr(mask), self._stream()), "espo_set_mask")
 
     def loss_fwd_bwd(self, logits, tokens, old_logp, dlogits=None, row_begin=0, grad_loss=None):
         """espo_loss_fwd_bwd: forward + backward of a chunk of complete rollouts."""
-        if logits.dtype != self.logits_dtype:
-            raise TypeError(f"logits dtype {logits.dtype} != context {self.logits_dtype}")
+        n = self._check_fwd(logits, tokens, old_logp, None)
+        self._check_scalar(grad_loss)
         if dlogits is None:
             dlogits = torch.empty(logits.shape, dtype=self.grad_dtype, device=logits.device)
+        self._check_grad(dlogits, "dlogits", n)
         _check(self._lib.espo_loss_fwd_bwd(self._h, _ptr(logits), int(logits.stride(0)),
                                            _ptr(tokens), _ptr(old_logp), _ptr(dlogits),
                                            int(dlogits.stride(0)), _ptr(grad_loss),
@@ -365,11 +437,14 @@ class Espo:
 
     def loss_fwd_factored(self, logits, tokens, old_logp, mask=None, grad=None, row_begin=0):
         """espo_loss_fwd_factored: the forward of these rows plus G = onehot(y) − softmax(λz)
-        written to `grad` (allocated if None; may be `logits` itself). Returns grad."""
-        if logits.dtype != self.logits_dtype:
-            raise TypeError(f"logits dtype {logits.dtype} != context {self.logits_dtype}")
+        written to `grad` (allocated if None; may be `logits` itself). Returns grad.
+        In compact mode rows without gradient are left as they were, so an allocated grad
+        is zero-initialised (a consumer's diag(scale)·G then never meets garbage)."""
+        n = self._check_fwd(logits, tokens, old_logp, mask)
         if grad is None:
-            grad = torch.empty(logits.shape, dtype=self.grad_dtype, device=logits.device)
+            alloc = torch.empty if self.cfg.zero_fill_inactive_rows else torch.zeros
+            grad = alloc(logits.shape, dtype=self.grad_dtype, device=logits.device)
+        self._check_grad(grad, "grad", n)
         _check(self._lib.espo_loss_fwd_factored(
             self._h, _ptr(logits), int(logits.stride(0)), _ptr(tokens), _ptr(old_logp), _ptr(mask),
             _ptr(grad), int(grad.stride(0)), int(row_begin), int(logits.shape[0]), self._stream()),
@@ -382,15 +457,20 @@ class Espo:
             n_rows = self.n_tokens - row_begin
         if out is None:
             out = torch.empty(n_rows, dtype=torch.float32, device=self.device)
+        check_tensor(out, "out", torch.float32, self.device, n_rows)
+        self._check_scalar(grad_loss)
         _check(self._lib.espo_loss_row_scale(self._h, _ptr(grad_loss), _ptr(out), int(row_begin),
                                              int(n_rows), self._stream()), "espo_loss_row_scale")
         return out
 
     def loss_fwd_partial(self, logits, tokens, old_logp, mask=None, row_begin=0, partial=None):
         """espo_loss_fwd_partial: this vocabulary shard's per-row {R, S, W, u_y} (f32[n, 4])."""
-        n = int(logits.shape[0])
+        n = self._check_fwd(logits, tokens, old_logp, mask)
         if partial is None:
             partial = torch.empty((n, 4), dtype=torch.float32, device=logits.device)
+        check_tensor(partial, "partial", torch.float32, self.device, n, 4)
+        if partial.dim() != 2 or partial.stride(0) != 4:
+            raise ValueError("partial must be a dense [n_rows, 4] tensor")
         _check(self._lib.espo_loss_fwd_partial(self._h, _ptr(logits), int(logits.stride(0)),
                                                _ptr(tokens), _ptr(old_logp), _ptr(mask),
                                                int(row_begin), n, _ptr(partial), self._stream()),
@@ -400,6 +480,10 @@ class Espo:
     def loss_fwd_combine(self, partials, row_begin=0):
         """espo_loss_fwd_combine over partials [n_shards, n_rows, 4] (device)."""
         partials = partials.contiguous()
+        if partials.dim() != 3 or partials.shape[2] != 4:
+            raise ValueError("partials must be [n_shards, n_rows, 4]")
+        if partials.dtype != torch.float32 or partials.device != self.device:
+            raise TypeError("partials must be float32 on the context's device")
         _check(self._lib.espo_loss_fwd_combine(self._h, _ptr(partials), int(partials.shape[0]),
                                                int(row_begin), int(partials.shape[1]),
                                                self._stream()), "espo_loss_fwd_combine")
@@ -407,7 +491,13 @@ class Espo:
     def lmhead_fwd(self, hidden, weight, tokens, old_logp, mask=None, row_begin=0):
         """espo_lmhead_fwd: fused LM head (tcgen05) + forward statistics; logits never
         materialised. hidden bf16 [n, d], weight bf16 [vocab, d]."""
+        check_tensor(hidden, "hidden", torch.bfloat16, self.device)
         n, d = int(hidden.shape[0]), int(hidden.shape[1])
+        full = self.vocab if self.cfg.vocab_local == 0 else None   # sharded: UNSUPPORTED below
+        check_tensor(weight, "weight", torch.bfloat16, self.device, full, d)
+        check_tensor(tokens, "tokens", torch.int32, self.device, n)
+        check_tensor(old_logp, "old_logp", torch.float32, self.device, n)
+        check_tensor(mask, "mask", torch.uint8, self.device, n, optional=True)
         _check(self._lib.espo_lmhead_fwd(self._h, _ptr(hidden), int(hidden.stride(0)),
                                          _ptr(weight), int(weight.stride(0)), d, _ptr(tokens),
                                          _ptr(old_logp), _ptr(mask), int(row_begin), n,
@@ -417,9 +507,18 @@ class Espo:
                    dh_dtype=None):
         """espo_lmhead_bwd: dhidden (overwritten, [n, d]) and dweight (f32 [vocab, d],
         accumulated) for rows [row_begin, row_begin + n) of the fused LM head."""
+        check_tensor(hidden, "hidden", torch.bfloat16, self.device)
         n, d = int(hidden.shape[0]), int(hidden.shape[1])
+        full = self.vocab if self.cfg.vocab_local == 0 else None
+        check_tensor(weight, "weight", torch.bfloat16, self.device, full, d)
+        self._check_scalar(grad_loss)
         if dhidden is None:
             dhidden = torch.empty((n, d), dtype=dh_dtype or torch.float32, device=hidden.device)
+        if dhidden is not False:
+            if dhidden.dtype not in _DT:
+                raise TypeError(f"dhidden dtype {dhidden.dtype} not float32/bfloat16")
+            check_tensor(dhidden, "dhidden", dhidden.dtype, self.device, n, d)
+        check_tensor(dweight, "dweight", torch.float32, self.device, full, d, optional=True)
         dt = _DT[dhidden.dtype] if dhidden is not False else F32
         dh = None if dhidden is False else dhidden
         _check(self._lib.espo_lmhead_bwd(self._h, _ptr(hidden), int(hidden.stride(0)),
@@ -448,18 +547,48 @@ class Espo:
 
     def loss_finalize(self, loss_out=None, stats_out=None):
         """espo_loss_finalize → (loss f32[1], stats f64[STATS_LEN]) device tensors."""
-        if loss_out is None:
-            loss_out = torch.empty(1, dtype=torch.float32, device=self.device)
-        if stats_out is None:
-            stats_out = torch.empty(STATS_LEN, dtype=torch.float64, device=self.device)
+        loss_out, stats_out = self._outs(loss_out, stats_out)
         _check(self._lib.espo_loss_finalize(self._h, _ptr(loss_out), _ptr(stats_out),
                                             self._stream()), "espo_loss_finalize")
         return loss_out, stats_out
 
+    def _outs(self, loss_out, stats_out):
+        if loss_out is None:
+            loss_out = torch.empty(1, dtype=torch.float32, device=self.device)
+        if stats_out is None:
+            stats_out = torch.empty(STATS_LEN, dtype=torch.float64, device=self.device)
+        check_tensor(loss_out, "loss_out", torch.float32, self.device, 1)
+        check_tensor(stats_out, "stats_out", torch.float64, self.device, STATS_LEN)
+        return loss_out, stats_out
+
+    def loss_reduce_local(self, partial_out=None):
+        """espo_loss_reduce_local → this rank's REDUCE_LEN fp64 terms (device), to be summed
+        over ranks by the caller's collective and passed to loss_finalize_reduced."""
+        if partial_out is None:
+            partial_out = torch.empty(REDUCE_LEN, dtype=torch.float64, device=self.device)
+        check_tensor(partial_out, "partial_out", torch.float64, self.device, REDUCE_LEN)
+        _check(self._lib.espo_loss_reduce_local(self._h, _ptr(partial_out), self._stream()),
+               "espo_loss_reduce_local")
+        return partial_out
+
+    def loss_finalize_reduced(self, reduced, loss_out=None, stats_out=None):
+        """espo_loss_finalize_reduced with the rank-summed terms → (loss, stats)."""
+        check_tensor(reduced, "reduced", torch.float64, self.device, REDUCE_LEN)
+        loss_out, stats_out = self._outs(loss_out, stats_out)
+        _check(self._lib.espo_loss_finalize_reduced(self._h, _ptr(reduced), _ptr(loss_out),
+                                                    _ptr(stats_out), self._stream()),
+               "espo_loss_finalize_reduced")
+        return loss_out, stats_out
+
     def loss_bwd(self, logits, dlogits=None, row_begin=0, grad_loss=None):
         """espo_loss_bwd: d(grad_loss·loss)/d logits for rows of this chunk."""
+        check_tensor(logits, "logits", self.logits_dtype, self.device, width=self.width)
+        if logits.dim() != 2:
+            raise ValueError("logits must be 2-D [rows, >= vocab]")
+        self._check_scalar(grad_loss)
         if dlogits is None:
             dlogits = torch.empty(logits.shape, dtype=self.grad_dtype, device=logits.device)
+        self._check_grad(dlogits, "dlogits", int(logits.shape[0]))
         _check(self._lib.espo_loss_bwd(self._h, _ptr(logits), int(logits.stride(0)),
                                        _ptr(dlogits), int(dlogits.stride(0)), _ptr(grad_loss),
                                        int(row_begin), int(logits.shape[0]), self._stream()),

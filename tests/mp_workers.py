@@ -84,3 +84,26 @@ def worker_subgroup_unique_id(rank, world, port, out_q):
     full = bootstrap_unique_id(rank)
     out_q.put((rank, None if uid is None else len(uid), len(full)))
     dist.destroy_process_group()
+
+
+def worker_bench_strong_batch(rank, world, port, out_q):
+    """bench.py's strong-scaling data path on the CPU (C0 recipe): this rank's share of the
+    global batch — global row id, token, old log-prob and the buffer row each local row reads."""
+    import torch
+    dist = _init(rank, world, port)
+    import bench
+    import espo_synth as S
+    w = S.WORKLOADS["C0"]
+    seed = S.config_seed(w.index)
+    d = bench.make_batch(w, seed, torch.device("cpu"), 64, lambda m: None,
+                         shard=(world, rank), drift=(0.04, 0.02))
+    bufrow = np.empty(d["T"], np.int64)
+    for b, e in d["chunks"]:
+        bufrow[b:e] = np.arange(e - b)
+    g = d["global_row"].numpy()
+    out = (rank, g.tolist(), d["tokens"].numpy().tolist(), d["old"].numpy().tolist(),
+           bufrow.tolist(), [list(c) for c in d["chunks"]], d["np"]["group_ids"].tolist(),
+           d["np"]["seq_offsets"].tolist())
+    dist.barrier()
+    out_q.put(out)
+    dist.destroy_process_group()

@@ -95,3 +95,32 @@ def test_host_only_entry_points(lib):
     assert lib.espo_loss_fwd(None, None, 0, None, None, None, 0, 0, 0, None) == 1
     lib.espo_launch_count.restype = ctypes.c_uint64
     assert lib.espo_launch_count(None) == 0
+
+
+def test_binding_argument_checks():
+    """The binding validates what the C ABI cannot see (it only gets addresses and pitches):
+    dtype (int64 tokens would be read as interleaved int32 pairs), inner stride, row count,
+    row width and device."""
+    import torch
+    from paper_2512_07710_b200.espo import check_tensor
+    cpu = torch.device("cpu")
+    check_tensor(torch.zeros(8, dtype=torch.int32), "tokens", torch.int32, cpu, 8)
+    check_tensor(None, "mask", torch.uint8, cpu, 8, optional=True)
+    with pytest.raises(TypeError):
+        check_tensor(torch.zeros(8, dtype=torch.int64), "tokens", torch.int32, cpu, 8)
+    with pytest.raises(ValueError):
+        check_tensor(torch.zeros(7, dtype=torch.int32), "tokens", torch.int32, cpu, 8)
+    with pytest.raises(ValueError):
+        check_tensor(torch.zeros(16, dtype=torch.int32)[::2], "tokens", torch.int32, cpu, 8)
+    with pytest.raises(ValueError):
+        check_tensor(None, "tokens", torch.int32, cpu, 8)
+    z = torch.zeros((4, 10), dtype=torch.bfloat16)
+    check_tensor(z, "logits", torch.bfloat16, cpu, 4, 10)
+    with pytest.raises(ValueError):
+        check_tensor(z, "logits", torch.bfloat16, cpu, 4, 11)          # row narrower than vocab
+    with pytest.raises(ValueError):
+        check_tensor(z.t(), "logits", torch.bfloat16, cpu)             # inner stride != 1
+    with pytest.raises(TypeError):
+        check_tensor(z, "dlogits", torch.float32, cpu, 4, 10)
+    with pytest.raises(ValueError):
+        check_tensor(z, "logits", torch.bfloat16, torch.device("cuda", 0), 4, 10)

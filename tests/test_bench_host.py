@@ -22,3 +22,56 @@ def test_cpu_baseline_all_cores_runs_the_oracle():
     r = bench.cpu_baseline_parallel("C0", L=4, max_procs=2)
     assert r["kind"] == "oracle" and r["unit"] == "tokens/s"
     assert 1 <= r["cores"] <= 2 and r["value"] > 0
+
+
+def test_group_chunks_stay_inside_groups():
+    gid = np.array([0, 0, 1, 1, 1, 2], dtype=np.int32)
+    so = np.array([0, 7, 12, 20, 21, 33, 40], dtype=np.int64)
+    ch = bench.group_chunks(so, gid, 8)
+    assert ch == [(0, 8), (8, 12), (12, 20), (20, 28), (28, 33), (33, 40)]
+    covered = np.zeros(40, int)
+    for b, e in ch:
+        covered[b:e] += 1
+    assert np.all(covered == 1)
+
+
+def test_resolve_world_rejects_mismatch(monkeypatch):
+    from types import SimpleNamespace as NS
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    with pytest.raises(SystemExit):
+        bench.resolve_world(NS(gpus=4, impl="ours"))
+    a = NS(gpus=None, impl="ours")
+    assert bench.resolve_world(a) == 2 and a.gpus == 2
+    monkeypatch.delenv("WORLD_SIZE")
+    a = NS(gpus=None, impl="ours")
+    assert bench.resolve_world(a) == 1 and a.gpus == 1
+
+
+def test_launcher_spawns_ranks_for_gpus_n():
+    """`bench.py --gpus 2` without torchrun re-executes itself under torch.distributed.run
+    (the driver's launch); the reference arm prints one JSON line from rank 0 only, with
+    n_gpus = 2 (CPU-only: that arm never touches a GPU)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, bench.__file__, "--impl", "reference", "--gpus", "2",
+                        "--config", "C0", "--steps", "1", "--warmup", "0"], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    out = json.loads(lines[0])
+    assert out["impl"] == "reference" and out["n_gpus"] == 2
+
+
+def test_strong_plan_covers_every_group_once():
+    import espo_synth as S
+    w = S.WORKLOADS["C4"]
+    seed = S.config_seed(w.index)
+    for world in (1, 2, 4, 8):
+        gid, so, rw, plan = bench.strong_plan(w, seed, world)
+        assert sorted(sum(plan, [])) == list(range(w.n_prompts))
+        loads = [sum(int(so[(g + 1) * w.G] - so[g * w.G]) for g in p) for p in plan]
+        assert max(loads) - min(loads) <= 2 * w.G * w.L     # LPT: within two groups' rows

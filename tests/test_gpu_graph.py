@@ -131,3 +131,54 @@ def test_graph_capture_single_pass():
     ctx.get_error()
     assert torch.equal(got_loss, loss) and torch.equal(got_dz, dz)
     ctx.close()
+
+
+def test_graph_capture_compact_mode():
+    """Compact mode (rows without gradient untouched) captures too: espo_prepare skips its
+    host copy of the rollout layout under capture and espo_loss_bwd's grid then covers whole
+    chunks; the replay on new data equals an eager run on that data, bitwise."""
+    from paper_2512_07710_b200.espo import STATS_LEN, Espo
+    dev = require_cuda()
+    a = workload_instance("C0")
+    b = workload_instance("C0", seed=4242)
+    T, V = a.T, a.V
+    buf = _inputs(a, dev)
+    ctx = Espo(V, logits_dtype=torch.float32, device=dev.index, zero_fill_inactive_rows=False)
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    stats = torch.empty(STATS_LEN, dtype=torch.float64, device=dev)
+    dz = torch.zeros((T, V), dtype=torch.float32, device=dev)
+    chunks = [(0, 300), (300, T)]
+
+    def step():
+        ctx.prepare(buf["rew"], buf["gid"], buf["off"], n_tokens=T)
+        for lo, hi in chunks:
+            ctx.loss_fwd(buf["z"][lo:hi], buf["tok"][lo:hi], buf["old"][lo:hi], buf["mask"][lo:hi],
+                         row_begin=lo)
+        ctx.loss_finalize(loss, stats)
+        for lo, hi in chunks:
+            ctx.loss_bwd(buf["z"][lo:hi], dz[lo:hi], row_begin=lo)
+
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream(dev).wait_stream(s)
+    ctx.get_error()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    nb = _inputs(b, dev)
+    for k in buf:
+        buf[k].copy_(nb[k])
+    dz.zero_()
+    g.replay()
+    torch.cuda.synchronize(dev)
+    ctx.get_error()
+    got_loss, got_dz = loss.clone(), dz.clone()
+    dz.zero_()
+    step()                                       # eager on the same (new) data
+    torch.cuda.synchronize(dev)
+    ctx.get_error()
+    assert torch.equal(got_loss, loss) and torch.equal(got_dz, dz)
+    assert torch.count_nonzero(got_dz.abs().sum(1)) > 0
+    ctx.close()

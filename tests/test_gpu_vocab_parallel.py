@@ -185,8 +185,10 @@ def test_peer_memory_recv_without_peer_times_out():
     inst = tiny_instance(19, V=256, group_sizes=(2,), L=4)
     ctxs = [Espo(256, logits_dtype=torch.float32, device=dev.index, vocab_shard=(128 * k, 128))
             for k in range(2)]
+    from paper_2512_07710_b200.espo import OPT_PEER_TIMEOUT_MS
     for c in ctxs:
         c.tp_p2p_buffer(16, 2)
+        c.set_option(OPT_PEER_TIMEOUT_MS, 300)     # default 120 s; bound the test's wait
     for k, c in enumerate(ctxs):
         c.tp_p2p_connect_local(ctxs, k)
     z = torch.zeros((inst.T, 128), dtype=torch.float32, device=dev)

@@ -86,3 +86,29 @@ def test_unique_id_bootstrap_over_subgroup():
     out = run_world(mp_workers.worker_subgroup_unique_id)
     assert out[1][1] == 128 and out[0][1] is None
     assert all(o[2] == 128 for o in out)
+
+
+def _strong_rows(out):
+    rows = {}
+    for _, g, tok, old, bufrow, *_ in out:
+        for t, y, o, b in zip(g, tok, old, bufrow):
+            assert t not in rows                        # every global row on exactly one rank
+            rows[t] = (y, o, b)
+    return rows
+
+
+def test_bench_strong_scaling_batch_is_independent_of_world():
+    """bench.py --scaling strong, host side: the world-2 ranks together hold exactly the rows
+    of the world-1 batch, each with the same token, old log-prob and logits buffer row — so
+    the kernels see identical inputs per global row whatever N is."""
+    one = _strong_rows(run_world(mp_workers.worker_bench_strong_batch, world=1))
+    two_out = run_world(mp_workers.worker_bench_strong_batch, world=2)
+    two = _strong_rows(two_out)
+    assert sorted(two) == sorted(one) == list(range(len(one)))
+    assert two == one
+    for _, _, _, _, _, chunks, gid, so in two_out:    # chunks never cross a prompt group
+        so = np.array(so)
+        for b, e in chunks:
+            r0 = int(np.searchsorted(so, b, side="right") - 1)
+            r1 = int(np.searchsorted(so, e - 1, side="right") - 1)
+            assert gid[r0] == gid[r1]
