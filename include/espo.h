@@ -421,7 +421,7 @@ espo_status espo_lmhead_fwd(espo_ctx_t ctx, const void* hidden, int64_t ldh, con
                             const uint8_t* mask, int64_t row_begin, int64_t n_rows,
                             espo_stream_t stream);
 
-/* ---- fused LM head backward (tcgen05 recompute + bf16 dz tile + two GEMMs) ----
+/* ---- fused LM head backward (tcgen05 recompute + bf16 dz tile + two tcgen05 GEMMs) ----
  * Gradients of grad_loss·loss through logits z = hidden·weightᵀ for the
  * rows [row_begin, row_begin + n_rows) of a finalized context whose forward ran through
  * espo_lmhead_fwd with the same hidden/weight:
@@ -431,11 +431,13 @@ espo_status espo_lmhead_fwd(espo_ctx_t ctx, const void* hidden, int64_t ldh, con
  *           ESPO_OPT_LMHEAD_BWD_ROWS × round_up(vocab, 256) bf16 (allocated on first use);
  *   dhidden[r, :] = Σ_v dz[r, v]·weight[v, :]          (overwritten; f32 or bf16 per dh_dtype)
  *   dweight[v, :] += Σ_r dz[r, v]·hidden[r, :]          (f32, ACCUMULATED: zero it once)
- * The two contractions are plain bf16 GEMMs with fp32 accumulation, run by cuBLAS (loaded
- * at run time from libcublas.so.12) on `stream`. Either output may be NULL (skipped). Shapes
- * and alignment as espo_lmhead_fwd; dhidden pitch lddh ≥ d, dweight pitch lddw ≥ d (16-byte
- * aligned). grad_loss_dev as espo_loss_bwd. Errors: ESPO_ERR_BAD_STATE before finalize,
- * ESPO_ERR_UNSUPPORTED on a vocabulary-sharded context, ESPO_ERR_BLAS if cuBLAS fails. */
+ * The two contractions are bf16 × bf16 → fp32 GEMMs on the library's own tcgen05 kernel
+ * (k_gemm.cuh: TMA-fed, TMEM accumulators; dz is read K-major for dh and MN-major for dW, W
+ * and hidden MN-major, so no operand is transposed or copied), on `stream`. Either output may
+ * be NULL (skipped). Shapes and alignment as espo_lmhead_fwd; dhidden pitch lddh ≥ d, dweight
+ * pitch lddw ≥ d (16-byte aligned). grad_loss_dev as espo_loss_bwd. Errors:
+ * ESPO_ERR_BAD_STATE before finalize, ESPO_ERR_UNSUPPORTED on a vocabulary-sharded context,
+ * ESPO_ERR_BLAS only with ESPO_OPT_LMHEAD_BWD_GEMM = 1 (cuBLAS A/B path) if cuBLAS fails. */
 espo_status espo_lmhead_bwd(espo_ctx_t ctx, const void* hidden, int64_t ldh, const void* weight,
                             int64_t ldw, int32_t d, void* dhidden, int64_t lddh, int32_t dh_dtype,
                             float* dweight, int64_t lddw, const float* grad_loss_dev,
@@ -491,10 +493,18 @@ typedef enum {
                                   with plain loads, 2 = 16 warps × 6 × 32 KB, 3 = default + TMEM
                                   stash of pass-1 exponentials, 4-5 = two CTAs per SM,
                                   6 = rolling pass-2/pass-1 interleave (A/B) */
-  ESPO_OPT_PEER_TIMEOUT_MS = 7 /* bound on every peer-memory wait of the TP exchange, in ms of
+  ESPO_OPT_PEER_TIMEOUT_MS = 7,/* bound on every peer-memory wait of the TP exchange, in ms of
                                   device wall time (default 120000); a timeout sets the sticky
                                   ESPO_ERR_PEER_TIMEOUT and invalidates the step (the chunk's
                                   row statistics are not written) */
+  ESPO_OPT_LMHEAD_BWD_GEMM = 8,/* espo_lmhead_bwd's dh / dW contractions: 0 = the library's
+                                  tcgen05 GEMM on CTA pairs (256 × 256 tiles, default), 1 = cuBLAS
+                                  (A/B measurement only), 2 = the tcgen05 GEMM, one CTA per
+                                  128 × 256 tile */
+  ESPO_OPT_GEMM_GROUP_M = 9,   /* dh GEMM tile order: M-blocks per raster group (0 = auto, 8) */
+  ESPO_OPT_GEMM_HINTS = 10     /* L2 policies of the backward GEMMs for A/B measurement: bits 0-7
+                                  dh, 8-15 dW, each A | B << 2 | C << 4 with 0 = normal,
+                                  1 = evict_first, 2 = evict_last; −1 = defaults */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

@@ -18,6 +18,7 @@
 #include "k_lmhead2.cuh"
 #include "k_reward.cuh"
 #include "k_tpx.cuh"
+#include "k_gemm.cuh"
 #include "k_fwdgrad.cuh"
 #include "workspace.cuh"
 
@@ -142,6 +143,9 @@ struct espo_ctx_s {
   int64_t rs_cap = 0;
   int lmh_bwd_rows = 8192;       // LM-head backward dz sub-chunk rows
   int lmh_2cta = 0;              // 1: CTA-pair (cta_group::2) LM-head kernels
+  int lmh_bwd_gemm = 0;          // dh / dW: 0 = tcgen05 CTA-pair GEMM, 1 = cuBLAS (A/B), 2 = one CTA
+  int gemm_group_m = 0;          // dh GEMM tile order: M-blocks per group (0 = auto)
+  int gemm_hints_dh = -1, gemm_hints_dw = -1;   // L2 policies of the two GEMMs (−1 = auto)
   void* lmh_dz = nullptr;        // [lmh_bwd_rows][round_up(V, 256)] bf16, grown on demand
   size_t lmh_dz_cap = 0;
   cublasHandle_t blas = nullptr;
@@ -452,6 +456,19 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
     case ESPO_OPT_FACTORED_IMPL:
       if (value < 0 || value > 6) return ESPO_ERR_INVALID_ARGUMENT;
       c->factored_impl = static_cast<int>(value);
+      return ESPO_OK;
+    case ESPO_OPT_LMHEAD_BWD_GEMM:
+      if (value < 0 || value > 2) return ESPO_ERR_INVALID_ARGUMENT;
+      c->lmh_bwd_gemm = static_cast<int>(value);
+      return ESPO_OK;
+    case ESPO_OPT_GEMM_HINTS:     // low 8 bits: dh, next 8 bits: dW (each A | B<<2 | C<<4); −1 auto
+      if (value < -1 || value > 0xFFFF) return ESPO_ERR_INVALID_ARGUMENT;
+      c->gemm_hints_dh = value < 0 ? -1 : int(value & 0xFF);
+      c->gemm_hints_dw = value < 0 ? -1 : int((value >> 8) & 0xFF);
+      return ESPO_OK;
+    case ESPO_OPT_GEMM_GROUP_M:
+      if (value < 0 || value > 1024) return ESPO_ERR_INVALID_ARGUMENT;
+      c->gemm_group_m = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_PEER_TIMEOUT_MS:
       if (value < 1 || value > int64_t(24) * 3600 * 1000) return ESPO_ERR_INVALID_ARGUMENT;
@@ -836,6 +853,44 @@ int lmhead_parts(const espo_ctx_s* c, int mblocks, int ntiles, int d) {
   if (c->lmh_parts > 0) parts = c->lmh_parts;
   return std::max(1, std::min(parts, std::min(64, ntiles)));
 }
+
+// C[M, N] (+)= A·B on the tcgen05 GEMM (k_gemm.cuh); maps built by the caller for the
+// operands' majorness (K-major A: box {64 K, 128 M}; MN-major: boxes {64 MN, 64 K}).
+// pair: CTA-pair kernel (256 × 256 tiles per cluster of 2), else one CTA per 128 × 256 tile.
+template <bool kAMN, bool kBMN, int kOut>
+espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensorMap& mb, int M,
+                             int N, int64_t K, void* C, int64_t ldc, bool pair, int group_m,
+                             int hints, cudaStream_t s) {
+  static unsigned long long attr = 0, attr2 = 0;
+  GemmParams p;
+  p.M = M;
+  p.N = N;
+  p.K = int(K);
+  const int bm = pair ? 2 * kGmBM : kGmBM;
+  p.mblk = (M + bm - 1) / bm;
+  p.nblk = (N + kGmBN - 1) / kGmBN;
+  p.kblk = int((K + kGmBK - 1) / kGmBK);
+  p.group_m = std::max(1, group_m);
+  p.hint_a = hints & 3;          // hints: 2 bits each for A, B, C
+  p.hint_b = (hints >> 2) & 3;
+  p.hint_c = (hints >> 4) & 3;
+  p.C = C;
+  p.ldc = ldc;
+  const int64_t tiles = int64_t(p.mblk) * p.nblk;
+  if (tiles == 0 || p.kblk == 0) return ESPO_OK;
+  if (tiles > INT32_MAX) return ESPO_ERR_INVALID_ARGUMENT;
+  if (pair) {
+    ESPO_CUDA(ensure_smem_attr(k_umma_gemm2<kAMN, kBMN, kOut>, int(kG2Smem), attr2));
+    const int clusters = int(std::min<int64_t>(tiles, c->num_sms / 2));
+    k_umma_gemm2<kAMN, kBMN, kOut><<<2 * clusters, kGmThreads, kG2Smem, s>>>(ma, mb, p);
+  } else {
+    ESPO_CUDA(ensure_smem_attr(k_umma_gemm<kAMN, kBMN, kOut>, int(kGmSmem), attr));
+    const int grid = int(std::min<int64_t>(tiles, c->num_sms));
+    k_umma_gemm<kAMN, kBMN, kOut><<<grid, kGmThreads, kGmSmem, s>>>(ma, mb, p);
+  }
+  ESPO_LAUNCHED(c);
+  return ESPO_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -934,16 +989,19 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
     ESPO_CUDA(cudaMalloc(&c->lmh_dz, need));
     c->lmh_dz_cap = need;
   }
-  if (!c->blas) {
-    if (!g_blas.load()) return ESPO_ERR_BLAS;
-    if (g_blas.create(&c->blas) != 0) {
-      c->blas = nullptr;
-      return ESPO_ERR_BLAS;
+  const bool use_blas = c->lmh_bwd_gemm == 1;
+  if (use_blas) {
+    if (!c->blas) {
+      if (!g_blas.load()) return ESPO_ERR_BLAS;
+      if (g_blas.create(&c->blas) != 0) {
+        c->blas = nullptr;
+        return ESPO_ERR_BLAS;
+      }
+      ESPO_CUDA(cudaMalloc(&c->blas_ws, kBlasWorkspace));
+      if (g_blas.set_workspace(c->blas, c->blas_ws, kBlasWorkspace) != 0) return ESPO_ERR_BLAS;
     }
-    ESPO_CUDA(cudaMalloc(&c->blas_ws, kBlasWorkspace));
-    if (g_blas.set_workspace(c->blas, c->blas_ws, kBlasWorkspace) != 0) return ESPO_ERR_BLAS;
+    if (g_blas.set_stream(c->blas, s) != 0) return ESPO_ERR_BLAS;
   }
-  if (g_blas.set_stream(c->blas, s) != 0) return ESPO_ERR_BLAS;
   // per-row records {g, −lse·log2e, g·q, y} for the whole chunk (K5's k_bwd_recs, zero-filling)
   BwdRec* rec = static_cast<BwdRec*>(c->ws.list);
   const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
@@ -952,8 +1010,9 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   static unsigned long long attr_mask = 0, attr_mask2 = 0;
   ESPO_CUDA(ensure_smem_attr(k_lmhead_dz, int(kLmSmem), attr_mask));
   ESPO_CUDA(ensure_smem_attr(k_lmhead2_dz, int(kL2Smem), attr_mask2));
-  CUtensorMap mw;
-  if (!make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, c->lmh_2cta ? kLmBN / 2 : kLmBN))
+  CUtensorMap mw, mw_mn;
+  if (!make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, c->lmh_2cta ? kLmBN / 2 : kLmBN) ||
+      !make_map_bf16(&mw_mn, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, 64))
     return ESPO_ERR_CUDA;
   const float one = 1.f, zero = 0.f;
   const char* hb = static_cast<const char*>(hidden);
@@ -982,6 +1041,36 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       k_lmhead_dz<<<dim3(parts, mblocks), kLmThreads, kLmSmem, s>>>(mh, mw, lp);
     ESPO_LAUNCHED(c);
     // z = h·Wᵀ (dz already carries λ, as K5's) ⇒ dh = dz·W and dW = dzᵀ·h
+    if (!use_blas) {
+      CUtensorMap mdz_k, mdz_mn, mh_mn;
+      if (!make_map_bf16(&mdz_k, c->lmh_dz, uint64_t(n), uint64_t(ldz), uint64_t(ldz) * 2, kGmBM) ||
+          !make_map_bf16(&mdz_mn, c->lmh_dz, uint64_t(n), uint64_t(ldz), uint64_t(ldz) * 2, 64) ||
+          !make_map_bf16(&mh_mn, hb + r0 * ldh * 2, uint64_t(n), uint64_t(d), uint64_t(ldh) * 2, 64))
+        return ESPO_ERR_CUDA;
+      espo_status st;
+      const bool pair = c->lmh_bwd_gemm == 0;
+      // tile order: dh has a long K (the vocabulary) and few tiles: groups of 8 M-blocks keep
+      // the resident tiles' A and B panels small; dW (K = rows): N fastest, so every M-block
+      // of dz is read once while h stays in L2
+      const int g_dh = c->gemm_group_m > 0 ? c->gemm_group_m : 8;
+      // L2 policies (2 bits each: A | B << 2 | C << 4; 1 = evict_first, 2 = evict_last):
+      // dh streams both panels once per wave; dW streams dz and the dW read-add-write while
+      // every tile re-reads h (64 MB at n = 8192, d = 4096), which should stay in L2
+      const int hint_dh = c->gemm_hints_dh >= 0 ? c->gemm_hints_dh : 0;
+      const int hint_dw = c->gemm_hints_dw >= 0 ? c->gemm_hints_dw : (1 | (2 << 2) | (1 << 4));
+      if (dhidden) {   // dh[n, d] = dz[n, V] · W[V, d]: A = dz K-major, B = W MN-major
+        char* dh = static_cast<char*>(dhidden) + r0 * lddh * int64_t(dsize(dh_dtype));
+        st = dh_dtype == ESPO_BF16
+                 ? launch_umma_gemm<false, true, kOutBF16>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, pair, g_dh, hint_dh, s)
+                 : launch_umma_gemm<false, true, kOutF32>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, pair, g_dh, hint_dh, s);
+        if (st != ESPO_OK) return st;
+      }
+      if (dweight) {   // dW[V, d] += dzᵀ[V, n] · h[n, d]: A = dz MN-major, B = h MN-major
+        st = launch_umma_gemm<true, true, kOutAddF32>(c, mdz_mn, mh_mn, V, d, n, dweight, lddw, pair, 1, hint_dw, s);
+        if (st != ESPO_OK) return st;
+      }
+      continue;
+    }
     if (dhidden) {   // column-major view: dhᵀ[d, n] = Wᵀ[d, V] · dzᵀ[V, n]
       char* dh = static_cast<char*>(dhidden) + r0 * lddh * int64_t(dsize(dh_dtype));
       if (g_blas.gemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, d, n, V, &one, weight, CUDA_R_16BF,

@@ -1,0 +1,492 @@
+// k_gemm.cuh — the two contractions of the LM-head backward on the 5th-gen tensor cores
+// (the Megatron log-prob recompute of PAPER.md:129-131): with logits
+// z = h·Wᵀ and the bf16 gradient tile dz = ∂(grad·loss)/∂z (k_lmhead_dz),
+//   dh = dz · W      M = rows,  N = d, K = vocabulary   A = dz  (K-major), B = W (MN-major)
+//   dW += dzᵀ · h    M = vocab, N = d, K = rows         A = dzᵀ (MN-major), B = h (MN-major)
+// Both operands stay in the layout the caller and k_lmhead_dz produce — no transposed
+// copies: tcgen05 reads MN-major bf16 tiles directly (instruction-descriptor bits 15/16).
+//
+// One persistent kernel: grid = min(tiles, SMs), tile = 128 × 256 outputs, tiles in
+// N-fastest order (the CTAs resident together share A row blocks and read the same B
+// K-slices in step, so both stay in L2). Warp roles (192 threads), as k_lmhead.cuh:
+// warp 0 — TMA producer (4-stage ring of {A 16 KB, B 32 KB} with 128-byte swizzle);
+// warp 1 — TMEM allocator and MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M = 128,
+// N = 256, K = 16, fp32 accumulators in two 256-column TMEM buffers, so tile i+1's MMAs
+// overlap tile i's epilogue); warps 2–5 — epilogue (thread i = row i of the tile,
+// tcgen05.ld 32 columns at a time, fp32/bf16 store or fp32 read-add-write).
+//
+// Shared-memory operand layouts (UMMA canonical forms, SWIZZLE_128B, 1024-B aligned):
+//  K-major : rows of 64 K-elements (128 B), 8-row groups 1024 B apart (one TMA box
+//            {64 K, rows}); +32 B per K = 16 step inside the swizzle atom.
+//  MN-major: lines of 64 MN-elements (128 B), one line per K index, 8-line groups 1024 B
+//            apart (SBO); 64-wide MN blocks 8 KB apart (LBO) = one TMA box {64 MN, 64 K}
+//            each; +2048 B (16 lines) per K = 16 step.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "k_lmhead.cuh"
+#include "k_lmhead2.cuh"
+
+namespace espo {
+
+constexpr int kGmBM = 128, kGmBN = 256, kGmBK = 64, kGmStages = 4;
+constexpr int kGmABytes = kGmBM * kGmBK * 2;    // 16 KB
+constexpr int kGmBBytes = kGmBN * kGmBK * 2;    // 32 KB
+constexpr int kGmStageBytes = kGmABytes + kGmBBytes;
+constexpr int kGmMNBox = 64 * kGmBK * 2;        // one MN-major TMA box {64 MN, 64 K}: 8 KB
+constexpr int kGmThreads = 192;
+constexpr size_t kGmSmem = size_t(kGmStages) * kGmStageBytes + 1024 + 256;
+
+enum GemmOut { kOutF32 = 0, kOutBF16 = 1, kOutAddF32 = 2 };
+
+struct GemmParams {
+  int M, N, K;        // C[M, N] (+)= A[M, K] · B[K, N]
+  int mblk, nblk, kblk;   // tile counts (tile = kGmBM × kGmBN, or 2·kGmBM × kGmBN for a pair)
+  int group_m;        // tile order: groups of group_m M-blocks, M fastest inside a group
+  int hint_a, hint_b, hint_c;   // L2 policy of A / B loads and C read-add-write: 0 normal,
+                                // 1 evict_first (streamed), 2 evict_last (reused)
+  void* C;
+  int64_t ldc;        // elements
+};
+
+// tile index → (M block, N block): groups of group_m M-blocks; inside a group M varies
+// fastest, so the tiles resident together cover ≈ group_m × (resident / group_m) blocks
+// (group_m = 1: N fastest)
+__device__ __forceinline__ void gemm_tile_coords(const GemmParams& p, int tile, int& mb, int& nb) {
+  const int per_group = p.group_m * p.nblk;
+  const int g = tile / per_group, rem = tile - g * per_group;
+  const int first = g * p.group_m;
+  const int gm = min(p.mblk - first, p.group_m);
+  mb = first + rem % gm;
+  nb = rem / gm;
+}
+
+// mbarrier wait bounded by the device's global timer: a protocol error traps (a CUDA error
+// the host sees) instead of hanging the GPU.
+__device__ __forceinline__ void gm_wait(uint64_t* bar, uint32_t parity) {
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+    if ((it & 255u) == 255u) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 20000000000ull) __trap();     // 20 s
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t l2_policy(int hint) {
+  uint64_t pol;
+  if (hint == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else if (hint == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair_hint(uint32_t dst, const CUtensorMap* map, int c0,
+                                                      int c1, uint32_t cluster_bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(cluster_bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ float4 ld_f4_hint(const float4* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_f4_hint(float4* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+
+// UMMA shared-memory descriptor for an MN-major SWIZZLE_128B operand (see header comment)
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr & 0x3FFFF) >> 4);        // start address
+  d |= uint64_t(kGmMNBox >> 4) << 16;           // LBO: next 64-element MN block
+  d |= uint64_t(1024 >> 4) << 32;               // SBO: next group of 8 K lines
+  d |= uint64_t(1) << 46;                       // version (Blackwell)
+  d |= uint64_t(2) << 61;                       // SWIZZLE_128B
+  return d;
+}
+
+template <bool kAMN, bool kBMN>
+__host__ __device__ constexpr uint32_t gemm_idesc() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kAMN) << 15) | (uint32_t(kBMN) << 16) |
+         (uint32_t(kGmBN >> 3) << 17) | (uint32_t(kGmBM >> 4) << 24);
+}
+
+// Epilogue of one tile for TMEM lane `row` (= output row r): 8 × 32 columns from TMEM →
+// C[r, n0 + …] as fp32, bf16 or fp32 read-add-write; rows ≥ M and columns ≥ N skipped.
+template <int kOut>
+__device__ __forceinline__ void gemm_store_tile(const GemmParams& p, uint32_t base, int r, int n0,
+                                                uint64_t pol_c) {
+#pragma unroll 1
+  for (int c = 0; c < kGmBN / 32; ++c) {
+    float x[32];
+    __syncwarp();
+    tmem_ld32(base + uint32_t(c * 32), x);
+    const int col0 = n0 + c * 32;
+    if (r >= p.M || col0 >= p.N) continue;
+    const bool full_cols = col0 + 32 <= p.N;
+    if constexpr (kOut == kOutBF16) {
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.C) + int64_t(r) * p.ldc + col0;
+      if (full_cols) {
+        uint32_t w[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
+          w[e] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        uint4* o4 = reinterpret_cast<uint4*>(o);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o4[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (col0 + e < p.N) o[e] = __float2bfloat16_rn(x[e]);
+      }
+    } else {
+      float* o = static_cast<float*>(p.C) + int64_t(r) * p.ldc + col0;
+      if (full_cols) {
+        float4* o4 = reinterpret_cast<float4*>(o);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float4 v = make_float4(x[4 * e], x[4 * e + 1], x[4 * e + 2], x[4 * e + 3]);
+          if constexpr (kOut == kOutAddF32) {
+            const float4 u = ld_f4_hint(o4 + e, pol_c);
+            v.x += u.x;
+            v.y += u.y;
+            v.z += u.z;
+            v.w += u.w;
+            st_f4_hint(o4 + e, v, pol_c);
+          } else {
+            o4[e] = v;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (col0 + e < p.N) o[e] = kOut == kOutAddF32 ? o[e] + x[e] : x[e];
+      }
+    }
+  }
+}
+
+template <bool kAMN, bool kBMN, int kOut>
+__global__ void __launch_bounds__(kGmThreads, 1)
+    k_umma_gemm(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);   // 1024-B aligned (SW128)
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kGmStages * kGmABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kGmStages * kGmStageBytes);
+  uint64_t* empty = full + kGmStages;
+  uint64_t* tfull = empty + kGmStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles = p.mblk * p.nblk;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGmStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kGmBM);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pa = l2_policy(p.hint_a), pb = l2_policy(p.hint_b);
+      uint32_t q = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        int mb, nb;
+        gemm_tile_coords(p, tile, mb, nb);
+        const int m0 = mb * kGmBM, n0 = nb * kGmBN;
+        for (int kb = 0; kb < p.kblk; ++kb, ++q) {
+          const int s = q % kGmStages;
+          const int k0 = kb * kGmBK;
+          gm_wait(&empty[s], ((q / kGmStages) & 1u) ^ 1u);
+          mbar_arrive_tx(&full[s], kGmStageBytes);
+          uint8_t* a = sA + s * kGmABytes;
+          uint8_t* b = sB + s * kGmBBytes;
+          if constexpr (kAMN) {
+#pragma unroll
+            for (int j = 0; j < kGmBM / 64; ++j) tma_load_2d_hint(a + j * kGmMNBox, &tmap_a, m0 + 64 * j, k0, &full[s], pa);
+          } else {
+            tma_load_2d_hint(a, &tmap_a, k0, m0, &full[s], pa);
+          }
+          if constexpr (kBMN) {
+#pragma unroll
+            for (int j = 0; j < kGmBN / 64; ++j) tma_load_2d_hint(b + j * kGmMNBox, &tmap_b, n0 + 64 * j, k0, &full[s], pb);
+          } else {
+            tma_load_2d_hint(b, &tmap_b, k0, n0, &full[s], pb);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = gemm_idesc<kAMN, kBMN>();
+      uint32_t q = 0;
+      int i = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+        const int acc = i & 1;
+        gm_wait(&tempty[acc], ((i >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t dt = tmem + uint32_t(acc * kGmBN);
+        for (int kb = 0; kb < p.kblk; ++kb, ++q) {
+          const int s = q % kGmStages;
+          gm_wait(&full[s], (q / kGmStages) & 1u);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * kGmABytes), b0 = smem_u32(sB + s * kGmBBytes);
+#pragma unroll
+          for (int k = 0; k < kGmBK / 16; ++k) {
+            const uint64_t ad = kAMN ? umma_desc_sw128_mn(a0 + k * 2048) : umma_desc_sw128(a0 + k * 32);
+            const uint64_t bd = kBMN ? umma_desc_sw128_mn(b0 + k * 2048) : umma_desc_sw128(b0 + k * 32);
+            tc_mma(dt, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint64_t pol_c = l2_policy(p.hint_c);
+    int i = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+      const int acc = i & 1;
+      int mb, nb;
+      gemm_tile_coords(p, tile, mb, nb);
+      const int m0 = mb * kGmBM, n0 = nb * kGmBN;
+      const int r = m0 + row;
+      gm_wait(&tfull[acc], (i >> 1) & 1u);
+      tc_fence_after();
+      const uint32_t base = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kGmBN);
+      gemm_store_tile<kOut>(p, base, r, n0, pol_c);
+      __syncwarp();
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// CTA-pair variant (tcgen05.mma.cta_group::2): one 256 × 256 tile per cluster of two SMs.
+// CTA `rank` loads its 128 rows of A and its 128 columns of B (half the B traffic of two
+// independent 128 × 256 tiles: per K-step 32 KB per CTA for 4.2 MFLOP instead of 48 KB); the
+// leader issues M = 256 MMAs over both CTAs' shared memory and commits to both CTAs' barriers
+// (multicast); each CTA's epilogue drains its own TMEM rows (the k_lmhead2.cuh protocol).
+constexpr int kG2Stages = 6;
+constexpr int kG2ABytes = 128 * kGmBK * 2;       // 16 KB: this CTA's 128 rows of A
+constexpr int kG2BBytes = 128 * kGmBK * 2;       // 16 KB: this CTA's 128 columns of B
+constexpr int kG2StageBytes = kG2ABytes + kG2BBytes;
+constexpr size_t kG2Smem = size_t(kG2Stages) * kG2StageBytes + 1024 + 256;
+
+template <bool kAMN, bool kBMN>
+__host__ __device__ constexpr uint32_t gemm2_idesc() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kAMN) << 15) | (uint32_t(kBMN) << 16) |
+         (uint32_t(kGmBN >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+}
+
+// bounded wait on a barrier of this CTA with cluster-scope acquire (remote arrivals)
+__device__ __forceinline__ void gm_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    if (ok) return;
+    if ((it & 255u) == 255u) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 20000000000ull) __trap();     // 20 s
+    }
+  }
+}
+
+template <bool kAMN, bool kBMN, int kOut>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
+    k_umma_gemm2(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                 const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kG2Stages * kG2ABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kG2Stages * kG2StageBytes);
+  uint64_t* empty = full + kG2Stages;
+  uint64_t* tfull = empty + kG2Stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t rank = cluster_rank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int tiles = p.mblk * p.nblk;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kG2Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kGmBM);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pa = l2_policy(p.hint_a), pb = l2_policy(p.hint_b);
+      uint32_t q = 0;
+      for (int tile = cluster; tile < tiles; tile += nclusters) {
+        int mb, nb;
+        gemm_tile_coords(p, tile, mb, nb);
+        const int m0 = mb * 2 * kGmBM + int(rank) * kGmBM;
+        const int n0 = nb * kGmBN + int(rank) * (kGmBN / 2);
+        for (int kb = 0; kb < p.kblk; ++kb, ++q) {
+          const int s = q % kG2Stages;
+          const int k0 = kb * kGmBK;
+          gm_wait_cluster(smem_u32(&empty[s]), ((q / kG2Stages) & 1u) ^ 1u);
+          const uint32_t leader_full = mapa_rank(smem_u32(&full[s]), 0);
+          if (rank == 0) arrive_expect_tx_u32(smem_u32(&full[s]), 2 * kG2StageBytes);
+          const uint32_t a = smem_u32(sA + s * kG2ABytes), b = smem_u32(sB + s * kG2BBytes);
+          if constexpr (kAMN) {
+            tma_load_2d_pair_hint(a, &tmap_a, m0, k0, leader_full, pa);
+            tma_load_2d_pair_hint(a + kGmMNBox, &tmap_a, m0 + 64, k0, leader_full, pa);
+          } else {
+            tma_load_2d_pair_hint(a, &tmap_a, k0, m0, leader_full, pa);
+          }
+          if constexpr (kBMN) {
+            tma_load_2d_pair_hint(b, &tmap_b, n0, k0, leader_full, pb);
+            tma_load_2d_pair_hint(b + kGmMNBox, &tmap_b, n0 + 64, k0, leader_full, pb);
+          } else {
+            tma_load_2d_pair_hint(b, &tmap_b, k0, n0, leader_full, pb);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer (leader)
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = gemm2_idesc<kAMN, kBMN>();
+      uint32_t q = 0;
+      int i = 0;
+      for (int tile = cluster; tile < tiles; tile += nclusters, ++i) {
+        const int acc = i & 1;
+        gm_wait_cluster(smem_u32(&tempty[acc]), ((i >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t dt = tmem + uint32_t(acc * kGmBN);
+        for (int kb = 0; kb < p.kblk; ++kb, ++q) {
+          const int s = q % kG2Stages;
+          gm_wait_cluster(smem_u32(&full[s]), (q / kG2Stages) & 1u);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * kG2ABytes), b0 = smem_u32(sB + s * kG2BBytes);
+#pragma unroll
+          for (int k = 0; k < kGmBK / 16; ++k) {
+            const uint64_t ad = kAMN ? umma_desc_sw128_mn(a0 + k * 2048) : umma_desc_sw128(a0 + k * 32);
+            const uint64_t bd = kBMN ? umma_desc_sw128_mn(b0 + k * 2048) : umma_desc_sw128(b0 + k * 32);
+            tc_mma_pair(dt, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit_pair(smem_u32(&empty[s]));     // slot s free in both CTAs
+        }
+        tc_commit_pair(smem_u32(&tfull[acc]));     // accumulator ready in both CTAs
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint64_t pol_c = l2_policy(p.hint_c);
+    const uint32_t leader_tempty0 = mapa_rank(smem_u32(&tempty[0]), 0);
+    const uint32_t leader_tempty1 = mapa_rank(smem_u32(&tempty[1]), 0);
+    int i = 0;
+    for (int tile = cluster; tile < tiles; tile += nclusters, ++i) {
+      const int acc = i & 1;
+      int mb, nb;
+      gemm_tile_coords(p, tile, mb, nb);
+      gm_wait_cluster(smem_u32(&tfull[acc]), (i >> 1) & 1u);
+      tc_fence_after();
+      const uint32_t base = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kGmBN);
+      gemm_store_tile<kOut>(p, base, mb * 2 * kGmBM + int(rank) * kGmBM + row, nb * kGmBN, pol_c);
+      __syncwarp();
+      tc_fence_before();
+      arrive_remote(acc ? leader_tempty1 : leader_tempty0);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();     // both CTAs done with TMEM and with remote barriers
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
+                 : "memory");
+  }
+}
+
+}  // namespace espo

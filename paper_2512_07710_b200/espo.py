@@ -29,6 +29,9 @@ OPT_FWD_IMPL, OPT_BWD_IMPL, OPT_BLOCKS_PER_SM, OPT_LMHEAD_PARTS, OPT_LMHEAD_BWD_
 OPT_LMHEAD_2CTA = 5
 OPT_FACTORED_IMPL = 6
 OPT_PEER_TIMEOUT_MS = 7
+OPT_LMHEAD_BWD_GEMM = 8
+OPT_GEMM_GROUP_M = 9
+OPT_GEMM_HINTS = 10
 REDUCE_LEN = 26          # ESPO_REDUCE_LEN: fp64 terms of espo_loss_reduce_local
 
 STATUS = {

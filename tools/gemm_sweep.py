@@ -1,0 +1,73 @@
+"""A/B sweep of the LM-head backward's GEMM settings (ESPO_OPT_LMHEAD_BWD_GEMM, _GEMM_GROUP_M,
+_GEMM_HINTS): time espo_lmhead_bwd on one 8192-row sub-chunk per setting, interleaved over
+rounds (median), same data. Prints one JSON line. usage: python tools/gemm_sweep.py [d] [n]"""
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_07710_b200.espo import (OPT_GEMM_GROUP_M, OPT_GEMM_HINTS,  # noqa: E402
+                                        OPT_LMHEAD_BWD_GEMM, Espo)
+
+
+def main(d=4096, n=8192, V=151936, rounds=5):
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(0)
+    h = (torch.randn(n, d, device=dev) / d ** 0.5 * 3).to(torch.bfloat16)
+    W = torch.randn(V, d, device=dev).to(torch.bfloat16)
+    tokens = torch.randint(0, V, (n,), device=dev, dtype=torch.int32)
+    G = 8
+    rewards = torch.tensor([1.0, 0.0] * (G // 2), device=dev)
+    gid = torch.zeros(G, dtype=torch.int32, device=dev)
+    so = torch.arange(G + 1, device=dev, dtype=torch.int64) * (n // G)
+    ctx = Espo(V, logits_dtype=torch.bfloat16, device=0)
+    ctx.prepare(rewards, gid, so, n_tokens=n)
+    ctx.lmhead_fwd(h, W, tokens, torch.zeros(n, device=dev))
+    ctx.loss_finalize()
+    old = (ctx.export_token_stats()["lp"] + 0.02 * torch.randn(n, device=dev)).contiguous()
+    ctx.prepare(rewards, gid, so, n_tokens=n)
+    ctx.lmhead_fwd(h, W, tokens, old)
+    ctx.loss_finalize()
+    dh = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
+    dW = torch.zeros((V, d), dtype=torch.float32, device=dev)
+    H = lambda a, b, c: a | (b << 2) | (c << 4)
+    dw_auto = H(1, 2, 1)
+    cfgs = {
+        "cublas": (1, 0, -1),
+        "1cta": (2, 0, -1),
+        "pair_auto": (0, 0, -1),
+        "pair_g4": (0, 4, -1),
+        "pair_g16": (0, 16, -1),
+        "pair_g1": (0, 1, -1),
+        "pair_nohints": (0, 0, 0),
+        "pair_dh_ef": (0, 0, H(1, 1, 0) | (dw_auto << 8)),
+        "pair_dw_noc": (0, 0, (H(1, 2, 0) << 8)),
+        "pair_dw_nolast": (0, 0, (H(1, 0, 1) << 8)),
+    }
+    times = {k: [] for k in cfgs}
+    for _ in range(rounds):
+        for k, (impl, gm, hints) in cfgs.items():
+            ctx.set_option(OPT_LMHEAD_BWD_GEMM, impl)
+            ctx.set_option(OPT_GEMM_GROUP_M, gm)
+            ctx.set_option(OPT_GEMM_HINTS, hints)
+            ctx.lmhead_bwd(h, W, dh, dW)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            ctx.lmhead_bwd(h, W, dh, dW)
+            e.record()
+            torch.cuda.synchronize()
+            times[k].append(s.elapsed_time(e))
+    ctx.get_error()
+    flops = 6.0 * n * V * d
+    out = {k: {"ms": statistics.median(v), "TFLOPs_3gemm": flops / (statistics.median(v) * 1e-3) / 1e12}
+           for k, v in times.items()}
+    out["config"] = {"n": n, "d": d, "V": V, "rounds": rounds}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    a = [int(x) for x in sys.argv[1:]]
+    main(*a)
