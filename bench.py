@@ -71,7 +71,7 @@ def parse():
     p.add_argument("--fwd-impl", type=int, default=0, help="0/2/3/4 = TMA ring variants, 1 = LDG")
     p.add_argument("--bwd-impl", type=int, default=0, help="0/7 = tiled grid, 1 = LDG, 2-6 = TMA rings")
     p.add_argument("--blocks-per-sm", type=int, default=0)
-    p.add_argument("--e2e-steps", type=int, default=1)
+    p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--e2e-host-rows", type=int, default=8192,
                    help="host ring rows (≥ the longest rollout; chunks pack whole rollouts)")
     p.add_argument("--no-e2e", action="store_true")

@@ -429,6 +429,9 @@ espo_status espo_lmhead_fwd(espo_ctx_t ctx, const void* hidden, int64_t ldh, con
  *           cores (same pipeline and K order as the forward, so the logits are bitwise the
  *           forward's) and rounded to bf16 into a context-owned scratch of
  *           ESPO_OPT_LMHEAD_BWD_ROWS × round_up(vocab, 256) bf16 (allocated on first use);
+ *           rows whose coefficient is 0 (clipped, masked, eliminated: dz_t = 0) are left out —
+ *           the rows with gradient are gathered (stable order) and only they are recomputed
+ *           and contracted (ESPO_OPT_LMHEAD_COMPACT; scratch 4 B/row + the gathered rows);
  *   dhidden[r, :] = Σ_v dz[r, v]·weight[v, :]          (overwritten; f32 or bf16 per dh_dtype)
  *   dweight[v, :] += Σ_r dz[r, v]·hidden[r, :]          (f32, ACCUMULATED: zero it once)
  * The two contractions are bf16 × bf16 → fp32 GEMMs on the library's own tcgen05 kernel
@@ -502,9 +505,11 @@ typedef enum {
                                   (A/B measurement only), 2 = the tcgen05 GEMM, one CTA per
                                   128 × 256 tile */
   ESPO_OPT_GEMM_GROUP_M = 9,   /* dh GEMM tile order: M-blocks per raster group (0 = auto, 8) */
-  ESPO_OPT_GEMM_HINTS = 10     /* L2 policies of the backward GEMMs for A/B measurement: bits 0-7
+  ESPO_OPT_GEMM_HINTS = 10,    /* L2 policies of the backward GEMMs for A/B measurement: bits 0-7
                                   dh, 8-15 dW, each A | B << 2 | C << 4 with 0 = normal,
                                   1 = evict_first, 2 = evict_last; −1 = defaults */
+  ESPO_OPT_LMHEAD_COMPACT = 11  /* espo_lmhead_bwd: 1 (default) = recompute and contract only the
+                                  rows with gradient (c_t ≠ 0; needs d % 8 == 0), 0 = all rows */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

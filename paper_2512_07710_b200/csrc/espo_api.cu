@@ -19,6 +19,7 @@
 #include "k_reward.cuh"
 #include "k_tpx.cuh"
 #include "k_gemm.cuh"
+#include "k_compact.cuh"
 #include "k_fwdgrad.cuh"
 #include "workspace.cuh"
 
@@ -145,6 +146,9 @@ struct espo_ctx_s {
   int lmh_2cta = 0;              // 1: CTA-pair (cta_group::2) LM-head kernels
   int lmh_bwd_gemm = 0;          // dh / dW: 0 = tcgen05 CTA-pair GEMM, 1 = cuBLAS (A/B), 2 = one CTA
   int gemm_group_m = 0;          // dh GEMM tile order: M-blocks per group (0 = auto)
+  int lmh_compact = 1;           // LM-head backward on the rows with gradient only (k_compact.cuh)
+  void* lmh_cmp = nullptr;       // row list, counts, gathered h rows and records, grown on demand
+  size_t lmh_cmp_cap = 0;
   int gemm_hints_dh = -1, gemm_hints_dw = -1;   // L2 policies of the two GEMMs (−1 = auto)
   void* lmh_dz = nullptr;        // [lmh_bwd_rows][round_up(V, 256)] bf16, grown on demand
   size_t lmh_dz_cap = 0;
@@ -417,6 +421,7 @@ espo_status espo_destroy(espo_ctx_t c) {
     if (c->lmh_partial) cudaFree(c->lmh_partial);
     if (c->rs_scratch) cudaFree(c->rs_scratch);
     if (c->lmh_dz) cudaFree(c->lmh_dz);
+    if (c->lmh_cmp) cudaFree(c->lmh_cmp);
     if (c->blas) g_blas.destroy(c->blas);
     if (c->blas_ws) cudaFree(c->blas_ws);
     for (void* q : c->x_opened) cudaIpcCloseMemHandle(q);
@@ -465,6 +470,10 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       if (value < -1 || value > 0xFFFF) return ESPO_ERR_INVALID_ARGUMENT;
       c->gemm_hints_dh = value < 0 ? -1 : int(value & 0xFF);
       c->gemm_hints_dw = value < 0 ? -1 : int((value >> 8) & 0xFF);
+      return ESPO_OK;
+    case ESPO_OPT_LMHEAD_COMPACT:
+      if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
+      c->lmh_compact = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_GEMM_GROUP_M:
       if (value < 0 || value > 1024) return ESPO_ERR_INVALID_ARGUMENT;
@@ -857,12 +866,22 @@ int lmhead_parts(const espo_ctx_s* c, int mblocks, int ntiles, int d) {
 // C[M, N] (+)= A·B on the tcgen05 GEMM (k_gemm.cuh); maps built by the caller for the
 // operands' majorness (K-major A: box {64 K, 128 M}; MN-major: boxes {64 MN, 64 K}).
 // pair: CTA-pair kernel (256 × 256 tiles per cluster of 2), else one CTA per 128 × 256 tile.
+struct GemmDyn {          // device-side row count of compacted operands (k_compact.cuh)
+  const int* count = nullptr;
+  int base = 0, which = 0;   // which: 1 = M, 2 = K
+  const int* row_map = nullptr;
+};
+
 template <bool kAMN, bool kBMN, int kOut>
 espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensorMap& mb, int M,
                              int N, int64_t K, void* C, int64_t ldc, bool pair, int group_m,
-                             int hints, cudaStream_t s) {
+                             int hints, cudaStream_t s, const GemmDyn& dyn = GemmDyn()) {
   static unsigned long long attr = 0, attr2 = 0;
   GemmParams p;
+  p.dyn_count = dyn.count;
+  p.dyn_base = dyn.base;
+  p.dyn_which = dyn.which;
+  p.row_map = dyn.row_map;
   p.M = M;
   p.N = N;
   p.K = int(K);
@@ -934,7 +953,7 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   static unsigned long long attr_mask = 0, attr_mask2 = 0;
   ESPO_CUDA(ensure_smem_attr(k_lmhead_fwd, int(kLmSmem), attr_mask));
   ESPO_CUDA(ensure_smem_attr(k_lmhead2_fwd, int(kL2Smem), attr_mask2));
-  LmParams lp;
+  LmParams lp{};
   lp.n_rows = int(n_rows);
   lp.row_begin = row_begin;
   lp.d = d;
@@ -1016,12 +1035,57 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
     return ESPO_ERR_CUDA;
   const float one = 1.f, zero = 0.f;
   const char* hb = static_cast<const char*>(hidden);
+  // rows with gradient only (k_compact.cuh): default for the tcgen05 GEMMs when d % 8 == 0
+  const bool compact = !use_blas && c->lmh_compact && d % 8 == 0;
+  int* list = nullptr;
+  int* total = nullptr;
+  __nv_bfloat16* hc = nullptr;
+  BwdRec* rec_c = nullptr;
+  const int64_t ldc = round_up(size_t(d), 8);
+  if (compact) {
+    const int nb = int((n_rows + kCmpBlock - 1) / kCmpBlock);
+    const size_t need_c = round_up(size_t(n_rows) * 4, 256) + round_up(size_t(nb + 1) * 4, 256) +
+                          round_up(size_t(sub) * ldc * 2, 256) + size_t(sub) * sizeof(BwdRec);
+    if (need_c > c->lmh_cmp_cap) {
+      if (c->lmh_cmp) cudaFree(c->lmh_cmp);
+      c->lmh_cmp = nullptr;
+      c->lmh_cmp_cap = 0;
+      ESPO_CUDA(cudaMalloc(&c->lmh_cmp, need_c));
+      c->lmh_cmp_cap = need_c;
+    }
+    uint8_t* b = static_cast<uint8_t*>(c->lmh_cmp);
+    list = reinterpret_cast<int*>(b);
+    b += round_up(size_t(n_rows) * 4, 256);
+    total = reinterpret_cast<int*>(b);              // [0] = total, [1 ..] = block counts
+    b += round_up(size_t(nb + 1) * 4, 256);
+    hc = reinterpret_cast<__nv_bfloat16*>(b);
+    b += round_up(size_t(sub) * ldc * 2, 256);
+    rec_c = reinterpret_cast<BwdRec*>(b);
+    k_cmp_count<<<nb, kCmpBlock, 0, s>>>(rec, int(n_rows), total + 1);
+    ESPO_LAUNCHED(c);
+    k_cmp_scatter<<<nb, kCmpBlock, 0, s>>>(rec, int(n_rows), total + 1, nb, list, total);
+    ESPO_LAUNCHED(c);
+    if (dhidden) {   // rows without gradient: dh = 0 (the GEMM writes only the listed rows)
+      k_zero_rows<<<int(n_rows), 256, 0, s>>>(rec, int(n_rows), dhidden,
+                                              lddh * int64_t(dsize(dh_dtype)), d * int(dsize(dh_dtype)));
+      ESPO_LAUNCHED(c);
+    }
+  }
   for (int64_t r0 = 0; r0 < n_rows; r0 += sub) {
+    // compact: r0 indexes the list of rows with gradient (sub-chunks past the count exit at
+    // once on the device); otherwise it is the chunk row
     const int n = int(std::min<int64_t>(sub, n_rows - r0));
     const int mblocks = (n + kLmBM - 1) / kLmBM;
     const int parts = lmhead_parts(c, mblocks, ntiles, d);
+    const char* hsrc = compact ? reinterpret_cast<const char*>(hc) : hb + r0 * ldh * 2;
+    const int64_t hld = compact ? ldc : ldh;
+    if (compact) {
+      k_cmp_gather<<<n, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(hidden), ldh, d, rec, list,
+                                     total, int(r0), n, hc, ldc, rec_c);
+      ESPO_LAUNCHED(c);
+    }
     CUtensorMap mh;
-    if (!make_map_bf16(&mh, hb + r0 * ldh * 2, uint64_t(n), uint64_t(d), uint64_t(ldh) * 2, kLmBM))
+    if (!make_map_bf16(&mh, hsrc, uint64_t(n), uint64_t(d), uint64_t(hld) * 2, kLmBM))
       return ESPO_ERR_CUDA;
     LmParams lp{};
     lp.n_rows = n;
@@ -1031,10 +1095,14 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
     lp.ntiles = ntiles;
     lp.parts = parts;
     lp.lam_log2e = c->cfg.logit_scale * kLog2e;
-    lp.rec = rec + r0;
+    lp.rec = compact ? rec_c : rec + r0;
     lp.dz = static_cast<__nv_bfloat16*>(c->lmh_dz);
     lp.ldz = ldz;
     lp.ws = c->ws;
+    if (compact) {
+      lp.dyn_count = total;
+      lp.dyn_base = int(r0);
+    }
     if (c->lmh_2cta)
       k_lmhead2_dz<<<dim3(2 * parts, (mblocks + 1) / 2), kLmThreads, kL2Smem, s>>>(mh, mw, lp);
     else
@@ -1045,7 +1113,7 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       CUtensorMap mdz_k, mdz_mn, mh_mn;
       if (!make_map_bf16(&mdz_k, c->lmh_dz, uint64_t(n), uint64_t(ldz), uint64_t(ldz) * 2, kGmBM) ||
           !make_map_bf16(&mdz_mn, c->lmh_dz, uint64_t(n), uint64_t(ldz), uint64_t(ldz) * 2, 64) ||
-          !make_map_bf16(&mh_mn, hb + r0 * ldh * 2, uint64_t(n), uint64_t(d), uint64_t(ldh) * 2, 64))
+          !make_map_bf16(&mh_mn, hsrc, uint64_t(n), uint64_t(d), uint64_t(hld) * 2, 64))
         return ESPO_ERR_CUDA;
       espo_status st;
       const bool pair = c->lmh_bwd_gemm == 0;
@@ -1058,15 +1126,23 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       // every tile re-reads h (64 MB at n = 8192, d = 4096), which should stay in L2
       const int hint_dh = c->gemm_hints_dh >= 0 ? c->gemm_hints_dh : 0;
       const int hint_dw = c->gemm_hints_dw >= 0 ? c->gemm_hints_dw : (1 | (2 << 2) | (1 << 4));
+      GemmDyn dyn_m, dyn_k;
+      if (compact) {
+        dyn_m.count = dyn_k.count = total;
+        dyn_m.base = dyn_k.base = int(r0);
+        dyn_m.which = 1;
+        dyn_k.which = 2;
+        dyn_m.row_map = list + r0;
+      }
       if (dhidden) {   // dh[n, d] = dz[n, V] · W[V, d]: A = dz K-major, B = W MN-major
-        char* dh = static_cast<char*>(dhidden) + r0 * lddh * int64_t(dsize(dh_dtype));
+        char* dh = static_cast<char*>(dhidden) + (compact ? 0 : r0 * lddh * int64_t(dsize(dh_dtype)));
         st = dh_dtype == ESPO_BF16
-                 ? launch_umma_gemm<false, true, kOutBF16>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, pair, g_dh, hint_dh, s)
-                 : launch_umma_gemm<false, true, kOutF32>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, pair, g_dh, hint_dh, s);
+                 ? launch_umma_gemm<false, true, kOutBF16>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, pair, g_dh, hint_dh, s, dyn_m)
+                 : launch_umma_gemm<false, true, kOutF32>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, pair, g_dh, hint_dh, s, dyn_m);
         if (st != ESPO_OK) return st;
       }
       if (dweight) {   // dW[V, d] += dzᵀ[V, n] · h[n, d]: A = dz MN-major, B = h MN-major
-        st = launch_umma_gemm<true, true, kOutAddF32>(c, mdz_mn, mh_mn, V, d, n, dweight, lddw, pair, 1, hint_dw, s);
+        st = launch_umma_gemm<true, true, kOutAddF32>(c, mdz_mn, mh_mn, V, d, n, dweight, lddw, pair, 1, hint_dw, s, dyn_k);
         if (st != ESPO_OK) return st;
       }
       continue;

@@ -48,7 +48,29 @@ struct GemmParams {
                                 // 1 evict_first (streamed), 2 evict_last (reused)
   void* C;
   int64_t ldc;        // elements
+  // compacted operands (k_compact.cuh): the true M (dyn_which = 1) or K (= 2) is
+  // clamp(*dyn_count − dyn_base, 0, M or K) rows, read on the device; row_map (nullable)
+  // sends output row r to C row row_map[r]
+  const int* dyn_count;
+  int dyn_base, dyn_which;
+  const int* row_map;
 };
+
+// the launch's sizes with a device-side row count applied (uniform in every thread)
+__device__ __forceinline__ GemmParams gemm_effective(const GemmParams& p, int bm) {
+  GemmParams q = p;
+  if (p.dyn_count) {
+    const int n = max(0, *p.dyn_count - p.dyn_base);
+    if (p.dyn_which == 1) {
+      q.M = min(p.M, n);
+      q.mblk = (q.M + bm - 1) / bm;
+    } else {
+      q.K = min(p.K, n);
+      q.kblk = (q.K + kGmBK - 1) / kGmBK;
+    }
+  }
+  return q;
+}
 
 // tile index → (M block, N block): groups of group_m M-blocks; inside a group M varies
 // fastest, so the tiles resident together cover ≈ group_m × (resident / group_m) blocks
@@ -149,9 +171,10 @@ __device__ __forceinline__ void gemm_store_tile(const GemmParams& p, uint32_t ba
     tmem_ld32(base + uint32_t(c * 32), x);
     const int col0 = n0 + c * 32;
     if (r >= p.M || col0 >= p.N) continue;
+    const int orow = p.row_map ? p.row_map[r] : r;
     const bool full_cols = col0 + 32 <= p.N;
     if constexpr (kOut == kOutBF16) {
-      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.C) + int64_t(r) * p.ldc + col0;
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.C) + int64_t(orow) * p.ldc + col0;
       if (full_cols) {
         uint32_t w[16];
 #pragma unroll
@@ -168,7 +191,7 @@ __device__ __forceinline__ void gemm_store_tile(const GemmParams& p, uint32_t ba
           if (col0 + e < p.N) o[e] = __float2bfloat16_rn(x[e]);
       }
     } else {
-      float* o = static_cast<float*>(p.C) + int64_t(r) * p.ldc + col0;
+      float* o = static_cast<float*>(p.C) + int64_t(orow) * p.ldc + col0;
       if (full_cols) {
         float4* o4 = reinterpret_cast<float4*>(o);
 #pragma unroll
@@ -197,7 +220,9 @@ __device__ __forceinline__ void gemm_store_tile(const GemmParams& p, uint32_t ba
 template <bool kAMN, bool kBMN, int kOut>
 __global__ void __launch_bounds__(kGmThreads, 1)
     k_umma_gemm(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                const GemmParams p) {
+                const GemmParams p0) {
+  const GemmParams p = gemm_effective(p0, kGmBM);
+  if (p.mblk * p.nblk == 0 || p.kblk == 0) return;   // nothing to add (uniform in the grid)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);   // 1024-B aligned (SW128)
@@ -361,7 +386,9 @@ __device__ __forceinline__ void gm_wait_cluster(uint32_t bar, uint32_t parity) {
 template <bool kAMN, bool kBMN, int kOut>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
     k_umma_gemm2(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                 const GemmParams p) {
+                 const GemmParams p0) {
+  const GemmParams p = gemm_effective(p0, 2 * kGmBM);
+  if (p.mblk * p.nblk == 0 || p.kblk == 0) return;   // nothing to add (uniform in the grid)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);

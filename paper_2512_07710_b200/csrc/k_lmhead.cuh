@@ -46,7 +46,17 @@ struct LmParams {
   __nv_bfloat16* dz;     // [n_rows][ldz] bf16 gradient tile output (k_lmhead_dz)
   int64_t ldz;           // ≥ ntiles·256 elements
   Workspace ws;
+  // k_lmhead_dz on compacted rows: rows ≥ round_up(clamp(*dyn_count − dyn_base, 0, n_rows),
+  // 256) are skipped (neither computed nor written)
+  const int* dyn_count;
+  int dyn_base;
 };
+
+__device__ __forceinline__ int lm_rows(const LmParams& p) {
+  if (!p.dyn_count) return p.n_rows;
+  const int n = max(0, *p.dyn_count - p.dyn_base);
+  return min(p.n_rows, (n + 255) / 256 * 256);
+}
 
 // --------------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
@@ -235,12 +245,14 @@ __device__ __forceinline__ void lmhead_body(const CUtensorMap& tmap_h, const CUt
   const int t_end = int((int64_t(p.ntiles) * (part + 1)) / p.parts);
   const int nk = (p.d + kLmBK - 1) / kLmBK;
 
+  const int n_rows = lm_rows(p);
+  if (m0 >= n_rows) return;                   // beyond the compacted rows: nothing to do
   // skip blocks without a valid row (eliminated groups, masked tails)
   if (threadIdx.x == 0) *s_any = 0;
   __syncthreads();
   if (threadIdx.x < kLmBM) {
     const int r = m0 + threadIdx.x;
-    if (r < p.n_rows) {
+    if (r < n_rows) {
       if constexpr (kDz) {
         if (p.rec[r].ng != 0.f) *s_any = 1;
       } else {
@@ -253,7 +265,7 @@ __device__ __forceinline__ void lmhead_body(const CUtensorMap& tmap_h, const CUt
   if (*s_any == 0) {
     if constexpr (kDz) {   // no gradient in this block: zero its rows of this part's columns
       const int c0 = t_begin * kLmBN / 8, c1 = t_end * kLmBN / 8;   // uint4 columns
-      const int nr = min(kLmBM, p.n_rows - m0);
+      const int nr = min(kLmBM, n_rows - m0);
       for (int rr = 0; rr < nr; ++rr) {
         uint4* o = reinterpret_cast<uint4*>(p.dz + int64_t(m0 + rr) * p.ldz);
         for (int c = c0 + int(threadIdx.x); c < c1; c += kLmThreads) o[c] = make_uint4(0, 0, 0, 0);
@@ -330,7 +342,7 @@ __device__ __forceinline__ void lmhead_body(const CUtensorMap& tmap_h, const CUt
       BwdRec rc;
       rc.ng = 0.f;
       rc.y = -1;
-      if (r < p.n_rows) rc = p.rec[r];
+      if (r < n_rows) rc = p.rec[r];
       int i = 0;
       for (int tile = t_begin; tile < t_end; ++tile, ++i) {
         const int acc = i & 1;
@@ -343,14 +355,14 @@ __device__ __forceinline__ void lmhead_body(const CUtensorMap& tmap_h, const CUt
           __syncwarp();
           tmem_ld32(base + uint32_t(c * 32), x);
           const int col0 = tile * kLmBN + c * 32;
-          if (r < p.n_rows) lm_store_dz(x, rc, col0, p.V, p.lam_log2e, p.dz + int64_t(r) * p.ldz + col0);
+          if (r < n_rows) lm_store_dz(x, rc, col0, p.V, p.lam_log2e, p.dz + int64_t(r) * p.ldz + col0);
         }
         __syncwarp();
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
       }
     } else {
-    const bool valid = r < p.n_rows && p.ws.flag[p.row_begin + r];
+    const bool valid = r < n_rows && p.ws.flag[p.row_begin + r];
     const int y = valid ? p.tokens[r] : -1;
     const float lamL = p.lam_log2e;
     float R = -INFINITY, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f, uy = __int_as_float(0x7fc00000);

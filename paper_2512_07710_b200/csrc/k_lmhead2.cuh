@@ -114,12 +114,15 @@ __device__ __forceinline__ void lmhead2_body(const CUtensorMap& tmap_h, const CU
   const int t_end = int((int64_t(p.ntiles) * (part + 1)) / p.parts);
   const int nk = (p.d + kLmBK - 1) / kLmBK;
 
+  // rows beyond the compacted count (lm_rows) count as absent; a pair whose rows are all
+  // absent still runs the barrier handshake below and leaves together
+  const int n_rows = lm_rows(p);
   // does this CTA have a row to work on? the pair proceeds unless both are empty
   if (threadIdx.x == 0) *s_any = 0;
   __syncthreads();
   if (threadIdx.x < kLmBM) {
     const int r = m0 + threadIdx.x;
-    if (r < p.n_rows) {
+    if (r < n_rows) {
       if constexpr (kDz) {
         if (p.rec[r].ng != 0.f) *s_any = 1;
       } else {
@@ -149,7 +152,7 @@ __device__ __forceinline__ void lmhead2_body(const CUtensorMap& tmap_h, const CU
     if constexpr (kDz) {   // no gradient in this pair: zero this CTA's rows of the part
       if (t_begin < t_end) {
         const int c0 = t_begin * kLmBN / 8, c1 = t_end * kLmBN / 8;
-        const int nr = max(0, min(kLmBM, p.n_rows - m0));
+        const int nr = max(0, min(kLmBM, n_rows - m0));
         for (int rr = 0; rr < nr; ++rr) {
           uint4* o = reinterpret_cast<uint4*>(p.dz + int64_t(m0 + rr) * p.ldz);
           for (int c = c0 + int(threadIdx.x); c < c1; c += kLmThreads) o[c] = make_uint4(0, 0, 0, 0);
@@ -221,7 +224,7 @@ __device__ __forceinline__ void lmhead2_body(const CUtensorMap& tmap_h, const CU
       BwdRec rc;
       rc.ng = 0.f;
       rc.y = -1;
-      if (r < p.n_rows) rc = p.rec[r];
+      if (r < n_rows) rc = p.rec[r];
       int i = 0;
       for (int tile = t_begin; tile < t_end; ++tile, ++i) {
         const int acc = i & 1;
@@ -234,14 +237,14 @@ __device__ __forceinline__ void lmhead2_body(const CUtensorMap& tmap_h, const CU
           __syncwarp();
           tmem_ld32(base + uint32_t(c * 32), x);
           const int col0 = tile * kLmBN + c * 32;
-          if (r < p.n_rows) lm_store_dz(x, rc, col0, p.V, p.lam_log2e, p.dz + int64_t(r) * p.ldz + col0);
+          if (r < n_rows) lm_store_dz(x, rc, col0, p.V, p.lam_log2e, p.dz + int64_t(r) * p.ldz + col0);
         }
         __syncwarp();
         tc_fence_before();
         arrive_remote(acc ? leader_tempty1 : leader_tempty0);
       }
     } else {
-      const bool valid = r < p.n_rows && p.ws.flag[p.row_begin + r];
+      const bool valid = r < n_rows && p.ws.flag[p.row_begin + r];
       const int y = valid ? p.tokens[r] : -1;
       const float lamL = p.lam_log2e;
       float R = -INFINITY, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f, uy = __int_as_float(0x7fc00000);

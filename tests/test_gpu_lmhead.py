@@ -250,7 +250,8 @@ def test_lmhead_bwd_native_gemm_equals_cublas(shape, native):
     the same bf16 products in fp32, only the summation order differs — within
     K·2^-24·Σ|terms| elementwise. Covers N tails (d = 1000 is not a multiple of 256), row
     tails, several sub-chunks and dW accumulation across them."""
-    from paper_2512_07710_b200.espo import OPT_LMHEAD_BWD_GEMM, OPT_LMHEAD_BWD_ROWS
+    from paper_2512_07710_b200.espo import (OPT_LMHEAD_BWD_GEMM, OPT_LMHEAD_BWD_ROWS,
+                                            OPT_LMHEAD_COMPACT)
     dev = require_cuda()
     ng, G, L, V, d = shape
     case = make_case(13, ng, G, L, V, d, zv_group=0)
@@ -259,6 +260,7 @@ def test_lmhead_bwd_native_gemm_equals_cublas(shape, native):
     for impl in (native, 1):
         ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
         ctx.set_option(OPT_LMHEAD_BWD_GEMM, impl)
+        ctx.set_option(OPT_LMHEAD_COMPACT, 0)     # same sub-chunks on both sides (cuBLAS: all rows)
         ctx.set_option(OPT_LMHEAD_BWD_ROWS, 256)
         tok = to_dev(case["tokens"], torch.int32, dev)
         ctx.prepare(to_dev(case["rewards"], torch.float32, dev),
@@ -288,3 +290,52 @@ def test_lmhead_bwd_native_gemm_equals_cublas(shape, native):
     assert np.all(np.abs(w0 - w1) <= lim_dW)
     assert np.linalg.norm(h0 - h1) <= 1e-4 * np.linalg.norm(h1)
     assert np.linalg.norm(w0 - w1 - 0) <= 1e-4 * np.linalg.norm(w1 - 0.25)
+
+
+@pytest.mark.parametrize("gemm,sub", [(0, 0), (2, 128)], ids=["pair", "1cta_sub128"])
+def test_lmhead_bwd_compaction_equals_all_rows(gemm, sub):
+    """ESPO_OPT_LMHEAD_COMPACT: the backward over the gathered rows with gradient only equals
+    the backward over all rows — dh bitwise (same per-row dot products in the same K order;
+    rows without gradient exactly 0), dW within the fp32 accumulation-order bound (the same
+    non-zero products summed in different K=16 groups)."""
+    from paper_2512_07710_b200.espo import (OPT_LMHEAD_BWD_GEMM, OPT_LMHEAD_BWD_ROWS,
+                                            OPT_LMHEAD_COMPACT)
+    dev = require_cuda()
+    V, d = 5003, 256
+    case = make_case(21, 4, 4, 45, V, d, zv_group=1)      # ZV group + masked tail
+    T = case["T"]
+    case["old"] = case["old"] + np.where(np.arange(T) % 3 == 0, 0.5, 0.0).astype(np.float32)
+    outs = []
+    for compact in (1, 0):
+        ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
+        ctx.set_option(OPT_LMHEAD_BWD_GEMM, gemm)
+        ctx.set_option(OPT_LMHEAD_COMPACT, compact)
+        if sub:
+            ctx.set_option(OPT_LMHEAD_BWD_ROWS, sub)
+        tok = to_dev(case["tokens"], torch.int32, dev)
+        ctx.prepare(to_dev(case["rewards"], torch.float32, dev),
+                    to_dev(case["group_ids"], torch.int32, dev), to_dev(case["so"], torch.int64, dev),
+                    n_tokens=T)
+        h = to_dev(case["h"], torch.bfloat16, dev)
+        W = to_dev(case["W"], torch.bfloat16, dev)
+        ctx.lmhead_fwd(h, W, tok, to_dev(case["old"], torch.float32, dev),
+                       to_dev(case["mask"], torch.uint8, dev))
+        _, st = ctx.loss_finalize()
+        dW = torch.zeros((V, d), dtype=torch.float32, device=dev)
+        dh = torch.full((T, d), float("nan"), dtype=torch.float32, device=dev)
+        half = T // 2 + 3
+        ctx.lmhead_bwd(h[:half], W, dh[:half], dW, row_begin=0)
+        ctx.lmhead_bwd(h[half:], W, dh[half:], dW, row_begin=half)
+        ctx.get_error()
+        g = ctx.export_token_stats()
+        outs.append((dh.cpu().numpy(), dW.cpu().numpy().astype(np.float64),
+                     (g["coef"] != 0).cpu().numpy(), stats_to_dict(st)))
+        ctx.close()
+    (h1, w1, nz, st), (h0, w0, _, _) = outs
+    assert 0 < nz.sum() < T and st["n_clipped_tokens"] > 0          # something to skip
+    assert np.array_equal(h1, h0)                                   # bitwise, zeros included
+    assert not np.any(h1[~nz])
+    ha = np.abs(case["h"].astype(np.float64))
+    lim = T * 2.0 ** -23 * (np.abs(w0).max() + 1e-30) + 2.0 ** -22 * np.abs(w0)
+    assert np.all(np.abs(w1 - w0) <= lim + T * 2.0 ** -24 * ha.max())
+    assert np.linalg.norm(w1 - w0) <= 1e-5 * np.linalg.norm(w0)
