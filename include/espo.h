@@ -500,16 +500,21 @@ typedef enum {
                                   device wall time (default 120000); a timeout sets the sticky
                                   ESPO_ERR_PEER_TIMEOUT and invalidates the step (the chunk's
                                   row statistics are not written) */
-  ESPO_OPT_LMHEAD_BWD_GEMM = 8,/* espo_lmhead_bwd's dh / dW contractions: 0 = the library's
-                                  tcgen05 GEMM on CTA pairs (256 × 256 tiles, default), 1 = cuBLAS
-                                  (A/B measurement only), 2 = the tcgen05 GEMM, one CTA per
-                                  128 × 256 tile */
-  ESPO_OPT_GEMM_GROUP_M = 9,   /* dh GEMM tile order: M-blocks per raster group (0 = auto, 8) */
+  ESPO_OPT_LMHEAD_BWD_GEMM = 8,/* espo_lmhead_bwd's dh / dW contractions on the library's
+                                  tcgen05 GEMM: 0 = CTA pairs, 256 × 512 tiles for dh (long K) and
+                                  256 × 256 for dW (default); 2 = one CTA per 128 × 256 tile;
+                                  3 = pairs 256 × 256 for both; 4 = pairs 256 × 512 for both;
+                                  1 = cuBLAS (A/B measurement only) */
+  ESPO_OPT_GEMM_GROUP_M = 9,   /* backward GEMM tile order: bits 0-15 = dh M-blocks per raster
+                                  group (0 = auto, 8); bits 16-31 = dW N-blocks per group (0 = all
+                                  of d, N fastest) */
   ESPO_OPT_GEMM_HINTS = 10,    /* L2 policies of the backward GEMMs for A/B measurement: bits 0-7
                                   dh, 8-15 dW, each A | B << 2 | C << 4 with 0 = normal,
                                   1 = evict_first, 2 = evict_last; −1 = defaults */
-  ESPO_OPT_LMHEAD_COMPACT = 11  /* espo_lmhead_bwd: 1 (default) = recompute and contract only the
+  ESPO_OPT_LMHEAD_COMPACT = 11, /* espo_lmhead_bwd: 1 (default) = recompute and contract only the
                                   rows with gradient (c_t ≠ 0; needs d % 8 == 0), 0 = all rows */
+  ESPO_OPT_GEMM_SYNC = 12      /* CTA-pair GEMM soft lockstep: bits 0-15 = chunk of K-steps
+                                  (0 = off), bits 16+ = slack in chunks (0 = 2) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

@@ -146,7 +146,11 @@ struct espo_ctx_s {
   int lmh_2cta = 0;              // 1: CTA-pair (cta_group::2) LM-head kernels
   int lmh_bwd_gemm = 0;          // dh / dW: 0 = tcgen05 CTA-pair GEMM, 1 = cuBLAS (A/B), 2 = one CTA
   int gemm_group_m = 0;          // dh GEMM tile order: M-blocks per group (0 = auto)
+  int gemm_group_n_dw = 0;       // dW GEMM tile order: N-blocks per group (0 = all)
   int lmh_compact = 1;           // LM-head backward on the rows with gradient only (k_compact.cuh)
+  int gemm_sync_chunk = 0, gemm_sync_slack = 2;  // GEMM soft lockstep (0 = off), k_gemm.cuh
+  void* gemm_sync = nullptr;     // per-wave progress counters
+  size_t gemm_sync_cap = 0;
   void* lmh_cmp = nullptr;       // row list, counts, gathered h rows and records, grown on demand
   size_t lmh_cmp_cap = 0;
   int gemm_hints_dh = -1, gemm_hints_dw = -1;   // L2 policies of the two GEMMs (−1 = auto)
@@ -422,6 +426,7 @@ espo_status espo_destroy(espo_ctx_t c) {
     if (c->rs_scratch) cudaFree(c->rs_scratch);
     if (c->lmh_dz) cudaFree(c->lmh_dz);
     if (c->lmh_cmp) cudaFree(c->lmh_cmp);
+    if (c->gemm_sync) cudaFree(c->gemm_sync);
     if (c->blas) g_blas.destroy(c->blas);
     if (c->blas_ws) cudaFree(c->blas_ws);
     for (void* q : c->x_opened) cudaIpcCloseMemHandle(q);
@@ -463,7 +468,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->factored_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_BWD_GEMM:
-      if (value < 0 || value > 2) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 4) return ESPO_ERR_INVALID_ARGUMENT;
       c->lmh_bwd_gemm = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_GEMM_HINTS:     // low 8 bits: dh, next 8 bits: dW (each A | B<<2 | C<<4); −1 auto
@@ -471,13 +476,19 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->gemm_hints_dh = value < 0 ? -1 : int(value & 0xFF);
       c->gemm_hints_dw = value < 0 ? -1 : int((value >> 8) & 0xFF);
       return ESPO_OK;
+    case ESPO_OPT_GEMM_SYNC:      // chunk (K-steps) | slack << 16; 0 = off
+      if (value < 0 || (value & 0xFFFF) > 4096 || (value >> 16) > 64) return ESPO_ERR_INVALID_ARGUMENT;
+      c->gemm_sync_chunk = int(value & 0xFFFF);
+      c->gemm_sync_slack = (value >> 16) ? int(value >> 16) : 2;
+      return ESPO_OK;
     case ESPO_OPT_LMHEAD_COMPACT:
       if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
       c->lmh_compact = static_cast<int>(value);
       return ESPO_OK;
-    case ESPO_OPT_GEMM_GROUP_M:
-      if (value < 0 || value > 1024) return ESPO_ERR_INVALID_ARGUMENT;
-      c->gemm_group_m = static_cast<int>(value);
+    case ESPO_OPT_GEMM_GROUP_M:   // bits 0-15: dh M-groups; bits 16-31: dW N-groups (0 = auto)
+      if (value < 0 || (value & 0xFFFF) > 1024 || (value >> 16) > 1024) return ESPO_ERR_INVALID_ARGUMENT;
+      c->gemm_group_m = static_cast<int>(value & 0xFFFF);
+      c->gemm_group_n_dw = static_cast<int>(value >> 16);
       return ESPO_OK;
     case ESPO_OPT_PEER_TIMEOUT_MS:
       if (value < 1 || value > int64_t(24) * 3600 * 1000) return ESPO_ERR_INVALID_ARGUMENT;
@@ -874,9 +885,12 @@ struct GemmDyn {          // device-side row count of compacted operands (k_comp
 
 template <bool kAMN, bool kBMN, int kOut>
 espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensorMap& mb, int M,
-                             int N, int64_t K, void* C, int64_t ldc, bool pair, int group_m,
+                             int N, int64_t K, void* C, int64_t ldc, int kind, int group_m,
                              int hints, cudaStream_t s, const GemmDyn& dyn = GemmDyn()) {
-  static unsigned long long attr = 0, attr2 = 0;
+  // kind: 0 = one CTA per 128 × 256 tile, 1 = CTA pair 256 × 256, 2 = CTA pair 256 × 512
+  static unsigned long long attr = 0, attr2 = 0, attr3 = 0;
+  const bool pair = kind != 0;
+  const int tn = kind == 2 ? 512 : kGmBN;
   GemmParams p;
   p.dyn_count = dyn.count;
   p.dyn_base = dyn.base;
@@ -887,9 +901,10 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
   p.K = int(K);
   const int bm = pair ? 2 * kGmBM : kGmBM;
   p.mblk = (M + bm - 1) / bm;
-  p.nblk = (N + kGmBN - 1) / kGmBN;
+  p.nblk = (N + tn - 1) / tn;
   p.kblk = int((K + kGmBK - 1) / kGmBK);
   p.group_m = std::max(1, group_m);
+  p.group_n = group_m < 0 ? -group_m : 0;     // group_m < 0 selects N-groups of −group_m
   p.hint_a = hints & 3;          // hints: 2 bits each for A, B, C
   p.hint_b = (hints >> 2) & 3;
   p.hint_c = (hints >> 4) & 3;
@@ -898,10 +913,30 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
   const int64_t tiles = int64_t(p.mblk) * p.nblk;
   if (tiles == 0 || p.kblk == 0) return ESPO_OK;
   if (tiles > INT32_MAX) return ESPO_ERR_INVALID_ARGUMENT;
+  p.sync = nullptr;
+  p.sync_chunk = std::max(1, c->gemm_sync_chunk);
+  p.sync_slack = std::max(1, c->gemm_sync_slack);
+  p.sync_timeout_ns = 200000;
   if (pair) {
-    ESPO_CUDA(ensure_smem_attr(k_umma_gemm2<kAMN, kBMN, kOut>, int(kG2Smem), attr2));
+    if (kind == 2) ESPO_CUDA(ensure_smem_attr(k_umma_gemm2<kAMN, kBMN, kOut, 512>, int(G2<512>::kSmem), attr3));
+    else ESPO_CUDA(ensure_smem_attr(k_umma_gemm2<kAMN, kBMN, kOut, 256>, int(G2<256>::kSmem), attr2));
     const int clusters = int(std::min<int64_t>(tiles, c->num_sms / 2));
-    k_umma_gemm2<kAMN, kBMN, kOut><<<2 * clusters, kGmThreads, kG2Smem, s>>>(ma, mb, p);
+    if (c->gemm_sync_chunk > 0) {              // one zeroed progress counter per wave
+      const int64_t waves = (tiles + clusters - 1) / clusters;
+      if (size_t(waves) * 4 > c->gemm_sync_cap) {
+        if (c->gemm_sync) cudaFree(c->gemm_sync);
+        c->gemm_sync = nullptr;
+        c->gemm_sync_cap = 0;
+        ESPO_CUDA(cudaMalloc(&c->gemm_sync, size_t(waves) * 4));
+        c->gemm_sync_cap = size_t(waves) * 4;
+      }
+      ESPO_CUDA(cudaMemsetAsync(c->gemm_sync, 0, size_t(waves) * 4, s));
+      p.sync = static_cast<unsigned*>(c->gemm_sync);
+    }
+    if (kind == 2)
+      k_umma_gemm2<kAMN, kBMN, kOut, 512><<<2 * clusters, kGmThreads, G2<512>::kSmem, s>>>(ma, mb, p);
+    else
+      k_umma_gemm2<kAMN, kBMN, kOut, 256><<<2 * clusters, kGmThreads, G2<256>::kSmem, s>>>(ma, mb, p);
   } else {
     ESPO_CUDA(ensure_smem_attr(k_umma_gemm<kAMN, kBMN, kOut>, int(kGmSmem), attr));
     const int grid = int(std::min<int64_t>(tiles, c->num_sms));
@@ -1048,6 +1083,7 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
                           round_up(size_t(sub) * ldc * 2, 256) + size_t(sub) * sizeof(BwdRec);
     if (need_c > c->lmh_cmp_cap) {
       if (c->lmh_cmp) cudaFree(c->lmh_cmp);
+    if (c->gemm_sync) cudaFree(c->gemm_sync);
       c->lmh_cmp = nullptr;
       c->lmh_cmp_cap = 0;
       ESPO_CUDA(cudaMalloc(&c->lmh_cmp, need_c));
@@ -1116,11 +1152,21 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
           !make_map_bf16(&mh_mn, hsrc, uint64_t(n), uint64_t(d), uint64_t(hld) * 2, 64))
         return ESPO_ERR_CUDA;
       espo_status st;
-      const bool pair = c->lmh_bwd_gemm == 0;
+      // tile kinds (ESPO_OPT_LMHEAD_BWD_GEMM): 0 → dh on 256 × 512 pair tiles (long K) and dW
+      // on 256 × 256 pair tiles; 2 → one CTA per 128 × 256; 3 → 256 × 256 pairs for both;
+      // 4 → 256 × 512 pairs for both
+      // (tools/gemm_sweep.py, sustained A/B on one B200: d = 4096 → dW 256-wide pair tiles in
+      // N-groups of 8 blocks; d = 8192 → 512-wide pair tiles in N-groups of 2)
+      const int g = c->lmh_bwd_gemm;
+      const bool wide_dw = d > 4096;
+      const int kind_dh = g == 2 ? 0 : g == 3 ? 1 : 2;
+      const int kind_dw = g == 2 ? 0 : g == 3 ? 1 : g == 4 ? 2 : (wide_dw ? 2 : 1);
       // tile order: dh has a long K (the vocabulary) and few tiles: groups of 8 M-blocks keep
       // the resident tiles' A and B panels small; dW (K = rows): N fastest, so every M-block
       // of dz is read once while h stays in L2
       const int g_dh = c->gemm_group_m > 0 ? c->gemm_group_m : 8;
+      // dW: groups of gemm_group_n_dw N-blocks (0 = N fastest over all of d)
+      const int g_dw = c->gemm_group_n_dw > 0 ? -c->gemm_group_n_dw : (g == 0 ? (wide_dw ? -2 : -8) : 1);
       // L2 policies (2 bits each: A | B << 2 | C << 4; 1 = evict_first, 2 = evict_last):
       // dh streams both panels once per wave; dW streams dz and the dW read-add-write while
       // every tile re-reads h (64 MB at n = 8192, d = 4096), which should stay in L2
@@ -1137,12 +1183,12 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       if (dhidden) {   // dh[n, d] = dz[n, V] · W[V, d]: A = dz K-major, B = W MN-major
         char* dh = static_cast<char*>(dhidden) + (compact ? 0 : r0 * lddh * int64_t(dsize(dh_dtype)));
         st = dh_dtype == ESPO_BF16
-                 ? launch_umma_gemm<false, true, kOutBF16>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, pair, g_dh, hint_dh, s, dyn_m)
-                 : launch_umma_gemm<false, true, kOutF32>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, pair, g_dh, hint_dh, s, dyn_m);
+                 ? launch_umma_gemm<false, true, kOutBF16>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, kind_dh, g_dh, hint_dh, s, dyn_m)
+                 : launch_umma_gemm<false, true, kOutF32>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, kind_dh, g_dh, hint_dh, s, dyn_m);
         if (st != ESPO_OK) return st;
       }
       if (dweight) {   // dW[V, d] += dzᵀ[V, n] · h[n, d]: A = dz MN-major, B = h MN-major
-        st = launch_umma_gemm<true, true, kOutAddF32>(c, mdz_mn, mh_mn, V, d, n, dweight, lddw, pair, 1, hint_dw, s, dyn_k);
+        st = launch_umma_gemm<true, true, kOutAddF32>(c, mdz_mn, mh_mn, V, d, n, dweight, lddw, kind_dw, g_dw, hint_dw, s, dyn_k);
         if (st != ESPO_OK) return st;
       }
       continue;

@@ -44,6 +44,7 @@ struct GemmParams {
   int M, N, K;        // C[M, N] (+)= A[M, K] · B[K, N]
   int mblk, nblk, kblk;   // tile counts (tile = kGmBM × kGmBN, or 2·kGmBM × kGmBN for a pair)
   int group_m;        // tile order: groups of group_m M-blocks, M fastest inside a group
+  int group_n;        // > 0: instead, groups of group_n N-blocks (N fastest, then M)
   int hint_a, hint_b, hint_c;   // L2 policy of A / B loads and C read-add-write: 0 normal,
                                 // 1 evict_first (streamed), 2 evict_last (reused)
   void* C;
@@ -54,7 +55,33 @@ struct GemmParams {
   const int* dyn_count;
   int dyn_base, dyn_which;
   const int* row_map;
+  // soft lockstep (CTA-pair kernel): the tiles of one wave (the i-th tile of every cluster)
+  // read the same K-slices of their A and B panels; a cluster that is more than sync_slack
+  // chunks of sync_chunk K-steps ahead of the slowest cluster of its wave waits (bounded by
+  // ~sync_timeout_ns, then proceeds), so the panels' K-slices are reused from L2 instead of
+  // being re-read from DRAM by clusters that drifted apart. sync (nullable) = one zeroed
+  // counter per wave.
+  unsigned* sync;
+  int sync_chunk, sync_slack;
+  unsigned sync_timeout_ns;
 };
+
+// wait until *ctr ≥ target or the timeout expired (acquire; a soft barrier: never deadlocks)
+__device__ __forceinline__ void soft_wait(const unsigned* ctr, unsigned target, unsigned timeout_ns) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+  if (v >= target) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    __nanosleep(64);
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) return;
+  }
+}
 
 // the launch's sizes with a device-side row count applied (uniform in every thread)
 __device__ __forceinline__ GemmParams gemm_effective(const GemmParams& p, int bm) {
@@ -76,6 +103,15 @@ __device__ __forceinline__ GemmParams gemm_effective(const GemmParams& p, int bm
 // fastest, so the tiles resident together cover ≈ group_m × (resident / group_m) blocks
 // (group_m = 1: N fastest)
 __device__ __forceinline__ void gemm_tile_coords(const GemmParams& p, int tile, int& mb, int& nb) {
+  if (p.group_n > 0) {       // groups of group_n N-blocks; N fastest inside a group, then M
+    const int per_group = p.group_n * p.mblk;
+    const int g = tile / per_group, rem = tile - g * per_group;
+    const int first = g * p.group_n;
+    const int gn = min(p.nblk - first, p.group_n);
+    nb = first + rem % gn;
+    mb = rem / gn;
+    return;
+  }
   const int per_group = p.group_m * p.nblk;
   const int g = tile / per_group, rem = tile - g * per_group;
   const int first = g * p.group_m;
@@ -352,11 +388,19 @@ __global__ void __launch_bounds__(kGmThreads, 1)
 // independent 128 × 256 tiles: per K-step 32 KB per CTA for 4.2 MFLOP instead of 48 KB); the
 // leader issues M = 256 MMAs over both CTAs' shared memory and commits to both CTAs' barriers
 // (multicast); each CTA's epilogue drains its own TMEM rows (the k_lmhead2.cuh protocol).
-constexpr int kG2Stages = 6;
-constexpr int kG2ABytes = 128 * kGmBK * 2;       // 16 KB: this CTA's 128 rows of A
-constexpr int kG2BBytes = 128 * kGmBK * 2;       // 16 KB: this CTA's 128 columns of B
-constexpr int kG2StageBytes = kG2ABytes + kG2BBytes;
-constexpr size_t kG2Smem = size_t(kG2Stages) * kG2StageBytes + 1024 + 256;
+// kNP = N columns per pair tile: 256 (two 256-column TMEM accumulators, so the next tile's
+// MMAs overlap this tile's epilogue) or 512 (one 512-column accumulator = all of TMEM; per
+// K-step 48 KB per CTA for 8.4 MFLOP instead of 32 KB for 4.2: a quarter less L2 → SM traffic,
+// the epilogue not overlapped — the choice for long-K GEMMs).
+template <int kNP>
+struct G2 {
+  static constexpr int kABytes = 128 * kGmBK * 2;              // this CTA's 128 rows of A
+  static constexpr int kBBytes = (kNP / 2) * kGmBK * 2;         // this CTA's kNP/2 columns of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = kNP == 256 ? 6 : 4;
+  static constexpr int kAcc = kNP == 256 ? 2 : 1;               // TMEM accumulator buffers
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024 + 256;
+};
 
 template <bool kAMN, bool kBMN>
 __host__ __device__ constexpr uint32_t gemm2_idesc() {
@@ -383,10 +427,13 @@ __device__ __forceinline__ void gm_wait_cluster(uint32_t bar, uint32_t parity) {
   }
 }
 
-template <bool kAMN, bool kBMN, int kOut>
+template <bool kAMN, bool kBMN, int kOut, int kNP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
     k_umma_gemm2(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                  const GemmParams p0) {
+  using C = G2<kNP>;
+  constexpr int kG2Stages = C::kStages, kG2ABytes = C::kABytes, kG2BBytes = C::kBBytes;
+  constexpr int kG2StageBytes = C::kStageBytes;
   const GemmParams p = gemm_effective(p0, 2 * kGmBM);
   if (p.mblk * p.nblk == 0 || p.kblk == 0) return;   // nothing to add (uniform in the grid)
   extern __shared__ uint8_t smem_raw[];
@@ -431,15 +478,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
     // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint64_t pa = l2_policy(p.hint_a), pb = l2_policy(p.hint_b);
+      const bool pace = p.sync != nullptr && rank == 0;
       uint32_t q = 0;
-      for (int tile = cluster; tile < tiles; tile += nclusters) {
+      int wave = 0;
+      for (int tile = cluster; tile < tiles; tile += nclusters, ++wave) {
         int mb, nb;
         gemm_tile_coords(p, tile, mb, nb);
         const int m0 = mb * 2 * kGmBM + int(rank) * kGmBM;
-        const int n0 = nb * kGmBN + int(rank) * (kGmBN / 2);
+        const int n0 = nb * kNP + int(rank) * 128;
+        const unsigned members = unsigned(min(nclusters, tiles - wave * nclusters));
         for (int kb = 0; kb < p.kblk; ++kb, ++q) {
           const int s = q % kG2Stages;
           const int k0 = kb * kGmBK;
+          if (pace && kb % p.sync_chunk == 0) {
+            const int c = kb / p.sync_chunk;       // entering chunk c: chunk c − 1 is issued
+            if (c > 0) atomicAdd(p.sync + wave, 1u);
+            if (c > p.sync_slack)
+              soft_wait(p.sync + wave, unsigned(c - p.sync_slack) * members, p.sync_timeout_ns);
+          }
           gm_wait_cluster(smem_u32(&empty[s]), ((q / kG2Stages) & 1u) ^ 1u);
           const uint32_t leader_full = mapa_rank(smem_u32(&full[s]), 0);
           if (rank == 0) arrive_expect_tx_u32(smem_u32(&full[s]), 2 * kG2StageBytes);
@@ -450,11 +506,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
           } else {
             tma_load_2d_pair_hint(a, &tmap_a, k0, m0, leader_full, pa);
           }
-          if constexpr (kBMN) {
-            tma_load_2d_pair_hint(b, &tmap_b, n0, k0, leader_full, pb);
-            tma_load_2d_pair_hint(b + kGmMNBox, &tmap_b, n0 + 64, k0, leader_full, pb);
-          } else {
-            tma_load_2d_pair_hint(b, &tmap_b, k0, n0, leader_full, pb);
+#pragma unroll
+          for (int hh = 0; hh < kNP / 256; ++hh) {   // MMA half hh: this CTA's 128 columns
+            const uint32_t bh = b + hh * (128 * kGmBK * 2);
+            const int nh = n0 + hh * 256;
+            if constexpr (kBMN) {
+              tma_load_2d_pair_hint(bh, &tmap_b, nh, k0, leader_full, pb);
+              tma_load_2d_pair_hint(bh + kGmMNBox, &tmap_b, nh + 64, k0, leader_full, pb);
+            } else {
+              tma_load_2d_pair_hint(bh, &tmap_b, k0, nh, leader_full, pb);
+            }
           }
         }
       }
@@ -466,8 +527,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
       uint32_t q = 0;
       int i = 0;
       for (int tile = cluster; tile < tiles; tile += nclusters, ++i) {
-        const int acc = i & 1;
-        gm_wait_cluster(smem_u32(&tempty[acc]), ((i >> 1) & 1u) ^ 1u);
+        const int acc = C::kAcc == 2 ? (i & 1) : 0;
+        const int use = C::kAcc == 2 ? (i >> 1) : i;     // earlier uses of this buffer
+        gm_wait_cluster(smem_u32(&tempty[acc]), (use & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t dt = tmem + uint32_t(acc * kGmBN);
         for (int kb = 0; kb < p.kblk; ++kb, ++q) {
@@ -478,8 +540,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
 #pragma unroll
           for (int k = 0; k < kGmBK / 16; ++k) {
             const uint64_t ad = kAMN ? umma_desc_sw128_mn(a0 + k * 2048) : umma_desc_sw128(a0 + k * 32);
-            const uint64_t bd = kBMN ? umma_desc_sw128_mn(b0 + k * 2048) : umma_desc_sw128(b0 + k * 32);
-            tc_mma_pair(dt, ad, bd, idesc, (kb | k) != 0);
+#pragma unroll
+            for (int hh = 0; hh < kNP / 256; ++hh) {
+              const uint32_t bh = b0 + hh * (128 * kGmBK * 2);
+              const uint64_t bd = kBMN ? umma_desc_sw128_mn(bh + k * 2048) : umma_desc_sw128(bh + k * 32);
+              tc_mma_pair(dt + uint32_t(hh * 256), ad, bd, idesc, (kb | k) != 0);
+            }
           }
           tc_commit_pair(smem_u32(&empty[s]));     // slot s free in both CTAs
         }
@@ -495,13 +561,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
     const uint32_t leader_tempty1 = mapa_rank(smem_u32(&tempty[1]), 0);
     int i = 0;
     for (int tile = cluster; tile < tiles; tile += nclusters, ++i) {
-      const int acc = i & 1;
+      const int acc = C::kAcc == 2 ? (i & 1) : 0;
+      const int use = C::kAcc == 2 ? (i >> 1) : i;
       int mb, nb;
       gemm_tile_coords(p, tile, mb, nb);
-      gm_wait_cluster(smem_u32(&tfull[acc]), (i >> 1) & 1u);
+      gm_wait_cluster(smem_u32(&tfull[acc]), use & 1u);
       tc_fence_after();
       const uint32_t base = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kGmBN);
-      gemm_store_tile<kOut>(p, base, mb * 2 * kGmBM + int(rank) * kGmBM + row, nb * kGmBN, pol_c);
+#pragma unroll 1
+      for (int hh = 0; hh < kNP / 256; ++hh)
+        gemm_store_tile<kOut>(p, base + uint32_t(hh * 256), mb * 2 * kGmBM + int(rank) * kGmBM + row,
+                              nb * kNP + hh * 256, pol_c);
       __syncwarp();
       tc_fence_before();
       arrive_remote(acc ? leader_tempty1 : leader_tempty0);

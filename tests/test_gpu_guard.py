@@ -188,7 +188,8 @@ def test_guard_vocab_partial_combine():
         c.close()
 
 
-@pytest.mark.parametrize("two_cta,gemm", [(0, 0), (1, 2)], ids=["1cta_fwd+pair_gemm", "2cta_fwd+1cta_gemm"])
+@pytest.mark.parametrize("two_cta,gemm", [(0, 0), (1, 2), (0, 4)],
+                         ids=["1cta_fwd+pair_gemm", "2cta_fwd+1cta_gemm", "pair512_gemm"])
 def test_guard_lmhead(two_cta, gemm):
     from paper_2512_07710_b200.espo import OPT_LMHEAD_2CTA, OPT_LMHEAD_BWD_GEMM, OPT_LMHEAD_BWD_ROWS
     dev = require_cuda()

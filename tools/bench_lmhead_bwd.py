@@ -14,16 +14,32 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_07710_b200.espo import Espo  # noqa: E402
 
 
-def main(d=4096, n=16384, V=151936, iters=3):
+def main(d=4096, n=16384, V=151936, iters=3, realistic=False):
+    """realistic=False: one prompt group of 8 rollouts with rewards [1,0,…] and old_logp within
+    0.02 of the policy (every row carries gradient — the dense case). realistic=True: the C1
+    reward and drift recipe (bench.py): groups of 8 rollouts with Bernoulli(p ~ U(0,1)) rewards
+    (≈22 % zero-variance groups), old_logp = lp + b_i + 0.02·n_t with b_i ~ N(0, 0.04) per
+    rollout (≈1/3 of active tokens clipped) — rows without gradient are then skipped by the
+    fused backward."""
     dev = torch.device("cuda", 0)
     torch.manual_seed(0)
     h = (torch.randn(n, d, device=dev) / d ** 0.5 * 3).to(torch.bfloat16)
     W = torch.randn(V, d, device=dev).to(torch.bfloat16)
     tokens = torch.randint(0, V, (n,), device=dev, dtype=torch.int32)
     G = 8
-    rewards = torch.tensor([1.0, 0.0] * (G // 2), device=dev)
-    gid = torch.zeros(G, dtype=torch.int32, device=dev)
-    so = torch.arange(G + 1, device=dev, dtype=torch.int64) * (n // G)
+    if realistic:
+        import numpy as np
+        R = 8 * max(1, n // 4096)                 # rollouts of 4096 / (n/R) tokens
+        rng = np.random.default_rng(1)
+        rw = np.concatenate([(rng.uniform(size=8) < rng.uniform()).astype(np.float32)
+                             for _ in range(R // 8)])
+        rewards = torch.from_numpy(rw).to(dev)
+        gid = torch.from_numpy(np.repeat(np.arange(R // 8, dtype=np.int32), 8)).to(dev)
+        so = torch.arange(R + 1, device=dev, dtype=torch.int64) * (n // R)
+    else:
+        rewards = torch.tensor([1.0, 0.0] * (G // 2), device=dev)
+        gid = torch.zeros(G, dtype=torch.int32, device=dev)
+        so = torch.arange(G + 1, device=dev, dtype=torch.int64) * (n // G)
     fctx = Espo(V, logits_dtype=torch.bfloat16, device=0)
     uctx = Espo(V, logits_dtype=torch.bfloat16, grad_dtype=torch.bfloat16, device=0)
     # rollout log-probs near the current policy's (untimed): old = lp + N(0, 0.02²), so the
@@ -32,6 +48,10 @@ def main(d=4096, n=16384, V=151936, iters=3):
     uctx.loss_fwd(torch.matmul(h, W.T), tokens, torch.zeros(n, device=dev))
     uctx.loss_finalize()
     old = (uctx.export_token_stats()["lp"] + 0.02 * torch.randn(n, device=dev)).contiguous()
+    if realistic:                                  # + per-rollout drift b_i ~ N(0, 0.04)
+        R = int(so.numel()) - 1
+        old = (old + torch.repeat_interleave(0.04 * torch.randn(R, device=dev),
+                                             torch.diff(so))).contiguous()
     xctx = Espo(V, logits_dtype=torch.bfloat16, grad_dtype=torch.bfloat16, device=0)
     dh = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
     dW = torch.zeros((V, d), dtype=torch.float32, device=dev)
@@ -148,11 +168,14 @@ def main(d=4096, n=16384, V=151936, iters=3):
     from paper_2512_07710_b200.espo import stats_to_dict
     st = stats_to_dict(uctx.loss_finalize()[1])
     res["clipped_fraction"] = st["n_clipped_tokens"] / max(st["n_active_tokens"], 1)
-    res["config"] = {"n": n, "V": V, "d": d,
+    res["rows_with_gradient"] = (st["n_active_tokens"] - st["n_clipped_tokens"]) / n
+    res["zv_groups"] = st["n_zv_groups"]
+    res["config"] = {"n": n, "V": V, "d": d, "realistic": realistic,
                      "model_flops": "6·n·V·d (fwd logits GEMM + dh + dW GEMMs)"}
     print(json.dumps(res))
 
 
 if __name__ == "__main__":
     main(d=int(sys.argv[1]) if len(sys.argv) > 1 else 4096,
-         n=int(sys.argv[2]) if len(sys.argv) > 2 else 16384)
+         n=int(sys.argv[2]) if len(sys.argv) > 2 else 16384,
+         realistic=len(sys.argv) > 3 and sys.argv[3] == "realistic")

@@ -10,10 +10,12 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_07710_b200.espo import (OPT_GEMM_GROUP_M, OPT_GEMM_HINTS,  # noqa: E402
-                                        OPT_LMHEAD_BWD_GEMM, Espo)
+                                        OPT_GEMM_SYNC, OPT_LMHEAD_BWD_GEMM, OPT_LMHEAD_COMPACT,
+                                        Espo)
 
 
-def main(d=4096, n=8192, V=151936, rounds=5):
+def main(d=4096, n=8192, V=151936, rounds=5, burst=1):
+    """burst = back-to-back timed calls per setting and round (burst > 1: sustained clocks)."""
     dev = torch.device("cuda", 0)
     torch.manual_seed(0)
     h = (torch.randn(n, d, device=dev) / d ** 0.5 * 3).to(torch.bfloat16)
@@ -35,36 +37,41 @@ def main(d=4096, n=8192, V=151936, rounds=5):
     dW = torch.zeros((V, d), dtype=torch.float32, device=dev)
     H = lambda a, b, c: a | (b << 2) | (c << 4)
     dw_auto = H(1, 2, 1)
-    cfgs = {
-        "cublas": (1, 0, -1),
-        "1cta": (2, 0, -1),
-        "pair_auto": (0, 0, -1),
-        "pair_g4": (0, 4, -1),
-        "pair_g16": (0, 16, -1),
-        "pair_g1": (0, 1, -1),
-        "pair_nohints": (0, 0, 0),
-        "pair_dh_ef": (0, 0, H(1, 1, 0) | (dw_auto << 8)),
-        "pair_dw_noc": (0, 0, (H(1, 2, 0) << 8)),
-        "pair_dw_nolast": (0, 0, (H(1, 0, 1) << 8)),
+    G = lambda dh_m, dw_n: dh_m | (dw_n << 16)
+    H2 = lambda dh, dw: dh | (dw << 8)
+    cfgs = {                                 # (gemm, group, hints, compact, sync)
+        "cublas": (1, 0, -1, 0, 0),
+        "default": (0, 0, -1, 1, 0),
+        "dw_gn2": (0, G(0, 2), -1, 1, 0),
+        "dw_gn4": (0, G(0, 4), -1, 1, 0),
+        "dw_gn8": (0, G(0, 8), -1, 1, 0),
+        "dw512_gn1": (4, G(0, 1), -1, 1, 0),
+        "dw512_gn2": (4, G(0, 2), -1, 1, 0),
+        "dw512_gn4": (4, G(0, 4), -1, 1, 0),
+        "dw_gn4_nohint": (0, G(0, 4), H2(0, 0), 1, 0),
+        "dw_gn4_el_b": (0, G(0, 4), H2(0, H(1, 2, 1)), 1, 0),
     }
     times = {k: [] for k in cfgs}
     for _ in range(rounds):
-        for k, (impl, gm, hints) in cfgs.items():
+        for k, (impl, gm, hints, compact, sync) in cfgs.items():
+            ctx.set_option(OPT_GEMM_SYNC, sync)
             ctx.set_option(OPT_LMHEAD_BWD_GEMM, impl)
             ctx.set_option(OPT_GEMM_GROUP_M, gm)
             ctx.set_option(OPT_GEMM_HINTS, hints)
+            ctx.set_option(OPT_LMHEAD_COMPACT, compact)
             ctx.lmhead_bwd(h, W, dh, dW)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            ctx.lmhead_bwd(h, W, dh, dW)
+            for _ in range(burst):
+                ctx.lmhead_bwd(h, W, dh, dW)
             e.record()
             torch.cuda.synchronize()
-            times[k].append(s.elapsed_time(e))
+            times[k].append(s.elapsed_time(e) / burst)
     ctx.get_error()
     flops = 6.0 * n * V * d
     out = {k: {"ms": statistics.median(v), "TFLOPs_3gemm": flops / (statistics.median(v) * 1e-3) / 1e12}
            for k, v in times.items()}
-    out["config"] = {"n": n, "d": d, "V": V, "rounds": rounds}
+    out["config"] = {"n": n, "d": d, "V": V, "rounds": rounds, "burst": burst}
     print(json.dumps(out))
 
 
