@@ -79,6 +79,15 @@ template <typename T> struct Vec;
 template <> struct Vec<float> {
   static constexpr int EPV = 4;
   static constexpr uint32_t kNegInfWord = 0xff800000u;  // −inf
+  static constexpr uint32_t kBigNegWord = 0xf149f2cau;  // −1e30 (finite: 0·(−1e30·λ) = 0)
+  // element e of the vector := −1e30 where (e == yoff || e >= keep); compile-time e only
+  __device__ __forceinline__ static uint4 patch(uint4 v, int yoff, int keep) {
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (e == yoff || e >= keep) w[e] = kBigNegWord;
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
   __device__ __forceinline__ static void unpack(const uint4& v, float* x) {
     x[0] = __uint_as_float(v.x); x[1] = __uint_as_float(v.y);
     x[2] = __uint_as_float(v.z); x[3] = __uint_as_float(v.w);
@@ -90,6 +99,16 @@ template <> struct Vec<float> {
 template <> struct Vec<__nv_bfloat16> {
   static constexpr int EPV = 8;
   static constexpr uint32_t kNegInfWord = 0xff80ff80u;  // two bf16 −inf
+  static constexpr uint32_t kBigNegWord = 0xf14af14au;  // two bf16 −1.0e30 (finite)
+  __device__ __forceinline__ static uint4 patch(uint4 v, int yoff, int keep) {
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (e == yoff || e >= keep)
+        w[e >> 1] = (e & 1) ? ((w[e >> 1] & 0x0000ffffu) | 0xf14a0000u)
+                            : ((w[e >> 1] & 0xffff0000u) | 0x0000f14au);
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
   __device__ __forceinline__ static void unpack(const uint4& v, float* x) {
     x[0] = bf16lo(v.x); x[1] = bf16hi(v.x); x[2] = bf16lo(v.y); x[3] = bf16hi(v.y);
     x[4] = bf16lo(v.z); x[5] = bf16hi(v.z); x[6] = bf16lo(v.w); x[7] = bf16hi(v.w);

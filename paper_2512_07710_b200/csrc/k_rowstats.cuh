@@ -411,6 +411,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
   const uint64_t pol = policy_evict_first();
   const uint4 ninf = make_uint4(Vec<Tin>::kNegInfWord, Vec<Tin>::kNegInfWord, Vec<Tin>::kNegInfWord,
                                 Vec<Tin>::kNegInfWord);
+  // General chunks (target vector, ragged end, past the row end) on the packed fast path:
+  // the excluded elements are replaced in registers by the finite −1e30 (2^(−1e30·λ·log2e
+  // − r) = 0 and 0·t = 0 exactly, where −inf would give 0·(−inf) = NaN), by the one lane
+  // holding the target / ragged vector; vectors past the row end load as −1e30. Valid while
+  // −1e30·λ·log2e stays finite (λ < 1e6; otherwise the SAFE batch form is used).
+  const bool bigneg = lamL < 1e6f;
+  const uint4 nbig = make_uint4(Vec<Tin>::kBigNegWord, Vec<Tin>::kBigNegWord,
+                                Vec<Tin>::kBigNegWord, Vec<Tin>::kBigNegWord);
+  const int keep_rag = p.V % EPV;          // valid elements of the ragged vector jrag
 
   // Row assignment: the first row of every warp is static (gw); after that, for rows of ≥ 16
   // ring chunks, warps CLAIM rows dynamically (atomic counter count[1], one row ahead) so
@@ -510,7 +519,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
 #pragma unroll
         for (int u = 0; u < SUB; ++u) {
           const int jl = h * 32 * SUB + lane + 32 * u;
-          v[u] = (jl < vlim) ? lds128(buf + jl * 16) : ninf;
+          v[u] = (jl < vlim) ? lds128(buf + jl * 16) : (bigneg ? nbig : ninf);
         }
         if (h == NSUB - 1) {
           __syncwarp();
@@ -518,10 +527,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_rowstats_tma(const FwdParams p,
         }
         const int j0 = c * VPC + h * 32 * SUB + lane;
         float bS, bW;
-        if (special_batch<SUB>(j0, vy, jrag) || j0 + 32 * (SUB - 1) >= nvec)
-          batch_safe<Tin, SUB>(v, j0, nvec, vy, yoff, p.V, lamL, ref, bS, bW);
-        else
+        if (bigneg) {
+#pragma unroll
+          for (int u = 0; u < SUB; ++u) {
+            const int j = j0 + 32 * u;
+            if (j == vy || j == jrag)              // one lane, one vector: patch in registers
+              v[u] = Vec<Tin>::patch(v[u], j == vy ? yoff : -1, j == jrag ? keep_rag : EPV);
+          }
           acc_batch<Tin, SUB, NPOLY>(v, lamL, -ref, bS, bW);
+        } else if (special_batch<SUB>(j0, vy, jrag) || j0 + 32 * (SUB - 1) >= nvec) {
+          batch_safe<Tin, SUB>(v, j0, nvec, vy, yoff, p.V, lamL, ref, bS, bW);
+        } else {
+          acc_batch<Tin, SUB, NPOLY>(v, lamL, -ref, bS, bW);
+        }
         if (!(bS < 0x1p100f) || !(fabsf(bW) < 0x1p110f)) {
           S -= cS;
           W -= cW;

@@ -23,9 +23,19 @@ def main(d=4096, n=16384, V=151936, iters=3, realistic=False):
     fused backward."""
     dev = torch.device("cuda", 0)
     torch.manual_seed(0)
-    h = (torch.randn(n, d, device=dev) / d ** 0.5 * 3).to(torch.bfloat16)
+    # realistic: logits std ≈ 7 (peaked next-token distributions, entropy ~1 nat, so Eq. 3's
+    # ε_τ is small and drifted rollouts clip) and tokens sampled from softmax (Gumbel-max)
+    h = (torch.randn(n, d, device=dev) / d ** 0.5 * (7 if realistic else 3)).to(torch.bfloat16)
     W = torch.randn(V, d, device=dev).to(torch.bfloat16)
-    tokens = torch.randint(0, V, (n,), device=dev, dtype=torch.int32)
+    if realistic:
+        tokens = torch.empty(n, dtype=torch.int32, device=dev)
+        for r0 in range(0, n, 2048):
+            z = torch.matmul(h[r0:r0 + 2048], W.T).float()
+            g = -torch.log(-torch.log(torch.rand_like(z).clamp_min(1e-20)))
+            tokens[r0:r0 + 2048] = (z + g).argmax(1).to(torch.int32)
+            del z, g
+    else:
+        tokens = torch.randint(0, V, (n,), device=dev, dtype=torch.int32)
     G = 8
     if realistic:
         import numpy as np
