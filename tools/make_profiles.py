@@ -141,7 +141,34 @@ def main(tag, out_dir="gpurun_out"):
     if os.path.exists(rep):
         open(os.path.join(dst, "ncu_factored.md"), "w").write(
             full_capture_md(rep, "k_fwd_grad_ring (factored-gradient sweep, default geometry)"))
-    for f in ("bench_full.json", "bench_full.err"):
+    for name, title in (("tp8", "K2 on 1/8-vocabulary shard rows (TP8 emulation, 8192-row chunk)"),
+                        ("gemm", "tcgen05 GEMMs of the LM-head backward (dh, dW), d = 4096, 8192-row sub-chunk"),
+                        ("lmdz", "k_lmhead_dz (LM-head backward recompute + dz epilogue), d = 4096")):
+        rep = os.path.join(src, f"prof_{name}.ncu-rep")
+        if os.path.exists(rep):
+            open(os.path.join(dst, f"ncu_{name}.md"), "w").write(full_capture_md(rep, title))
+    for ll_name, title in (("launches_lmhead_bwd", "LM-head backward, d = 4096, 8192 rows: per-launch "
+                            "time and DRAM bytes (ncu --cache-control none --clock-control none)"),
+                           ("launches_lmhead_bwd_cublas", "same, dh/dW on cuBLAS (A/B option)")):
+        lp = os.path.join(src, ll_name + ".csv")
+        if os.path.exists(lp):
+            import io
+            import contextlib
+            sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+            import launch_table
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                launch_table.main(lp, 20.0)
+            shutil.copy(lp, os.path.join(dst, ll_name + ".csv"))
+            open(os.path.join(dst, ll_name + ".md"), "w").write(
+                f"# {title}
+
+```
+" + buf.getvalue() + "```
+")
+    for f in ("bench_full.json", "bench_full.err", "gpu_tests.log", "smoke.log", "bench_tp8.json",
+              "bench_C4_strong_verify.json", "bench_lmhead_bwd_dense.json",
+              "bench_lmhead_bwd_realistic.json", "gemm_sweep.json"):
         p = os.path.join(src, f)
         if os.path.exists(p):
             shutil.copy(p, os.path.join(dst, f))
