@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // espo_api.cu — libespo host side: the C ABI of include/espo.h (context, validation,
 // workspace, launches, NCCL). Kernels live in the k_*.cuh headers of this directory.
 #include <dlfcn.h>
@@ -148,6 +150,12 @@ struct espo_ctx_s {
   int gemm_group_m = 0;          // dh GEMM tile order: M-blocks per group (0 = auto)
   int gemm_group_n_dw = 0;       // dW GEMM tile order: N-blocks per group (0 = all)
   int lmh_compact = 1;           // LM-head backward on the rows with gradient only (k_compact.cuh)
+  int lmh_impl = 0;              // LM-head fwd / dz: 0 = on the tcgen05 GEMM core (k_gemm.cuh),
+                                 // 1 = the dedicated kernels (k_lmhead*.cuh)
+  uint8_t* lmh_live = nullptr;   // per 256-row block liveness (fwd on the GEMM core)
+  int lmh_group_m = 0, lmh_hints = 0;   // LM-head fwd / dz on the GEMM core: raster (0 = auto),
+                                        // L2 policies
+  size_t lmh_live_cap = 0;
   int gemm_sync_chunk = 0, gemm_sync_slack = 2;  // GEMM soft lockstep (0 = off), k_gemm.cuh
   void* gemm_sync = nullptr;     // per-wave progress counters
   size_t gemm_sync_cap = 0;
@@ -178,7 +186,10 @@ struct espo_ctx_s {
 namespace {
 inline cudaStream_t S(espo_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
-espo_status cuda_status(cudaError_t e) {
+espo_status cuda_status(cudaError_t e, int line = 0) {
+  if (e != cudaSuccess && std::getenv("ESPO_DEBUG"))     // diagnostics only: which call failed
+    std::fprintf(stderr, "[libespo] espo_api.cu:%d: %s (%s)\n", line, cudaGetErrorName(e),
+                 cudaGetErrorString(e));
   return e == cudaSuccess ? ESPO_OK
                           : (e == cudaErrorMemoryAllocation ? ESPO_ERR_OUT_OF_MEMORY : ESPO_ERR_CUDA);
 }
@@ -186,14 +197,14 @@ espo_status cuda_status(cudaError_t e) {
 #define ESPO_CUDA(x)                                  \
   do {                                                \
     cudaError_t e_ = (x);                             \
-    if (e_ != cudaSuccess) return cuda_status(e_);    \
+    if (e_ != cudaSuccess) return cuda_status(e_, __LINE__); \
   } while (0)
 
 #define ESPO_LAUNCHED(ctx)                                   \
   do {                                                       \
     (ctx)->launches++;                                       \
     cudaError_t e_ = cudaGetLastError();                     \
-    if (e_ != cudaSuccess) return cuda_status(e_);           \
+    if (e_ != cudaSuccess) return cuda_status(e_, __LINE__); \
   } while (0)
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -426,6 +437,7 @@ espo_status espo_destroy(espo_ctx_t c) {
     if (c->rs_scratch) cudaFree(c->rs_scratch);
     if (c->lmh_dz) cudaFree(c->lmh_dz);
     if (c->lmh_cmp) cudaFree(c->lmh_cmp);
+    if (c->lmh_live) cudaFree(c->lmh_live);
     if (c->gemm_sync) cudaFree(c->gemm_sync);
     if (c->blas) g_blas.destroy(c->blas);
     if (c->blas_ws) cudaFree(c->blas_ws);
@@ -480,6 +492,15 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       if (value < 0 || (value & 0xFFFF) > 4096 || (value >> 16) > 64) return ESPO_ERR_INVALID_ARGUMENT;
       c->gemm_sync_chunk = int(value & 0xFFFF);
       c->gemm_sync_slack = (value >> 16) ? int(value >> 16) : 2;
+      return ESPO_OK;
+    case ESPO_OPT_LMHEAD_RASTER:  // bits 0-15 group_m (0 = 8; negative = N-groups), 16-23 hints
+      if (value < 0 || (value & 0xFFFF) > 1024) return ESPO_ERR_INVALID_ARGUMENT;
+      c->lmh_group_m = int(value & 0xFFFF);
+      c->lmh_hints = int((value >> 16) & 0xFF);
+      return ESPO_OK;
+    case ESPO_OPT_LMHEAD_IMPL:
+      if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
+      c->lmh_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_COMPACT:
       if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
@@ -858,10 +879,15 @@ bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
   cuuint64_t strides[1] = {pitch_bytes};
   cuuint32_t box[2] = {uint32_t(kLmBK), box_rows};
   cuuint32_t estr[2] = {1, 1};
-  return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-         CUDA_SUCCESS;
+  const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && std::getenv("ESPO_DEBUG"))
+    std::fprintf(stderr, "[libespo] cuTensorMapEncodeTiled failed (%d): rows %llu cols %llu pitch %llu box %u\n",
+                 int(r), (unsigned long long)rows, (unsigned long long)cols,
+                 (unsigned long long)pitch_bytes, box_rows);
+  return r == CUDA_SUCCESS;
 }
 // vocabulary parts per row block: enough CTAs for ≥ 2 waves; beyond that the best split
 // measured on B200 (tools/bench_lmhead.py, n = 32,768, V = 151,936) is 4 parts for d ≤ 4096
@@ -877,6 +903,12 @@ int lmhead_parts(const espo_ctx_s* c, int mblocks, int ntiles, int d) {
 // C[M, N] (+)= A·B on the tcgen05 GEMM (k_gemm.cuh); maps built by the caller for the
 // operands' majorness (K-major A: box {64 K, 128 M}; MN-major: boxes {64 MN, 64 K}).
 // pair: CTA-pair kernel (256 × 256 tiles per cluster of 2), else one CTA per 128 × 256 tile.
+// M-tiles per raster group of the LM-head GEMM-core kernels: 32 at d ≤ 4096, 64 above
+// (tools/bench_lmhead_fwd_ab.py, tools/gemm_sweep.py: sustained A/B on one B200)
+int lmh_raster(const espo_ctx_s* c, int d) {
+  return c->lmh_group_m > 0 ? c->lmh_group_m : (d > 4096 ? 64 : 32);
+}
+
 struct GemmDyn {          // device-side row count of compacted operands (k_compact.cuh)
   const int* count = nullptr;
   int base = 0, which = 0;   // which: 1 = M, 2 = K
@@ -886,12 +918,15 @@ struct GemmDyn {          // device-side row count of compacted operands (k_comp
 template <bool kAMN, bool kBMN, int kOut>
 espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensorMap& mb, int M,
                              int N, int64_t K, void* C, int64_t ldc, int kind, int group_m,
-                             int hints, cudaStream_t s, const GemmDyn& dyn = GemmDyn()) {
+                             int hints, cudaStream_t s, const GemmDyn& dyn = GemmDyn(),
+                             const LmEpi* lm = nullptr) {
   // kind: 0 = one CTA per 128 × 256 tile, 1 = CTA pair 256 × 256, 2 = CTA pair 256 × 512
   static unsigned long long attr = 0, attr2 = 0, attr3 = 0;
   const bool pair = kind != 0;
   const int tn = kind == 2 ? 512 : kGmBN;
   GemmParams p;
+  p.lm = lm ? *lm : LmEpi{};
+  if ((kOut == kOutLmFwd || kOut == kOutLmDz) && kind == 0) return ESPO_ERR_INVALID_ARGUMENT;
   p.dyn_count = dyn.count;
   p.dyn_base = dyn.base;
   p.dyn_which = dyn.which;
@@ -978,11 +1013,62 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
     ESPO_CUDA(cudaMalloc(&c->lmh_partial, need));
     c->lmh_cap = need;
   }
+  const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  if (c->lmh_impl == 0) {
+    // on the tcgen05 GEMM core: CTA-pair 256 × 512 tiles of z = h·Wᵀ in a grouped raster, each
+    // tile's rows reduced to a partial {R, S, W, u_y} (k_gemm.cuh kOutLmFwd), then merged over
+    // the tiles like vocabulary shards; M-tiles without a valid row are skipped
+    const int nt = (V + 511) / 512;
+    const int nlive = int((n_rows + 255) / 256);
+    const size_t needp = size_t(nt) * size_t(n_rows) * 16;
+    if (needp > c->lmh_cap) {
+      if (c->lmh_partial) cudaFree(c->lmh_partial);
+      c->lmh_partial = nullptr;
+      c->lmh_cap = 0;
+      ESPO_CUDA(cudaMalloc(&c->lmh_partial, needp));
+      c->lmh_cap = needp;
+    }
+    if (size_t(nlive) > c->lmh_live_cap) {
+      if (c->lmh_live) cudaFree(c->lmh_live);
+      c->lmh_live = nullptr;
+      c->lmh_live_cap = 0;
+      ESPO_CUDA(cudaMalloc(&c->lmh_live, size_t(nlive)));
+      c->lmh_live_cap = size_t(nlive);
+    }
+    CUtensorMap mh, mw;
+    if (!make_map_bf16(&mh, hidden, uint64_t(n_rows), uint64_t(d), uint64_t(ldh) * 2, kGmBM) ||
+        !make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, 128))
+      return ESPO_ERR_CUDA;
+    k_lmh_rows<<<pre_grid, 256, 0, s>>>(tokens, old_logp, mask, row_begin, n_rows, V, c->ws);
+    ESPO_LAUNCHED(c);
+    k_block_live<<<nlive, 256, 0, s>>>(c->ws.flag + row_begin, int(n_rows), 256, c->lmh_live);
+    ESPO_LAUNCHED(c);
+    LmEpi lm{};
+    lm.tokens = tokens;
+    lm.flag = c->ws.flag + row_begin;
+    lm.mlive = c->lmh_live;
+    lm.partial = reinterpret_cast<float4*>(c->lmh_partial);
+    lm.lamL = c->cfg.logit_scale * kLog2e;
+    lm.V = V;
+    lm.n_rows = int(n_rows);
+    lm.err = c->ws.err;
+    st = launch_umma_gemm<false, false, kOutLmFwd>(c, mh, mw, int(n_rows), V, d, nullptr, 0, 2,
+                                                   lmh_raster(c, d), c->lmh_hints, s, GemmDyn(), &lm);
+    if (st != ESPO_OK) return st;
+    {
+      const int grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+      k_fwd_combine64<<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(c->lmh_partial), nt,
+                                           row_begin, n_rows, c->ws);
+      ESPO_LAUNCHED(c);
+    }
+    c->covered[row_begin] = row_begin + n_rows;
+    c->n_covered += n_rows;
+    return ESPO_OK;
+  }
   CUtensorMap mh, mw;
   if (!make_map_bf16(&mh, hidden, uint64_t(n_rows), uint64_t(d), uint64_t(ldh) * 2, kLmBM) ||
       !make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, c->lmh_2cta ? kLmBN / 2 : kLmBN))
     return ESPO_ERR_CUDA;
-  const int pre_grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
   k_lmh_rows<<<pre_grid, 256, 0, s>>>(tokens, old_logp, mask, row_begin, n_rows, V, c->ws);
   ESPO_LAUNCHED(c);
   static unsigned long long attr_mask = 0, attr_mask2 = 0;
@@ -1033,7 +1119,8 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   cudaStream_t s = S(stream);
   const int V = c->cfg.vocab;
   const int ntiles = (V + kLmBN - 1) / kLmBN;
-  const int64_t ldz = int64_t(ntiles) * kLmBN;
+  // dz scratch pitch: a multiple of the dz tile width (256, or 512 on the GEMM core)
+  const int64_t ldz = c->lmh_impl == 0 ? round_up(size_t(V), 512) : int64_t(ntiles) * kLmBN;
   const int sub = int(std::min<int64_t>(c->lmh_bwd_rows, round_up(size_t(n_rows), kLmBM)));
   const size_t need = size_t(sub) * size_t(ldz) * 2;
   if (need > c->lmh_dz_cap) {
@@ -1064,9 +1151,10 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
   static unsigned long long attr_mask = 0, attr_mask2 = 0;
   ESPO_CUDA(ensure_smem_attr(k_lmhead_dz, int(kLmSmem), attr_mask));
   ESPO_CUDA(ensure_smem_attr(k_lmhead2_dz, int(kL2Smem), attr_mask2));
-  CUtensorMap mw, mw_mn;
+  CUtensorMap mw, mw_mn, mw_k128;
   if (!make_map_bf16(&mw, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, c->lmh_2cta ? kLmBN / 2 : kLmBN) ||
-      !make_map_bf16(&mw_mn, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, 64))
+      !make_map_bf16(&mw_mn, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, 64) ||
+      !make_map_bf16(&mw_k128, weight, uint64_t(V), uint64_t(d), uint64_t(ldw) * 2, 128))
     return ESPO_ERR_CUDA;
   const float one = 1.f, zero = 0.f;
   const char* hb = static_cast<const char*>(hidden);
@@ -1083,7 +1171,6 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
                           round_up(size_t(sub) * ldc * 2, 256) + size_t(sub) * sizeof(BwdRec);
     if (need_c > c->lmh_cmp_cap) {
       if (c->lmh_cmp) cudaFree(c->lmh_cmp);
-    if (c->gemm_sync) cudaFree(c->gemm_sync);
       c->lmh_cmp = nullptr;
       c->lmh_cmp_cap = 0;
       ESPO_CUDA(cudaMalloc(&c->lmh_cmp, need_c));
@@ -1139,11 +1226,31 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       lp.dyn_count = total;
       lp.dyn_base = int(r0);
     }
-    if (c->lmh_2cta)
+    if (c->lmh_impl == 0) {    // recompute on the GEMM core, dz epilogue (kOutLmDz)
+      LmEpi lm{};
+      lm.rec = lp.rec;
+      lm.dz = lp.dz;
+      lm.ldz = ldz;
+      lm.lamL = lp.lam_log2e;
+      lm.V = V;
+      lm.n_rows = n;
+      lm.err = c->ws.err;
+      GemmDyn dz_dyn;
+      if (compact) {             // rows up to the next 256 (their records are zero): dz = 0
+        dz_dyn.count = total;
+        dz_dyn.base = int(r0);
+        dz_dyn.which = 3;
+      }
+      const espo_status st = launch_umma_gemm<false, false, kOutLmDz>(
+          c, mh, mw_k128, n, int(ldz), d, nullptr, 0, 2, lmh_raster(c, d), c->lmh_hints, s, dz_dyn, &lm);
+      if (st != ESPO_OK) return st;
+    } else if (c->lmh_2cta) {
       k_lmhead2_dz<<<dim3(2 * parts, (mblocks + 1) / 2), kLmThreads, kL2Smem, s>>>(mh, mw, lp);
-    else
+      ESPO_LAUNCHED(c);
+    } else {
       k_lmhead_dz<<<dim3(parts, mblocks), kLmThreads, kLmSmem, s>>>(mh, mw, lp);
-    ESPO_LAUNCHED(c);
+      ESPO_LAUNCHED(c);
+    }
     // z = h·Wᵀ (dz already carries λ, as K5's) ⇒ dh = dz·W and dW = dzᵀ·h
     if (!use_blas) {
       CUtensorMap mdz_k, mdz_mn, mh_mn;

@@ -100,3 +100,18 @@ __global__ void __launch_bounds__(256) k_zero_rows(const BwdRec* rec, int n, voi
 }
 
 }  // namespace espo
+
+namespace espo {
+// per block of `rows_per_block` chunk rows: 1 if any row is valid (flag) — the LM-head forward
+// on the GEMM core skips M-tiles without a row to compute (eliminated groups, masked tails)
+__global__ void __launch_bounds__(256) k_block_live(const uint8_t* flag, int n_rows,
+                                                    int rows_per_block, uint8_t* live) {
+  const int b = blockIdx.x;
+  int any = 0;
+  for (int r = b * rows_per_block + threadIdx.x; r < min(n_rows, (b + 1) * rows_per_block);
+       r += blockDim.x)
+    any |= flag[r];
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) live[b] = any ? 1 : 0;
+}
+}  // namespace espo

@@ -38,7 +38,26 @@ constexpr int kGmMNBox = 64 * kGmBK * 2;        // one MN-major TMA box {64 MN, 
 constexpr int kGmThreads = 192;
 constexpr size_t kGmSmem = size_t(kGmStages) * kGmStageBytes + 1024 + 256;
 
-enum GemmOut { kOutF32 = 0, kOutBF16 = 1, kOutAddF32 = 2 };
+enum GemmOut { kOutF32 = 0, kOutBF16 = 1, kOutAddF32 = 2, kOutLmFwd = 3, kOutLmDz = 4 };
+
+// Epilogue data of the LM-head kernels on this GEMM (C = logits tile z = h·Wᵀ, never stored):
+// kOutLmFwd — per row and tile, the base-2 partial {R, S, W, u_y} of the tile's columns
+// (K2's reduction, lm_row_chunk), written to partial[n-block][row]; k_fwd_combine merges the
+// tiles exactly like vocabulary shards. kOutLmDz — K5's dz = λg(1[v=y] − p_v) of every element
+// from the row's record, rounded to bf16 into dz[row][col] (lm_store_dz).
+struct LmEpi {
+  const int32_t* tokens;   // chunk-relative sampled tokens (fwd)
+  const uint8_t* flag;     // chunk-relative valid flags (fwd)
+  const BwdRec* rec;       // per-row backward records (dz)
+  const uint8_t* mlive;    // per M-tile: 0 = no row to compute, the tile is skipped (nullable)
+  float4* partial;         // [n-blocks][n_rows] (fwd)
+  __nv_bfloat16* dz;       // [rows][ldz] (dz)
+  int64_t ldz;
+  float lamL;              // λ·log2(e)
+  int V;                   // vocabulary columns (columns ≥ V are excluded / written as 0)
+  int n_rows;              // partial row stride
+  int* err;
+};
 
 struct GemmParams {
   int M, N, K;        // C[M, N] (+)= A[M, K] · B[K, N]
@@ -64,6 +83,7 @@ struct GemmParams {
   unsigned* sync;
   int sync_chunk, sync_slack;
   unsigned sync_timeout_ns;
+  LmEpi lm;               // kOutLmFwd / kOutLmDz only
 };
 
 // wait until *ctr ≥ target or the timeout expired (acquire; a soft barrier: never deadlocks)
@@ -88,8 +108,8 @@ __device__ __forceinline__ GemmParams gemm_effective(const GemmParams& p, int bm
   GemmParams q = p;
   if (p.dyn_count) {
     const int n = max(0, *p.dyn_count - p.dyn_base);
-    if (p.dyn_which == 1) {
-      q.M = min(p.M, n);
+    if (p.dyn_which == 1 || p.dyn_which == 3) {   // 3: rows up to the next 256 (zero records)
+      q.M = min(p.M, p.dyn_which == 3 ? (n + 255) / 256 * 256 : n);
       q.mblk = (q.M + bm - 1) / bm;
     } else {
       q.K = min(p.K, n);
@@ -250,6 +270,34 @@ __device__ __forceinline__ void gemm_store_tile(const GemmParams& p, uint32_t ba
           if (col0 + e < p.N) o[e] = kOut == kOutAddF32 ? o[e] + x[e] : x[e];
       }
     }
+  }
+}
+
+// LM-head epilogues over 256 TMEM columns (tile columns n0 .. n0 + 255) for output row r.
+// Forward: (R, S, W, cS, cW, uy) carry across the calls for the tile's halves.
+__device__ __forceinline__ void lm_fwd_cols(const GemmParams& p, uint32_t base, int r, int n0,
+                                            float& R, float& S, float& W, float& cS, float& cW,
+                                            float& uy, bool valid, int y) {
+#pragma unroll 1
+  for (int c = 0; c < 256 / 32; ++c) {
+    float x[32];
+    __syncwarp();
+    tmem_ld32(base + uint32_t(c * 32), x);
+    const int col0 = n0 + c * 32;
+    if (!valid || col0 >= p.lm.V) continue;
+    lm_row_chunk(x, col0, y, p.lm.V, p.lm.lamL, R, S, W, cS, cW, uy, p.lm.err);
+  }
+}
+__device__ __forceinline__ void lm_dz_cols(const GemmParams& p, uint32_t base, int r, int n0,
+                                           const BwdRec& rc) {
+#pragma unroll 1
+  for (int c = 0; c < 256 / 32; ++c) {
+    float x[32];
+    __syncwarp();
+    tmem_ld32(base + uint32_t(c * 32), x);
+    const int col0 = n0 + c * 32;
+    if (r >= p.M || col0 >= p.lm.ldz) continue;
+    lm_store_dz(x, rc, col0, p.lm.V, p.lm.lamL, p.lm.dz + int64_t(r) * p.lm.ldz + col0);
   }
 }
 
@@ -484,6 +532,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
       for (int tile = cluster; tile < tiles; tile += nclusters, ++wave) {
         int mb, nb;
         gemm_tile_coords(p, tile, mb, nb);
+        if (p.lm.mlive && !p.lm.mlive[mb]) continue;     // no row to compute: skipped tile
         const int m0 = mb * 2 * kGmBM + int(rank) * kGmBM;
         const int n0 = nb * kNP + int(rank) * 128;
         const unsigned members = unsigned(min(nclusters, tiles - wave * nclusters));
@@ -526,9 +575,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
       constexpr uint32_t idesc = gemm2_idesc<kAMN, kBMN>();
       uint32_t q = 0;
       int i = 0;
-      for (int tile = cluster; tile < tiles; tile += nclusters, ++i) {
+      for (int tile = cluster; tile < tiles; tile += nclusters) {
+        if (p.lm.mlive) {
+          int mb, nb;
+          gemm_tile_coords(p, tile, mb, nb);
+          if (!p.lm.mlive[mb]) continue;
+        }
         const int acc = C::kAcc == 2 ? (i & 1) : 0;
         const int use = C::kAcc == 2 ? (i >> 1) : i;     // earlier uses of this buffer
+        ++i;
         gm_wait_cluster(smem_u32(&tempty[acc]), (use & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t dt = tmem + uint32_t(acc * kGmBN);
@@ -560,18 +615,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
     const uint32_t leader_tempty0 = mapa_rank(smem_u32(&tempty[0]), 0);
     const uint32_t leader_tempty1 = mapa_rank(smem_u32(&tempty[1]), 0);
     int i = 0;
-    for (int tile = cluster; tile < tiles; tile += nclusters, ++i) {
-      const int acc = C::kAcc == 2 ? (i & 1) : 0;
-      const int use = C::kAcc == 2 ? (i >> 1) : i;
+    for (int tile = cluster; tile < tiles; tile += nclusters) {
       int mb, nb;
       gemm_tile_coords(p, tile, mb, nb);
+      if (p.lm.mlive && !p.lm.mlive[mb]) continue;
+      const int acc = C::kAcc == 2 ? (i & 1) : 0;
+      const int use = C::kAcc == 2 ? (i >> 1) : i;
+      ++i;
       gm_wait_cluster(smem_u32(&tfull[acc]), use & 1u);
       tc_fence_after();
       const uint32_t base = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kGmBN);
+      const int r = mb * 2 * kGmBM + int(rank) * kGmBM + row;
+      if constexpr (kOut == kOutLmFwd) {
+        const bool valid = r < p.M && p.lm.flag[r];
+        const int y = valid ? p.lm.tokens[r] : -1;
+        float R = -INFINITY, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f, uy = __int_as_float(0x7fc00000);
 #pragma unroll 1
-      for (int hh = 0; hh < kNP / 256; ++hh)
-        gemm_store_tile<kOut>(p, base + uint32_t(hh * 256), mb * 2 * kGmBM + int(rank) * kGmBM + row,
-                              nb * kNP + hh * 256, pol_c);
+        for (int hh = 0; hh < kNP / 256; ++hh)
+          lm_fwd_cols(p, base + uint32_t(hh * 256), r, nb * kNP + hh * 256, R, S, W, cS, cW, uy,
+                      valid, y);
+        if (valid) p.lm.partial[int64_t(nb) * p.lm.n_rows + r] = make_float4(R, S - cS, W - cW, uy);
+      } else if constexpr (kOut == kOutLmDz) {
+        BwdRec rc;
+        rc.ng = 0.f;
+        rc.y = -1;
+        if (r < p.M) rc = p.lm.rec[r];
+#pragma unroll 1
+        for (int hh = 0; hh < kNP / 256; ++hh)
+          lm_dz_cols(p, base + uint32_t(hh * 256), r, nb * kNP + hh * 256, rc);
+      } else {
+#pragma unroll 1
+        for (int hh = 0; hh < kNP / 256; ++hh)
+          gemm_store_tile<kOut>(p, base + uint32_t(hh * 256), r, nb * kNP + hh * 256, pol_c);
+      }
       __syncwarp();
       tc_fence_before();
       arrive_remote(acc ? leader_tempty1 : leader_tempty0);

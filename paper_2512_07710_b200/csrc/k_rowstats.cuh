@@ -170,6 +170,36 @@ __global__ void __launch_bounds__(256) k_fwd_combine(const float4* partials, int
   }
 }
 
+// The same merge for many partials per row (the LM head on the GEMM core: one per 512-column
+// vocabulary tile, ~300 at V = 151,936): the rebased sums accumulate in fp64, one rounding at
+// the end, so the merge adds no error that grows with the tile count.
+__global__ void __launch_bounds__(256) k_fwd_combine64(const float4* partials, int n_shards,
+                                                       int64_t row_begin, int64_t n_rows,
+                                                       Workspace ws) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = row_begin + r;
+    if (!ws.flag[t]) continue;
+    float R = -INFINITY, uy = __int_as_float(0x7fc00000);
+    for (int k = 0; k < n_shards; ++k) {
+      const float4 a = partials[int64_t(k) * n_rows + r];
+      R = fmaxf(R, a.x);
+      if (!isnan(a.w)) uy = a.w;
+    }
+    double S = 0.0, W = 0.0;
+    for (int k = 0; k < n_shards; ++k) {
+      const float4 a = partials[int64_t(k) * n_rows + r];
+      if (a.x == -INFINITY || (a.y == 0.f && a.z == 0.f)) continue;
+      const double dd = double(a.x) - double(R);          // ≤ 0
+      const double sc = exp2(dd);
+      W += sc * (dd * double(a.y) + double(a.z));
+      S += sc * double(a.y);
+    }
+    if (isnan(uy)) set_error(ws.err, ESPO_ERR_INVALID_ARGUMENT);  // no tile holds the target
+    finish_stats(R, float(S), float(W), uy, ws, t);
+  }
+}
+
 // Slow path for one batch: NaN/+inf detection and a max-based reference. Re-unpacks the
 // packed vectors (kept in registers) instead of holding U·EPV floats.
 template <typename Tin, int U, int STRIDE = 32>   // vector k of the batch is j0 + STRIDE·k

@@ -34,6 +34,8 @@ OPT_GEMM_GROUP_M = 9
 OPT_GEMM_HINTS = 10
 OPT_LMHEAD_COMPACT = 11
 OPT_GEMM_SYNC = 12
+OPT_LMHEAD_IMPL = 13
+OPT_LMHEAD_RASTER = 14
 REDUCE_LEN = 26          # ESPO_REDUCE_LEN: fp64 terms of espo_loss_reduce_local
 
 STATUS = {

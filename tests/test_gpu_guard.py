@@ -188,10 +188,12 @@ def test_guard_vocab_partial_combine():
         c.close()
 
 
-@pytest.mark.parametrize("two_cta,gemm", [(0, 0), (1, 2), (0, 4)],
-                         ids=["1cta_fwd+pair_gemm", "2cta_fwd+1cta_gemm", "pair512_gemm"])
-def test_guard_lmhead(two_cta, gemm):
-    from paper_2512_07710_b200.espo import OPT_LMHEAD_2CTA, OPT_LMHEAD_BWD_GEMM, OPT_LMHEAD_BWD_ROWS
+@pytest.mark.parametrize("impl,two_cta,gemm", [(0, 0, 0), (1, 0, 0), (1, 1, 2), (0, 0, 4)],
+                         ids=["gemm_core", "1cta_fwd+pair_gemm", "2cta_fwd+1cta_gemm",
+                              "gemm_core+pair512"])
+def test_guard_lmhead(impl, two_cta, gemm):
+    from paper_2512_07710_b200.espo import (OPT_LMHEAD_2CTA, OPT_LMHEAD_BWD_GEMM,
+                                            OPT_LMHEAD_BWD_ROWS, OPT_LMHEAD_IMPL)
     dev = require_cuda()
     rng = np.random.default_rng(5)
     V, d, G, L = 3001, 320, 4, 70                   # V, d, n: none a multiple of the tiles
@@ -206,6 +208,7 @@ def test_guard_lmhead(two_cta, gemm):
     res = []
     for _ in range(2):
         c = Espo(V, logits_dtype=torch.bfloat16, device=dev.index)
+        c.set_option(OPT_LMHEAD_IMPL, impl)
         c.set_option(OPT_LMHEAD_2CTA, two_cta)
         c.set_option(OPT_LMHEAD_BWD_GEMM, gemm)
         c.set_option(OPT_LMHEAD_BWD_ROWS, 128)        # several backward sub-chunks

@@ -1,0 +1,68 @@
+"""A/B of the fused LM-head forward implementations against cuBLAS on one 32,768-row chunk,
+V = 151,936: ESPO_OPT_LMHEAD_IMPL 0 (GEMM core, pair 256×512 tiles, per-tile partials) over a
+few raster groups, impl 1 (dedicated one-CTA kernel), and torch.matmul bf16 (cuBLAS, writing
+the logits). Settings interleaved over rounds, `burst` calls back to back each (sustained
+clocks). usage: python tools/bench_lmhead_fwd_ab.py [d] [rounds] [burst]"""
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_07710_b200.espo import OPT_LMHEAD_IMPL, OPT_LMHEAD_RASTER, Espo  # noqa: E402
+
+
+def main(d=4096, rounds=3, burst=4, n=32768, V=151936):
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(0)
+    h = (torch.randn(n, d, device=dev) / d ** 0.5 * 3).to(torch.bfloat16)
+    W = torch.randn(V, d, device=dev).to(torch.bfloat16)
+    tokens = torch.randint(0, V, (n,), device=dev, dtype=torch.int32)
+    old = torch.full((n,), -1.0, device=dev)
+    G = 8
+    rewards = torch.tensor([1.0, 0.0] * (G // 2), device=dev)
+    gid = torch.zeros(G, dtype=torch.int32, device=dev)
+    so = torch.arange(G + 1, device=dev, dtype=torch.int64) * (n // G)
+    ctx = Espo(V, logits_dtype=torch.bfloat16, device=0)
+    cfgs = {"gemm_g16": (0, 16, 0), "gemm_g32": (0, 32, 0), "gemm_g64": (0, 64, 0),
+            "gemm_g128": (0, 128, 0), "gemm_g32_Ael": (0, 32, 2), "gemm_g32_Bef": (0, 32, 1 << 2),
+            "gemm_g64_Ael_Bef": (0, 64, 2 | (1 << 2)), "dedicated_1cta": (1, 8, 0), "cublas": None}
+    times = {k: [] for k in cfgs}
+    losses = {}
+    for _ in range(rounds):
+        for k, c in cfgs.items():
+            if c is None:
+                fn = lambda: torch.matmul(h, W.T)
+            else:
+                impl, g, hints = c
+                ctx.set_option(OPT_LMHEAD_IMPL, impl)
+                ctx.set_option(OPT_LMHEAD_RASTER, g | (hints << 16))
+
+                def fn():
+                    ctx.prepare(rewards, gid, so, n_tokens=n)
+                    ctx.lmhead_fwd(h, W, tokens, old)
+                    return ctx.loss_finalize()[0]
+            fn()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(burst):
+                out = fn()
+            e.record()
+            torch.cuda.synchronize()
+            times[k].append(s.elapsed_time(e) / burst)
+            if c is not None:
+                losses[k] = float(out.item())
+    ctx.get_error()
+    res = {k: {"ms": statistics.median(v),
+               "TFLOPs": 2.0 * n * V * d / (statistics.median(v) * 1e-3) / 1e12}
+           for k, v in times.items()}
+    res["loss_by_impl"] = losses
+    res["config"] = {"n": n, "V": V, "d": d, "rounds": rounds, "burst": burst}
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    a = [int(x) for x in sys.argv[1:]]
+    main(*a)

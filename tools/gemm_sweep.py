@@ -11,7 +11,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_07710_b200.espo import (OPT_GEMM_GROUP_M, OPT_GEMM_HINTS,  # noqa: E402
                                         OPT_GEMM_SYNC, OPT_LMHEAD_BWD_GEMM, OPT_LMHEAD_COMPACT,
-                                        Espo)
+                                        OPT_LMHEAD_IMPL, OPT_LMHEAD_RASTER, Espo)
 
 
 def main(d=4096, n=8192, V=151936, rounds=5, burst=1):
@@ -39,22 +39,22 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1):
     dw_auto = H(1, 2, 1)
     G = lambda dh_m, dw_n: dh_m | (dw_n << 16)
     H2 = lambda dh, dw: dh | (dw << 8)
-    cfgs = {                                 # (gemm, group, hints, compact, sync)
-        "cublas": (1, 0, -1, 0, 0),
-        "default": (0, 0, -1, 1, 0),
-        "dw_gn2": (0, G(0, 2), -1, 1, 0),
-        "dw_gn4": (0, G(0, 4), -1, 1, 0),
-        "dw_gn8": (0, G(0, 8), -1, 1, 0),
-        "dw512_gn1": (4, G(0, 1), -1, 1, 0),
-        "dw512_gn2": (4, G(0, 2), -1, 1, 0),
-        "dw512_gn4": (4, G(0, 4), -1, 1, 0),
-        "dw_gn4_nohint": (0, G(0, 4), H2(0, 0), 1, 0),
-        "dw_gn4_el_b": (0, G(0, 4), H2(0, H(1, 2, 1)), 1, 0),
+    cfgs = {                     # (gemm, group, hints, compact, sync, lmhead impl, lm raster)
+        "cublas": (1, 0, -1, 0, 0, 1, 0),
+        "default": (0, 0, -1, 1, 0, 0, 0),
+        "dz_dedicated": (0, 0, -1, 1, 0, 1, 0),
+        "dz_g16": (0, 0, -1, 1, 0, 0, 16),
+        "dz_g32": (0, 0, -1, 1, 0, 0, 32),
+        "dz_g64": (0, 0, -1, 1, 0, 0, 64),
+        "dz_g32_dw512_gn2": (4, G(0, 2), -1, 1, 0, 0, 32),
+        "dz_g32_dw_gn8": (0, G(0, 8), -1, 1, 0, 0, 32),
     }
     times = {k: [] for k in cfgs}
     for _ in range(rounds):
-        for k, (impl, gm, hints, compact, sync) in cfgs.items():
+        for k, (impl, gm, hints, compact, sync, lmi, lmr) in cfgs.items():
             ctx.set_option(OPT_GEMM_SYNC, sync)
+            ctx.set_option(OPT_LMHEAD_IMPL, lmi)
+            ctx.set_option(OPT_LMHEAD_RASTER, lmr)
             ctx.set_option(OPT_LMHEAD_BWD_GEMM, impl)
             ctx.set_option(OPT_GEMM_GROUP_M, gm)
             ctx.set_option(OPT_GEMM_HINTS, hints)

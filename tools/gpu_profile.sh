@@ -29,5 +29,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_u
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_lmhead_dz" -s 0 -c 1 -o gpurun_out/prof_lmdz python tools/lmhead_bwd_once.py 4096 8192 0 > gpurun_out/ncu_lmdz.log 2>&1; echo "ncu lmdz exit=$?"
 # summarise on the box (ncu reports are large): the profiles/ tree comes back under gpurun_out/
 python tools/make_profiles.py $TAG > gpurun_out/make_profiles.log 2>&1; echo "make_profiles exit=$?"
-mkdir -p gpurun_out/raw_$TAG && cp gpurun_out/*.ncu-rep gpurun_out/raw_$TAG/ 2>/dev/null
+du -sh gpurun_out; ls -la gpurun_out/*.ncu-rep 2>/dev/null | head -20
 rm -rf gpurun_out/profiles_new && cp -r profiles gpurun_out/profiles_new && rm -f gpurun_out/*.ncu-rep
+find gpurun_out -type f -size +20M -print -delete

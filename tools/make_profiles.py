@@ -161,11 +161,7 @@ def main(tag, out_dir="gpurun_out"):
                 launch_table.main(lp, 20.0)
             shutil.copy(lp, os.path.join(dst, ll_name + ".csv"))
             open(os.path.join(dst, ll_name + ".md"), "w").write(
-                f"# {title}
-
-```
-" + buf.getvalue() + "```
-")
+                f"# {title}\n\n```\n" + buf.getvalue() + "```\n")
     for f in ("bench_full.json", "bench_full.err", "gpu_tests.log", "smoke.log", "bench_tp8.json",
               "bench_C4_strong_verify.json", "bench_lmhead_bwd_dense.json",
               "bench_lmhead_bwd_realistic.json", "gemm_sweep.json"):
