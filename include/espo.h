@@ -522,7 +522,8 @@ typedef enum {
                                   / _PARTS apply) */
   ESPO_OPT_LMHEAD_RASTER = 14  /* impl 0: bits 0-15 = M-tiles per raster group (0 = auto: 32 at
                                   d ≤ 4096, 64 above), bits
-                                  16-23 = L2 policies (A | B << 2, 1 evict_first, 2 evict_last) */
+                                  16-23 = L2 policies (A | B << 2, 1 evict_first, 2 evict_last),
+                                  bit 24 = 256 × 256 tiles (double-buffered) instead of 256 × 512 */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

@@ -153,6 +153,8 @@ struct espo_ctx_s {
   int lmh_impl = 0;              // LM-head fwd / dz: 0 = on the tcgen05 GEMM core (k_gemm.cuh),
                                  // 1 = the dedicated kernels (k_lmhead*.cuh)
   uint8_t* lmh_live = nullptr;   // per 256-row block liveness (fwd on the GEMM core)
+  int lmh_tile256 = 0;           // LM-head GEMM-core tiles: 0 = 256 × 512 (one accumulator),
+                                 // 1 = 256 × 256 (double-buffered, epilogue overlapped)
   int lmh_group_m = 0, lmh_hints = 0;   // LM-head fwd / dz on the GEMM core: raster (0 = auto),
                                         // L2 policies
   size_t lmh_live_cap = 0;
@@ -497,6 +499,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       if (value < 0 || (value & 0xFFFF) > 1024) return ESPO_ERR_INVALID_ARGUMENT;
       c->lmh_group_m = int(value & 0xFFFF);
       c->lmh_hints = int((value >> 16) & 0xFF);
+      c->lmh_tile256 = int((value >> 24) & 1);
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_IMPL:
       if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
@@ -969,9 +972,9 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
       p.sync = static_cast<unsigned*>(c->gemm_sync);
     }
     if (kind == 2)
-      k_umma_gemm2<kAMN, kBMN, kOut, 512><<<2 * clusters, kGmThreads, G2<512>::kSmem, s>>>(ma, mb, p);
+      k_umma_gemm2<kAMN, kBMN, kOut, 512><<<2 * clusters, kG2Threads, G2<512>::kSmem, s>>>(ma, mb, p);
     else
-      k_umma_gemm2<kAMN, kBMN, kOut, 256><<<2 * clusters, kGmThreads, G2<256>::kSmem, s>>>(ma, mb, p);
+      k_umma_gemm2<kAMN, kBMN, kOut, 256><<<2 * clusters, kG2Threads, G2<256>::kSmem, s>>>(ma, mb, p);
   } else {
     ESPO_CUDA(ensure_smem_attr(k_umma_gemm<kAMN, kBMN, kOut>, int(kGmSmem), attr));
     const int grid = int(std::min<int64_t>(tiles, c->num_sms));
@@ -1018,7 +1021,8 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
     // on the tcgen05 GEMM core: CTA-pair 256 × 512 tiles of z = h·Wᵀ in a grouped raster, each
     // tile's rows reduced to a partial {R, S, W, u_y} (k_gemm.cuh kOutLmFwd), then merged over
     // the tiles like vocabulary shards; M-tiles without a valid row are skipped
-    const int nt = (V + 511) / 512;
+    const int tw = c->lmh_tile256 ? 256 : 512;
+    const int nt = 2 * ((V + tw - 1) / tw);   // one partial per (tile, column half)
     const int nlive = int((n_rows + 255) / 256);
     const size_t needp = size_t(nt) * size_t(n_rows) * 16;
     if (needp > c->lmh_cap) {
@@ -1052,8 +1056,9 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
     lm.V = V;
     lm.n_rows = int(n_rows);
     lm.err = c->ws.err;
-    st = launch_umma_gemm<false, false, kOutLmFwd>(c, mh, mw, int(n_rows), V, d, nullptr, 0, 2,
-                                                   lmh_raster(c, d), c->lmh_hints, s, GemmDyn(), &lm);
+    st = launch_umma_gemm<false, false, kOutLmFwd>(c, mh, mw, int(n_rows), V, d, nullptr, 0,
+                                                   c->lmh_tile256 ? 1 : 2, lmh_raster(c, d),
+                                                   c->lmh_hints, s, GemmDyn(), &lm);
     if (st != ESPO_OK) return st;
     {
       const int grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
@@ -1242,7 +1247,8 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
         dz_dyn.which = 3;
       }
       const espo_status st = launch_umma_gemm<false, false, kOutLmDz>(
-          c, mh, mw_k128, n, int(ldz), d, nullptr, 0, 2, lmh_raster(c, d), c->lmh_hints, s, dz_dyn, &lm);
+          c, mh, mw_k128, n, int(ldz), d, nullptr, 0, c->lmh_tile256 ? 1 : 2, lmh_raster(c, d),
+          c->lmh_hints, s, dz_dyn, &lm);
       if (st != ESPO_OK) return st;
     } else if (c->lmh_2cta) {
       k_lmhead2_dz<<<dim3(2 * parts, (mblocks + 1) / 2), kLmThreads, kL2Smem, s>>>(mh, mw, lp);

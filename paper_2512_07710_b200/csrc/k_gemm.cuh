@@ -36,6 +36,8 @@ constexpr int kGmBBytes = kGmBN * kGmBK * 2;    // 32 KB
 constexpr int kGmStageBytes = kGmABytes + kGmBBytes;
 constexpr int kGmMNBox = 64 * kGmBK * 2;        // one MN-major TMA box {64 MN, 64 K}: 8 KB
 constexpr int kGmThreads = 192;
+constexpr int kG2Threads = 320;   // CTA-pair kernel: producer, MMA, 8 epilogue warps (two per
+                                  // TMEM lane quarter, each draining half of the tile's columns)
 constexpr size_t kGmSmem = size_t(kGmStages) * kGmStageBytes + 1024 + 256;
 
 enum GemmOut { kOutF32 = 0, kOutBF16 = 1, kOutAddF32 = 2, kOutLmFwd = 3, kOutLmDz = 4 };
@@ -219,9 +221,9 @@ __host__ __device__ constexpr uint32_t gemm_idesc() {
 // C[r, n0 + …] as fp32, bf16 or fp32 read-add-write; rows ≥ M and columns ≥ N skipped.
 template <int kOut>
 __device__ __forceinline__ void gemm_store_tile(const GemmParams& p, uint32_t base, int r, int n0,
-                                                uint64_t pol_c) {
+                                                uint64_t pol_c, int nchunk = kGmBN / 32) {
 #pragma unroll 1
-  for (int c = 0; c < kGmBN / 32; ++c) {
+  for (int c = 0; c < nchunk; ++c) {
     float x[32];
     __syncwarp();
     tmem_ld32(base + uint32_t(c * 32), x);
@@ -277,9 +279,9 @@ __device__ __forceinline__ void gemm_store_tile(const GemmParams& p, uint32_t ba
 // Forward: (R, S, W, cS, cW, uy) carry across the calls for the tile's halves.
 __device__ __forceinline__ void lm_fwd_cols(const GemmParams& p, uint32_t base, int r, int n0,
                                             float& R, float& S, float& W, float& cS, float& cW,
-                                            float& uy, bool valid, int y) {
+                                            float& uy, bool valid, int y, int nchunk) {
 #pragma unroll 1
-  for (int c = 0; c < 256 / 32; ++c) {
+  for (int c = 0; c < nchunk; ++c) {
     float x[32];
     __syncwarp();
     tmem_ld32(base + uint32_t(c * 32), x);
@@ -289,9 +291,9 @@ __device__ __forceinline__ void lm_fwd_cols(const GemmParams& p, uint32_t base, 
   }
 }
 __device__ __forceinline__ void lm_dz_cols(const GemmParams& p, uint32_t base, int r, int n0,
-                                           const BwdRec& rc) {
+                                           const BwdRec& rc, int nchunk) {
 #pragma unroll 1
-  for (int c = 0; c < 256 / 32; ++c) {
+  for (int c = 0; c < nchunk; ++c) {
     float x[32];
     __syncwarp();
     tmem_ld32(base + uint32_t(c * 32), x);
@@ -476,7 +478,7 @@ __device__ __forceinline__ void gm_wait_cluster(uint32_t bar, uint32_t parity) {
 }
 
 template <bool kAMN, bool kBMN, int kOut, int kNP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
     k_umma_gemm2(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                  const GemmParams p0) {
   using C = G2<kNP>;
@@ -507,7 +509,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * kGmBM);
+      mbar_init(&tempty[a], 2 * (kG2Threads - 64));   // every epilogue thread of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -611,6 +613,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
     // ------------------------------------------------------------------ epilogue
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
+    const int chalf = (warp - 2) >> 2;                 // which half of the tile's columns
+    constexpr int kCols = kNP / 2, kChunks = kCols / 32;
     const uint64_t pol_c = l2_policy(p.hint_c);
     const uint32_t leader_tempty0 = mapa_rank(smem_u32(&tempty[0]), 0);
     const uint32_t leader_tempty1 = mapa_rank(smem_u32(&tempty[1]), 0);
@@ -624,29 +628,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGmThreads, 1)
       ++i;
       gm_wait_cluster(smem_u32(&tfull[acc]), use & 1u);
       tc_fence_after();
-      const uint32_t base = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kGmBN);
+      const uint32_t base = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kGmBN) +
+                            uint32_t(chalf * kCols);
       const int r = mb * 2 * kGmBM + int(rank) * kGmBM + row;
+      const int c0 = nb * kNP + chalf * kCols;         // first tile column this thread drains
       if constexpr (kOut == kOutLmFwd) {
         const bool valid = r < p.M && p.lm.flag[r];
         const int y = valid ? p.lm.tokens[r] : -1;
         float R = -INFINITY, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f, uy = __int_as_float(0x7fc00000);
-#pragma unroll 1
-        for (int hh = 0; hh < kNP / 256; ++hh)
-          lm_fwd_cols(p, base + uint32_t(hh * 256), r, nb * kNP + hh * 256, R, S, W, cS, cW, uy,
-                      valid, y);
-        if (valid) p.lm.partial[int64_t(nb) * p.lm.n_rows + r] = make_float4(R, S - cS, W - cW, uy);
+        lm_fwd_cols(p, base, r, c0, R, S, W, cS, cW, uy, valid, y, kChunks);
+        if (valid)        // one partial per (tile, column half): partial[2·nb + half][row]
+          p.lm.partial[int64_t(2 * nb + chalf) * p.lm.n_rows + r] = make_float4(R, S - cS, W - cW, uy);
       } else if constexpr (kOut == kOutLmDz) {
         BwdRec rc;
         rc.ng = 0.f;
         rc.y = -1;
         if (r < p.M) rc = p.lm.rec[r];
-#pragma unroll 1
-        for (int hh = 0; hh < kNP / 256; ++hh)
-          lm_dz_cols(p, base + uint32_t(hh * 256), r, nb * kNP + hh * 256, rc);
+        lm_dz_cols(p, base, r, c0, rc, kChunks);
       } else {
-#pragma unroll 1
-        for (int hh = 0; hh < kNP / 256; ++hh)
-          gemm_store_tile<kOut>(p, base + uint32_t(hh * 256), r, nb * kNP + hh * 256, pol_c);
+        gemm_store_tile<kOut>(p, base, r, c0, pol_c, kChunks);
       }
       __syncwarp();
       tc_fence_before();

@@ -43,11 +43,10 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1):
         "cublas": (1, 0, -1, 0, 0, 1, 0),
         "default": (0, 0, -1, 1, 0, 0, 0),
         "dz_dedicated": (0, 0, -1, 1, 0, 1, 0),
+        "dz_t256_g32": (0, 0, -1, 1, 0, 0, 32 | (1 << 24)),
+        "dz_t256_g64": (0, 0, -1, 1, 0, 0, 64 | (1 << 24)),
         "dz_g16": (0, 0, -1, 1, 0, 0, 16),
-        "dz_g32": (0, 0, -1, 1, 0, 0, 32),
         "dz_g64": (0, 0, -1, 1, 0, 0, 64),
-        "dz_g32_dw512_gn2": (4, G(0, 2), -1, 1, 0, 0, 32),
-        "dz_g32_dw_gn8": (0, G(0, 8), -1, 1, 0, 0, 32),
     }
     times = {k: [] for k in cfgs}
     for _ in range(rounds):
