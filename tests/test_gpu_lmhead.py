@@ -351,3 +351,56 @@ def test_lmhead_bwd_compaction_equals_all_rows(gemm, sub):
     lim = T * 2.0 ** -23 * (np.abs(w0).max() + 1e-30) + 2.0 ** -22 * np.abs(w0)
     assert np.all(np.abs(w1 - w0) <= lim + T * 2.0 ** -24 * ha.max())
     assert np.linalg.norm(w1 - w0) <= 1e-5 * np.linalg.norm(w0)
+
+
+@pytest.mark.parametrize("kern", ["gemm", "1cta"])
+def test_lmhead_degenerate_shapes(kern):
+    """Edge cases of the GEMM-core LM head: every row of a zero-variance group (no live M-tile,
+    no row with gradient: dh = 0, dW unchanged, loss 0), a single row, V smaller than one
+    512-column tile, d = 8 (one K-step, mostly zero-filled by TMA), rows not a multiple of 256."""
+    dev = require_cuda()
+    # all rows eliminated
+    V, d, G, L = 700, 64, 4, 33
+    case = make_case(31, 1, G, L, V, d, zv_group=0)
+    T = case["T"]
+    ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
+    set_kernel(ctx, kern)
+    ctx.prepare(to_dev(case["rewards"], torch.float32, dev), to_dev(case["group_ids"], torch.int32, dev),
+                to_dev(case["so"], torch.int64, dev), n_tokens=T)
+    h = to_dev(case["h"], torch.bfloat16, dev)
+    W = to_dev(case["W"], torch.bfloat16, dev)
+    ctx.lmhead_fwd(h, W, to_dev(case["tokens"], torch.int32, dev), to_dev(case["old"], torch.float32, dev))
+    loss, st = ctx.loss_finalize()
+    dW = torch.full((V, d), 0.5, dtype=torch.float32, device=dev)
+    dh, _ = ctx.lmhead_bwd(h, W, None, dW)
+    ctx.get_error()
+    assert float(loss.item()) == 0.0 and stats_to_dict(st)["n_active_rollouts"] == 0
+    assert not torch.any(dh) and torch.all(dW == 0.5)
+    ctx.close()
+    # tiny shapes against the oracle: one 2-rollout group of 1-token rollouts at d = 8, and
+    # 3 × 37 rows with V = 300 (< one tile)
+    for (ng, G, L, V, d) in ((1, 2, 1, 300, 8), (1, 3, 37, 300, 40)):
+        case = make_case(37, ng, G, L, V, d)
+        case["mask"][:] = 1
+        T = case["T"]
+        ctx = Espo(V, logits_dtype=torch.float32, device=dev.index)
+        set_kernel(ctx, kern)
+        ctx.prepare(to_dev(case["rewards"], torch.float32, dev), to_dev(case["group_ids"], torch.int32, dev),
+                    to_dev(case["so"], torch.int64, dev), n_tokens=T)
+        h = to_dev(case["h"], torch.bfloat16, dev)
+        W = to_dev(case["W"], torch.bfloat16, dev)
+        ctx.lmhead_fwd(h, W, to_dev(case["tokens"], torch.int32, dev), to_dev(case["old"], torch.float32, dev),
+                       to_dev(case["mask"], torch.uint8, dev))
+        loss, _ = ctx.loss_finalize()
+        dW = torch.zeros((V, d), dtype=torch.float32, device=dev)
+        dh, _ = ctx.lmhead_bwd(h, W, None, dW)
+        ctx.get_error()
+        ctx.close()
+        cfg = oracle_cfg(V)
+        ref = O.espo_loss(case["z64"], case["tokens"], case["old"], case["mask"], case["rewards"],
+                          case["group_ids"], case["so"], cfg)
+        assert float(loss.item()) == pytest.approx(ref.loss, rel=1e-4, abs=1e-6)
+        _, dh_ref, dW_ref = O.lmhead_grads(ref, case["h"], case["W"], case["tokens"], cfg)
+        got_h, got_w = dh.cpu().numpy().astype(np.float64), dW.cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(got_h - dh_ref) <= 5e-3 * np.linalg.norm(dh_ref) + 1e-12
+        assert np.linalg.norm(got_w - dW_ref) <= 5e-3 * np.linalg.norm(dW_ref) + 1e-12
