@@ -57,8 +57,9 @@ def parse():
                         "over the ranks by prompt group (LPT)")
     p.add_argument("--verify", action="store_true",
                    help="untimed extra pass: order-independent digest of every dlogits row")
-    p.add_argument("--drift-seq", type=float, default=0.04,
-                   help="std of the per-rollout log-prob drift of the rollout engine")
+    p.add_argument("--drift-seq", type=float, default=0.01,
+                   help="std of the per-rollout log-prob drift of the rollout engine (SURVEY "
+                        "§8(d) recipe: b_i ~ N(0, 0.01))")
     p.add_argument("--drift-tok", type=float, default=0.02,
                    help="std of the per-token log-prob drift")
     p.add_argument("--steps", type=int, default=5)
@@ -230,7 +231,7 @@ def group_chunks(local_so, local_gid, Rc):
 
 
 def make_batch(w, seed, dev, buffer_rows, log, single_pass=False, shard=None,
-               drift=(0.04, 0.02)):
+               drift=(0.01, 0.02)):
     """Device-resident synthetic batch: chunk buffer + per-token arrays. shard = (world,
     rank): strong scaling, this rank's groups of the global batch (seed shared by all ranks)."""
     import torch
