@@ -1061,7 +1061,7 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
                                                    c->lmh_hints, s, GemmDyn(), &lm);
     if (st != ESPO_OK) return st;
     {
-      const int grid = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+      const int grid = static_cast<int>(std::min<int64_t>((n_rows + 7) / 8, int64_t(c->num_sms) * 16));
       k_fwd_combine64<<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(c->lmh_partial), nt,
                                            row_begin, n_rows, c->ws);
       ESPO_LAUNCHED(c);

@@ -170,33 +170,48 @@ __global__ void __launch_bounds__(256) k_fwd_combine(const float4* partials, int
   }
 }
 
-// The same merge for many partials per row (the LM head on the GEMM core: one per 512-column
-// vocabulary tile, ~300 at V = 151,936): the rebased sums accumulate in fp64, one rounding at
-// the end, so the merge adds no error that grows with the tile count.
+// The same merge for many partials per row (the LM head on the GEMM core: two per 512-column
+// vocabulary tile, ~600 at V = 151,936): one warp per row with the lanes striding over the
+// partials (a thread per row left most SMs idle: 315 µs per 8192 rows), the rebased terms
+// 2^(R_k − R)·S_k summed in fp64 (one rounding at the end: no error growth with the count).
 __global__ void __launch_bounds__(256) k_fwd_combine64(const float4* partials, int n_shards,
                                                        int64_t row_begin, int64_t n_rows,
                                                        Workspace ws) {
-  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows;
-       r += int64_t(gridDim.x) * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n_rows; r += nw) {
     const int64_t t = row_begin + r;
-    if (!ws.flag[t]) continue;
+    if (!ws.flag[t]) continue;                       // warp-uniform
     float R = -INFINITY, uy = __int_as_float(0x7fc00000);
-    for (int k = 0; k < n_shards; ++k) {
+    for (int k = lane; k < n_shards; k += 32) {
       const float4 a = partials[int64_t(k) * n_rows + r];
       R = fmaxf(R, a.x);
       if (!isnan(a.w)) uy = a.w;
     }
+    R = warp_max(R);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {             // the one owner's u_y to every lane
+      const float u = __shfl_xor_sync(0xffffffffu, uy, o);
+      if (isnan(uy)) uy = u;
+    }
     double S = 0.0, W = 0.0;
-    for (int k = 0; k < n_shards; ++k) {
+    for (int k = lane; k < n_shards; k += 32) {
       const float4 a = partials[int64_t(k) * n_rows + r];
       if (a.x == -INFINITY || (a.y == 0.f && a.z == 0.f)) continue;
-      const double dd = double(a.x) - double(R);          // ≤ 0
-      const double sc = exp2(dd);
-      W += sc * (dd * double(a.y) + double(a.z));
-      S += sc * double(a.y);
+      const float d = a.x - R;                       // ≤ 0
+      const float sc = ex2(d);
+      W += double(sc) * (double(d) * double(a.y) + double(a.z));
+      S += double(sc) * double(a.y);
     }
-    if (isnan(uy)) set_error(ws.err, ESPO_ERR_INVALID_ARGUMENT);  // no tile holds the target
-    finish_stats(R, float(S), float(W), uy, ws, t);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      S += __shfl_xor_sync(0xffffffffu, S, o);
+      W += __shfl_xor_sync(0xffffffffu, W, o);
+    }
+    if (lane == 0) {
+      if (isnan(uy)) set_error(ws.err, ESPO_ERR_INVALID_ARGUMENT);  // no tile holds the target
+      finish_stats(R, float(S), float(W), uy, ws, t);
+    }
   }
 }
 
