@@ -404,3 +404,50 @@ def test_lmhead_degenerate_shapes(kern):
         got_h, got_w = dh.cpu().numpy().astype(np.float64), dW.cpu().numpy().astype(np.float64)
         assert np.linalg.norm(got_h - dh_ref) <= 5e-3 * np.linalg.norm(dh_ref) + 1e-12
         assert np.linalg.norm(got_w - dW_ref) <= 5e-3 * np.linalg.norm(dW_ref) + 1e-12
+
+
+@pytest.mark.parametrize("kern", ["gemm", "1cta"])
+def test_lmhead_rlzvp_mode_matches_logits_path(kern):
+    """RL-ZVP (zero-variance groups read, entropy-guided advantages): the fused LM head reads
+    the ZV rows too (their M-tiles are live) and gives the logits path's statistics, loss and
+    gradients (dh, dW within the bf16-dz bound)."""
+    from paper_2512_07710_b200.espo import ZV_RLZVP
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dev = require_cuda()
+    V, d = 3004, 256            # fp32 logits rows of the unfused path: 16-byte pitch
+    case = make_case(41, 3, 4, 40, V, d, zv_group=1)
+    T = case["T"]
+    outs = {}
+    for fused in (True, False):
+        ctx = Espo(V, logits_dtype=torch.float32, device=dev.index, zv_mode=ZV_RLZVP, zvp_beta=0.2)
+        set_kernel(ctx, kern)
+        tok = to_dev(case["tokens"], torch.int32, dev)
+        old = to_dev(case["old"], torch.float32, dev)
+        mask = to_dev(case["mask"], torch.uint8, dev)
+        ctx.prepare(to_dev(case["rewards"], torch.float32, dev), to_dev(case["group_ids"], torch.int32, dev),
+                    to_dev(case["so"], torch.int64, dev), n_tokens=T)
+        h = to_dev(case["h"], torch.bfloat16, dev)
+        W = to_dev(case["W"], torch.bfloat16, dev)
+        if fused:
+            ctx.lmhead_fwd(h, W, tok, old, mask)
+            loss, st = ctx.loss_finalize()
+            dW = torch.zeros((V, d), dtype=torch.float32, device=dev)
+            dh, _ = ctx.lmhead_bwd(h, W, None, dW)
+        else:
+            z = (h.float() @ W.float().T).contiguous()
+            ctx.loss_fwd(z, tok, old, mask)
+            loss, st = ctx.loss_finalize()
+            dz = ctx.loss_bwd(z)
+            dh = dz @ W.float()
+            dW = dz.T @ h.float()
+        ctx.get_error()
+        outs[fused] = (float(loss.item()), stats_to_dict(st), dh.cpu().numpy().astype(np.float64),
+                       dW.cpu().numpy().astype(np.float64),
+                       {k: v.cpu().numpy() for k, v in ctx.export_token_stats().items()})
+        ctx.close()
+    (lf, sf, hf, wf, tf), (lu, su, hu, wu, tu) = outs[True], outs[False]
+    assert sf["n_zv_groups"] == 1 and sf["n_active_rollouts"] == su["n_active_rollouts"] == 12
+    assert np.array_equal(tf["valid"], tu["valid"])
+    assert lf == pytest.approx(lu, rel=2e-3, abs=1e-6)
+    assert np.linalg.norm(hf - hu) <= 4e-3 * np.linalg.norm(hu)
+    assert np.linalg.norm(wf - wu) <= 4e-3 * np.linalg.norm(wu)
