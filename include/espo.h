@@ -504,6 +504,8 @@ typedef enum {
                                   tcgen05 GEMM: 0 = CTA pairs, 256 × 512 tiles for dh (long K) and
                                   256 × 256 for dW (default); 2 = one CTA per 128 × 256 tile;
                                   3 = pairs 256 × 256 for both; 4 = pairs 256 × 512 for both;
+                                  5 = 4-CTA clusters (two pairs sharing A by TMA multicast,
+                                  256 × 512 each) for both; 6 = those for dh, default dW;
                                   1 = cuBLAS (A/B measurement only) */
   ESPO_OPT_GEMM_GROUP_M = 9,   /* backward GEMM tile order: bits 0-15 = dh M-blocks per raster
                                   group (0 = auto, 8); bits 16-31 = dW N-blocks per group (0 = all
@@ -523,7 +525,8 @@ typedef enum {
   ESPO_OPT_LMHEAD_RASTER = 14  /* impl 0: bits 0-15 = M-tiles per raster group (0 = auto: 32 at
                                   d ≤ 4096, 64 above), bits
                                   16-23 = L2 policies (A | B << 2, 1 evict_first, 2 evict_last),
-                                  bit 24 = 256 × 256 tiles (double-buffered) instead of 256 × 512 */
+                                  bit 24 = 256 × 256 tiles (double-buffered) instead of 256 × 512,
+                                  bit 25 = 4-CTA clusters (two pairs sharing A by TMA multicast) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

@@ -153,6 +153,7 @@ struct espo_ctx_s {
   int lmh_impl = 0;              // LM-head fwd / dz: 0 = on the tcgen05 GEMM core (k_gemm.cuh),
                                  // 1 = the dedicated kernels (k_lmhead*.cuh)
   uint8_t* lmh_live = nullptr;   // per 256-row block liveness (fwd on the GEMM core)
+  int lmh_mcast = 0;             // LM-head GEMM core on 4-CTA clusters (A multicast to two pairs)
   int lmh_tile256 = 0;           // LM-head GEMM-core tiles: 0 = 256 × 512 (one accumulator),
                                  // 1 = 256 × 256 (double-buffered, epilogue overlapped)
   int lmh_group_m = 0, lmh_hints = 0;   // LM-head fwd / dz on the GEMM core: raster (0 = auto),
@@ -482,7 +483,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->factored_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_BWD_GEMM:
-      if (value < 0 || value > 4) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 6) return ESPO_ERR_INVALID_ARGUMENT;
       c->lmh_bwd_gemm = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_GEMM_HINTS:     // low 8 bits: dh, next 8 bits: dW (each A | B<<2 | C<<4); −1 auto
@@ -500,6 +501,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->lmh_group_m = int(value & 0xFFFF);
       c->lmh_hints = int((value >> 16) & 0xFF);
       c->lmh_tile256 = int((value >> 24) & 1);
+      c->lmh_mcast = int((value >> 25) & 1);
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_IMPL:
       if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
@@ -912,6 +914,37 @@ int lmh_raster(const espo_ctx_s* c, int d) {
   return c->lmh_group_m > 0 ? c->lmh_group_m : (d > 4096 ? 64 : 32);
 }
 
+// Clusters of `csize` CTAs (one per SM at this smem size) that can be resident at once: a
+// persistent grid must not exceed it — a cluster that is not resident only starts when a
+// resident one exits, i.e. after the whole tile loop (GPCs whose SM count is not a multiple
+// of the cluster size leave SMs idle). Cached per kernel; falls back to SMs / csize.
+template <typename K>
+int max_resident_clusters(K kernel, int csize, int threads, size_t smem, int num_sms,
+                          int& cache) {
+  if (cache > 0) return cache;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(csize * (num_sms / csize)), 1, 1);
+  cfg.blockDim = dim3(unsigned(threads), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = unsigned(csize);
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = num_sms / csize;
+  }
+  cache = std::min(n, num_sms / csize);
+  if (std::getenv("ESPO_DEBUG"))
+    std::fprintf(stderr, "[libespo] resident clusters of %d CTAs (%zu B smem): %d (SMs %d)\n",
+                 csize, smem, cache, num_sms);
+  return cache;
+}
+
 struct GemmDyn {          // device-side row count of compacted operands (k_compact.cuh)
   const int* count = nullptr;
   int base = 0, which = 0;   // which: 1 = M, 2 = K
@@ -923,10 +956,11 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
                              int N, int64_t K, void* C, int64_t ldc, int kind, int group_m,
                              int hints, cudaStream_t s, const GemmDyn& dyn = GemmDyn(),
                              const LmEpi* lm = nullptr) {
-  // kind: 0 = one CTA per 128 × 256 tile, 1 = CTA pair 256 × 256, 2 = CTA pair 256 × 512
-  static unsigned long long attr = 0, attr2 = 0, attr3 = 0;
+  // kind: 0 = one CTA per 128 × 256 tile, 1 = CTA pair 256 × 256, 2 = CTA pair 256 × 512,
+  // 3 = two CTA pairs per cluster sharing A by multicast, 256 × 512 tiles each
+  static unsigned long long attr = 0, attr2 = 0, attr3 = 0, attr4 = 0;
   const bool pair = kind != 0;
-  const int tn = kind == 2 ? 512 : kGmBN;
+  const int tn = (kind == 2 || kind == 3) ? 512 : kGmBN;
   GemmParams p;
   p.lm = lm ? *lm : LmEpi{};
   if ((kOut == kOutLmFwd || kOut == kOutLmDz) && kind == 0) return ESPO_ERR_INVALID_ARGUMENT;
@@ -955,10 +989,22 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
   p.sync_chunk = std::max(1, c->gemm_sync_chunk);
   p.sync_slack = std::max(1, c->gemm_sync_slack);
   p.sync_timeout_ns = 200000;
-  if (pair) {
+  static int res2 = 0, res3 = 0, res4 = 0;   // resident clusters per kernel (this process's GPU)
+  if (kind == 3) {
+    ESPO_CUDA(ensure_smem_attr(k_umma_gemm4<kAMN, kBMN, kOut, 512>, int(G2<512>::kSmem), attr4));
+    const int64_t super = int64_t(p.mblk) * ((p.nblk + 1) / 2);
+    const int clusters = int(std::min<int64_t>(
+        super, max_resident_clusters(k_umma_gemm4<kAMN, kBMN, kOut, 512>, 4, kG2Threads,
+                                     G2<512>::kSmem, c->num_sms, res4)));
+    k_umma_gemm4<kAMN, kBMN, kOut, 512><<<4 * clusters, kG2Threads, G2<512>::kSmem, s>>>(ma, mb, p);
+  } else if (pair) {
     if (kind == 2) ESPO_CUDA(ensure_smem_attr(k_umma_gemm2<kAMN, kBMN, kOut, 512>, int(G2<512>::kSmem), attr3));
     else ESPO_CUDA(ensure_smem_attr(k_umma_gemm2<kAMN, kBMN, kOut, 256>, int(G2<256>::kSmem), attr2));
-    const int clusters = int(std::min<int64_t>(tiles, c->num_sms / 2));
+    const int clusters = int(std::min<int64_t>(
+        tiles, kind == 2 ? max_resident_clusters(k_umma_gemm2<kAMN, kBMN, kOut, 512>, 2, kG2Threads,
+                                                 G2<512>::kSmem, c->num_sms, res3)
+                         : max_resident_clusters(k_umma_gemm2<kAMN, kBMN, kOut, 256>, 2, kG2Threads,
+                                                 G2<256>::kSmem, c->num_sms, res2)));
     if (c->gemm_sync_chunk > 0) {              // one zeroed progress counter per wave
       const int64_t waves = (tiles + clusters - 1) / clusters;
       if (size_t(waves) * 4 > c->gemm_sync_cap) {
@@ -1057,8 +1103,8 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
     lm.n_rows = int(n_rows);
     lm.err = c->ws.err;
     st = launch_umma_gemm<false, false, kOutLmFwd>(c, mh, mw, int(n_rows), V, d, nullptr, 0,
-                                                   c->lmh_tile256 ? 1 : 2, lmh_raster(c, d),
-                                                   c->lmh_hints, s, GemmDyn(), &lm);
+                                                   c->lmh_tile256 ? 1 : c->lmh_mcast ? 3 : 2,
+                                                   lmh_raster(c, d), c->lmh_hints, s, GemmDyn(), &lm);
     if (st != ESPO_OK) return st;
     {
       const int grid = static_cast<int>(std::min<int64_t>((n_rows + 7) / 8, int64_t(c->num_sms) * 16));
@@ -1247,8 +1293,8 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
         dz_dyn.which = 3;
       }
       const espo_status st = launch_umma_gemm<false, false, kOutLmDz>(
-          c, mh, mw_k128, n, int(ldz), d, nullptr, 0, c->lmh_tile256 ? 1 : 2, lmh_raster(c, d),
-          c->lmh_hints, s, dz_dyn, &lm);
+          c, mh, mw_k128, n, int(ldz), d, nullptr, 0, c->lmh_tile256 ? 1 : c->lmh_mcast ? 3 : 2,
+          lmh_raster(c, d), c->lmh_hints, s, dz_dyn, &lm);
       if (st != ESPO_OK) return st;
     } else if (c->lmh_2cta) {
       k_lmhead2_dz<<<dim3(2 * parts, (mblocks + 1) / 2), kLmThreads, kL2Smem, s>>>(mh, mw, lp);
@@ -1272,8 +1318,8 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       // N-groups of 8 blocks; d = 8192 → 512-wide pair tiles in N-groups of 2)
       const int g = c->lmh_bwd_gemm;
       const bool wide_dw = d > 4096;
-      const int kind_dh = g == 2 ? 0 : g == 3 ? 1 : 2;
-      const int kind_dw = g == 2 ? 0 : g == 3 ? 1 : g == 4 ? 2 : (wide_dw ? 2 : 1);
+      const int kind_dh = g == 2 ? 0 : g == 3 ? 1 : (g == 5 || g == 6) ? 3 : 2;
+      const int kind_dw = g == 2 ? 0 : g == 3 ? 1 : g == 4 ? 2 : g == 5 ? 3 : (wide_dw ? 2 : 1);
       // tile order: dh has a long K (the vocabulary) and few tiles: groups of 8 M-blocks keep
       // the resident tiles' A and B panels small; dW (K = rows): N fastest, so every M-block
       // of dz is read once while h stays in L2

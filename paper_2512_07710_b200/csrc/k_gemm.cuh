@@ -477,15 +477,40 @@ __device__ __forceinline__ void gm_wait_cluster(uint32_t bar, uint32_t parity) {
   }
 }
 
-template <bool kAMN, bool kBMN, int kOut, int kNP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
-    k_umma_gemm2(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                 const GemmParams p0) {
+// Multicast A: the same A K-slice (rows of one pair's M-tile) lands in the CTAs of `mask`
+// (one CTA per pair); each destination pair's leader barrier collects the bytes (the barrier
+// operand is the issuing pair leader's, peer bit 0 — the 2-SM multicast form).
+__device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, int c0,
+                                                    int c1, uint32_t leader_bar, uint16_t mask,
+                                                    uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "h"(mask), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+// tcgen05.commit of the pair's MMAs to the barrier at this offset in every CTA of `mask`
+__device__ __forceinline__ void tc_commit_mask(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar), "h"(mask)
+      : "memory");
+}
+
+// kPairs = CTA pairs per cluster: 1, or 2 — the two pairs compute the tiles (m, 2j) and
+// (m, 2j + 1), share the A K-slices through TMA multicast (half the A traffic from L2, and the
+// pairs move in lockstep: a stage is refilled only when both consumed it).
+template <bool kAMN, bool kBMN, int kOut, int kNP, int kPairs>
+__device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUtensorMap& tmap_b,
+                                           const GemmParams& p0) {
   using C = G2<kNP>;
   constexpr int kG2Stages = C::kStages, kG2ABytes = C::kABytes, kG2BBytes = C::kBBytes;
   constexpr int kG2StageBytes = C::kStageBytes;
   const GemmParams p = gemm_effective(p0, 2 * kGmBM);
   if (p.mblk * p.nblk == 0 || p.kblk == 0) return;   // nothing to add (uniform in the grid)
+  // super-tiles of kPairs N-blocks (pair `pair` takes N-block nbp·kPairs + pair)
+  GemmParams ps = p;
+  ps.nblk = (p.nblk + kPairs - 1) / kPairs;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -497,15 +522,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const uint32_t rank = cluster_rank();
+  const uint32_t crank = cluster_rank();
+  const uint32_t rank = crank & 1u, pair = crank >> 1, leader = crank & ~1u;
+  const uint16_t pair_mask = uint16_t(3u << (2 * pair));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-  const int tiles = p.mblk * p.nblk;
+  const int cluster = blockIdx.x / (2 * kPairs), nclusters = gridDim.x / (2 * kPairs);
+  const int tiles = ps.mblk * ps.nblk;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kG2Stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kPairs);                 // every pair's commit frees the stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -533,7 +560,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
       int wave = 0;
       for (int tile = cluster; tile < tiles; tile += nclusters, ++wave) {
         int mb, nb;
-        gemm_tile_coords(p, tile, mb, nb);
+        gemm_tile_coords(ps, tile, mb, nb);
+        nb = nb * kPairs + int(pair);
         if (p.lm.mlive && !p.lm.mlive[mb]) continue;     // no row to compute: skipped tile
         const int m0 = mb * 2 * kGmBM + int(rank) * kGmBM;
         const int n0 = nb * kNP + int(rank) * 128;
@@ -548,10 +576,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
               soft_wait(p.sync + wave, unsigned(c - p.sync_slack) * members, p.sync_timeout_ns);
           }
           gm_wait_cluster(smem_u32(&empty[s]), ((q / kG2Stages) & 1u) ^ 1u);
-          const uint32_t leader_full = mapa_rank(smem_u32(&full[s]), 0);
+          const uint32_t leader_full = mapa_rank(smem_u32(&full[s]), leader);
           if (rank == 0) arrive_expect_tx_u32(smem_u32(&full[s]), 2 * kG2StageBytes);
           const uint32_t a = smem_u32(sA + s * kG2ABytes), b = smem_u32(sB + s * kG2BBytes);
-          if constexpr (kAMN) {
+          if constexpr (kPairs == 2) {
+            // pair 0's CTAs load the A K-slice of their 128 rows for both pairs
+            if (pair == 0) {
+              const uint16_t mc = uint16_t((1u << rank) | (1u << (rank + 2)));
+              if constexpr (kAMN) {
+                tma_load_2d_pair_mc(a, &tmap_a, m0, k0, leader_full, mc, pa);
+                tma_load_2d_pair_mc(a + kGmMNBox, &tmap_a, m0 + 64, k0, leader_full, mc, pa);
+              } else {
+                tma_load_2d_pair_mc(a, &tmap_a, k0, m0, leader_full, mc, pa);
+              }
+            }
+          } else if constexpr (kAMN) {
             tma_load_2d_pair_hint(a, &tmap_a, m0, k0, leader_full, pa);
             tma_load_2d_pair_hint(a + kGmMNBox, &tmap_a, m0 + 64, k0, leader_full, pa);
           } else {
@@ -580,7 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
       for (int tile = cluster; tile < tiles; tile += nclusters) {
         if (p.lm.mlive) {
           int mb, nb;
-          gemm_tile_coords(p, tile, mb, nb);
+          gemm_tile_coords(ps, tile, mb, nb);
           if (!p.lm.mlive[mb]) continue;
         }
         const int acc = C::kAcc == 2 ? (i & 1) : 0;
@@ -604,9 +643,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
               tc_mma_pair(dt + uint32_t(hh * 256), ad, bd, idesc, (kb | k) != 0);
             }
           }
-          tc_commit_pair(smem_u32(&empty[s]));     // slot s free in both CTAs
+          // slot s consumed by this pair: arrive on the empty barrier of every CTA of the
+          // cluster (with shared A, a stage is free only once both pairs consumed it)
+          tc_commit_mask(smem_u32(&empty[s]), kPairs == 2 ? uint16_t(0xF) : pair_mask);
         }
-        tc_commit_pair(smem_u32(&tfull[acc]));     // accumulator ready in both CTAs
+        tc_commit_mask(smem_u32(&tfull[acc]), pair_mask);   // accumulator ready in the pair
       }
     }
   } else {
@@ -616,12 +657,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
     const int chalf = (warp - 2) >> 2;                 // which half of the tile's columns
     constexpr int kCols = kNP / 2, kChunks = kCols / 32;
     const uint64_t pol_c = l2_policy(p.hint_c);
-    const uint32_t leader_tempty0 = mapa_rank(smem_u32(&tempty[0]), 0);
-    const uint32_t leader_tempty1 = mapa_rank(smem_u32(&tempty[1]), 0);
+    const uint32_t leader_tempty0 = mapa_rank(smem_u32(&tempty[0]), leader);
+    const uint32_t leader_tempty1 = mapa_rank(smem_u32(&tempty[1]), leader);
     int i = 0;
     for (int tile = cluster; tile < tiles; tile += nclusters) {
       int mb, nb;
-      gemm_tile_coords(p, tile, mb, nb);
+      gemm_tile_coords(ps, tile, mb, nb);
+      nb = nb * kPairs + int(pair);
       if (p.lm.mlive && !p.lm.mlive[mb]) continue;
       const int acc = C::kAcc == 2 ? (i & 1) : 0;
       const int use = C::kAcc == 2 ? (i >> 1) : i;
@@ -637,7 +679,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
         const int y = valid ? p.lm.tokens[r] : -1;
         float R = -INFINITY, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f, uy = __int_as_float(0x7fc00000);
         lm_fwd_cols(p, base, r, c0, R, S, W, cS, cW, uy, valid, y, kChunks);
-        if (valid)        // one partial per (tile, column half): partial[2·nb + half][row]
+        if (valid && nb < p.nblk)   // one partial per (tile, column half): partial[2·nb + half][row]
           p.lm.partial[int64_t(2 * nb + chalf) * p.lm.n_rows + r] = make_float4(R, S - cS, W - cW, uy);
       } else if constexpr (kOut == kOutLmDz) {
         BwdRec rc;
@@ -654,12 +696,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
     }
   }
   tc_fence_before();
-  cluster_sync_all();     // both CTAs done with TMEM and with remote barriers
+  cluster_sync_all();     // all CTAs done with TMEM and with remote barriers
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
                  : "memory");
   }
+}
+
+template <bool kAMN, bool kBMN, int kOut, int kNP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
+    k_umma_gemm2(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                 const GemmParams p0) {
+  gemm2_body<kAMN, kBMN, kOut, kNP, 1>(tmap_a, tmap_b, p0);
+}
+
+template <bool kAMN, bool kBMN, int kOut, int kNP>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kG2Threads, 1)
+    k_umma_gemm4(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                 const GemmParams p0) {
+  gemm2_body<kAMN, kBMN, kOut, kNP, 2>(tmap_a, tmap_b, p0);
 }
 
 }  // namespace espo

@@ -40,13 +40,16 @@ def make_case(seed, n_groups, G, L, V, d, zv_group=None, lam=1.0):
                 old=old, mask=mask, T=T, R=R)
 
 
-KERNELS = ["gemm", "1cta", "2cta"]   # ESPO_OPT_LMHEAD_IMPL 0 (GEMM core) / 1 with one CTA / pairs
+# ESPO_OPT_LMHEAD_IMPL 0 (GEMM core; "gemm_mc": 4-CTA clusters with A multicast) / 1 with one
+# CTA / pairs
+KERNELS = ["gemm", "gemm_mc", "1cta", "2cta"]
 
 
 def set_kernel(ctx, kern):
-    from paper_2512_07710_b200.espo import OPT_LMHEAD_2CTA, OPT_LMHEAD_IMPL
-    ctx.set_option(OPT_LMHEAD_IMPL, 0 if kern == "gemm" else 1)
+    from paper_2512_07710_b200.espo import OPT_LMHEAD_2CTA, OPT_LMHEAD_IMPL, OPT_LMHEAD_RASTER
+    ctx.set_option(OPT_LMHEAD_IMPL, 0 if kern.startswith("gemm") else 1)
     ctx.set_option(OPT_LMHEAD_2CTA, int(kern == "2cta"))
+    ctx.set_option(OPT_LMHEAD_RASTER, (1 << 25) if kern == "gemm_mc" else 0)
 
 
 def run_path(case, dev, fused, V, kern="gemm"):
@@ -204,8 +207,8 @@ def test_lmhead_kernels_agree():
         t = {k: v.cpu().numpy() for k, v in ctx.export_token_stats().items()}
         outs.append((float(loss.item()), t, dh.cpu().numpy(), dW.cpu().numpy()))
         ctx.close()
-    (l0, t0, h0, w0) = outs[1]
-    for (l1, t1, h1, w1) in (outs[0], outs[2]):
+    (l0, t0, h0, w0) = outs[KERNELS.index("1cta")]
+    for (l1, t1, h1, w1) in outs:
         v = t0["valid"].astype(bool)
         assert np.array_equal(v, t1["valid"].astype(bool))
         # each kernel is within the K2 bounds of the oracle (2e-6 / 2e-6 / 1e-5 relative to
@@ -253,7 +256,8 @@ def test_lmhead_errors_and_state():
     sh.close()
 
 
-@pytest.mark.parametrize("native", [0, 2, 3, 4], ids=["pair_default", "1cta", "pair256", "pair512"])
+@pytest.mark.parametrize("native", [0, 2, 3, 4, 5, 6],
+                         ids=["pair_default", "1cta", "pair256", "pair512", "mcast", "mcast_dh"])
 @pytest.mark.parametrize("shape", [(3, 4, 50, 20000, 1000), (2, 4, 130, 5000, 2048)],
                          ids=["V20000_d1000_ntail", "V5000_d2048"])
 def test_lmhead_bwd_native_gemm_equals_cublas(shape, native):

@@ -26,9 +26,10 @@ def main(d=4096, rounds=3, burst=4, n=32768, V=151936):
     gid = torch.zeros(G, dtype=torch.int32, device=dev)
     so = torch.arange(G + 1, device=dev, dtype=torch.int64) * (n // G)
     ctx = Espo(V, logits_dtype=torch.bfloat16, device=0)
-    cfgs = {"gemm_g16": (0, 16, 0), "gemm_g32": (0, 32, 0), "gemm_g64": (0, 64, 0),
-            "gemm_g128": (0, 128, 0), "t256_g32": (0, 32, 1 << 8), "t256_g64": (0, 64, 1 << 8),
-            "t256_g128": (0, 128, 1 << 8), "dedicated_1cta": (1, 8, 0), "cublas": None}
+    MC = 1 << 9                      # (hints << 16): bit 25 of the raster option = multicast
+    cfgs = {"gemm_g32": (0, 32, 0), "gemm_g64": (0, 64, 0), "mc_g16": (0, 16, MC),
+            "mc_g32": (0, 32, MC), "mc_g64": (0, 64, MC), "mc_g128": (0, 128, MC),
+            "dedicated_1cta": (1, 8, 0), "cublas": None}
     times = {k: [] for k in cfgs}
     losses = {}
     for _ in range(rounds):

@@ -39,14 +39,15 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1):
     dw_auto = H(1, 2, 1)
     G = lambda dh_m, dw_n: dh_m | (dw_n << 16)
     H2 = lambda dh, dw: dh | (dw << 8)
+    MC = 1 << 25
     cfgs = {                     # (gemm, group, hints, compact, sync, lmhead impl, lm raster)
         "cublas": (1, 0, -1, 0, 0, 1, 0),
         "default": (0, 0, -1, 1, 0, 0, 0),
-        "dz_dedicated": (0, 0, -1, 1, 0, 1, 0),
-        "dz_t256_g32": (0, 0, -1, 1, 0, 0, 32 | (1 << 24)),
-        "dz_t256_g64": (0, 0, -1, 1, 0, 0, 64 | (1 << 24)),
-        "dz_g16": (0, 0, -1, 1, 0, 0, 16),
-        "dz_g64": (0, 0, -1, 1, 0, 0, 64),
+        "dz_mc": (0, 0, -1, 1, 0, 0, MC),
+        "dz_mc_dh_mc": (6, 0, -1, 1, 0, 0, MC),
+        "all_mc": (5, 0, -1, 1, 0, 0, MC),
+        "dh_mc": (6, 0, -1, 1, 0, 0, 0),
+        "all_mc_g16": (5, 16, -1, 1, 0, 0, MC | 16),
     }
     times = {k: [] for k in cfgs}
     for _ in range(rounds):
