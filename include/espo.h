@@ -526,7 +526,9 @@ typedef enum {
                                   d ≤ 4096, 64 above), bits
                                   16-23 = L2 policies (A | B << 2, 1 evict_first, 2 evict_last),
                                   bit 24 = 256 × 256 tiles (double-buffered) instead of 256 × 512,
-                                  bit 25 = 4-CTA clusters (two pairs sharing A by TMA multicast) */
+                                  bit 25 = 4-CTA clusters (two pairs sharing A by TMA multicast),
+                                  bit 26 = no split-K for the backward's dh GEMM (default: split in
+                                  two when it has fewer than 6 waves of tiles) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

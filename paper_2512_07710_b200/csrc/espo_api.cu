@@ -154,6 +154,9 @@ struct espo_ctx_s {
                                  // 1 = the dedicated kernels (k_lmhead*.cuh)
   uint8_t* lmh_live = nullptr;   // per 256-row block liveness (fwd on the GEMM core)
   int lmh_mcast = 0;             // LM-head GEMM core on 4-CTA clusters (A multicast to two pairs)
+  int lmh_split_k = 1;           // dh GEMM split-K over 2 when it has < 6 waves of tiles
+  void* lmh_split = nullptr;     // its fp32 scratch [rows][d], grown on demand
+  size_t lmh_split_cap = 0;
   int lmh_tile256 = 0;           // LM-head GEMM-core tiles: 0 = 256 × 512 (one accumulator),
                                  // 1 = 256 × 256 (double-buffered, epilogue overlapped)
   int lmh_group_m = 0, lmh_hints = 0;   // LM-head fwd / dz on the GEMM core: raster (0 = auto),
@@ -440,6 +443,7 @@ espo_status espo_destroy(espo_ctx_t c) {
     if (c->rs_scratch) cudaFree(c->rs_scratch);
     if (c->lmh_dz) cudaFree(c->lmh_dz);
     if (c->lmh_cmp) cudaFree(c->lmh_cmp);
+    if (c->lmh_split) cudaFree(c->lmh_split);
     if (c->lmh_live) cudaFree(c->lmh_live);
     if (c->gemm_sync) cudaFree(c->gemm_sync);
     if (c->blas) g_blas.destroy(c->blas);
@@ -502,6 +506,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->lmh_hints = int((value >> 16) & 0xFF);
       c->lmh_tile256 = int((value >> 24) & 1);
       c->lmh_mcast = int((value >> 25) & 1);
+      c->lmh_split_k = int(((value >> 26) & 1) ^ 1);   // bit 26: no split-K for dh
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_IMPL:
       if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
@@ -955,7 +960,8 @@ template <bool kAMN, bool kBMN, int kOut>
 espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensorMap& mb, int M,
                              int N, int64_t K, void* C, int64_t ldc, int kind, int group_m,
                              int hints, cudaStream_t s, const GemmDyn& dyn = GemmDyn(),
-                             const LmEpi* lm = nullptr) {
+                             const LmEpi* lm = nullptr, float* split_out = nullptr,
+                             int64_t split_ld = 0) {
   // kind: 0 = one CTA per 128 × 256 tile, 1 = CTA pair 256 × 256, 2 = CTA pair 256 × 512,
   // 3 = two CTA pairs per cluster sharing A by multicast, 256 × 512 tiles each
   static unsigned long long attr = 0, attr2 = 0, attr3 = 0, attr4 = 0;
@@ -963,6 +969,10 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
   const int tn = (kind == 2 || kind == 3) ? 512 : kGmBN;
   GemmParams p;
   p.lm = lm ? *lm : LmEpi{};
+  p.ksplit = split_out ? 2 : 1;                 // split-K over 2 (kOutF32 on pairs only)
+  p.split_out = split_out;
+  p.split_ld = split_ld;
+  if (split_out && (kOut != kOutF32 || kind == 0)) return ESPO_ERR_INVALID_ARGUMENT;
   if ((kOut == kOutLmFwd || kOut == kOutLmDz) && kind == 0) return ESPO_ERR_INVALID_ARGUMENT;
   p.dyn_count = dyn.count;
   p.dyn_base = dyn.base;
@@ -1341,10 +1351,35 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       }
       if (dhidden) {   // dh[n, d] = dz[n, V] · W[V, d]: A = dz K-major, B = W MN-major
         char* dh = static_cast<char*>(dhidden) + (compact ? 0 : r0 * lddh * int64_t(dsize(dh_dtype)));
+        // dh has few, long tiles (K = the vocabulary): at 8192 rows and d = 4096 only 256
+        // pair tiles = 3.5 waves of 74 pairs (the 4th half empty). Below 6 waves, split K in
+        // two (deterministic: K-half 1 into a scratch, added by k_split_fixup)
+        float* split = nullptr;
+        if (dh_dtype == ESPO_F32 && kind_dh != 0 && d % 4 == 0 && c->lmh_split_k) {
+          const int64_t tiles = int64_t((n + 255) / 256) * ((d + (kind_dh == 1 ? 255 : 511)) / (kind_dh == 1 ? 256 : 512));
+          if (tiles < 6 * (c->num_sms / 2)) {
+            const size_t need_s = size_t(n) * size_t(d) * 4;
+            if (need_s > c->lmh_split_cap) {
+              if (c->lmh_split) cudaFree(c->lmh_split);
+              c->lmh_split = nullptr;
+              c->lmh_split_cap = 0;
+              ESPO_CUDA(cudaMalloc(&c->lmh_split, need_s));
+              c->lmh_split_cap = need_s;
+            }
+            split = static_cast<float*>(c->lmh_split);
+          }
+        }
         st = dh_dtype == ESPO_BF16
                  ? launch_umma_gemm<false, true, kOutBF16>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, kind_dh, g_dh, hint_dh, s, dyn_m)
-                 : launch_umma_gemm<false, true, kOutF32>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, kind_dh, g_dh, hint_dh, s, dyn_m);
+                 : launch_umma_gemm<false, true, kOutF32>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, kind_dh, g_dh, hint_dh, s, dyn_m,
+                                                          nullptr, split, d);
         if (st != ESPO_OK) return st;
+        if (split) {
+          const int grid = c->num_sms * 8;
+          k_split_fixup<<<grid, 256, 0, s>>>(reinterpret_cast<float*>(dh), lddh, split, d, n, d,
+                                             dyn_m.count, dyn_m.base, dyn_m.row_map);
+          ESPO_LAUNCHED(c);
+        }
       }
       if (dweight) {   // dW[V, d] += dzᵀ[V, n] · h[n, d]: A = dz MN-major, B = h MN-major
         st = launch_umma_gemm<true, true, kOutAddF32>(c, mdz_mn, mh_mn, V, d, n, dweight, lddw, kind_dw, g_dw, hint_dw, s, dyn_k);

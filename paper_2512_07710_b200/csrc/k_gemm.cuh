@@ -86,6 +86,12 @@ struct GemmParams {
   int sync_chunk, sync_slack;
   unsigned sync_timeout_ns;
   LmEpi lm;               // kOutLmFwd / kOutLmDz only
+  // split-K over 2 (kOutF32, CTA-pair kernels): work item t < 2·tiles covers tile t % tiles
+  // for K-half t / tiles; K-half 0 writes C, K-half 1 writes split_out[row][col] (fp32,
+  // pitch split_ld, compact row index); k_split_fixup adds it into C afterwards
+  int ksplit;
+  float* split_out;
+  int64_t split_ld;
 };
 
 // wait until *ctr ≥ target or the timeout expired (acquire; a soft barrier: never deadlocks)
@@ -528,6 +534,13 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cluster = blockIdx.x / (2 * kPairs), nclusters = gridDim.x / (2 * kPairs);
   const int tiles = ps.mblk * ps.nblk;
+  const int ks_n = (kOut == kOutF32 && p.ksplit == 2) ? 2 : 1;
+  const int items = tiles * ks_n;
+  auto krange = [&](int t, int& kb0, int& kb1) {   // K-blocks of work item t
+    const int ks = t / tiles;
+    kb0 = ks_n == 1 ? 0 : (ks * p.kblk) / 2;
+    kb1 = ks_n == 1 ? p.kblk : ((ks + 1) * p.kblk) / 2;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kG2Stages; ++s) {
@@ -558,15 +571,16 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
       const bool pace = p.sync != nullptr && rank == 0;
       uint32_t q = 0;
       int wave = 0;
-      for (int tile = cluster; tile < tiles; tile += nclusters, ++wave) {
-        int mb, nb;
-        gemm_tile_coords(ps, tile, mb, nb);
+      for (int item = cluster; item < items; item += nclusters, ++wave) {
+        int mb, nb, kb0, kb1;
+        gemm_tile_coords(ps, item % tiles, mb, nb);
         nb = nb * kPairs + int(pair);
+        krange(item, kb0, kb1);
         if (p.lm.mlive && !p.lm.mlive[mb]) continue;     // no row to compute: skipped tile
         const int m0 = mb * 2 * kGmBM + int(rank) * kGmBM;
         const int n0 = nb * kNP + int(rank) * 128;
-        const unsigned members = unsigned(min(nclusters, tiles - wave * nclusters));
-        for (int kb = 0; kb < p.kblk; ++kb, ++q) {
+        const unsigned members = unsigned(min(nclusters, items - wave * nclusters));
+        for (int kb = kb0; kb < kb1; ++kb, ++q) {
           const int s = q % kG2Stages;
           const int k0 = kb * kGmBK;
           if (pace && kb % p.sync_chunk == 0) {
@@ -616,19 +630,21 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
       constexpr uint32_t idesc = gemm2_idesc<kAMN, kBMN>();
       uint32_t q = 0;
       int i = 0;
-      for (int tile = cluster; tile < tiles; tile += nclusters) {
+      for (int item = cluster; item < items; item += nclusters) {
         if (p.lm.mlive) {
           int mb, nb;
-          gemm_tile_coords(ps, tile, mb, nb);
+          gemm_tile_coords(ps, item % tiles, mb, nb);
           if (!p.lm.mlive[mb]) continue;
         }
+        int kb0, kb1;
+        krange(item, kb0, kb1);
         const int acc = C::kAcc == 2 ? (i & 1) : 0;
         const int use = C::kAcc == 2 ? (i >> 1) : i;     // earlier uses of this buffer
         ++i;
         gm_wait_cluster(smem_u32(&tempty[acc]), (use & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t dt = tmem + uint32_t(acc * kGmBN);
-        for (int kb = 0; kb < p.kblk; ++kb, ++q) {
+        for (int kb = kb0; kb < kb1; ++kb, ++q) {
           const int s = q % kG2Stages;
           gm_wait_cluster(smem_u32(&full[s]), (q / kG2Stages) & 1u);
           tc_fence_after();
@@ -640,7 +656,7 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
             for (int hh = 0; hh < kNP / 256; ++hh) {
               const uint32_t bh = b0 + hh * (128 * kGmBK * 2);
               const uint64_t bd = kBMN ? umma_desc_sw128_mn(bh + k * 2048) : umma_desc_sw128(bh + k * 32);
-              tc_mma_pair(dt + uint32_t(hh * 256), ad, bd, idesc, (kb | k) != 0);
+              tc_mma_pair(dt + uint32_t(hh * 256), ad, bd, idesc, (kb != kb0) || (k != 0));
             }
           }
           // slot s consumed by this pair: arrive on the empty barrier of every CTA of the
@@ -660,11 +676,16 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
     const uint32_t leader_tempty0 = mapa_rank(smem_u32(&tempty[0]), leader);
     const uint32_t leader_tempty1 = mapa_rank(smem_u32(&tempty[1]), leader);
     int i = 0;
-    for (int tile = cluster; tile < tiles; tile += nclusters) {
+    GemmParams p1 = p;                                  // K-half 1 of a split: the scratch
+    p1.C = p.split_out;
+    p1.ldc = p.split_ld;
+    p1.row_map = nullptr;
+    for (int item = cluster; item < items; item += nclusters) {
       int mb, nb;
-      gemm_tile_coords(ps, tile, mb, nb);
+      gemm_tile_coords(ps, item % tiles, mb, nb);
       nb = nb * kPairs + int(pair);
       if (p.lm.mlive && !p.lm.mlive[mb]) continue;
+      const bool second = item >= tiles;
       const int acc = C::kAcc == 2 ? (i & 1) : 0;
       const int use = C::kAcc == 2 ? (i >> 1) : i;
       ++i;
@@ -688,7 +709,7 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
         if (r < p.M) rc = p.lm.rec[r];
         lm_dz_cols(p, base, r, c0, rc, kChunks);
       } else {
-        gemm_store_tile<kOut>(p, base, r, c0, pol_c, kChunks);
+        gemm_store_tile<kOut>(second ? p1 : p, base, r, c0, pol_c, kChunks);
       }
       __syncwarp();
       tc_fence_before();
@@ -716,6 +737,28 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kG2Threads, 1)
     k_umma_gemm4(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                  const GemmParams p0) {
   gemm2_body<kAMN, kBMN, kOut, kNP, 2>(tmap_a, tmap_b, p0);
+}
+
+// C[row_map ? row_map[r] : r][0, N) += split[r][0, N) for r < the (device) row count.
+__global__ void __launch_bounds__(256) k_split_fixup(float* C, int64_t ldc, const float* split,
+                                                     int64_t lds, int M, int N, const int* dyn_count,
+                                                     int dyn_base, const int* row_map) {
+  int m = M;
+  if (dyn_count) m = min(M, max(0, *dyn_count - dyn_base));
+  const int nv = N / 4;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < int64_t(m) * nv;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(i / nv), v = int(i % nv);
+    const int orow = row_map ? row_map[r] : r;
+    float4* o = reinterpret_cast<float4*>(C + int64_t(orow) * ldc) + v;
+    const float4 a = reinterpret_cast<const float4*>(split + int64_t(r) * lds)[v];
+    float4 b = *o;
+    b.x += a.x;
+    b.y += a.y;
+    b.z += a.z;
+    b.w += a.w;
+    *o = b;
+  }
 }
 
 }  // namespace espo

@@ -40,15 +40,14 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1):
     G = lambda dh_m, dw_n: dh_m | (dw_n << 16)
     H2 = lambda dh, dw: dh | (dw << 8)
     MC = 1 << 25
+    NOSPLIT = 1 << 26
     cfgs = {                     # (gemm, group, hints, compact, sync, lmhead impl, lm raster)
         "cublas": (1, 0, -1, 0, 0, 1, 0),
         "default": (0, 0, -1, 1, 0, 0, 0),
-        "dz_mc": (0, 0, -1, 1, 0, 0, MC),
-        "dz_mc_dh_mc": (6, 0, -1, 1, 0, 0, MC),
-        "all_mc": (5, 0, -1, 1, 0, 0, MC),
-        "dh_mc": (6, 0, -1, 1, 0, 0, 0),
-        "all_mc_g16": (5, 16, -1, 1, 0, 0, MC | 16),
+        "nosplit": (0, 0, -1, 1, 0, 0, NOSPLIT),
+        "dh256": (0, 0, -1, 1, 0, 0, 0),
     }
+    cfgs["dh256"] = (3, G(0, 8), -1, 1, 0, 0, 0)
     times = {k: [] for k in cfgs}
     for _ in range(rounds):
         for k, (impl, gm, hints, compact, sync, lmi, lmr) in cfgs.items():
