@@ -1,19 +1,28 @@
-// k_gemm.cuh — the two contractions of the LM-head backward on the 5th-gen tensor cores
-// (the Megatron log-prob recompute of PAPER.md:129-131): with logits
-// z = h·Wᵀ and the bf16 gradient tile dz = ∂(grad·loss)/∂z (k_lmhead_dz),
+// k_gemm.cuh — the library's tcgen05 GEMM core: the fused LM head's contractions (SURVEY §8(f)
+// row 1; the Megatron log-prob recompute of PAPER.md:129-131). With logits z = h·Wᵀ:
+//   forward   z tiles → per-row partials {R, S, W, u_y}  A = h (K-major), B = W (K-major)
+//   recompute z tiles → dz = ∂(grad·loss)/∂z (bf16)     A = h (K-major), B = W (K-major)
 //   dh = dz · W      M = rows,  N = d, K = vocabulary   A = dz  (K-major), B = W (MN-major)
 //   dW += dzᵀ · h    M = vocab, N = d, K = rows         A = dzᵀ (MN-major), B = h (MN-major)
-// Both operands stay in the layout the caller and k_lmhead_dz produce — no transposed
+// Every operand stays in the layout the caller (or the recompute) produced — no transposed
 // copies: tcgen05 reads MN-major bf16 tiles directly (instruction-descriptor bits 15/16).
 //
-// One persistent kernel: grid = min(tiles, SMs), tile = 128 × 256 outputs, tiles in
-// N-fastest order (the CTAs resident together share A row blocks and read the same B
-// K-slices in step, so both stay in L2). Warp roles (192 threads), as k_lmhead.cuh:
-// warp 0 — TMA producer (4-stage ring of {A 16 KB, B 32 KB} with 128-byte swizzle);
-// warp 1 — TMEM allocator and MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M = 128,
-// N = 256, K = 16, fp32 accumulators in two 256-column TMEM buffers, so tile i+1's MMAs
-// overlap tile i's epilogue); warps 2–5 — epilogue (thread i = row i of the tile,
-// tcgen05.ld 32 columns at a time, fp32/bf16 store or fp32 read-add-write).
+// Persistent, warp-specialised kernels: warp 0 = TMA producer (a ring of {A, B} K-slices with
+// 128-byte swizzle), warp 1 = TMEM allocator and the one thread issuing tcgen05.mma
+// (kind::f16, fp32 accumulators in TMEM, completion by tcgen05.commit → mbarrier), the other
+// warps = epilogue (tcgen05.ld 32 columns at a time: fp32 / bf16 store, fp32 read-add-write,
+// or the LM-head reductions). Variants:
+//   k_umma_gemm   one CTA per 128 × 256 tile, two TMEM accumulators (epilogue overlapped);
+//   k_umma_gemm2  CTA pairs (cta_group::2, M = 256 split over the pair's SMs, B columns split
+//                 likewise): 256 × 256 tiles (two accumulators) or 256 × 512 (one 512-column
+//                 accumulator = all of TMEM, a quarter less L2 → SM traffic per FLOP), 8
+//                 epilogue warps; grouped tile raster, L2 cache-policy hints, device-side row
+//                 counts (compacted operands), split-K over 2 (deterministic), optional soft
+//                 lockstep between clusters;
+//   k_umma_gemm4  two pairs per cluster sharing A through TMA multicast (an option: only 33
+//                 four-CTA clusters are resident on a B200, 132 of 148 SMs).
+// Grids are sized from the resident cluster count (host side). Every barrier wait is bounded by
+// the global timer: a protocol error traps instead of hanging the GPU.
 //
 // Shared-memory operand layouts (UMMA canonical forms, SWIZZLE_128B, 1024-B aligned):
 //  K-major : rows of 64 K-elements (128 B), 8-row groups 1024 B apart (one TMA box
