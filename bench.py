@@ -55,6 +55,9 @@ def parse():
     p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                    help="weak: a batch of --config per rank; strong: one global batch split "
                         "over the ranks by prompt group (LPT)")
+    p.add_argument("--emulate-ranks", type=int, default=0,
+                   help="with --scaling strong on one GPU: run the N ranks' shards one after "
+                        "another (split finalize for the exchange); projected step = slowest rank")
     p.add_argument("--verify", action="store_true",
                    help="untimed extra pass: order-independent digest of every dlogits row")
     p.add_argument("--drift-seq", type=float, default=0.01,
@@ -96,7 +99,10 @@ def parse():
     p.add_argument("--vocab-shards", type=int, default=1,
                    help="S > 1: vocabulary-parallel leg, S shard contexts back to back on this "
                         "GPU (partials gathered by a device copy)")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.emulate_ranks and (a.scaling != "strong" or (a.gpus or 1) != 1 or a.impl != "ours"):
+        p.error("--emulate-ranks N needs --scaling strong on one GPU (our arm)")
+    return a
 
 
 # ------------------------------------------------------------------------------ launch
@@ -231,9 +237,10 @@ def group_chunks(local_so, local_gid, Rc):
 
 
 def make_batch(w, seed, dev, buffer_rows, log, single_pass=False, shard=None,
-               drift=(0.01, 0.02)):
+               drift=(0.01, 0.02), bufs=None):
     """Device-resident synthetic batch: chunk buffer + per-token arrays. shard = (world,
-    rank): strong scaling, this rank's groups of the global batch (seed shared by all ranks)."""
+    rank): strong scaling, this rank's groups of the global batch (seed shared by all ranks).
+    bufs = (buf, buf_tok, buf_lp) of an earlier call with the same seed: reused, not redrawn."""
     import torch
     V = w.V
     t0 = time.time()
@@ -255,15 +262,19 @@ def make_batch(w, seed, dev, buffer_rows, log, single_pass=False, shard=None,
     else:                       # the same buffer for every N: bounded by the largest group
         from paper_2512_07710_b200.sharding import group_spans
         Rc = max(1, min(buffer_rows, max(int(g_so[b] - g_so[a]) for a, b in group_spans(g_gid))))
-    buf = S.make_logit_rows_torch(Rc, V, seed, dev, torch.bfloat16)
-    buf_tok = S.sample_tokens_gumbel_torch(buf, seed)
-    # bench setup only (untimed): rollout-engine log-probs = log_softmax + drift
-    buf_lp = torch.empty(Rc, dtype=torch.float32, device=dev)
-    for r0 in range(0, Rc, 2048):
-        r1 = min(Rc, r0 + 2048)
-        ls = torch.log_softmax(buf[r0:r1].float(), dim=1)
-        buf_lp[r0:r1] = ls.gather(1, buf_tok[r0:r1].long().unsqueeze(1)).squeeze(1)
-        del ls
+    if bufs is not None:
+        buf, buf_tok, buf_lp = bufs
+        assert buf.shape[0] == Rc
+    else:
+        buf = S.make_logit_rows_torch(Rc, V, seed, dev, torch.bfloat16)
+        buf_tok = S.sample_tokens_gumbel_torch(buf, seed)
+        # bench setup only (untimed): rollout-engine log-probs = log_softmax + drift
+        buf_lp = torch.empty(Rc, dtype=torch.float32, device=dev)
+        for r0 in range(0, Rc, 2048):
+            r1 = min(Rc, r0 + 2048)
+            ls = torch.log_softmax(buf[r0:r1].float(), dim=1)
+            buf_lp[r0:r1] = ls.gather(1, buf_tok[r0:r1].long().unsqueeze(1)).squeeze(1)
+            del ls
     # chunks: fixed R_c tiles (two sweeps), R_c tiles of each group (strong scaling) or
     # whole-rollout packs (single pass); batch row t reads buffer row t − (its chunk's first row)
     if single_pass:
@@ -312,34 +323,128 @@ def make_batch(w, seed, dev, buffer_rows, log, single_pass=False, shard=None,
                         chunk_of_row=None))
 
 
+def chunk_digest(dlog_rows, grow_rows):
+    """Order-independent 64-bit digest of dlogits rows (bit patterns) with their global ids."""
+    import torch
+    w32 = dlog_rows.view(torch.int32)
+    s1 = w32.sum(1, dtype=torch.int64).cpu().numpy().astype(np.uint64)
+    s2 = w32[:, ::7].sum(1, dtype=torch.int64).cpu().numpy().astype(np.uint64)
+    gid = grow_rows.astype(np.uint64)
+    with np.errstate(over="ignore"):
+        x = gid * np.uint64(0x9E3779B97F4A7C15) ^ s1 * np.uint64(0xBF58476D1CE4E5B9) ^ \
+            s2 * np.uint64(0x94D049BB133111EB)
+        x ^= x >> np.uint64(31)
+        x *= np.uint64(0xD6E8FEB86659FD93)
+        x ^= x >> np.uint64(32)
+        return int(x.sum(dtype=np.uint64))
+
+
+def emulate_ranks(args, w, dev, log):
+    """`--emulate-ranks N` (strong scaling on ONE GPU, for evidence only — not a multi-GPU
+    measurement): the N ranks' shards of the global batch run one after another on this GPU,
+    each on its own context; the one exchange of the pass is done with the split finalize
+    (every rank's espo_loss_reduce_local vector summed on the device, then
+    espo_loss_finalize_reduced on each rank), so every rank's dlogits rows are those a real
+    N-GPU run computes. Per rank, its step (fwd sweeps + reduce_local, then finalize_reduced +
+    bwd sweeps) is timed with CUDA events; the projected N-GPU step = the slowest rank's time
+    (the NCCL all-reduce of 26 doubles, ~10-20 µs, is not included). Prints one JSON line."""
+    import torch
+    from paper_2512_07710_b200.espo import REDUCE_LEN, Espo, stats_to_dict
+    N = args.emulate_ranks
+    seed = S.config_seed(w.index)
+    ranks, bufs = [], None
+    for r in range(N):
+        d = make_batch(w, seed, dev, args.buffer_rows, log, shard=(N, r),
+                       drift=(args.drift_seq, args.drift_tok), bufs=bufs)
+        bufs = (d["buf"], d["buf_tok"], d["buf_lp"])
+        ctx = Espo(w.V, logits_dtype=torch.bfloat16, device=dev.index)
+        ranks.append((d, ctx))
+    dlog = torch.empty((bufs[0].shape[0], w.V), dtype=torch.bfloat16, device=dev)
+    red = torch.zeros(REDUCE_LEN, dtype=torch.float64, device=dev)
+
+    def step(times=None, digest=None):
+        parts = []
+        for r, (d, ctx) in enumerate(ranks):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ctx.prepare(d["rewards"], d["group_ids"], d["seq_offsets"], n_tokens=d["T"])
+            for b, e in d["chunks"]:
+                ctx.loss_fwd(d["buf"][:e - b], d["tokens"][b:e], d["old"][b:e], None, row_begin=b)
+            parts.append(ctx.loss_reduce_local())
+            e1.record()
+            if times is not None:
+                times[r].append((e0, e1))
+        red.zero_()
+        for p_ in parts:                          # the all-reduce, in rank order
+            red.add_(p_)
+        out = None
+        for r, (d, ctx) in enumerate(ranks):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            loss, stats = ctx.loss_finalize_reduced(red)
+            for b, e in d["chunks"]:
+                ctx.loss_bwd(d["buf"][:e - b], dlog[:e - b], row_begin=b)
+                if digest is not None:
+                    gid = d["global_row"][b:e].cpu().numpy()
+                    digest[0] = (digest[0] + chunk_digest(dlog[:e - b], gid)) & ((1 << 64) - 1)
+            e1.record()
+            if times is not None:
+                times[r].append((e0, e1))
+            out = (loss, stats)
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    times = [[] for _ in range(N)]
+    for _ in range(args.steps):
+        loss, stats = step(times)
+    torch.cuda.synchronize(dev)
+    per_rank = [sum(a.elapsed_time(b) for a, b in t) / args.steps for t in times]
+    for _, ctx in ranks:
+        ctx.get_error()
+    digest = [0]
+    if args.verify:
+        step(digest=digest)
+        torch.cuda.synchronize(dev)
+    T_total = sum(d["T"] for d, _ in ranks)
+    ms = max(per_rank)
+    st = stats_to_dict(stats)
+    out = {"metric": "ESPO loss fwd+bwd tokens/sec (projected from emulated ranks)",
+           "value_projected": T_total / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1,
+           "emulated_ranks": N, "steps": args.steps, "warmup": args.warmup,
+           "scaling": "strong (emulated: ranks run one after another on one GPU)",
+           "ms_per_step_max_rank": ms, "ms_per_rank": per_rank,
+           "rank_tokens": [d["T"] for d, _ in ranks],
+           "imbalance_max_over_mean": ms / (sum(per_rank) / N),
+           "loss_f64": st["loss"],
+           "dlogits_digest": ("%016x" % digest[0]) if args.verify else None,
+           "config": {"workload": f"{w.name} global batch split over {N} emulated ranks (LPT plan)",
+                      "global_batch_tokens": T_total, "drift": {"seq_sigma": args.drift_seq}},
+           "note": "evidence of load balance and of N-independent results (dlogits digest, loss) "
+                   "of the strong-scaling path; not a multi-GPU measurement"}
+    print(json.dumps(out), flush=True)
+    for _, ctx in ranks:
+        ctx.close()
+
+
 def dlogits_digest(ctx, d, dlog, log):
     """Untimed verification pass (--verify): one more full step; after each backward chunk,
     per-row sums of the dlogits bits (all elements, and every 7th 32-bit word) are mixed with
     the row's GLOBAL id and summed mod 2^64. The sum is order-independent, so rank digests
     add up (all-reduce) to the digest one GPU would print for the same global batch."""
     import torch
-    T, Rc, buf = d["T"], d["Rc"], d["buf"]
-    M = np.uint64(0xFFFFFFFFFFFFFFFF)
+    T, buf = d["T"], d["buf"]
     ctx.prepare(d["rewards"], d["group_ids"], d["seq_offsets"], n_tokens=T)
     for b, e in d["chunks"]:
         ctx.loss_fwd(buf[:e - b], d["tokens"][b:e], d["old"][b:e], None, row_begin=b)
     loss, stats = ctx.loss_finalize()
-    acc = np.uint64(0)
+    acc = 0
     grow = d["global_row"]
-    with np.errstate(over="ignore"):
-        for b, e in d["chunks"]:
-            ctx.loss_bwd(buf[:e - b], dlog[:e - b], row_begin=b)
-            w32 = dlog[:e - b].view(torch.int32)
-            s1 = w32.sum(1, dtype=torch.int64).cpu().numpy().astype(np.uint64)
-            s2 = w32[:, ::7].sum(1, dtype=torch.int64).cpu().numpy().astype(np.uint64)
-            gid = (np.arange(b, e, dtype=np.uint64) if grow is None else
-                   grow[b:e].cpu().numpy().astype(np.uint64))
-            x = gid * np.uint64(0x9E3779B97F4A7C15) ^ s1 * np.uint64(0xBF58476D1CE4E5B9) ^ \
-                s2 * np.uint64(0x94D049BB133111EB)
-            x ^= x >> np.uint64(31)
-            x *= np.uint64(0xD6E8FEB86659FD93)
-            x ^= x >> np.uint64(32)
-            acc = (acc + (x.sum(dtype=np.uint64) & M)) & M
+    for b, e in d["chunks"]:
+        ctx.loss_bwd(buf[:e - b], dlog[:e - b], row_begin=b)
+        gid = np.arange(b, e, dtype=np.int64) if grow is None else grow[b:e].cpu().numpy()
+        acc = (acc + chunk_digest(dlog[:e - b], gid)) & ((1 << 64) - 1)
     ctx.get_error()
     return int(acc), loss, stats
 
@@ -669,6 +774,11 @@ def main_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
     w = S.WORKLOADS[args.config]
+    if args.emulate_ranks > 0:
+        if world != 1:
+            raise SystemExit("--emulate-ranks runs on one process")
+        emulate_ranks(args, w, dev, log)
+        return
     strong = args.scaling == "strong"
     if strong and (args.single_pass or args.vocab_shards > 1):
         raise SystemExit("--scaling strong runs the two-sweep (or --factored) path")

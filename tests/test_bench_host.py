@@ -75,3 +75,33 @@ def test_strong_plan_covers_every_group_once():
         assert sorted(sum(plan, [])) == list(range(w.n_prompts))
         loads = [sum(int(so[(g + 1) * w.G] - so[g * w.G]) for g in p) for p in plan]
         assert max(loads) - min(loads) <= 2 * w.G * w.L     # LPT: within two groups' rows
+
+
+def test_chunk_digest_is_additive_over_row_splits():
+    """--verify / --emulate-ranks: the digest of a row set is the mod-2^64 sum of the digests
+    of any split of it (what makes rank digests comparable with the N = 1 digest), and it
+    sees a one-ulp change in any row or a swapped pair of global ids."""
+    import torch
+    g = torch.Generator().manual_seed(3)
+    z = torch.randn(37, 50, generator=g).to(torch.bfloat16)
+    gid = np.arange(100, 137, dtype=np.int64)
+    full = bench.chunk_digest(z, gid)
+    perm = np.random.default_rng(0).permutation(37)
+    a, b = perm[:11], perm[11:]
+    parts = (bench.chunk_digest(z[torch.from_numpy(a)], gid[a]) +
+             bench.chunk_digest(z[torch.from_numpy(b)], gid[b])) & ((1 << 64) - 1)
+    assert parts == full
+    z2 = z.clone()
+    z2.view(torch.int16)[5, 7] += 1
+    assert bench.chunk_digest(z2, gid) != full
+    gid2 = gid.copy()
+    gid2[[3, 4]] = gid2[[4, 3]]
+    assert bench.chunk_digest(z, gid2) != full
+
+
+def test_emulate_ranks_requires_strong_single_process(monkeypatch):
+    monkeypatch.setattr("sys.argv", ["bench.py", "--emulate-ranks", "2"])
+    with pytest.raises(SystemExit):
+        bench.parse()                                     # weak scaling: rejected
+    monkeypatch.setattr("sys.argv", ["bench.py", "--emulate-ranks", "2", "--scaling", "strong"])
+    assert bench.parse().emulate_ranks == 2

@@ -8,6 +8,9 @@ timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; e
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo "bench exit=$?"
 timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-factored-leg --vocab-shards 8 > gpurun_out/bench_tp8.json 2>/dev/null; echo "tp8 exit=$?"
 timeout 900 python bench.py --scaling strong --config C4 --steps 1 --warmup 3 --verify --no-e2e --no-cpu-baseline --no-factored-leg > gpurun_out/bench_C4_strong_verify.json 2>/dev/null; echo "c4 strong exit=$?"
+for n in 2 4 8; do timeout 600 python bench.py --scaling strong --emulate-ranks $n --steps 5 --warmup 3 --verify > gpurun_out/bench_C1_emulate$n.json 2>/dev/null; echo "emulate $n exit=$?"; done
+timeout 600 python bench.py --scaling strong --steps 5 --warmup 3 --verify --no-e2e --no-cpu-baseline --no-factored-leg > gpurun_out/bench_C1_strong_verify.json 2>/dev/null; echo "c1 strong exit=$?"
+timeout 900 python bench.py --scaling strong --config C4 --emulate-ranks 8 --steps 1 --warmup 3 --verify > gpurun_out/bench_C4_emulate8.json 2>/dev/null; echo "c4 emulate8 exit=$?"
 P="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-factored-leg"
 $P > gpurun_out/plain_ll.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $P > gpurun_out/ncu_ll.log 2>&1; echo "launch list exit=$?"
 $P > gpurun_out/plain_tr.log 2>&1 && ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"k_rowstats|k_fwd_rows|k_dlogits|k_bwd_rows|k_bwd_recs" -s 768 --csv --log-file gpurun_out/traffic.csv $P > gpurun_out/ncu_tr.log 2>&1; echo "traffic exit=$?"

@@ -163,7 +163,9 @@ def main(tag, out_dir="gpurun_out"):
             open(os.path.join(dst, ll_name + ".md"), "w").write(
                 f"# {title}\n\n```\n" + buf.getvalue() + "```\n")
     for f in ("bench_full.json", "bench_full.err", "gpu_tests.log", "smoke.log", "bench_tp8.json",
-              "bench_C4_strong_verify.json", "bench_lmhead_bwd_dense.json",
+              "bench_C4_strong_verify.json", "bench_C1_strong_verify.json",
+              "bench_C1_emulate2.json", "bench_C1_emulate4.json", "bench_C1_emulate8.json",
+              "bench_C4_emulate8.json", "bench_lmhead_bwd_dense.json",
               "bench_lmhead_bwd_realistic.json", "gemm_sweep.json"):
         p = os.path.join(src, f)
         if os.path.exists(p):
