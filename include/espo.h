@@ -480,7 +480,7 @@ int32_t espo_comm_size(espo_ctx_t ctx);
 typedef enum {
   ESPO_OPT_FWD_IMPL = 0,       /* 0 = TMA bulk-copy smem ring (default), 1 = LDG.128 warp per
                                   row, 2..7 = other ring geometries, 8 = default geometry in
-                                  scalar FP32 (K2) */
+                                  scalar FP32, 9..11 = (row, tile) grid (K2) */
   ESPO_OPT_BWD_IMPL = 1,       /* 0 = tiled (row, 32 KB tile) grid (default), 1 = LDG.128 warp
                                   per row, 2..6 = TMA ring geometries, 7 = 16 KB tiles,
                                   8 = tiles with scalar FP32, 9 = tiles over the compact row

@@ -686,7 +686,7 @@ espo_status launch_sweep_fwd(espo_ctx_t c, const void* logits, int64_t ld, const
     k_fwd_rows<float><<<pre_grid, 256, 0, s>>>(logits, ld, tokens, old_logp, mask, row_begin, n_rows,
                                                V, v0, p.V, p.lam_log2e, c->ws, list, c->ws.count);
   ESPO_LAUNCHED(c);
-  if (c->fwd_impl >= 9 && partial == nullptr && nx == 0) {
+  if (c->fwd_impl >= 9 && c->fwd_impl <= 11 && partial == nullptr && nx == 0) {
     // tiled: (listed row, 32 KB tile) blocks → per-tile partials → k_fwd_combine
     const int epv = bf ? 8 : 4;
     const int ntiles = (((p.V + epv - 1) / epv) + 256 * 8 - 1) / (256 * 8);

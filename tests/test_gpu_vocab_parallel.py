@@ -91,6 +91,38 @@ def test_vocab_parallel_bf16_ragged_eight_shards():
     check_dlogits_f32(g["dlogits"], oracle_dlogits(ref2, inst, cfg, np.arange(inst.T)))
 
 
+@pytest.mark.parametrize("impl", [0, 1], ids=["tma", "ldg"])
+def test_vocab_parallel_reference_seeding_extreme_range(impl):
+    """Rows whose target lies in another shard start each lane from its first vector's
+    largest element (K2 seed_ref). Logits 100 above that in later vectors (2^144: the batch
+    sums overflow) must still take the max-referenced fallback, and a −inf first vector must
+    leave the lane unseeded; parity with the oracle and with the unsharded run. (The far
+    elements are moved down, not the near ones up: logits of magnitude 100 would carry fp32
+    rounding of ~1e-5 relative into p, beyond the test's element bound.)"""
+    from tests._instances import exact_lp
+    import espo_synth as S
+    dev = require_cuda()
+    inst = tiny_instance(23, V=2048, group_sizes=(4, 4), L=12, sigma_seq=0.0, sigma_tok=0.0)
+    for t in range(0, inst.T, 2):
+        inst.logits[t, :600] -= 100.0                # later vectors of shard 1 (600..999)
+        inst.logits[t, 1000:] -= 100.0               # lie 100 above everything else
+        inst.logits[t, 1536:1600] = -np.inf          # first vectors of shard 3
+    inst.tokens[inst.tokens >= 1536] = 1700          # targets stay finite
+    inst.old_logp = S.drift_old_logp(exact_lp(inst.logits, inst.tokens), inst.seq_offsets, 4)
+    shards = [(0, 512), (512, 512), (1024, 512), (1536, 512)]
+    g = run_sharded(inst, dev, shards, fwd_impl=impl, bwd_impl=impl)
+    cfg = oracle_cfg(inst.V)
+    ref = inst.run(cfg)
+    assert np.nanmin(ref.lp) < -90
+    check_exact_fields(g, ref)
+    check_token_stats(g, ref)
+    ref2, _ = decision_aware_reference(g, inst, ref, cfg)
+    check_loss(g, ref2, 1e-5)
+    check_dlogits_f32(g["dlogits"], oracle_dlogits(ref2, inst, cfg, np.arange(inst.T)))
+    u = run_gpu(inst, dev)          # lp ≈ −100 carries ~1e-5 relative fp32 rounding into
+    assert g["loss"] == pytest.approx(u["loss"], rel=5e-5)    # the ratios of either run
+
+
 def test_sharded_context_requires_partial_path():
     """A sharded context without a TP communicator cannot run the fused espo_loss_fwd."""
     from paper_2512_07710_b200.espo import EspoError

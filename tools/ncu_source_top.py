@@ -1,14 +1,14 @@
 """Top source lines of an ncu report by warp-stall samples (`ncu -i rep --page source --csv`),
 so a capture can be summarised on the GPU box and only a small table brought back.
-usage: python tools/ncu_source_top.py report.ncu-rep [n]"""
+usage: python tools/ncu_source_top.py report.ncu-rep [n] [samples|inst] [cuda|sass]"""
 import csv
 import io
 import subprocess
 import sys
 
 
-def main(rep, n=40):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda"],
+def main(rep, n=40, key="samples", view="cuda"):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", view],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if not rows:
@@ -28,9 +28,10 @@ def main(rep, n=40):
     for r in rows[1:]:
         try:
             samp = float(r[i_samp]) if i_samp is not None and r[i_samp] else 0.0
+            inst = float(r[i_inst]) if i_inst is not None and r[i_inst] else 0.0
         except ValueError:
             continue
-        data.append((samp, r))
+        data.append((inst if key == "inst" else samp, r))
     tot = sum(x[0] for x in data) or 1.0
     print(f"columns: {hdr}")
     for samp, r in sorted(data, key=lambda x: -x[0])[:n]:
@@ -41,4 +42,5 @@ def main(rep, n=40):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40,
+         sys.argv[3] if len(sys.argv) > 3 else "samples", sys.argv[4] if len(sys.argv) > 4 else "cuda")
