@@ -515,20 +515,25 @@ typedef enum {
                                   1 = evict_first, 2 = evict_last; −1 = defaults */
   ESPO_OPT_LMHEAD_COMPACT = 11, /* espo_lmhead_bwd: 1 (default) = recompute and contract only the
                                   rows with gradient (c_t ≠ 0; needs d % 8 == 0), 0 = all rows */
-  ESPO_OPT_GEMM_SYNC = 12,     /* CTA-pair GEMM soft lockstep: bits 0-15 = chunk of K-steps
-                                  (0 = off), bits 16+ = slack in chunks (0 = 2) */
+  ESPO_OPT_GEMM_SYNC = 12,     /* soft lockstep of the backward's dh / dW CTA-pair GEMMs:
+                                  bits 0-15 = chunk of K-steps (0 = off, default), bits 16+ =
+                                  slack in chunks (0 = 2); the LM-head forward / dz GEMMs have
+                                  their own (ESPO_OPT_LMHEAD_RASTER bit 27) */
   ESPO_OPT_LMHEAD_IMPL = 13,   /* fused LM-head forward and backward recompute: 0 (default) = on
                                   the tcgen05 GEMM core (CTA-pair 256 × 512 tiles in a grouped
                                   raster, per-tile partials merged like vocabulary shards);
                                   1 = the dedicated kernels (part × row-block grid; ESPO_OPT_LMHEAD_2CTA
                                   / _PARTS apply) */
-  ESPO_OPT_LMHEAD_RASTER = 14  /* impl 0: bits 0-15 = M-tiles per raster group (0 = auto: 32 at
-                                  d ≤ 4096, 64 above), bits
-                                  16-23 = L2 policies (A | B << 2, 1 evict_first, 2 evict_last),
-                                  bit 24 = 256 × 256 tiles (double-buffered) instead of 256 × 512,
-                                  bit 25 = 4-CTA clusters (two pairs sharing A by TMA multicast),
-                                  bit 26 = no split-K for the backward's dh GEMM (default: split in
-                                  two when it has fewer than 6 waves of tiles) */
+  ESPO_OPT_LMHEAD_RASTER = 14  /* impl 0: bits 0-15 = M-tiles per raster group (0 = auto: 16),
+                                  bits 16-23 = L2 policies (A | B << 2, 1 evict_first, 2
+                                  evict_last), bit 24 = 256 × 256 tiles (double-buffered) instead
+                                  of 256 × 512, bit 25 = 4-CTA clusters (two pairs sharing A by
+                                  TMA multicast), bit 26 = no split-K for the backward's dh GEMM
+                                  (default: split in two when it has fewer than 6 waves of
+                                  tiles), bit 27 = no soft lockstep of the forward / dz GEMM
+                                  (default on: a cluster more than 2 chunks of 8 K-steps ahead
+                                  of the slowest cluster of its wave waits, so the wave's
+                                  operand panels are read from DRAM once) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

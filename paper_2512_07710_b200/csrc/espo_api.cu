@@ -161,6 +161,7 @@ struct espo_ctx_s {
                                  // 1 = 256 × 256 (double-buffered, epilogue overlapped)
   int lmh_group_m = 0, lmh_hints = 0;   // LM-head fwd / dz on the GEMM core: raster (0 = auto),
                                         // L2 policies
+  int lmh_sync = 8 | (2 << 16);  // their soft lockstep (chunk of K-steps | slack << 16; 0 = off)
   size_t lmh_live_cap = 0;
   int gemm_sync_chunk = 0, gemm_sync_slack = 2;  // GEMM soft lockstep (0 = off), k_gemm.cuh
   void* gemm_sync = nullptr;     // per-wave progress counters
@@ -507,6 +508,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->lmh_tile256 = int((value >> 24) & 1);
       c->lmh_mcast = int((value >> 25) & 1);
       c->lmh_split_k = int(((value >> 26) & 1) ^ 1);   // bit 26: no split-K for dh
+      c->lmh_sync = ((value >> 27) & 1) ? 0 : 8 | (2 << 16);   // bit 27: no lockstep
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_IMPL:
       if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
@@ -916,7 +918,8 @@ int lmhead_parts(const espo_ctx_s* c, int mblocks, int ntiles, int d) {
 // M-tiles per raster group of the LM-head GEMM-core kernels: 32 at d ≤ 4096, 64 above
 // (tools/bench_lmhead_fwd_ab.py, tools/gemm_sweep.py: sustained A/B on one B200)
 int lmh_raster(const espo_ctx_s* c, int d) {
-  return c->lmh_group_m > 0 ? c->lmh_group_m : (d > 4096 ? 64 : 32);
+  (void)d;
+  return c->lmh_group_m > 0 ? c->lmh_group_m : 16;
 }
 
 // Clusters of `csize` CTAs (one per SM at this smem size) that can be resident at once: a
@@ -961,7 +964,7 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
                              int N, int64_t K, void* C, int64_t ldc, int kind, int group_m,
                              int hints, cudaStream_t s, const GemmDyn& dyn = GemmDyn(),
                              const LmEpi* lm = nullptr, float* split_out = nullptr,
-                             int64_t split_ld = 0) {
+                             int64_t split_ld = 0, int sync_opt = -1) {
   // kind: 0 = one CTA per 128 × 256 tile, 1 = CTA pair 256 × 256, 2 = CTA pair 256 × 512,
   // 3 = two CTA pairs per cluster sharing A by multicast, 256 × 512 tiles each
   static unsigned long long attr = 0, attr2 = 0, attr3 = 0, attr4 = 0;
@@ -996,8 +999,10 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
   if (tiles == 0 || p.kblk == 0) return ESPO_OK;
   if (tiles > INT32_MAX) return ESPO_ERR_INVALID_ARGUMENT;
   p.sync = nullptr;
-  p.sync_chunk = std::max(1, c->gemm_sync_chunk);
-  p.sync_slack = std::max(1, c->gemm_sync_slack);
+  // soft lockstep: the caller's setting (chunk | slack << 16, 0 = off) or the context option
+  const int sync_chunk = sync_opt >= 0 ? (sync_opt & 0xFFFF) : c->gemm_sync_chunk;
+  p.sync_chunk = std::max(1, sync_chunk);
+  p.sync_slack = std::max(1, sync_opt >= 0 ? (sync_opt >> 16) : c->gemm_sync_slack);
   p.sync_timeout_ns = 200000;
   static int res2 = 0, res3 = 0, res4 = 0;   // resident clusters per kernel (this process's GPU)
   if (kind == 3) {
@@ -1015,7 +1020,7 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
                                                  G2<512>::kSmem, c->num_sms, res3)
                          : max_resident_clusters(k_umma_gemm2<kAMN, kBMN, kOut, 256>, 2, kG2Threads,
                                                  G2<256>::kSmem, c->num_sms, res2)));
-    if (c->gemm_sync_chunk > 0) {              // one zeroed progress counter per wave
+    if (sync_chunk > 0) {                      // one zeroed progress counter per wave
       const int64_t waves = (tiles + clusters - 1) / clusters;
       if (size_t(waves) * 4 > c->gemm_sync_cap) {
         if (c->gemm_sync) cudaFree(c->gemm_sync);
@@ -1114,7 +1119,8 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
     lm.err = c->ws.err;
     st = launch_umma_gemm<false, false, kOutLmFwd>(c, mh, mw, int(n_rows), V, d, nullptr, 0,
                                                    c->lmh_tile256 ? 1 : c->lmh_mcast ? 3 : 2,
-                                                   lmh_raster(c, d), c->lmh_hints, s, GemmDyn(), &lm);
+                                                   lmh_raster(c, d), c->lmh_hints, s, GemmDyn(), &lm,
+                                                   nullptr, 0, c->lmh_sync);
     if (st != ESPO_OK) return st;
     {
       const int grid = static_cast<int>(std::min<int64_t>((n_rows + 7) / 8, int64_t(c->num_sms) * 16));
@@ -1304,7 +1310,7 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       }
       const espo_status st = launch_umma_gemm<false, false, kOutLmDz>(
           c, mh, mw_k128, n, int(ldz), d, nullptr, 0, c->lmh_tile256 ? 1 : c->lmh_mcast ? 3 : 2,
-          lmh_raster(c, d), c->lmh_hints, s, dz_dyn, &lm);
+          lmh_raster(c, d), c->lmh_hints, s, dz_dyn, &lm, nullptr, 0, c->lmh_sync);
       if (st != ESPO_OK) return st;
     } else if (c->lmh_2cta) {
       k_lmhead2_dz<<<dim3(2 * parts, (mblocks + 1) / 2), kLmThreads, kL2Smem, s>>>(mh, mw, lp);

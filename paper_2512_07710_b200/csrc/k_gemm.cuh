@@ -585,7 +585,13 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
         gemm_tile_coords(ps, item % tiles, mb, nb);
         nb = nb * kPairs + int(pair);
         krange(item, kb0, kb1);
-        if (p.lm.mlive && !p.lm.mlive[mb]) continue;     // no row to compute: skipped tile
+        if (p.lm.mlive && !p.lm.mlive[mb]) {             // no row to compute: skipped tile
+          if (pace)        // it still reports every chunk, so its wave never waits for it
+            for (int kb = (kb0 + p.sync_chunk - 1) / p.sync_chunk * p.sync_chunk; kb < kb1;
+                 kb += p.sync_chunk)
+              if (kb > 0) atomicAdd(p.sync + wave, 1u);
+          continue;
+        }
         const int m0 = mb * 2 * kGmBM + int(rank) * kGmBM;
         const int n0 = nb * kNP + int(rank) * 128;
         const unsigned members = unsigned(min(nclusters, items - wave * nclusters));

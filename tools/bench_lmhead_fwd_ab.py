@@ -2,7 +2,11 @@
 V = 151,936: ESPO_OPT_LMHEAD_IMPL 0 (GEMM core, pair 256×512 tiles, per-tile partials) over a
 few raster groups, impl 1 (dedicated one-CTA kernel), and torch.matmul bf16 (cuBLAS, writing
 the logits). Settings interleaved over rounds, `burst` calls back to back each (sustained
-clocks). usage: python tools/bench_lmhead_fwd_ab.py [d] [rounds] [burst]"""
+clocks). usage: python tools/bench_lmhead_fwd_ab.py [d] [rounds] [burst] [set]
+sets "sync" / "sync2" (raster groups × lockstep chunk / slack) were measured while
+ESPO_OPT_GEMM_SYNC still governed these launches (tools/experiments/r2aq.sh, r2ar.sh); now a 4th
+element 0 turns the forward's lockstep off (ESPO_OPT_LMHEAD_RASTER bit 27) and any other value
+keeps the default (8 K-steps, slack 2). Set "default2": the default against the earlier rasters."""
 import json
 import os
 import statistics
@@ -11,10 +15,11 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2512_07710_b200.espo import OPT_LMHEAD_IMPL, OPT_LMHEAD_RASTER, Espo  # noqa: E402
+from paper_2512_07710_b200.espo import (OPT_GEMM_SYNC, OPT_LMHEAD_IMPL, OPT_LMHEAD_RASTER,  # noqa: E402
+                                        Espo)
 
 
-def main(d=4096, rounds=3, burst=4, n=32768, V=151936):
+def main(d=4096, rounds=3, burst=4, which="default", n=32768, V=151936):
     dev = torch.device("cuda", 0)
     torch.manual_seed(0)
     h = (torch.randn(n, d, device=dev) / d ** 0.5 * 3).to(torch.bfloat16)
@@ -30,6 +35,19 @@ def main(d=4096, rounds=3, burst=4, n=32768, V=151936):
     cfgs = {"gemm_g32": (0, 32, 0), "gemm_g64": (0, 64, 0), "mc_g16": (0, 16, MC),
             "mc_g32": (0, 32, MC), "mc_g64": (0, 64, MC), "mc_g128": (0, 128, MC),
             "dedicated_1cta": (1, 8, 0), "cublas": None}
+    if which == "sync":          # (impl, group, hints, lockstep chunk | slack << 16)
+        cfgs = {"gemm_g32": (0, 32, 0, 0), "g32_sync8": (0, 32, 0, 8 | 2 << 16),
+                "g16_sync8": (0, 16, 0, 8 | 2 << 16), "g12_sync8": (0, 12, 0, 8 | 2 << 16),
+                "g12": (0, 12, 0, 0), "g32_sync4": (0, 32, 0, 4 | 1 << 16), "cublas": None}
+    if which == "default2":      # the default (g16 + lockstep) against the earlier g32
+        cfgs = {"default": (0, 0, 0), "g32_nolock": (0, 32, 0, 0), "g64_nolock": (0, 64, 0, 0),
+                "cublas": None}
+    if which == "sync2":
+        cfgs = {"g16_s8_2": (0, 16, 0, 8 | 2 << 16), "g16_s16_2": (0, 16, 0, 16 | 2 << 16),
+                "g16_s8_4": (0, 16, 0, 8 | 4 << 16), "g16_s4_2": (0, 16, 0, 4 | 2 << 16),
+                "g24_s8_2": (0, 24, 0, 8 | 2 << 16), "g8_s8_2": (0, 8, 0, 8 | 2 << 16),
+                "g32_s8_2": (0, 32, 0, 8 | 2 << 16), "g16_s8_1": (0, 16, 0, 8 | 1 << 16),
+                "cublas": None}
     times = {k: [] for k in cfgs}
     losses = {}
     for _ in range(rounds):
@@ -37,9 +55,12 @@ def main(d=4096, rounds=3, burst=4, n=32768, V=151936):
             if c is None:
                 fn = lambda: torch.matmul(h, W.T)
             else:
-                impl, g, hints = c
+                impl, g, hints = c[:3]
                 ctx.set_option(OPT_LMHEAD_IMPL, impl)
                 ctx.set_option(OPT_LMHEAD_RASTER, g | (hints << 16))
+                ctx.set_option(OPT_GEMM_SYNC, 0)
+                if len(c) > 3 and c[3] == 0:
+                    ctx.set_option(OPT_LMHEAD_RASTER, g | (hints << 16) | (1 << 27))
 
                 def fn():
                     ctx.prepare(rewards, gid, so, n_tokens=n)
@@ -65,5 +86,5 @@ def main(d=4096, rounds=3, burst=4, n=32768, V=151936):
 
 
 if __name__ == "__main__":
-    a = [int(x) for x in sys.argv[1:]]
+    a = [int(x) for x in sys.argv[1:4]] + sys.argv[4:5]
     main(*a)

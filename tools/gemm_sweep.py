@@ -48,6 +48,9 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1):
         "dh256": (0, 0, -1, 1, 0, 0, 0),
     }
     cfgs["dh256"] = (3, G(0, 8), -1, 1, 0, 0, 0)
+    NOLOCK = 1 << 27
+    cfgs["dz_g32_nolock"] = (0, 0, -1, 1, 0, 0, 32 | NOLOCK)     # round-2 dz raster
+    cfgs["dz_g16_nolock"] = (0, 0, -1, 1, 0, 0, 16 | NOLOCK)
     times = {k: [] for k in cfgs}
     for _ in range(rounds):
         for k, (impl, gm, hints, compact, sync, lmi, lmr) in cfgs.items():
