@@ -533,7 +533,11 @@ typedef enum {
                                   tiles), bit 27 = no soft lockstep of the forward / dz GEMM
                                   (default on: a cluster more than 2 chunks of 8 K-steps ahead
                                   of the slowest cluster of its wave waits, so the wave's
-                                  operand panels are read from DRAM once) */
+                                  operand panels are read from DRAM once), bit 28 =
+                                  every 256 × 512 CTA-pair GEMM (also dh / dW) releases its
+                                  accumulator whole instead of in halves (default: the next
+                                  tile's first K-steps on columns 0-255 overlap the epilogue's
+                                  read of 256-511) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

@@ -162,6 +162,7 @@ struct espo_ctx_s {
   int lmh_group_m = 0, lmh_hints = 0;   // LM-head fwd / dz on the GEMM core: raster (0 = auto),
                                         // L2 policies
   int lmh_sync = 8 | (2 << 16);  // their soft lockstep (chunk of K-steps | slack << 16; 0 = off)
+  int gemm_half_release = 1;     // CTA-pair 256 × 512 GEMMs: accumulator released in halves
   size_t lmh_live_cap = 0;
   int gemm_sync_chunk = 0, gemm_sync_slack = 2;  // GEMM soft lockstep (0 = off), k_gemm.cuh
   void* gemm_sync = nullptr;     // per-wave progress counters
@@ -509,6 +510,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->lmh_mcast = int((value >> 25) & 1);
       c->lmh_split_k = int(((value >> 26) & 1) ^ 1);   // bit 26: no split-K for dh
       c->lmh_sync = ((value >> 27) & 1) ? 0 : 8 | (2 << 16);   // bit 27: no lockstep
+      c->gemm_half_release = int(((value >> 28) & 1) ^ 1);    // bit 28: whole-accumulator release
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_IMPL:
       if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
@@ -975,6 +977,7 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
   p.ksplit = split_out ? 2 : 1;                 // split-K over 2 (kOutF32 on pairs only)
   p.split_out = split_out;
   p.split_ld = split_ld;
+  p.half_release = c->gemm_half_release;
   if (split_out && (kOut != kOutF32 || kind == 0)) return ESPO_ERR_INVALID_ARGUMENT;
   if ((kOut == kOutLmFwd || kOut == kOutLmDz) && kind == 0) return ESPO_ERR_INVALID_ARGUMENT;
   p.dyn_count = dyn.count;

@@ -15,10 +15,11 @@
 //   k_umma_gemm   one CTA per 128 × 256 tile, two TMEM accumulators (epilogue overlapped);
 //   k_umma_gemm2  CTA pairs (cta_group::2, M = 256 split over the pair's SMs, B columns split
 //                 likewise): 256 × 256 tiles (two accumulators) or 256 × 512 (one 512-column
-//                 accumulator = all of TMEM, a quarter less L2 → SM traffic per FLOP), 8
-//                 epilogue warps; grouped tile raster, L2 cache-policy hints, device-side row
-//                 counts (compacted operands), split-K over 2 (deterministic), optional soft
-//                 lockstep between clusters;
+//                 accumulator = all of TMEM, a quarter less L2 → SM traffic per FLOP, released
+//                 in two column halves so the next tile's first K-steps overlap the epilogue),
+//                 8 epilogue warps; grouped tile raster, L2 cache-policy hints, device-side row
+//                 counts (compacted operands), split-K over 2 (deterministic), soft lockstep
+//                 between the clusters of a wave;
 //   k_umma_gemm4  two pairs per cluster sharing A through TMA multicast (an option: only 33
 //                 four-CTA clusters are resident on a B200, 132 of 148 SMs).
 // Grids are sized from the resident cluster count (host side). Every barrier wait is bounded by
@@ -101,6 +102,8 @@ struct GemmParams {
   int ksplit;
   float* split_out;
   int64_t split_ld;
+  int half_release;       // 512-column accumulators: overlap the next tile's first K-steps on
+                          // half 0 with the epilogue's read of half 1 (1, default) or not (0)
 };
 
 // wait until *ctr ≥ target or the timeout expired (acquire; a soft barrier: never deadlocks)
@@ -659,7 +662,43 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
         gm_wait_cluster(smem_u32(&tempty[acc]), (use & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t dt = tmem + uint32_t(acc * kGmBN);
-        for (int kb = kb0; kb < kb1; ++kb, ++q) {
+        int kbs = kb0;
+        if constexpr (kNP == 512) {
+          // One 512-column accumulator, released in halves (tempty[0] = columns 0-255 read,
+          // tempty[1] = 256-511): the first P K-steps go to half 0 only, while the epilogue
+          // still reads the previous tile's half 1; their half-1 MMAs follow from the same
+          // (still held) stages once half 1 is free. Hides half of the epilogue.
+          const int P = p.half_release ? min(kG2Stages, kb1 - kb0) : 0;
+          for (int j = 0; j < P; ++j) {
+            const uint32_t qj = q + uint32_t(j);
+            const int s = qj % kG2Stages;
+            gm_wait_cluster(smem_u32(&full[s]), (qj / kG2Stages) & 1u);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + s * kG2ABytes), b0 = smem_u32(sB + s * kG2BBytes);
+#pragma unroll
+            for (int k = 0; k < kGmBK / 16; ++k) {
+              const uint64_t ad = kAMN ? umma_desc_sw128_mn(a0 + k * 2048) : umma_desc_sw128(a0 + k * 32);
+              const uint64_t bd = kBMN ? umma_desc_sw128_mn(b0 + k * 2048) : umma_desc_sw128(b0 + k * 32);
+              tc_mma_pair(dt, ad, bd, idesc, (j != 0) || (k != 0));
+            }
+          }
+          gm_wait_cluster(smem_u32(&tempty[1]), (use & 1u) ^ 1u);
+          tc_fence_after();
+          for (int j = 0; j < P; ++j, ++q) {
+            const int s = q % kG2Stages;
+            const uint32_t a0 = smem_u32(sA + s * kG2ABytes);
+            const uint32_t bh = smem_u32(sB + s * kG2BBytes) + 128 * kGmBK * 2;
+#pragma unroll
+            for (int k = 0; k < kGmBK / 16; ++k) {
+              const uint64_t ad = kAMN ? umma_desc_sw128_mn(a0 + k * 2048) : umma_desc_sw128(a0 + k * 32);
+              const uint64_t bd = kBMN ? umma_desc_sw128_mn(bh + k * 2048) : umma_desc_sw128(bh + k * 32);
+              tc_mma_pair(dt + 256u, ad, bd, idesc, (j != 0) || (k != 0));
+            }
+            tc_commit_mask(smem_u32(&empty[s]), kPairs == 2 ? uint16_t(0xF) : pair_mask);
+          }
+          kbs = kb0 + P;
+        }
+        for (int kb = kbs; kb < kb1; ++kb, ++q) {
           const int s = q % kG2Stages;
           gm_wait_cluster(smem_u32(&full[s]), (q / kG2Stages) & 1u);
           tc_fence_after();
@@ -706,9 +745,49 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
       ++i;
       gm_wait_cluster(smem_u32(&tfull[acc]), use & 1u);
       tc_fence_after();
+      const int r = mb * 2 * kGmBM + int(rank) * kGmBM + row;
+      if constexpr (kNP == 512) {
+        // both warp groups drain accumulator half 0 (128 columns each), release it, then half 1
+        const uint32_t lb = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(chalf * 128);
+        const int cb = nb * kNP + chalf * 128;
+        if constexpr (kOut == kOutLmFwd) {
+          const bool valid = r < p.M && p.lm.flag[r];
+          const int y = valid ? p.lm.tokens[r] : -1;
+          float R = -INFINITY, S = 0.f, W = 0.f, cS = 0.f, cW = 0.f, uy = __int_as_float(0x7fc00000);
+#pragma unroll 1
+          for (int hh = 0; hh < 2; ++hh) {
+            lm_fwd_cols(p, lb + uint32_t(hh * 256), r, cb + hh * 256, R, S, W, cS, cW, uy, valid, y, 4);
+            __syncwarp();
+            tc_fence_before();
+            arrive_remote(hh ? leader_tempty1 : leader_tempty0);
+          }
+          if (valid && nb < p.nblk)   // one partial per (tile, column group): partial[2·nb + chalf][row]
+            p.lm.partial[int64_t(2 * nb + chalf) * p.lm.n_rows + r] = make_float4(R, S - cS, W - cW, uy);
+        } else if constexpr (kOut == kOutLmDz) {
+          BwdRec rc;
+          rc.ng = 0.f;
+          rc.y = -1;
+          if (r < p.M) rc = p.lm.rec[r];
+#pragma unroll 1
+          for (int hh = 0; hh < 2; ++hh) {
+            lm_dz_cols(p, lb + uint32_t(hh * 256), r, cb + hh * 256, rc, 4);
+            __syncwarp();
+            tc_fence_before();
+            arrive_remote(hh ? leader_tempty1 : leader_tempty0);
+          }
+        } else {
+#pragma unroll 1
+          for (int hh = 0; hh < 2; ++hh) {
+            gemm_store_tile<kOut>(second ? p1 : p, lb + uint32_t(hh * 256), r, cb + hh * 256, pol_c, 4);
+            __syncwarp();
+            tc_fence_before();
+            arrive_remote(hh ? leader_tempty1 : leader_tempty0);
+          }
+        }
+        continue;
+      }
       const uint32_t base = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * kGmBN) +
                             uint32_t(chalf * kCols);
-      const int r = mb * 2 * kGmBM + int(rank) * kGmBM + row;
       const int c0 = nb * kNP + chalf * kCols;         // first tile column this thread drains
       if constexpr (kOut == kOutLmFwd) {
         const bool valid = r < p.M && p.lm.flag[r];

@@ -42,6 +42,8 @@ def main(d=4096, rounds=3, burst=4, which="default", n=32768, V=151936):
     if which == "default2":      # the default (g16 + lockstep) against the earlier g32
         cfgs = {"default": (0, 0, 0), "g32_nolock": (0, 32, 0, 0), "g64_nolock": (0, 64, 0, 0),
                 "cublas": None}
+    if which == "half":          # accumulator released in halves (default) or whole (bit 28)
+        cfgs = {"default": (0, 0, 0), "whole_release": (0, 0, 1 << 12), "cublas": None}
     if which == "sync2":
         cfgs = {"g16_s8_2": (0, 16, 0, 8 | 2 << 16), "g16_s16_2": (0, 16, 0, 16 | 2 << 16),
                 "g16_s8_4": (0, 16, 0, 8 | 4 << 16), "g16_s4_2": (0, 16, 0, 4 | 2 << 16),

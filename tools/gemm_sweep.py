@@ -1,6 +1,7 @@
 """A/B sweep of the LM-head backward's GEMM settings (ESPO_OPT_LMHEAD_BWD_GEMM, _GEMM_GROUP_M,
 _GEMM_HINTS): time espo_lmhead_bwd on one 8192-row sub-chunk per setting, interleaved over
-rounds (median), same data. Prints one JSON line. usage: python tools/gemm_sweep.py [d] [n]"""
+rounds (median), same data. Prints one JSON line.
+usage: python tools/gemm_sweep.py [d] [n] [V] [rounds] [burst] [set: default | sync]"""
 import json
 import os
 import statistics
@@ -14,7 +15,7 @@ from paper_2512_07710_b200.espo import (OPT_GEMM_GROUP_M, OPT_GEMM_HINTS,  # noq
                                         OPT_LMHEAD_IMPL, OPT_LMHEAD_RASTER, Espo)
 
 
-def main(d=4096, n=8192, V=151936, rounds=5, burst=1):
+def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
     """burst = back-to-back timed calls per setting and round (burst > 1: sustained clocks)."""
     dev = torch.device("cuda", 0)
     torch.manual_seed(0)
@@ -51,6 +52,17 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1):
     NOLOCK = 1 << 27
     cfgs["dz_g32_nolock"] = (0, 0, -1, 1, 0, 0, 32 | NOLOCK)     # round-2 dz raster
     cfgs["dz_g16_nolock"] = (0, 0, -1, 1, 0, 0, 16 | NOLOCK)
+    if which == "half":          # 512-column accumulators released in halves (default) or whole
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "whole_release": (0, 0, -1, 1, 0, 0, 1 << 28)}
+    if which == "sync":          # soft lockstep of the dh / dW GEMMs (ESPO_OPT_GEMM_SYNC)
+        L = lambda ch, sl: ch | (sl << 16)
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "sync8": (0, 0, -1, 1, L(8, 2), 0, 0), "sync16": (0, 0, -1, 1, L(16, 2), 0, 0),
+                "sync32": (0, 0, -1, 1, L(32, 2), 0, 0),
+                "sync16_dh16": (0, G(16, 0), -1, 1, L(16, 2), 0, 0),
+                "sync16_dh4": (0, G(4, 0), -1, 1, L(16, 2), 0, 0),
+                "sync16_dw4": (0, G(0, 4), -1, 1, L(16, 2), 0, 0)}
     times = {k: [] for k in cfgs}
     for _ in range(rounds):
         for k, (impl, gm, hints, compact, sync, lmi, lmr) in cfgs.items():
@@ -78,5 +90,5 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1):
 
 
 if __name__ == "__main__":
-    a = [int(x) for x in sys.argv[1:]]
+    a = [int(x) for x in sys.argv[1:6]] + sys.argv[6:7]
     main(*a)
