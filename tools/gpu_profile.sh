@@ -25,6 +25,10 @@ $Q --factored > gpurun_out/plain_fq.log 2>&1 && ncu --set full --clock-control n
 timeout 900 python tools/bench_lmhead_bwd.py 4096 16384 > gpurun_out/bench_lmhead_bwd_dense.json 2>/dev/null; echo "lmhead bwd dense exit=$?"
 timeout 900 python tools/bench_lmhead_bwd.py 4096 32768 realistic > gpurun_out/bench_lmhead_bwd_realistic.json 2>/dev/null; echo "lmhead bwd realistic exit=$?"
 timeout 900 python tools/gemm_sweep.py 4096 8192 151936 3 6 > gpurun_out/gemm_sweep.json 2>/dev/null; echo "gemm sweep exit=$?"
+timeout 900 python tools/bench_lmhead_fwd_ab.py 4096 3 4 default2 > gpurun_out/bench_lmhead_fwd_d4096.json 2>/dev/null; echo "lmhead fwd 4096 exit=$?"
+timeout 900 python tools/bench_lmhead_fwd_ab.py 8192 2 3 default2 > gpurun_out/bench_lmhead_fwd_d8192.json 2>/dev/null; echo "lmhead fwd 8192 exit=$?"
+MF=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,sm__cycles_elapsed.avg.per_second,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum
+for d in 4096 8192; do timeout 300 ncu --metrics $MF --clock-control none --csv -k regex:"k_umma_gemm" -s 1 -c 1 python tools/lmhead_fwd_once.py $d 32768 0 0 2 > gpurun_out/ncu_lmhead_fwd_d$d.csv 2>&1; echo "ncu lmhead fwd $d exit=$?"; done
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,sm__cycles_elapsed.avg.per_second
 timeout 600 ncu --metrics $M --clock-control none --cache-control none --csv --log-file gpurun_out/launches_lmhead_bwd.csv python tools/lmhead_bwd_once.py 4096 8192 0 > /dev/null 2>&1; echo "lm ll exit=$?"
 timeout 600 ncu --metrics $M --clock-control none --cache-control none --csv --log-file gpurun_out/launches_lmhead_bwd_cublas.csv python tools/lmhead_bwd_once.py 4096 8192 1 > /dev/null 2>&1; echo "lm ll cublas exit=$?"

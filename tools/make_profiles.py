@@ -166,6 +166,8 @@ def main(tag, out_dir="gpurun_out"):
               "bench_C4_strong_verify.json", "bench_C1_strong_verify.json",
               "bench_C1_emulate2.json", "bench_C1_emulate4.json", "bench_C1_emulate8.json",
               "bench_C4_emulate8.json", "bench_lmhead_bwd_dense.json",
+              "bench_lmhead_fwd_d4096.json", "bench_lmhead_fwd_d8192.json",
+              "ncu_lmhead_fwd_d4096.csv", "ncu_lmhead_fwd_d8192.csv",
               "bench_lmhead_bwd_realistic.json", "gemm_sweep.json"):
         p = os.path.join(src, f)
         if os.path.exists(p):
