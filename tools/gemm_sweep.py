@@ -55,6 +55,13 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
     if which == "half":          # 512-column accumulators released in halves (default) or whole
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
                 "whole_release": (0, 0, -1, 1, 0, 0, 1 << 28)}
+    if which == "dw":            # dW on 256 × 512 pair tiles (kind 4: dh too) × N-groups × lockstep
+        L = lambda ch, sl: ch | (sl << 16)
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "dw512_n8": (4, G(0, 8), -1, 1, 0, 0, 0), "dw512_n4": (4, G(0, 4), -1, 1, 0, 0, 0),
+                "dw512_n2": (4, G(0, 2), -1, 1, 0, 0, 0),
+                "dw512_n8_sync8": (4, G(0, 8), -1, 1, L(8, 2), 0, 0),
+                "default_sync8": (0, 0, -1, 1, L(8, 2), 0, 0)}
     if which == "sync":          # soft lockstep of the dh / dW GEMMs (ESPO_OPT_GEMM_SYNC)
         L = lambda ch, sl: ch | (sl << 16)
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
