@@ -516,9 +516,10 @@ typedef enum {
   ESPO_OPT_LMHEAD_COMPACT = 11, /* espo_lmhead_bwd: 1 (default) = recompute and contract only the
                                   rows with gradient (c_t ≠ 0; needs d % 8 == 0), 0 = all rows */
   ESPO_OPT_GEMM_SYNC = 12,     /* soft lockstep of the backward's dh / dW CTA-pair GEMMs:
-                                  bits 0-15 = chunk of K-steps (0 = off, default), bits 16+ =
-                                  slack in chunks (0 = 2); the LM-head forward / dz GEMMs have
-                                  their own (ESPO_OPT_LMHEAD_RASTER bit 27) */
+                                  bits 0-15 = chunk of K-steps (0 = off, default), bits 16-31 =
+                                  slack in chunks (0 = 2); bits 32-47 / 48-63 = the same for the
+                                  dW GEMM alone (0 = as above); the LM-head forward / dz GEMMs
+                                  have their own (ESPO_OPT_LMHEAD_RASTER bit 27) */
   ESPO_OPT_LMHEAD_IMPL = 13,   /* fused LM-head forward and backward recompute: 0 (default) = on
                                   the tcgen05 GEMM core (CTA-pair 256 × 512 tiles in a grouped
                                   raster, per-tile partials merged like vocabulary shards);

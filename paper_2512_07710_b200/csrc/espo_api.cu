@@ -163,6 +163,7 @@ struct espo_ctx_s {
                                         // L2 policies
   int lmh_sync = 8 | (2 << 16);  // their soft lockstep (chunk of K-steps | slack << 16; 0 = off)
   int gemm_half_release = 1;     // CTA-pair 256 × 512 GEMMs: accumulator released in halves
+  int gemm_sync_dw = -1;         // dW GEMM's own lockstep (chunk | slack << 16; −1 = as dh)
   size_t lmh_live_cap = 0;
   int gemm_sync_chunk = 0, gemm_sync_slack = 2;  // GEMM soft lockstep (0 = off), k_gemm.cuh
   void* gemm_sync = nullptr;     // per-wave progress counters
@@ -497,11 +498,17 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->gemm_hints_dh = value < 0 ? -1 : int(value & 0xFF);
       c->gemm_hints_dw = value < 0 ? -1 : int((value >> 8) & 0xFF);
       return ESPO_OK;
-    case ESPO_OPT_GEMM_SYNC:      // chunk (K-steps) | slack << 16; 0 = off
-      if (value < 0 || (value & 0xFFFF) > 4096 || (value >> 16) > 64) return ESPO_ERR_INVALID_ARGUMENT;
-      c->gemm_sync_chunk = int(value & 0xFFFF);
-      c->gemm_sync_slack = (value >> 16) ? int(value >> 16) : 2;
+    case ESPO_OPT_GEMM_SYNC: {    // chunk (K-steps) | slack << 16 (dh and dW); bits 32+: the
+                                  // same for dW alone (0 = as dh); 0 = off
+      const int64_t lo = value & 0xFFFFFFFFll, hi = value >> 32;
+      if (value < 0 || (lo & 0xFFFF) > 4096 || (lo >> 16) > 64 || (hi & 0xFFFF) > 4096 ||
+          (hi >> 16) > 64)
+        return ESPO_ERR_INVALID_ARGUMENT;
+      c->gemm_sync_chunk = int(lo & 0xFFFF);
+      c->gemm_sync_slack = (lo >> 16) ? int(lo >> 16) : 2;
+      c->gemm_sync_dw = hi ? int((hi & 0xFFFF) | ((hi >> 16 ? hi >> 16 : 2) << 16)) : -1;
       return ESPO_OK;
+    }
     case ESPO_OPT_LMHEAD_RASTER:  // bits 0-15 group_m (0 = 8; negative = N-groups), 16-23 hints
       if (value < 0 || (value & 0xFFFF) > 1024) return ESPO_ERR_INVALID_ARGUMENT;
       c->lmh_group_m = int(value & 0xFFFF);
@@ -1391,7 +1398,8 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
         }
       }
       if (dweight) {   // dW[V, d] += dzᵀ[V, n] · h[n, d]: A = dz MN-major, B = h MN-major
-        st = launch_umma_gemm<true, true, kOutAddF32>(c, mdz_mn, mh_mn, V, d, n, dweight, lddw, kind_dw, g_dw, hint_dw, s, dyn_k);
+        st = launch_umma_gemm<true, true, kOutAddF32>(c, mdz_mn, mh_mn, V, d, n, dweight, lddw, kind_dw, g_dw, hint_dw, s, dyn_k,
+                                                      nullptr, nullptr, 0, c->gemm_sync_dw);
         if (st != ESPO_OK) return st;
       }
       continue;

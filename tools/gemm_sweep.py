@@ -62,6 +62,13 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
                 "dw512_n2": (4, G(0, 2), -1, 1, 0, 0, 0),
                 "dw512_n8_sync8": (4, G(0, 8), -1, 1, L(8, 2), 0, 0),
                 "default_sync8": (0, 0, -1, 1, L(8, 2), 0, 0)}
+    if which == "syncdw":        # soft lockstep of the dW GEMM alone (bits 32+)
+        Ldw = lambda ch, sl: (ch | (sl << 16)) << 32
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "dw_sync4": (0, 0, -1, 1, Ldw(4, 2), 0, 0), "dw_sync8": (0, 0, -1, 1, Ldw(8, 2), 0, 0),
+                "dw_sync16": (0, 0, -1, 1, Ldw(16, 2), 0, 0), "dw_sync8_s1": (0, 0, -1, 1, Ldw(8, 1), 0, 0),
+                "dw_sync8_n4": (0, G(0, 4), -1, 1, Ldw(8, 2), 0, 0),
+                "dw_sync8_n16": (0, G(0, 16), -1, 1, Ldw(8, 2), 0, 0)}
     if which == "sync":          # soft lockstep of the dh / dW GEMMs (ESPO_OPT_GEMM_SYNC)
         L = lambda ch, sl: ch | (sl << 16)
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
