@@ -508,7 +508,7 @@ typedef enum {
                                   256 × 512 each) for both; 6 = those for dh, default dW;
                                   1 = cuBLAS (A/B measurement only) */
   ESPO_OPT_GEMM_GROUP_M = 9,   /* backward GEMM tile order: bits 0-15 = dh M-blocks per raster
-                                  group (0 = auto, 8); bits 16-31 = dW N-blocks per group (0 = all
+                                  group (0 = auto: 8, 16 above d = 4096); bits 16-31 = dW N-blocks per group (0 = all
                                   of d, N fastest) */
   ESPO_OPT_GEMM_HINTS = 10,    /* L2 policies of the backward GEMMs for A/B measurement: bits 0-7
                                   dh, 8-15 dW, each A | B << 2 | C << 4 with 0 = normal,
@@ -516,10 +516,11 @@ typedef enum {
   ESPO_OPT_LMHEAD_COMPACT = 11, /* espo_lmhead_bwd: 1 (default) = recompute and contract only the
                                   rows with gradient (c_t ≠ 0; needs d % 8 == 0), 0 = all rows */
   ESPO_OPT_GEMM_SYNC = 12,     /* soft lockstep of the backward's dh / dW CTA-pair GEMMs:
-                                  bits 0-15 = chunk of K-steps (0 = off, default), bits 16-31 =
-                                  slack in chunks (0 = 2); bits 32-47 / 48-63 = the same for the
-                                  dW GEMM alone (0 = as above); the LM-head forward / dz GEMMs
-                                  have their own (ESPO_OPT_LMHEAD_RASTER bit 27) */
+                                  bits 0-15 = chunk of K-steps (0 = off), bits 16-31 = slack in
+                                  chunks (0 = 2); bits 32-47 / 48-63 = the same for the dW GEMM
+                                  alone (0 = as above). Not set (or −1): on (16 K-steps, slack 2)
+                                  for d > 4096, off below. The LM-head forward / dz GEMMs have their
+                                  own (ESPO_OPT_LMHEAD_RASTER bit 27) */
   ESPO_OPT_LMHEAD_IMPL = 13,   /* fused LM-head forward and backward recompute: 0 (default) = on
                                   the tcgen05 GEMM core (CTA-pair 256 × 512 tiles in a grouped
                                   raster, per-tile partials merged like vocabulary shards);

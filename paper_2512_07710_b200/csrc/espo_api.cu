@@ -164,6 +164,7 @@ struct espo_ctx_s {
   int lmh_sync = 8 | (2 << 16);  // their soft lockstep (chunk of K-steps | slack << 16; 0 = off)
   int gemm_half_release = 1;     // CTA-pair 256 × 512 GEMMs: accumulator released in halves
   int gemm_sync_dw = -1;         // dW GEMM's own lockstep (chunk | slack << 16; −1 = as dh)
+  int gemm_sync_set = 0;         // ESPO_OPT_GEMM_SYNC given (else: auto, on at d > 4096)
   size_t lmh_live_cap = 0;
   int gemm_sync_chunk = 0, gemm_sync_slack = 2;  // GEMM soft lockstep (0 = off), k_gemm.cuh
   void* gemm_sync = nullptr;     // per-wave progress counters
@@ -500,6 +501,13 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       return ESPO_OK;
     case ESPO_OPT_GEMM_SYNC: {    // chunk (K-steps) | slack << 16 (dh and dW); bits 32+: the
                                   // same for dW alone (0 = as dh); 0 = off
+      if (value == -1) {          // back to the automatic choice
+        c->gemm_sync_chunk = 0;
+        c->gemm_sync_slack = 2;
+        c->gemm_sync_dw = -1;
+        c->gemm_sync_set = 0;
+        return ESPO_OK;
+      }
       const int64_t lo = value & 0xFFFFFFFFll, hi = value >> 32;
       if (value < 0 || (lo & 0xFFFF) > 4096 || (lo >> 16) > 64 || (hi & 0xFFFF) > 4096 ||
           (hi >> 16) > 64)
@@ -507,6 +515,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->gemm_sync_chunk = int(lo & 0xFFFF);
       c->gemm_sync_slack = (lo >> 16) ? int(lo >> 16) : 2;
       c->gemm_sync_dw = hi ? int((hi & 0xFFFF) | ((hi >> 16 ? hi >> 16 : 2) << 16)) : -1;
+      c->gemm_sync_set = 1;
       return ESPO_OK;
     }
     case ESPO_OPT_LMHEAD_RASTER:  // bits 0-15 group_m (0 = 8; negative = N-groups), 16-23 hints
@@ -1349,7 +1358,12 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       // tile order: dh has a long K (the vocabulary) and few tiles: groups of 8 M-blocks keep
       // the resident tiles' A and B panels small; dW (K = rows): N fastest, so every M-block
       // of dz is read once while h stays in L2
-      const int g_dh = c->gemm_group_m > 0 ? c->gemm_group_m : 8;
+      const int g_dh = c->gemm_group_m > 0 ? c->gemm_group_m : (wide_dw ? 16 : 8);
+      // soft lockstep of dh / dW: the option if given, else on (16 K-steps, slack 2) above
+      // d = 4096 (sustained sweep: d = 8192 sub-chunk 52.5 → 50.0 ms; at d = 4096 it costs 2–5 %)
+      const int sync_auto = (!c->gemm_sync_set && wide_dw) ? (16 | (2 << 16)) : -1;
+      const int sync_dh = sync_auto;
+      const int sync_dw = c->gemm_sync_dw >= 0 ? c->gemm_sync_dw : sync_auto;
       // dW: groups of gemm_group_n_dw N-blocks (0 = N fastest over all of d)
       const int g_dw = c->gemm_group_n_dw > 0 ? -c->gemm_group_n_dw : (g == 0 ? (wide_dw ? -2 : -8) : 1);
       // L2 policies (2 bits each: A | B << 2 | C << 4; 1 = evict_first, 2 = evict_last):
@@ -1386,9 +1400,10 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
           }
         }
         st = dh_dtype == ESPO_BF16
-                 ? launch_umma_gemm<false, true, kOutBF16>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, kind_dh, g_dh, hint_dh, s, dyn_m)
+                 ? launch_umma_gemm<false, true, kOutBF16>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, kind_dh, g_dh, hint_dh, s, dyn_m,
+                                                           nullptr, nullptr, 0, sync_dh)
                  : launch_umma_gemm<false, true, kOutF32>(c, mdz_k, mw_mn, n, d, ldz, dh, lddh, kind_dh, g_dh, hint_dh, s, dyn_m,
-                                                          nullptr, split, d);
+                                                          nullptr, split, d, sync_dh);
         if (st != ESPO_OK) return st;
         if (split) {
           const int grid = c->num_sms * 8;
@@ -1399,7 +1414,7 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       }
       if (dweight) {   // dW[V, d] += dzᵀ[V, n] · h[n, d]: A = dz MN-major, B = h MN-major
         st = launch_umma_gemm<true, true, kOutAddF32>(c, mdz_mn, mh_mn, V, d, n, dweight, lddw, kind_dw, g_dw, hint_dw, s, dyn_k,
-                                                      nullptr, nullptr, 0, c->gemm_sync_dw);
+                                                      nullptr, nullptr, 0, sync_dw);
         if (st != ESPO_OK) return st;
       }
       continue;

@@ -589,10 +589,8 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
         nb = nb * kPairs + int(pair);
         krange(item, kb0, kb1);
         if (p.lm.mlive && !p.lm.mlive[mb]) {             // no row to compute: skipped tile
-          if (pace)        // it still reports every chunk, so its wave never waits for it
-            for (int kb = (kb0 + p.sync_chunk - 1) / p.sync_chunk * p.sync_chunk; kb < kb1;
-                 kb += p.sync_chunk)
-              if (kb > 0) atomicAdd(p.sync + wave, 1u);
+          if (pace && kb1 > kb0)   // it still reports every chunk, so its wave never waits for it
+            atomicAdd(p.sync + wave, unsigned((kb1 - kb0 - 1) / p.sync_chunk));
           continue;
         }
         const int m0 = mb * 2 * kGmBM + int(rank) * kGmBM;
@@ -601,8 +599,9 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
         for (int kb = kb0; kb < kb1; ++kb, ++q) {
           const int s = q % kG2Stages;
           const int k0 = kb * kGmBK;
-          if (pace && kb % p.sync_chunk == 0) {
-            const int c = kb / p.sync_chunk;       // entering chunk c: chunk c − 1 is issued
+          // chunks count from the item's first K-step (a split-K half starts mid-K)
+          if (pace && (kb - kb0) % p.sync_chunk == 0) {
+            const int c = (kb - kb0) / p.sync_chunk;   // entering chunk c: chunk c − 1 is issued
             if (c > 0) atomicAdd(p.sync + wave, 1u);
             if (c > p.sync_slack)
               soft_wait(p.sync + wave, unsigned(c - p.sync_slack) * members, p.sync_timeout_ns);

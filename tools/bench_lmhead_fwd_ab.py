@@ -60,7 +60,7 @@ def main(d=4096, rounds=3, burst=4, which="default", n=32768, V=151936):
                 impl, g, hints = c[:3]
                 ctx.set_option(OPT_LMHEAD_IMPL, impl)
                 ctx.set_option(OPT_LMHEAD_RASTER, g | (hints << 16))
-                ctx.set_option(OPT_GEMM_SYNC, 0)
+                ctx.set_option(OPT_GEMM_SYNC, -1)
                 if len(c) > 3 and c[3] == 0:
                     ctx.set_option(OPT_LMHEAD_RASTER, g | (hints << 16) | (1 << 27))
 

@@ -42,24 +42,24 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
     H2 = lambda dh, dw: dh | (dw << 8)
     MC = 1 << 25
     NOSPLIT = 1 << 26
-    cfgs = {                     # (gemm, group, hints, compact, sync, lmhead impl, lm raster)
-        "cublas": (1, 0, -1, 0, 0, 1, 0),
-        "default": (0, 0, -1, 1, 0, 0, 0),
-        "nosplit": (0, 0, -1, 1, 0, 0, NOSPLIT),
-        "dh256": (0, 0, -1, 1, 0, 0, 0),
+    cfgs = {                     # (gemm, group, hints, compact, sync (-1 auto), lmhead impl, lm raster)
+        "cublas": (1, 0, -1, 0, -1, 1, 0),
+        "default": (0, 0, -1, 1, -1, 0, 0),
+        "nosplit": (0, 0, -1, 1, -1, 0, NOSPLIT),
+        "dh256": (0, 0, -1, 1, -1, 0, 0),
     }
-    cfgs["dh256"] = (3, G(0, 8), -1, 1, 0, 0, 0)
+    cfgs["dh256"] = (3, G(0, 8), -1, 1, -1, 0, 0)
     NOLOCK = 1 << 27
-    cfgs["dz_g32_nolock"] = (0, 0, -1, 1, 0, 0, 32 | NOLOCK)     # round-2 dz raster
-    cfgs["dz_g16_nolock"] = (0, 0, -1, 1, 0, 0, 16 | NOLOCK)
+    cfgs["dz_g32_nolock"] = (0, 0, -1, 1, -1, 0, 32 | NOLOCK)    # round-2 dz raster
+    cfgs["dz_g16_nolock"] = (0, 0, -1, 1, -1, 0, 16 | NOLOCK)
     if which == "half":          # 512-column accumulators released in halves (default) or whole
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
-                "whole_release": (0, 0, -1, 1, 0, 0, 1 << 28)}
+                "whole_release": (0, 0, -1, 1, -1, 0, 1 << 28)}
     if which == "dw":            # dW on 256 × 512 pair tiles (kind 4: dh too) × N-groups × lockstep
         L = lambda ch, sl: ch | (sl << 16)
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
-                "dw512_n8": (4, G(0, 8), -1, 1, 0, 0, 0), "dw512_n4": (4, G(0, 4), -1, 1, 0, 0, 0),
-                "dw512_n2": (4, G(0, 2), -1, 1, 0, 0, 0),
+                "dw512_n8": (4, G(0, 8), -1, 1, -1, 0, 0), "dw512_n4": (4, G(0, 4), -1, 1, -1, 0, 0),
+                "dw512_n2": (4, G(0, 2), -1, 1, -1, 0, 0),
                 "dw512_n8_sync8": (4, G(0, 8), -1, 1, L(8, 2), 0, 0),
                 "default_sync8": (0, 0, -1, 1, L(8, 2), 0, 0)}
     if which == "syncdw":        # soft lockstep of the dW GEMM alone (bits 32+)
@@ -72,6 +72,7 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
     if which == "sync":          # soft lockstep of the dh / dW GEMMs (ESPO_OPT_GEMM_SYNC)
         L = lambda ch, sl: ch | (sl << 16)
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "nolock": (0, 0, -1, 1, 0, 0, 0), "nolock_dh8": (0, G(8, 0), -1, 1, 0, 0, 0),
                 "sync8": (0, 0, -1, 1, L(8, 2), 0, 0), "sync16": (0, 0, -1, 1, L(16, 2), 0, 0),
                 "sync32": (0, 0, -1, 1, L(32, 2), 0, 0),
                 "sync16_dh16": (0, G(16, 0), -1, 1, L(16, 2), 0, 0),

@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_07710_b200.espo import OPT_GEMM_SYNC, OPT_LMHEAD_BWD_GEMM, Espo  # noqa: E402
 
 
-def main(d=4096, n=8192, gemm=0, sync=0, V=151936):
+def main(d=4096, n=8192, gemm=0, sync=-1, V=151936):
     dev = torch.device("cuda", 0)
     torch.manual_seed(0)
     h = (torch.randn(n, d, device=dev) / d ** 0.5 * 3).to(torch.bfloat16)
