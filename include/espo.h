@@ -415,7 +415,10 @@ espo_status espo_loss_row_scale(espo_ctx_t ctx, const float* grad_loss_dev, floa
  * weight bf16 [vocab, ldw ≥ d] (the LM-head matrix, row v = vocabulary entry v), fp32
  * accumulation on the tensor cores; tokens/old_logp/mask as in espo_loss_fwd. 16-byte aligned
  * bases and pitches. Counts as the forward call for these rows. The first call may allocate
- * a small per-row partial buffer (16 B × rows × vocabulary parts). Unsharded contexts only. */
+ * a small per-row partial buffer (16 B × rows × vocabulary parts) and the GEMM's lockstep
+ * counters (4 B per wave of tiles); like espo_lmhead_bwd's scratch they only grow, so a step
+ * can be captured into a CUDA graph after one eager step of the same size (no call
+ * synchronises with the host; tests/test_gpu_graph.py). Unsharded contexts only. */
 espo_status espo_lmhead_fwd(espo_ctx_t ctx, const void* hidden, int64_t ldh, const void* weight,
                             int64_t ldw, int32_t d, const int32_t* tokens, const float* old_logp,
                             const uint8_t* mask, int64_t row_begin, int64_t n_rows,

@@ -182,3 +182,64 @@ def test_graph_capture_compact_mode():
     assert torch.equal(got_loss, loss) and torch.equal(got_dz, dz)
     assert torch.count_nonzero(got_dz.abs().sum(1)) > 0
     ctx.close()
+
+
+@pytest.mark.parametrize("d", [256, 4160])
+def test_graph_capture_lmhead(d):
+    """The fused LM head (GEMM-core forward with the soft lockstep, compacted backward with
+    split-K dh; d = 4160 also runs the dh / dW lockstep) captured after one warm-up step: the
+    replay reproduces the eager loss, dhidden and dweight bit for bit — the lockstep's progress
+    counters are zeroed inside the graph, and no call synchronises with the host."""
+    from paper_2512_07710_b200.espo import Espo
+    dev = require_cuda()
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    n, V = 1024, 4104
+    h = (torch.randn(n, d, device=dev, generator=g) / d ** 0.5 * 3).to(torch.bfloat16)
+    W = torch.randn(V, d, device=dev, generator=g).to(torch.bfloat16)
+    tok = torch.randint(0, V, (n,), device=dev, dtype=torch.int32, generator=g)
+    G = 8
+    rew = torch.tensor([1.0, 0.0, 1.0, 1.0, 0.0, 0.0, 1.0, 0.0], device=dev)
+    gid = torch.zeros(G, dtype=torch.int32, device=dev)
+    off = torch.arange(G + 1, device=dev, dtype=torch.int64) * (n // G)
+    ctx = Espo(V, logits_dtype=torch.bfloat16, device=dev.index)
+    ctx.prepare(rew, gid, off, n_tokens=n)
+    ctx.lmhead_fwd(h, W, tok, torch.zeros(n, device=dev))
+    ctx.loss_finalize()
+    old = (ctx.export_token_stats()["lp"] + 0.05 * torch.randn(n, device=dev, generator=g))
+    old = old.contiguous()
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    from paper_2512_07710_b200.espo import STATS_LEN
+    stats = torch.empty(STATS_LEN, dtype=torch.float64, device=dev)
+    dh = torch.empty((n, d), dtype=torch.float32, device=dev)
+    dW = torch.empty((V, d), dtype=torch.float32, device=dev)
+
+    def step():
+        ctx.prepare(rew, gid, off, n_tokens=n)
+        ctx.lmhead_fwd(h, W, tok, old)
+        ctx.loss_finalize(loss, stats)
+        dW.zero_()
+        ctx.lmhead_bwd(h, W, dh, dW)
+
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        step()                                   # warm-up: grows every scratch buffer
+    torch.cuda.current_stream(dev).wait_stream(s)
+    ctx.get_error()
+    e_loss, e_dh, e_dW = loss.clone(), dh.clone(), dW.clone()
+    assert float(e_dh.abs().max()) > 0 and float(e_dW.abs().max()) > 0
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    for _ in range(2):
+        loss.zero_()
+        dh.fill_(float("nan"))
+        dW.fill_(float("nan"))
+        graph.replay()
+        torch.cuda.synchronize(dev)
+        ctx.get_error()
+        assert torch.equal(loss, e_loss)
+        assert torch.equal(dh, e_dh)
+        assert torch.equal(dW, e_dW)
+    ctx.close()
