@@ -476,13 +476,17 @@ __host__ __device__ constexpr uint32_t gemm2_idesc() {
          (uint32_t(kGmBN >> 3) << 17) | (uint32_t(256 >> 4) << 24);
 }
 
-// bounded wait on a barrier of this CTA with cluster-scope acquire (remote arrivals)
+// bounded wait on a barrier of this CTA that the peer CTA also arrives on (TMA bytes, MMA
+// commits, remote epilogue arrivals). The default (CTA-scope) acquire suffices: what the
+// barrier guards is shared memory written through the async proxy and TMEM, ordered by
+// complete_tx and the tcgen05 fences. A .acquire.cluster wait compiled to an L1 invalidation
+// (CCTL.IVALL) per poll: 63 % of the forward GEMM's stall samples, 307 M executions per call.
 __device__ __forceinline__ void gm_wait_cluster(uint32_t bar, uint32_t parity) {
   uint64_t t0 = 0;
   for (uint32_t it = 0;; ++it) {
     uint32_t ok;
     asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         "selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
     if (ok) return;

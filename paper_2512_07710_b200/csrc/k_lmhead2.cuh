@@ -54,7 +54,7 @@ __device__ __forceinline__ void bounded_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
   for (uint32_t it = 0; it < (1u << 22); ++it) {
     asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         "selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
     if (ok) return;
