@@ -188,15 +188,17 @@ def test_guard_vocab_partial_combine():
         c.close()
 
 
-@pytest.mark.parametrize("impl,two_cta,gemm", [(0, 0, 0), (1, 0, 0), (1, 1, 2), (0, 0, 4)],
+@pytest.mark.parametrize("impl,two_cta,gemm,d", [(0, 0, 0, 320), (1, 0, 0, 320), (1, 1, 2, 320),
+                                                 (0, 0, 4, 320), (0, 0, 0, 4168)],
                          ids=["gemm_core", "1cta_fwd+pair_gemm", "2cta_fwd+1cta_gemm",
-                              "gemm_core+pair512"])
-def test_guard_lmhead(impl, two_cta, gemm):
+                              "gemm_core+pair512", "gemm_core_wide_lockstep"])
+def test_guard_lmhead(impl, two_cta, gemm, d):
+    """d = 4168 > 4096 also runs the dh / dW soft lockstep, 512-wide dW tiles and split-K dh."""
     from paper_2512_07710_b200.espo import (OPT_LMHEAD_2CTA, OPT_LMHEAD_BWD_GEMM,
                                             OPT_LMHEAD_BWD_ROWS, OPT_LMHEAD_IMPL)
     dev = require_cuda()
     rng = np.random.default_rng(5)
-    V, d, G, L = 3001, 320, 4, 70                   # V, d, n: none a multiple of the tiles
+    V, G, L = 3001, 4, 70                           # V, d, n: none a multiple of the tiles
     T = G * L
     hv = torch.from_numpy((rng.standard_normal((T, d)) / np.sqrt(d) * 3).astype(np.float32)).to(dev)
     Wv = torch.from_numpy(rng.standard_normal((V, d)).astype(np.float32)).to(dev)
