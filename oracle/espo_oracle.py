@@ -401,7 +401,7 @@ class OracleResult:
 
 def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
               cfg: OracleConfig, row_key=None, inject_bucket=None, inject_kappa=None,
-              stats_cache=None) -> OracleResult:
+              stats_cache=None, entropy=None) -> OracleResult:
     """O6: J = (1/D) Σ_i J_i, loss = −J (reading Q13), where for active
     rollout i with non-empty buckets τ:  J_i = Σ_τ (1/(nb_i·|y_τ|)) Σ_{t∈τ} ℓ_t  and
     D = number of active rollouts (reading Q10; NORM_TOKEN: J_i = Σ_t ℓ_t, D = T_active).
@@ -411,6 +411,12 @@ def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
     that are bit-identical share one O2 evaluation (memoised on (key, y)).
     ``inject_bucket``/``inject_kappa`` (per-token arrays) replace the oracle's own
     bucket / clip decisions (P11 decision-aware protocol).
+    ``entropy`` (per-token array, optional): caller-supplied selection entropies — reading
+    Q4's alternative (SURVEY.md §8(c)-2 Q4; SPEC.md:460 takes the rollout policy's
+    entropies) — used in place of the computed H_t wherever the method uses e_t: the
+    partition (O3), ε_τ (O4, Eq. 3), RL-ZVP's token advantages
+     and the mean-entropy statistic. lse, lp, q and H themselves still come
+    from the logits (O2); the gradient is unchanged in form (entropies are detached).
     """
     tokens = np.asarray(tokens)
     old_logp = np.asarray(old_logp, dtype=np.float32).astype(np.float64)
@@ -475,6 +481,8 @@ def espo_loss(logits, tokens, old_logp, mask, rewards, group_ids, seq_offsets,
             lse_a[t], lp_a[t], H_a[t], q_a[t] = st
             lp[j], H[j] = st[1], st[2]
         old = old_logp[valid]
+        if entropy is not None:      # caller-supplied selection entropies (reading Q4 alt.)
+            H = np.asarray(entropy, dtype=np.float64)[valid]
         # per-token advantages: the group's Â broadcast, or RL-ZVP's a_t
         A_t = zvp_token_advantages(H, float(rewards32[i]), cfg) if zvp else np.full(n, A)
         adv_tok[valid] = A_t

@@ -200,3 +200,38 @@ def test_hand_worked_k2_quantile_end_to_end():
         exp = np.where(np.isfinite(z), -g / m, 0.0)
         exp[int(inst["tokens"][t])] += g
         np.testing.assert_allclose(dz, exp, rtol=0, atol=tol)
+
+
+# ------------------------------------------- caller-supplied selection entropies (Q4 alt.)
+def test_supplied_entropies_reach_partition_and_clip():
+    """Reading Q4's alternative (the rollout policy's entropies): entropies
+    given by the caller replace e_t in the partition and in Eq. 3's ε_τ
+    (PAPER.md:119), nowhere else. Worked by hand: two rollouts of one group, rewards (1, 0)
+    ⇒ Â = ±0.5/(0.5 + 1e-6); every row uniform over V = 4 (lp = −ln 4, H = ln 4 exactly) and
+    old = lp in fp32 (v = 1 to 4e-9: old is −ln 4 rounded to fp32). Computed entropies are all equal ⇒ one bucket, ∂J_i/∂lp_t = Â/5.
+    Supplied e = (5, 4, 3, 2, 1): n_low = ⌊4·5/5⌋ = 4, θ = 4 (4th smallest) ⇒ high = {t0},
+    low = {t1..t4}; ∂J_i/∂lp_t = Â/(2·1) for t0 and Â/(2·4) for the others;
+    ε_high = 0.4·5/ln 4, ε_low = 0.4·(10/4)/ln 4; J_i = Â either way (v = 1)."""
+    cfg = O.OracleConfig(vocab=4)
+    z = np.zeros((10, 4))
+    tok = np.array([0, 1, 2, 3, 0, 1, 2, 3, 0, 1])
+    old = np.full(10, -math.log(4.0), dtype=np.float32)
+    so = np.array([0, 5, 10])
+    rew = np.array([1.0, 0.0], dtype=np.float32)
+    gid = np.array([0, 0], dtype=np.int32)
+    base = O.espo_loss(z, tok, old, None, rew, gid, so, cfg)
+    A = 0.5 / (0.5 + 1e-6)
+    np.testing.assert_allclose(base.coef[:5], A / 5, rtol=1e-7)
+    same = O.espo_loss(z, tok, old, None, rew, gid, so, cfg, entropy=base.H)
+    assert same.loss == base.loss and np.array_equal(same.coef, base.coef)
+    e = np.array([5, 4, 3, 2, 1, 5, 4, 3, 2, 1], dtype=np.float32)
+    got = O.espo_loss(z, tok, old, None, rew, gid, so, cfg, entropy=e)
+    assert got.bucket[:5].tolist() == [1, 0, 0, 0, 0] and got.nb[0] == 2
+    np.testing.assert_allclose(got.coef[:5], [A / 2] + [A / 8] * 4, rtol=1e-7)
+    np.testing.assert_allclose(got.coef[5:], [-A / 2] + [-A / 8] * 4, rtol=1e-7)
+    lnV = math.log(4.0)
+    np.testing.assert_allclose(got.eps_tok[:5], [0.4 * 5 / lnV] + [0.4 * 2.5 / lnV] * 4,
+                               rtol=1e-12)
+    np.testing.assert_allclose(got.J_i, [A, -A], rtol=1e-7)
+    np.testing.assert_allclose(got.H, base.H, rtol=0, atol=0)       # O2 untouched
+    np.testing.assert_allclose(got.stats["mean_entropy"], 3.0, rtol=1e-12)
