@@ -355,6 +355,24 @@ espo_status espo_attach_cp(espo_ctx_t ctx, const void* cp_unique_id, int32_t cp_
 espo_status espo_cp_gather_local(espo_ctx_t ctx, const espo_ctx_t* ranks, int32_t cp_world,
                                  espo_stream_t stream);
 
+/* ---- caller-supplied selection entropies (reading Q4's alternative) ----
+ * By default the entropies that pick each rollout's entropy buckets and set
+ * Eq. 3's ε_τ are the sweep's own, of the π_θ logits given to the forward
+ * (reading Q4). SPEC.md:460 takes the rollout policy's entropies instead; a trainer that has
+ * them (from the inference engine) passes them here: after espo_prepare and before finalize,
+ * entropy f32 [n_rows] (device, nats, finite and ≥ 0; −0 is taken as +0) for rows
+ * [row_begin, row_begin + n_rows), in chunks of any order that do not overlap (else
+ * ESPO_ERR_BAD_STATE). Once called in a step, every row of [0, T) must be covered before
+ * finalize (else ESPO_ERR_BAD_STATE). K3 then uses these values wherever the method uses e_t —
+ * the partition, ε_τ, RL-ZVP's token advantages and stats.mean_entropy — while
+ * lse / lp / q and the exported per-token H stay the sweep's; dlogits keep their form (the
+ * entropies are detached). The values are copied (the caller keeps ownership; a T-float
+ * buffer is allocated on first use). A negative value → sticky ESPO_ERR_INVALID_ARGUMENT,
+ * NaN / ±inf → sticky ESPO_ERR_NONFINITE_INPUT (espo_get_error; the loss is then NaN). Not
+ * with single-pass mode or context parallelism (ESPO_ERR_UNSUPPORTED). */
+espo_status espo_set_entropies(espo_ctx_t ctx, const float* entropy, int64_t row_begin,
+                               int64_t n_rows, espo_stream_t stream);
+
 /* ---- single-pass mode: forward and backward of a chunk in one call ----
  * The loss normaliser D (N active rollouts; T_active in TOKEN mode) depends only on the
  * zero-variance filter and the mask (readings Q10, Q11), and every other

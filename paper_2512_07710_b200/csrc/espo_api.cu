@@ -123,6 +123,10 @@ struct espo_ctx_s {
   State state = State::Created;
   bool single_pass = false;  // espo_set_mask called: chunks run fwd → K3 → bwd at once
   std::map<int64_t, int64_t> covered;  // fwd chunks: begin → end
+  float* hsel = nullptr;         // caller-supplied selection entropies [T] (espo_set_entropies)
+  size_t hsel_cap = 0;
+  std::map<int64_t, int64_t> hsel_cov;   // their chunks: begin → end
+  int64_t n_hsel = 0;
   int64_t n_covered = 0;
   uint64_t launches = 0;
   int fwd_impl = 0, bwd_impl = 0;
@@ -448,6 +452,7 @@ espo_status espo_destroy(espo_ctx_t c) {
     if (c->lmh_dz) cudaFree(c->lmh_dz);
     if (c->lmh_cmp) cudaFree(c->lmh_cmp);
     if (c->lmh_split) cudaFree(c->lmh_split);
+    if (c->hsel) cudaFree(c->hsel);
     if (c->lmh_live) cudaFree(c->lmh_live);
     if (c->gemm_sync) cudaFree(c->gemm_sync);
     if (c->blas) g_blas.destroy(c->blas);
@@ -580,6 +585,8 @@ espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* grou
   c->T = n_tokens;
   c->covered.clear();
   c->n_covered = 0;
+  c->hsel_cov.clear();
+  c->n_hsel = 0;
   c->single_pass = false;
   c->cp_gathered = false;
   PrepParams p;
@@ -842,6 +849,7 @@ SeqParams seq_params(espo_ctx_t c, int64_t row_lo, int64_t row_hi) {
   sp.inv_logV = 1.0 / std::log(static_cast<double>(cf.vocab));
   sp.zvp_beta = cf.zvp_beta;
   sp.ws = c->ws;
+  if (c->n_hsel > 0) sp.ws.H = c->hsel;    // caller-supplied selection entropies (K3 only)
   return sp;
 }
 }  // namespace
@@ -1701,6 +1709,7 @@ espo_status reduce_local(espo_ctx_t c, cudaStream_t s) {
 espo_status finalize_check(espo_ctx_t c) {
   const int64_t need = c->cp_world > 1 ? cp_hi(c) - cp_lo(c) : c->T;
   if (c->state != State::Prepared || c->n_covered != need) return ESPO_ERR_BAD_STATE;
+  if (c->n_hsel != 0 && c->n_hsel != c->T) return ESPO_ERR_BAD_STATE;   // partial entropies
   if (c->cp_world > 1 && !c->cp_comm && !c->cp_gathered) return ESPO_ERR_BAD_STATE;
   return ESPO_OK;
 }
@@ -1919,9 +1928,40 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
   return launch_bwd(c, logits, ld, dlogits, ldg, grad_loss_dev, row_begin, n_rows, S(stream));
 }
 
+espo_status espo_set_entropies(espo_ctx_t c, const float* entropy, int64_t row_begin,
+                               int64_t n_rows, espo_stream_t stream) {
+  if (!c) return ESPO_ERR_INVALID_ARGUMENT;
+  if (c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
+  if (c->single_pass || c->cp_world > 1) return ESPO_ERR_UNSUPPORTED;
+  if (n_rows < 0 || row_begin < 0 || row_begin + n_rows > c->T) return ESPO_ERR_INVALID_ARGUMENT;
+  if (n_rows == 0) return ESPO_OK;
+  if (!entropy) return ESPO_ERR_INVALID_ARGUMENT;
+  const int64_t b = row_begin, e = row_begin + n_rows;
+  auto it = c->hsel_cov.upper_bound(b);            // chunks must not overlap
+  if (it != c->hsel_cov.begin() && std::prev(it)->second > b) return ESPO_ERR_BAD_STATE;
+  if (it != c->hsel_cov.end() && it->first < e) return ESPO_ERR_BAD_STATE;
+  DevGuard g(c->device);
+  const size_t need = size_t(std::max<int64_t>(c->T, 1)) * sizeof(float);
+  if (need > c->hsel_cap) {
+    if (c->hsel) cudaFree(c->hsel);
+    c->hsel = nullptr;
+    c->hsel_cap = 0;
+    ESPO_CUDA(cudaMalloc(&c->hsel, need));
+    c->hsel_cap = need;
+  }
+  cudaStream_t s = S(stream);
+  const int grid = int(std::min<int64_t>((n_rows + 255) / 256, int64_t(c->num_sms) * 8));
+  k_set_entropies<<<grid, 256, 0, s>>>(entropy, c->hsel + row_begin, n_rows, c->ws.err);
+  ESPO_LAUNCHED(c);
+  c->hsel_cov[b] = e;
+  c->n_hsel += n_rows;
+  return ESPO_OK;
+}
+
 espo_status espo_set_mask(espo_ctx_t c, const uint8_t* mask, espo_stream_t stream) {
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Prepared || c->n_covered != 0 || c->cp_world > 1) return ESPO_ERR_BAD_STATE;
+  if (c->n_hsel != 0) return ESPO_ERR_UNSUPPORTED;   // supplied entropies: two-sweep mode only
   DevGuard g(c->device);
   cudaStream_t s = S(stream);
   if (c->R > 0) {

@@ -469,6 +469,19 @@ __global__ void k_finalize_scalar(const Workspace ws, int norm, float logit_scal
 }
 
 // Copies for the introspection API.
+// espo_set_entropies: caller-supplied selection entropies into the context's copy (reading Q4's
+// alternative). −0 becomes +0 (K3's radix select orders the fp32 bits of e ≥ 0);
+// a negative value or NaN / ±inf sets the sticky error.
+__global__ void k_set_entropies(const float* src, float* dst, int64_t n, int* err) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float x = src[i];
+    if (!(fabsf(x) <= 3.4e38f)) set_error(err, ESPO_ERR_NONFINITE_INPUT);
+    else if (x < 0.f) set_error(err, ESPO_ERR_INVALID_ARGUMENT);
+    dst[i] = x + 0.f;
+  }
+}
+
 __global__ void k_export_tokens(const Workspace ws, int64_t b, int64_t n, float* lse, float* lp,
                                 float* H, float* q, float* coef, uint8_t* bucket, uint8_t* clip,
                                 uint8_t* valid) {

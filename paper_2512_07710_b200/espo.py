@@ -50,7 +50,7 @@ EXPORTED_SYMBOLS = [
     "espo_config_default", "espo_get_unique_id", "espo_create", "espo_destroy", "espo_prepare",
     "espo_loss_fwd", "espo_loss_finalize", "espo_loss_bwd", "espo_get_error",
     "espo_status_string", "espo_export_token_stats", "espo_export_rollout_stats",
-    "espo_launch_count", "espo_set_option", "espo_loss_fwd_partial", "espo_loss_fwd_combine",
+    "espo_launch_count", "espo_set_option", "espo_set_entropies", "espo_loss_fwd_partial", "espo_loss_fwd_combine",
     "espo_attach_tp", "espo_lmhead_fwd", "espo_lmhead_bwd", "espo_set_mask", "espo_loss_fwd_bwd", "espo_tp_p2p_buffer", "espo_tp_p2p_open",
     "espo_tp_p2p_connect_local", "espo_tp_p2p_unmap", "espo_loss_fwd_p2p_send", "espo_loss_fwd_p2p_recv",
     "espo_attach_cp", "espo_cp_gather_local", "espo_reward_shaping_default",
@@ -136,6 +136,7 @@ def load_library():
         "espo_launch_count": (ctypes.c_uint64, [P]),
         "espo_comm_size": (I32, [P]),
         "espo_set_option": (I32, [P, I32, I64]),
+        "espo_set_entropies": (I32, [P, P, I64, I64, P]),
         "espo_loss_fwd_partial": (I32, [P, P, I64, P, P, P, I64, I64, P, P]),
         "espo_loss_fwd_combine": (I32, [P, P, I32, I64, I64, P]),
         "espo_attach_tp": (I32, [P, P, I32, I32]),
@@ -601,6 +602,17 @@ class Espo:
                                        int(row_begin), int(logits.shape[0]), self._stream()),
                "espo_loss_bwd")
         return dlogits
+
+    def set_entropies(self, entropy, row_begin=0):
+        """espo_set_entropies: caller-supplied selection entropies (f32 [n], nats) for rows
+        [row_begin, row_begin + n): used for the entropy buckets, Eq. 3's ε and RL-ZVP
+        instead of the sweep's own (reading Q4's alternative)."""
+        check_tensor(entropy, "entropy", torch.float32, self.device)
+        if entropy.dim() != 1:
+            raise ValueError("entropy must be a 1-D float32 tensor")
+        _check(self._lib.espo_set_entropies(self._h, _ptr(entropy), int(row_begin),
+                                            int(entropy.shape[0]), self._stream()),
+               "espo_set_entropies")
 
     def get_error(self):
         """espo_get_error: synchronises the current stream; raises on a device error."""

@@ -38,7 +38,8 @@ def to_dev(a, dtype, dev):
 
 
 def run_gpu(inst, dev, cfgkw=None, logits_dtype=torch.float32, grad_dtype=None, chunks=None,
-            fwd_impl=0, bwd_impl=0, ld_pad=0, in_place=False, grad_loss=None, factored=False, factored_impl=0, sync_after_prepare=False):
+            fwd_impl=0, bwd_impl=0, ld_pad=0, in_place=False, grad_loss=None, factored=False, factored_impl=0, sync_after_prepare=False,
+            entropy=None, entropy_chunks=None):
     """Full pass on the GPU. chunks: list of (begin, end) for fwd (bwd uses the same).
     factored: espo_loss_fwd_factored per chunk + espo_loss_row_scale; "dlogits" is then
     scale_t · G_t formed in fp64 here (no second rounding), "G"/"scale" are returned too."""
@@ -64,6 +65,10 @@ def run_gpu(inst, dev, cfgkw=None, logits_dtype=torch.float32, grad_dtype=None, 
                 zv_out=zv_out)
     if sync_after_prepare:     # lets host-side copies taken at prepare land before the sweeps
         torch.cuda.synchronize(dev)
+    if entropy is not None:    # caller-supplied selection entropies (espo_set_entropies)
+        ent = torch.from_numpy(np.asarray(entropy, dtype=np.float32)).to(dev)
+        for b, e in (entropy_chunks or [(0, T)]):
+            ctx.set_entropies(ent[b:e], row_begin=b)
     chunks = chunks or [(0, T)]
     gl = None if grad_loss is None else torch.tensor([grad_loss], dtype=torch.float32, device=dev)
     if factored:
@@ -133,9 +138,11 @@ def check_token_stats(g, ref):
     assert not bad.any(), ("q", got[bad][:5], want[bad][:5])
 
 
-def decision_aware_reference(g, inst, ref, cfg, flip_frac=1e-4):
+def decision_aware_reference(g, inst, ref, cfg, flip_frac=1e-4, **run_kw):
     """P11.4: every bucket / clip disagreement must sit within δ of the oracle's kink; the
-    oracle is then re-run with the GPU's decisions injected."""
+    oracle is then re-run with the GPU's decisions injected (run_kw: further arguments of
+    the oracle run, e.g. supplied entropies)."""
+    Hsel = np.asarray(run_kw["entropy"], dtype=np.float64) if run_kw.get("entropy") is not None else ref.H
     v = ref.kappa >= 0
     n_tok = int(v.sum())
     gb = g["tok"]["bucket"].astype(np.int64)
@@ -145,7 +152,7 @@ def decision_aware_reference(g, inst, ref, cfg, flip_frac=1e-4):
         db = np.flatnonzero(v & (gb != ref.bucket))
         for t in db:
             i = int(np.searchsorted(inst.seq_offsets, t, side="right") - 1)
-            margin = min(abs(ref.H[t] - th) for th in ref.theta[i])
+            margin = min(abs(Hsel[t] - th) for th in ref.theta[i])
             assert margin < 1e-5, ("bucket flip far from threshold", t, margin)
         flips += len(db)
     dc = np.flatnonzero(v & (gc != (1 - ref.kappa)))
@@ -159,7 +166,7 @@ def decision_aware_reference(g, inst, ref, cfg, flip_frac=1e-4):
         return ref, 0
     kap = np.where(v, 1 - gc, -1)
     ref2 = inst.run(cfg, inject_bucket=gb if cfg.partition == O.PARTITION_QUANTILE else None,
-                    inject_kappa=kap)
+                    inject_kappa=kap, **run_kw)
     return ref2, flips
 
 
