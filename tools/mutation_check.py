@@ -19,6 +19,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 # (name, old text, new text) applied to oracle/espo_oracle.py
 MUTATIONS = [
+    ("supplied_entropies_ignored (reading Q4's alternative not wired)",
+     "            H = np.asarray(entropy, dtype=np.float64)[valid]\n",
+     "            pass\n"),
     ("eps_from_sequence_mean_entropy (Eq. 3 over the whole sequence, not per bucket)",
      "        s, eps = bucket_ratio_clip(lp[sel], old[sel], H[sel], cfg)\n",
      "        s, _ = bucket_ratio_clip(lp[sel], old[sel], H[sel], cfg)\n"
