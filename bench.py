@@ -71,7 +71,8 @@ def parse():
     p.add_argument("--config", default="C1", help="C1 (default), C2, C3, C4 (BASELINE.json)")
     p.add_argument("--compact", action="store_true",
                    help="compact mode: rows without gradient are not zero-filled (C3)")
-    p.add_argument("--buffer-rows", type=int, default=32768)
+    p.add_argument("--buffer-rows", type=int, default=65536,
+                   help="rows per chunk call (the chunk buffer is rows × V bf16: 19.9 GB at C1)")
     p.add_argument("--fwd-impl", type=int, default=0, help="0/2/3/4 = TMA ring variants, 1 = LDG")
     p.add_argument("--bwd-impl", type=int, default=0, help="0/7 = tiled grid, 1 = LDG, 2-6 = TMA rings")
     p.add_argument("--blocks-per-sm", type=int, default=0)
@@ -878,10 +879,16 @@ def main_ours(args):
     step_gbs = step_bytes / (ms_step * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    # ncu DRAM bytes of the dominant kernel, captured on the default C1 step (profiles/): only
+    # for that workload; per launch for this run's chunking (the step's bytes do not depend
+    # on how the rows are cut into calls)
+    if os.path.exists(tpath) and args.config == "C1" and S_ == 1 and not args.compact and \
+            args.zv_mode == "mask" and not args.single_pass:
         tr = json.load(open(tpath))
-        traffic = tr.get("factored_bytes_per_launch") if args.factored else \
-            None if args.single_pass else tr.get("bwd_bytes_per_launch")
+        key = "factored" if args.factored else "bwd"
+        per, nl = tr.get(f"{key}_bytes_per_launch"), tr.get(f"{key}_launches")
+        if per is not None and nl:
+            traffic = per * nl / (n_chunks * world if strong else n_chunks)
 
     # the same workload through the factored-gradient API (one sweep per row; the consumer
     # applies the row scale), reported beside the headline — not in place of it

@@ -13,7 +13,8 @@ timeout 600 python bench.py --scaling strong --steps 5 --warmup 3 --verify --no-
 timeout 900 python bench.py --scaling strong --config C4 --emulate-ranks 8 --steps 1 --warmup 3 --verify > gpurun_out/bench_C4_emulate8.json 2>/dev/null; echo "c4 emulate8 exit=$?"
 P="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-factored-leg"
 $P > gpurun_out/plain_ll.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $P > gpurun_out/ncu_ll.log 2>&1; echo "launch list exit=$?"
-$P > gpurun_out/plain_tr.log 2>&1 && ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"k_rowstats|k_fwd_rows|k_dlogits|k_bwd_rows|k_bwd_recs" -s 768 --csv --log-file gpurun_out/traffic.csv $P > gpurun_out/ncu_tr.log 2>&1; echo "traffic exit=$?"
+# traffic: skip the 3 warm-up steps (C1 at 65,536-row chunks: 32 calls × 4 kernels per step)
+$P > gpurun_out/plain_tr.log 2>&1 && ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"k_rowstats|k_fwd_rows|k_dlogits|k_bwd_rows|k_bwd_recs" -s 384 --csv --log-file gpurun_out/traffic.csv $P > gpurun_out/ncu_tr.log 2>&1; echo "traffic exit=$?"
 Q="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-factored-leg --buffer-rows 8192"
 $Q > gpurun_out/plain_q.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_rowstats_tma" -s 60 -c 1 -o gpurun_out/prof_fwd $Q > gpurun_out/ncu_fwd.log 2>&1; echo "ncu fwd exit=$?"
 $Q > gpurun_out/plain_q2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_dlogits" -s 60 -c 2 -o gpurun_out/prof_bwd $Q > gpurun_out/ncu_bwd.log 2>&1; echo "ncu bwd exit=$?"
