@@ -129,9 +129,10 @@ def main(tag, out_dir="gpurun_out"):
                   "msecond": 1e6}.get(u, 1)
             per.setdefault(int(r["ID"]), {})[r["Metric Name"]] = float(r["Metric Value"].replace(",", "")) * sc
         ids = sorted(per)
-        last = ids[-64:] if len(ids) >= 64 else ids
         jp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         t = json.load(open(jp)) if os.path.exists(jp) else {}
+        n_step = int(t.get("bwd_launches") or 64)     # calls per step of the default chunking
+        last = ids[-n_step:] if len(ids) >= n_step else ids
         t["factored_bytes_per_launch"] = sum(per[i].get("dram__bytes_read.sum", 0) + per[i].get("dram__bytes_write.sum", 0) for i in last) / max(len(last), 1)
         t["factored_launches"] = len(last)
         t["factored_ms_total"] = sum(per[i].get("gpu__time_duration.sum", 0) for i in last) / 1e6
