@@ -991,8 +991,11 @@ def main_ours(args):
                       "clip_frac": n_clip / n_act if n_act else 0.0,
                       "note": "old_logp = lp + b_i + tok_sigma*n_t, b_i ~ N(0, seq_sigma); clipped "
                               "tokens need no logits read in the backward (c_t = 0)"},
-            "chunk_rows": d["Rc"], "l2": "inputs larger than L2 (chunk buffer "
-                                         f"{d['Rc'] * V * 2 / 1e9:.2f} GB > 126 MB)",
+            "chunk_rows": d["Rc"],
+            "l2": (f"inputs larger than L2 (chunk buffer {d['Rc'] * V * 2 / 1e9:.2f} GB > 126 MB)"
+                   if d["Rc"] * V * 2 > 126e6 else
+                   f"inputs fit in L2 ({d['Rc'] * V * 2 / 1e6:.1f} MB): a parity-size config, "
+                   "not a bench line"),
             "fwd_impl": ["tma16x2x6k_s4_f32x2 (rows >= 64 KB; 16x3x4k below)", "ldg", "tma16x2x7k_s2_f32x2", "tma14x2x7k_s2_f32x2", "tma20x2x5k_s2_f32x2", "tma16x3x4k_s4_f32x2", "tma16x2x6k_s4_poly1", "tma18x2x6k_s4_f32x2", "tma16x2x6k_s4_scalar", "tile32k_b4", "tile32k_b3", "tile32k_b2"][args.fwd_impl],
             "bwd_impl": ["tile32k_f32x2", "ldg", "tma16x3x4k", "tma16x2x4k", "tma12x4x4k", "tma8x6x4k", "tma8x4x4k", "tile16k", "tile32k_scalar", "tlist32k_r4", "tlist32k_r8", "tlist32k_r16"][args.bwd_impl],
             "achieved_hbm_gbs_step": step_gbs, "frac_of_8TBs_step": step_gbs / NOMINAL_HBM_GBS,

@@ -11,6 +11,8 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: no-ops unless a profiler is attached
+
 #include "common.cuh"
 #include "k_dlogits.cuh"
 #include "k_rowstats.cuh"
@@ -33,6 +35,15 @@ using namespace espo;
 // ------------------------------------------------------------------------------ NCCL
 // Resolved at run time from libnccl.so.2 (the copy torch already loaded, when present),
 // so a world == 1 context never needs NCCL and there is no link-time dependency.
+
+// Host-side NVTX range around each public call (what a trainer sees on an nsys / ncu NVTX
+// timeline: which ESPO call enqueued which kernels); free when no tool is attached.
+struct EspoRange {
+  explicit EspoRange(const char* name) { nvtxRangePushA(name); }
+  ~EspoRange() { nvtxRangePop(); }
+};
+#define ESPO_RANGE(name) EspoRange espo_range_(name)
+
 namespace {
 typedef struct { char internal[ESPO_UNIQUE_ID_BYTES]; } nccl_uid;
 typedef void* nccl_comm;
@@ -388,6 +399,7 @@ espo_status espo_get_unique_id(void* out_id) {
 
 espo_status espo_create(const espo_config* cfg, const void* nccl_unique_id, int32_t rank,
                         int32_t world, int32_t cuda_device, espo_ctx_t* out) {
+  ESPO_RANGE("espo_create");
   if (!cfg || !out) return ESPO_ERR_INVALID_ARGUMENT;
   *out = nullptr;
   if (world < 1 || rank < 0 || rank >= world) return ESPO_ERR_INVALID_ARGUMENT;
@@ -437,6 +449,7 @@ espo_status espo_create(const espo_config* cfg, const void* nccl_unique_id, int3
 }
 
 espo_status espo_destroy(espo_ctx_t c) {
+  ESPO_RANGE("espo_destroy");
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   {
     DevGuard g(c->device);
@@ -571,6 +584,7 @@ int32_t espo_comm_size(espo_ctx_t c) {
 espo_status espo_prepare(espo_ctx_t c, const float* rewards, const int32_t* group_ids,
                          const int64_t* seq_offsets, int32_t n_rollouts, int64_t n_tokens,
                          float* adv_out, uint8_t* zv_out, espo_stream_t stream) {
+  ESPO_RANGE("espo_prepare");
   if (!c || !rewards || !group_ids || !seq_offsets) return ESPO_ERR_INVALID_ARGUMENT;
   if (n_rollouts < 0 || n_tokens < 0 || n_tokens > (int64_t(1) << 40))
     return ESPO_ERR_INVALID_ARGUMENT;
@@ -859,6 +873,7 @@ extern "C" {
 espo_status espo_loss_fwd(espo_ctx_t c, const void* logits, int64_t ld, const int32_t* tokens,
                           const float* old_logp, const uint8_t* mask, int64_t row_begin,
                           int64_t n_rows, uint32_t flags, espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_fwd");
   if (flags != 0) return ESPO_ERR_INVALID_ARGUMENT;
   espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
   if (st != ESPO_OK || n_rows == 0) return st;
@@ -874,6 +889,7 @@ espo_status espo_loss_fwd_partial(espo_ctx_t c, const void* logits, int64_t ld,
                                   const int32_t* tokens, const float* old_logp,
                                   const uint8_t* mask, int64_t row_begin, int64_t n_rows,
                                   float* partial, espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_fwd_partial");
   espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
   if (st != ESPO_OK || n_rows == 0) return st;
   if (!partial || !aligned16(partial)) return ESPO_ERR_INVALID_ARGUMENT;
@@ -883,6 +899,7 @@ espo_status espo_loss_fwd_partial(espo_ctx_t c, const void* logits, int64_t ld,
 
 espo_status espo_loss_fwd_combine(espo_ctx_t c, const float* partials, int32_t n_shards,
                                   int64_t row_begin, int64_t n_rows, espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_fwd_combine");
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Prepared || c->single_pass) return ESPO_ERR_BAD_STATE;
   if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T ||
@@ -1079,6 +1096,7 @@ espo_status espo_lmhead_fwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
                             int64_t ldw, int32_t d, const int32_t* tokens, const float* old_logp,
                             const uint8_t* mask, int64_t row_begin, int64_t n_rows,
                             espo_stream_t stream) {
+  ESPO_RANGE("espo_lmhead_fwd");
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Prepared || c->single_pass) return ESPO_ERR_BAD_STATE;
   if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T || d < 1)
@@ -1194,6 +1212,7 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
                             int64_t ldw, int32_t d, void* dhidden, int64_t lddh, int32_t dh_dtype,
                             float* dweight, int64_t lddw, const float* grad_loss_dev,
                             int64_t row_begin, int64_t n_rows, espo_stream_t stream) {
+  ESPO_RANGE("espo_lmhead_bwd");
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Finalized) return ESPO_ERR_BAD_STATE;
   if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T || d < 1)
@@ -1460,6 +1479,7 @@ espo_status espo_reshape_rewards(espo_ctx_t c, const espo_reward_shaping* prm,
                                  const int64_t* seq_offsets, int32_t n_rollouts,
                                  int64_t n_tokens, float* rewards_out, float* len_pen_out,
                                  float* rep_pen_out, espo_stream_t stream) {
+  ESPO_RANGE("espo_reshape_rewards");
   if (!c || !prm || !base_rewards || !seq_offsets || !rewards_out || n_rollouts < 0 ||
       n_tokens < 0 || (n_tokens > 0 && !tokens))
     return ESPO_ERR_INVALID_ARGUMENT;
@@ -1609,6 +1629,7 @@ espo_status espo_loss_fwd_p2p_send(espo_ctx_t c, const void* logits, int64_t ld,
                                    const int32_t* tokens, const float* old_logp,
                                    const uint8_t* mask, int64_t row_begin, int64_t n_rows,
                                    espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_fwd_p2p_send");
   espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
   if (st != ESPO_OK || n_rows == 0) return st;
   if (!c->tp_p2p || c->single_pass) return ESPO_ERR_BAD_STATE;
@@ -1620,6 +1641,7 @@ espo_status espo_loss_fwd_p2p_send(espo_ctx_t c, const void* logits, int64_t ld,
 
 espo_status espo_loss_fwd_p2p_recv(espo_ctx_t c, int64_t row_begin, int64_t n_rows,
                                    espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_fwd_p2p_recv");
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Prepared || !c->tp_p2p || c->single_pass) return ESPO_ERR_BAD_STATE;
   if (n_rows < 0 || n_rows > c->x_cap || row_begin < 0 || row_begin + n_rows > c->T)
@@ -1656,6 +1678,7 @@ espo_status espo_attach_cp(espo_ctx_t c, const void* cp_unique_id, int32_t cp_ra
 
 espo_status espo_cp_gather_local(espo_ctx_t c, const espo_ctx_t* ranks, int32_t cp_world,
                                  espo_stream_t stream) {
+  ESPO_RANGE("espo_cp_gather_local");
   if (!c || !ranks || cp_world != c->cp_world || cp_world < 2 || ranks[c->cp_rank] != c)
     return ESPO_ERR_INVALID_ARGUMENT;
   if (c->cp_comm || c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
@@ -1717,6 +1740,7 @@ espo_status finalize_check(espo_ctx_t c) {
 
 espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_dev,
                                espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_finalize");
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   espo_status st = finalize_check(c);
   if (st != ESPO_OK) return st;
@@ -1735,6 +1759,7 @@ espo_status espo_loss_finalize(espo_ctx_t c, float* loss_dev, espo_stats* stats_
 }
 
 espo_status espo_loss_reduce_local(espo_ctx_t c, double* partial_out, espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_reduce_local");
   if (!c || !partial_out) return ESPO_ERR_INVALID_ARGUMENT;
   espo_status st = finalize_check(c);
   if (st != ESPO_OK) return st;
@@ -1749,6 +1774,7 @@ espo_status espo_loss_reduce_local(espo_ctx_t c, double* partial_out, espo_strea
 
 espo_status espo_loss_finalize_reduced(espo_ctx_t c, const double* reduced, float* loss_dev,
                                        espo_stats* stats_dev, espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_finalize_reduced");
   if (!c || !reduced) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Reduced) return ESPO_ERR_BAD_STATE;
   DevGuard g(c->device);
@@ -1915,6 +1941,7 @@ extern "C" {
 espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dlogits, int64_t ldg,
                           const float* grad_loss_dev, int64_t row_begin, int64_t n_rows,
                           espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_bwd");
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Finalized || c->single_pass) return ESPO_ERR_BAD_STATE;
   if (n_rows < 0 || n_rows > INT32_MAX || row_begin < 0 || row_begin + n_rows > c->T)
@@ -1930,6 +1957,7 @@ espo_status espo_loss_bwd(espo_ctx_t c, const void* logits, int64_t ld, void* dl
 
 espo_status espo_set_entropies(espo_ctx_t c, const float* entropy, int64_t row_begin,
                                int64_t n_rows, espo_stream_t stream) {
+  ESPO_RANGE("espo_set_entropies");
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Prepared) return ESPO_ERR_BAD_STATE;
   if (c->single_pass || c->cp_world > 1) return ESPO_ERR_UNSUPPORTED;
@@ -1959,6 +1987,7 @@ espo_status espo_set_entropies(espo_ctx_t c, const float* entropy, int64_t row_b
 }
 
 espo_status espo_set_mask(espo_ctx_t c, const uint8_t* mask, espo_stream_t stream) {
+  ESPO_RANGE("espo_set_mask");
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Prepared || c->n_covered != 0 || c->cp_world > 1) return ESPO_ERR_BAD_STATE;
   if (c->n_hsel != 0) return ESPO_ERR_UNSUPPORTED;   // supplied entropies: two-sweep mode only
@@ -1986,6 +2015,7 @@ espo_status espo_loss_fwd_bwd(espo_ctx_t c, const void* logits, int64_t ld, cons
                               const float* old_logp, void* dlogits, int64_t ldg,
                               const float* grad_loss_dev, int64_t row_begin, int64_t n_rows,
                               espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_fwd_bwd");
   espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows, true);
   if (st != ESPO_OK) return st;
   if (n_rows == 0) return ESPO_OK;
@@ -2054,6 +2084,7 @@ espo_status espo_loss_fwd_factored(espo_ctx_t c, const void* logits, int64_t ld,
                                    const int32_t* tokens, const float* old_logp,
                                    const uint8_t* mask, void* grad, int64_t ldg, int64_t row_begin,
                                    int64_t n_rows, espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_fwd_factored");
   espo_status st = check_fwd_args(c, logits, ld, tokens, old_logp, row_begin, n_rows);
   if (st != ESPO_OK || n_rows == 0) return st;
   if (c->cfg.vocab_local > 0 && c->cfg.vocab_local < c->cfg.vocab) return ESPO_ERR_BAD_STATE;
@@ -2140,6 +2171,7 @@ espo_status espo_loss_fwd_factored(espo_ctx_t c, const void* logits, int64_t ld,
 
 espo_status espo_loss_row_scale(espo_ctx_t c, const float* grad_loss_dev, float* scale_out,
                                 int64_t row_begin, int64_t n_rows, espo_stream_t stream) {
+  ESPO_RANGE("espo_loss_row_scale");
   if (!c) return ESPO_ERR_INVALID_ARGUMENT;
   if (c->state != State::Finalized) return ESPO_ERR_BAD_STATE;
   if (n_rows < 0 || row_begin < 0 || row_begin + n_rows > c->T) return ESPO_ERR_INVALID_ARGUMENT;
