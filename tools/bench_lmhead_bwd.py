@@ -124,22 +124,13 @@ def main(d=4096, n=16384, V=151936, iters=3, realistic=False):
     uctx.get_error()
     xctx.get_error()
     res["agreement_vs_unfused"] = agree
-    # fused backward alone (recompute + dz + 2 GEMMs)
+    # fused backward alone (recompute + dz + 2 GEMMs): the library's tcgen05 GEMMs (0), cuBLAS
+    # GEMMs (ESPO_OPT_LMHEAD_BWD_GEMM = 1) and one-CTA tiles (2), interleaved over 3 rounds
+    # with a warm-up call each (medians), so no setting inherits another's thermal state
+    from paper_2512_07710_b200.espo import OPT_LMHEAD_BWD_GEMM
     fctx.prepare(rewards, gid, so, n_tokens=n)
     fctx.lmhead_fwd(h, W, tokens, old)
     fctx.loss_finalize()
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(iters):
-        fctx.lmhead_bwd(h, W, dh, dW)
-    e.record()
-    torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / iters
-    res["fused_bwd_only"] = {"ms": ms, "TFLOPs_3gemm": 6.0 * n * V * d / (ms * 1e-3) / 1e12,
-                             "gemm": "tcgen05 (k_gemm.cuh)"}
-    # the same backward with dh / dW on cuBLAS (ESPO_OPT_LMHEAD_BWD_GEMM = 1), for the A/B
-    from paper_2512_07710_b200.espo import OPT_LMHEAD_BWD_GEMM
     fctx.set_option(OPT_LMHEAD_BWD_GEMM, 1)
     dh2, dW2 = torch.empty_like(dh), torch.zeros_like(dW)
     fctx.lmhead_bwd(h, W, dh2, dW2)
@@ -150,29 +141,26 @@ def main(d=4096, n=16384, V=151936, iters=3, realistic=False):
     res["native_vs_cublas"] = {"dh_rel": float((dh.float() - dh2.float()).norm() / dh2.float().norm()),
                                "dW_rel": float((dW - dW2).norm() / dW2.norm())}
     del dh2, dW2
-    fctx.set_option(OPT_LMHEAD_BWD_GEMM, 1)
-    for _ in range(2):
-        fctx.lmhead_bwd(h, W, dh, dW)
-    torch.cuda.synchronize()
-    s.record()
-    for _ in range(iters):
-        fctx.lmhead_bwd(h, W, dh, dW)
-    e.record()
-    torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / iters
-    res["fused_bwd_only_cublas"] = {"ms": ms, "TFLOPs_3gemm": 6.0 * n * V * d / (ms * 1e-3) / 1e12}
-    fctx.set_option(OPT_LMHEAD_BWD_GEMM, 2)                 # one CTA per 128 x 256 tile
-    for _ in range(2):
-        fctx.lmhead_bwd(h, W, dh, dW)
-    torch.cuda.synchronize()
-    s.record()
-    for _ in range(iters):
-        fctx.lmhead_bwd(h, W, dh, dW)
-    e.record()
-    torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / iters
+    import statistics
+    times = {0: [], 1: [], 2: []}
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        for g in (0, 1, 2):
+            fctx.set_option(OPT_LMHEAD_BWD_GEMM, g)
+            fctx.lmhead_bwd(h, W, dh, dW)
+            torch.cuda.synchronize()
+            s.record()
+            for _ in range(iters):
+                fctx.lmhead_bwd(h, W, dh, dW)
+            e.record()
+            torch.cuda.synchronize()
+            times[g].append(s.elapsed_time(e) / iters)
     fctx.set_option(OPT_LMHEAD_BWD_GEMM, 0)
-    res["fused_bwd_only_1cta"] = {"ms": ms, "TFLOPs_3gemm": 6.0 * n * V * d / (ms * 1e-3) / 1e12}
+    for g, key in ((0, "fused_bwd_only"), (1, "fused_bwd_only_cublas"), (2, "fused_bwd_only_1cta")):
+        ms = statistics.median(times[g])
+        res[key] = {"ms": ms, "TFLOPs_3gemm": 6.0 * n * V * d / (ms * 1e-3) / 1e12,
+                    "rounds_ms": times[g]}
+    res["fused_bwd_only"]["gemm"] = "tcgen05 (k_gemm.cuh)"
     uctx.prepare(rewards, gid, so, n_tokens=n)
     uctx.loss_fwd(torch.matmul(h, W.T), tokens, old)
     from paper_2512_07710_b200.espo import stats_to_dict

@@ -11,7 +11,8 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_07710_b200.espo import (OPT_GEMM_GROUP_M, OPT_GEMM_HINTS,  # noqa: E402
-                                        OPT_GEMM_SYNC, OPT_LMHEAD_BWD_GEMM, OPT_LMHEAD_COMPACT,
+                                        OPT_GEMM_SYNC, OPT_LMHEAD_BWD_GEMM, OPT_LMHEAD_BWD_ROWS,
+                                        OPT_LMHEAD_COMPACT,
                                         OPT_LMHEAD_IMPL, OPT_LMHEAD_RASTER, Espo)
 
 
@@ -43,7 +44,10 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
     MC = 1 << 25
     NOSPLIT = 1 << 26
     cfgs = {                     # (gemm, group, hints, compact, sync (-1 auto), lmhead impl, lm raster)
-        "cublas": (1, 0, -1, 0, -1, 1, 0),
+        # cuBLAS doing dh / dW on the same GEMM-core recompute and row compaction (only the two
+        # GEMMs differ; until the end of round 2 this leg ran the dedicated dz kernel and no
+        # compaction, which flattered the native default by ~2 ms per sub-chunk)
+        "cublas": (1, 0, -1, 1, -1, 0, 0),
         "default": (0, 0, -1, 1, -1, 0, 0),
         "nosplit": (0, 0, -1, 1, -1, 0, NOSPLIT),
         "dh256": (0, 0, -1, 1, -1, 0, 0),
@@ -52,6 +56,24 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
     NOLOCK = 1 << 27
     cfgs["dz_g32_nolock"] = (0, 0, -1, 1, -1, 0, 32 | NOLOCK)    # round-2 dz raster
     cfgs["dz_g16_nolock"] = (0, 0, -1, 1, -1, 0, 16 | NOLOCK)
+    rows_opt = {}
+    if which == "rows":          # backward sub-chunk rows (A / B panel sizes of dW and dh)
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "rows4096": cfgs["default"], "rows16384": cfgs["default"],
+                "cublas_rows16384": cfgs["cublas"]}
+        rows_opt = {"rows4096": 4096, "rows16384": 16384, "cublas_rows16384": 16384}
+    if which == "mc":            # TMA multicast across two CTA pairs (4-CTA clusters)
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "mc_both": (5, 0, -1, 1, -1, 0, 0), "mc_dh": (6, 0, -1, 1, -1, 0, 0),
+                "mc_dh_nosplit": (6, 0, -1, 1, -1, 0, 1 << 26),
+                "dw256_g1": (0, G(0, 1), -1, 1, -1, 0, 0)}
+    if which == "dwr":           # dW raster / L2 policies / tile width (dense sub-chunks)
+        Hd = lambda a, b, c: (a | (b << 2) | (c << 4)) << 8          # dW's byte of GEMM_HINTS
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "dw_n16": (0, G(0, 16), -1, 1, -1, 0, 0), "dw_n4": (0, G(0, 4), -1, 1, -1, 0, 0),
+                "dw_n16_Bnorm": (0, G(0, 16), Hd(1, 0, 1), 1, -1, 0, 0),
+                "dw_n8_allnorm": (0, G(0, 8), Hd(0, 0, 0), 1, -1, 0, 0),
+                "dw512_n8": (4, G(0, 8), -1, 1, -1, 0, 0)}
     if which == "half":          # 512-column accumulators released in halves (default) or whole
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
                 "whole_release": (0, 0, -1, 1, -1, 0, 1 << 28)}
@@ -69,6 +91,12 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
                 "dw_sync16": (0, 0, -1, 1, Ldw(16, 2), 0, 0), "dw_sync8_s1": (0, 0, -1, 1, Ldw(8, 1), 0, 0),
                 "dw_sync8_n4": (0, G(0, 4), -1, 1, Ldw(8, 2), 0, 0),
                 "dw_sync8_n16": (0, G(0, 16), -1, 1, Ldw(8, 2), 0, 0)}
+    if which == "syncdw2":       # dW lockstep with more slack (chunk, slack in chunks)
+        Ldw = lambda ch, sl: (ch | (sl << 16)) << 32
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "dw_8_4": (0, 0, -1, 1, Ldw(8, 4), 0, 0), "dw_8_8": (0, 0, -1, 1, Ldw(8, 8), 0, 0),
+                "dw_16_4": (0, 0, -1, 1, Ldw(16, 4), 0, 0), "dw_4_8": (0, 0, -1, 1, Ldw(4, 8), 0, 0),
+                "dw_4_16": (0, 0, -1, 1, Ldw(4, 16), 0, 0), "dw_32_2": (0, 0, -1, 1, Ldw(32, 2), 0, 0)}
     if which == "sync":          # soft lockstep of the dh / dW GEMMs (ESPO_OPT_GEMM_SYNC)
         L = lambda ch, sl: ch | (sl << 16)
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
@@ -88,6 +116,7 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
             ctx.set_option(OPT_GEMM_GROUP_M, gm)
             ctx.set_option(OPT_GEMM_HINTS, hints)
             ctx.set_option(OPT_LMHEAD_COMPACT, compact)
+            ctx.set_option(OPT_LMHEAD_BWD_ROWS, rows_opt.get(k, 0))
             ctx.lmhead_bwd(h, W, dh, dW)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()

@@ -1,16 +1,18 @@
 """One espo_lmhead_bwd call (after a warm-up call) on synthetic h, W — the target of the
 ncu launch list / full captures of the backward's kernels (k_lmhead_dz, k_umma_gemm).
-usage: python tools/lmhead_bwd_once.py [d] [n] [gemm: 0 pair | 1 cuBLAS | 2 one CTA] [sync]"""
+usage: python tools/lmhead_bwd_once.py [d] [n] [gemm: 0 pair | 1 cuBLAS | 2 one CTA] [sync]
+       [group option] [hints option]   (ESPO_OPT_GEMM_GROUP_M / _GEMM_HINTS; -1 = default)"""
 import os
 import sys
 
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2512_07710_b200.espo import OPT_GEMM_SYNC, OPT_LMHEAD_BWD_GEMM, Espo  # noqa: E402
+from paper_2512_07710_b200.espo import (OPT_GEMM_GROUP_M, OPT_GEMM_HINTS, OPT_GEMM_SYNC,  # noqa: E402
+                                        OPT_LMHEAD_BWD_GEMM, Espo)
 
 
-def main(d=4096, n=8192, gemm=0, sync=-1, V=151936):
+def main(d=4096, n=8192, gemm=0, sync=-1, group=-1, hints=-1, V=151936):
     dev = torch.device("cuda", 0)
     torch.manual_seed(0)
     h = (torch.randn(n, d, device=dev) / d ** 0.5 * 3).to(torch.bfloat16)
@@ -23,6 +25,9 @@ def main(d=4096, n=8192, gemm=0, sync=-1, V=151936):
     ctx = Espo(V, logits_dtype=torch.bfloat16, device=0)
     ctx.set_option(OPT_LMHEAD_BWD_GEMM, gemm)
     ctx.set_option(OPT_GEMM_SYNC, sync)
+    if group >= 0:
+        ctx.set_option(OPT_GEMM_GROUP_M, group)
+    ctx.set_option(OPT_GEMM_HINTS, hints)
     ctx.prepare(rewards, gid, so, n_tokens=n)
     ctx.lmhead_fwd(h, W, tokens, torch.zeros(n, device=dev))
     ctx.loss_finalize()
