@@ -67,6 +67,12 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
                 "mc_both": (5, 0, -1, 1, -1, 0, 0), "mc_dh": (6, 0, -1, 1, -1, 0, 0),
                 "mc_dh_nosplit": (6, 0, -1, 1, -1, 0, 1 << 26),
                 "dw256_g1": (0, G(0, 1), -1, 1, -1, 0, 0)}
+    if which == "dwel":          # dW: A (dz panels) evict_last, B evict_last, C evict_first
+        Hd = lambda a, b, c: (a | (b << 2) | (c << 4)) << 8
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "n16_el": (0, G(0, 16), Hd(2, 2, 1), 1, -1, 0, 0),
+                "n8_el": (0, G(0, 8), Hd(2, 2, 1), 1, -1, 0, 0),
+                "n16_el_sync16": (0, G(0, 16), Hd(2, 2, 1), 1, (16 | (4 << 16)) << 32, 0, 0)}
     if which == "dwr":           # dW raster / L2 policies / tile width (dense sub-chunks)
         Hd = lambda a, b, c: (a | (b << 2) | (c << 4)) << 8          # dW's byte of GEMM_HINTS
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
