@@ -560,7 +560,11 @@ typedef enum {
                                   every 256 × 512 CTA-pair GEMM (also dh / dW) releases its
                                   accumulator whole instead of in halves (default: the next
                                   tile's first K-steps on columns 0-255 overlap the epilogue's
-                                  read of 256-511) */
+                                  read of 256-511), bit 29 = static round-robin tile order for
+                                  every CTA-pair GEMM (default: a dynamic scheduler — each pair
+                                  takes the next tile from an atomic counter, so the tiles in
+                                  flight stay a contiguous window of the raster; the backward's
+                                  dz recompute then runs without the lockstep) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

@@ -178,6 +178,8 @@ struct espo_ctx_s {
                                         // L2 policies
   int lmh_sync = 8 | (2 << 16);  // their soft lockstep (chunk of K-steps | slack << 16; 0 = off)
   int gemm_half_release = 1;     // CTA-pair 256 × 512 GEMMs: accumulator released in halves
+  int gemm_dyn = 1;              // CTA-pair GEMMs: dynamic tile scheduler (atomic counter)
+  int* gemm_tctr = nullptr;      // its counter
   int gemm_sync_dw = -1;         // dW GEMM's own lockstep (chunk | slack << 16; −1 = as dh)
   int gemm_sync_set = 0;         // ESPO_OPT_GEMM_SYNC given (else: auto, on at d > 4096)
   size_t lmh_live_cap = 0;
@@ -468,6 +470,7 @@ espo_status espo_destroy(espo_ctx_t c) {
     if (c->hsel) cudaFree(c->hsel);
     if (c->lmh_live) cudaFree(c->lmh_live);
     if (c->gemm_sync) cudaFree(c->gemm_sync);
+    if (c->gemm_tctr) cudaFree(c->gemm_tctr);
     if (c->blas) g_blas.destroy(c->blas);
     if (c->blas_ws) cudaFree(c->blas_ws);
     for (void* q : c->x_opened) cudaIpcCloseMemHandle(q);
@@ -545,6 +548,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->lmh_split_k = int(((value >> 26) & 1) ^ 1);   // bit 26: no split-K for dh
       c->lmh_sync = ((value >> 27) & 1) ? 0 : 8 | (2 << 16);   // bit 27: no lockstep
       c->gemm_half_release = int(((value >> 28) & 1) ^ 1);    // bit 28: whole-accumulator release
+      c->gemm_dyn = int(((value >> 29) & 1) ^ 1);             // bit 29: static round robin
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_IMPL:
       if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
@@ -1019,6 +1023,7 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
   p.split_out = split_out;
   p.split_ld = split_ld;
   p.half_release = c->gemm_half_release;
+  p.tile_ctr = nullptr;
   if (split_out && (kOut != kOutF32 || kind == 0)) return ESPO_ERR_INVALID_ARGUMENT;
   if ((kOut == kOutLmFwd || kOut == kOutLmDz) && kind == 0) return ESPO_ERR_INVALID_ARGUMENT;
   p.dyn_count = dyn.count;
@@ -1064,6 +1069,11 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
                                                  G2<512>::kSmem, c->num_sms, res3)
                          : max_resident_clusters(k_umma_gemm2<kAMN, kBMN, kOut, 256>, 2, kG2Threads,
                                                  G2<256>::kSmem, c->num_sms, res2)));
+    if (c->gemm_dyn) {                         // dynamic tile scheduler: a zeroed counter
+      if (!c->gemm_tctr) ESPO_CUDA(cudaMalloc(&c->gemm_tctr, sizeof(int)));
+      ESPO_CUDA(cudaMemsetAsync(c->gemm_tctr, 0, sizeof(int), s));
+      p.tile_ctr = c->gemm_tctr;
+    }
     if (sync_chunk > 0) {                      // one zeroed progress counter per wave
       const int64_t waves = (tiles + clusters - 1) / clusters;
       if (size_t(waves) * 4 > c->gemm_sync_cap) {
@@ -1356,7 +1366,8 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       }
       const espo_status st = launch_umma_gemm<false, false, kOutLmDz>(
           c, mh, mw_k128, n, int(ldz), d, nullptr, 0, c->lmh_tile256 ? 1 : c->lmh_mcast ? 3 : 2,
-          lmh_raster(c, d), c->lmh_hints, s, dz_dyn, &lm, nullptr, 0, c->lmh_sync);
+          lmh_raster(c, d), c->lmh_hints, s, dz_dyn, &lm, nullptr, 0,
+          c->gemm_dyn ? 0 : c->lmh_sync);   // dz: with the dynamic scheduler, no lockstep (measured)
       if (st != ESPO_OK) return st;
     } else if (c->lmh_2cta) {
       k_lmhead2_dz<<<dim3(2 * parts, (mblocks + 1) / 2), kLmThreads, kL2Smem, s>>>(mh, mw, lp);

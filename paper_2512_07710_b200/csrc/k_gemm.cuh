@@ -104,6 +104,11 @@ struct GemmParams {
   int64_t split_ld;
   int half_release;       // 512-column accumulators: overlap the next tile's first K-steps on
                           // half 0 with the epilogue's read of half 1 (1, default) or not (0)
+  // dynamic tile scheduler (CTA-pair kernel; nullable = static round robin): a zeroed
+  // counter; each pair's leader takes the next work item with an atomic add and hands it to
+  // the pair's other roles through a small shared-memory queue, so the items in flight stay a
+  // contiguous window of the raster (a static round robin spreads them as clusters drift)
+  int* tile_ctr;
 };
 
 // wait until *ctr ≥ target or the timeout expired (acquire; a soft barrier: never deadlocks)
@@ -476,6 +481,29 @@ __host__ __device__ constexpr uint32_t gemm2_idesc() {
          (uint32_t(kGmBN >> 3) << 17) | (uint32_t(256 >> 4) << 24);
 }
 
+constexpr int kTQ = 4;   // dynamic scheduler: work-item queue depth per CTA pair
+
+// bounded wait with cluster-scope acquire: for the work-item queue, whose value the leader
+// stores into this CTA's shared memory from the other SM before its remote arrive (rarely
+// polled: the leader publishes items up to kTQ ahead)
+__device__ __forceinline__ void gm_wait_acq_cluster(uint32_t bar, uint32_t parity) {
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    if (ok) return;
+    if ((it & 255u) == 255u) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 20000000000ull) __trap();     // 20 s
+    }
+  }
+}
+
 // bounded wait on a barrier of this CTA that the peer CTA also arrives on (TMA bytes, MMA
 // commits, remote epilogue arrivals). The default (CTA-scope) acquire suffices: what the
 // barrier guards is shared memory written through the async proxy and TMEM, ordered by
@@ -542,7 +570,10 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
   uint64_t* empty = full + kG2Stages;
   uint64_t* tfull = empty + kG2Stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tq_full = tempty + 2;                   // dynamic scheduler: item queue slots
+  uint64_t* tq_empty = tq_full + kTQ;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq_empty + kTQ);
+  int* tq_ring = reinterpret_cast<int*>(tmem_slot + 1);
 
   const uint32_t crank = cluster_rank();
   const uint32_t rank = crank & 1u, pair = crank >> 1, leader = crank & ~1u;
@@ -557,6 +588,29 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
     kb0 = ks_n == 1 ? 0 : (ks * p.kblk) / 2;
     kb1 = ks_n == 1 ? p.kblk : ((ks + 1) * p.kblk) / 2;
   };
+  // dynamic scheduler: item k of this pair sits in queue slot k % kTQ of both CTAs; the
+  // leader's producer writes it (−1 = no more work), every other role of the pair takes it and
+  // releases the slot on the leader's tq_empty (1 + 1 + 2·8 arrivals: peer producer, MMA
+  // issuer, the epilogue warps of both CTAs)
+  const bool dyn = kPairs == 1 && p.tile_ctr != nullptr;
+  const uint32_t peer = crank | 1u;
+  auto tq_take = [&](int k) -> int {                // one thread
+    const int s = k % kTQ;
+    gm_wait_acq_cluster(smem_u32(&tq_full[s]), uint32_t(k / kTQ) & 1u);
+    const int it = *reinterpret_cast<volatile int*>(&tq_ring[s]);
+    if (rank == 0) mbar_arrive(&tq_empty[s]);
+    else arrive_remote(mapa_rank(smem_u32(&tq_empty[s]), leader));
+    return it;
+  };
+  auto tq_put = [&](int k, int it) {                // the leader's producer
+    const int s = k % kTQ;
+    gm_wait_cluster(smem_u32(&tq_empty[s]), (uint32_t(k / kTQ) & 1u) ^ 1u);
+    tq_ring[s] = it;
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa_rank(smem_u32(&tq_ring[s]), peer)),
+                 "r"(it) : "memory");
+    mbar_arrive(&tq_full[s]);
+    arrive_remote(mapa_rank(smem_u32(&tq_full[s]), peer));
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kG2Stages; ++s) {
@@ -566,6 +620,10 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * (kG2Threads - 64));   // every epilogue thread of both CTAs
+    }
+    for (int s = 0; s < kTQ; ++s) {
+      mbar_init(&tq_full[s], 1);
+      mbar_init(&tq_empty[s], 2 + 2 * ((kG2Threads - 64) / 32));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -586,15 +644,48 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
       const uint64_t pa = l2_policy(p.hint_a), pb = l2_policy(p.hint_b);
       const bool pace = p.sync != nullptr && rank == 0;
       uint32_t q = 0;
-      int wave = 0;
-      for (int item = cluster; item < items; item += nclusters, ++wave) {
+      int k_tq = 0, item_s = cluster;
+      // a skipped tile (no row to compute) still reports every chunk, so its wave never waits
+      auto skip_report = [&](int it) {
+        int kb0s, kb1s;
+        krange(it, kb0s, kb1s);
+        if (pace && kb1s > kb0s)
+          atomicAdd(p.sync + it / nclusters, unsigned((kb1s - kb0s - 1) / p.sync_chunk));
+      };
+      auto dead = [&](int it) {
+        if (!p.lm.mlive) return false;
+        int mbd, nbd;
+        gemm_tile_coords(ps, it % tiles, mbd, nbd);
+        return !p.lm.mlive[mbd];
+      };
+      for (;;) {
+        int item;
+        if (dyn) {
+          if (rank == 0) {
+            item = atomicAdd(p.tile_ctr, 1);
+            while (item < items && dead(item)) {
+              skip_report(item);
+              item = atomicAdd(p.tile_ctr, 1);
+            }
+            if (item >= items) item = -1;
+            tq_put(k_tq, item);
+          } else {
+            item = tq_take(k_tq);
+          }
+          ++k_tq;
+          if (item < 0) break;
+        } else {
+          item = item_s;
+          if (item >= items) break;
+          item_s += nclusters;
+        }
+        const int wave = item / nclusters;
         int mb, nb, kb0, kb1;
         gemm_tile_coords(ps, item % tiles, mb, nb);
         nb = nb * kPairs + int(pair);
         krange(item, kb0, kb1);
-        if (p.lm.mlive && !p.lm.mlive[mb]) {             // no row to compute: skipped tile
-          if (pace && kb1 > kb0)   // it still reports every chunk, so its wave never waits for it
-            atomicAdd(p.sync + wave, unsigned((kb1 - kb0 - 1) / p.sync_chunk));
+        if (dead(item)) {                                 // static schedule: skipped tile
+          skip_report(item);
           continue;
         }
         const int m0 = mb * 2 * kGmBM + int(rank) * kGmBM;
@@ -651,7 +742,17 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
       constexpr uint32_t idesc = gemm2_idesc<kAMN, kBMN>();
       uint32_t q = 0;
       int i = 0;
-      for (int item = cluster; item < items; item += nclusters) {
+      int k_tq = 0, item_s = cluster;
+      for (;;) {
+        int item;
+        if (dyn) {
+          item = tq_take(k_tq++);
+          if (item < 0) break;
+        } else {
+          item = item_s;
+          if (item >= items) break;
+          item_s += nclusters;
+        }
         if (p.lm.mlive) {
           int mb, nb;
           gemm_tile_coords(ps, item % tiles, mb, nb);
@@ -737,7 +838,20 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
     p1.C = p.split_out;
     p1.ldc = p.split_ld;
     p1.row_map = nullptr;
-    for (int item = cluster; item < items; item += nclusters) {
+    int k_tq = 0, item_s = cluster;
+    for (;;) {
+      int item;
+      if (dyn) {
+        int it = 0;
+        if (lane == 0) it = tq_take(k_tq);
+        item = __shfl_sync(0xffffffffu, it, 0);
+        ++k_tq;
+        if (item < 0) break;
+      } else {
+        item = item_s;
+        if (item >= items) break;
+        item_s += nclusters;
+      }
       int mb, nb;
       gemm_tile_coords(ps, item % tiles, mb, nb);
       nb = nb * kPairs + int(pair);

@@ -455,3 +455,45 @@ def test_lmhead_rlzvp_mode_matches_logits_path(kern):
     assert lf == pytest.approx(lu, rel=2e-3, abs=1e-6)
     assert np.linalg.norm(hf - hu) <= 4e-3 * np.linalg.norm(hu)
     assert np.linalg.norm(wf - wu) <= 4e-3 * np.linalg.norm(wu)
+
+
+@pytest.mark.parametrize("d", [256, 4160])
+def test_dynamic_tile_scheduler_is_bitwise_the_static_one(d):
+    """The CTA-pair GEMMs take their work items from an atomic counter (handed to the pair's
+    roles through a shared-memory queue; the default) or a static round robin
+    (ESPO_OPT_LMHEAD_RASTER bit 29). Each tile is still computed by one pair in the same K order and merged in
+    the same fixed order, so the forward statistics, loss, dhidden and dweight must be bitwise
+    those of the static schedule — with dead M-tiles skipped (a zero-variance group), the soft
+    lockstep on, and (d = 4160) split-K dh and the dh / dW lockstep."""
+    from paper_2512_07710_b200.espo import OPT_LMHEAD_RASTER, Espo, stats_to_dict
+    dev = require_cuda()
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    G, L, V = 8, 64, 4104
+    R = 3 * G
+    n = R * L
+    h = (torch.randn(n, d, device=dev, generator=g) / d ** 0.5 * 3).to(torch.bfloat16)
+    W = torch.randn(V, d, device=dev, generator=g).to(torch.bfloat16)
+    tok = torch.randint(0, V, (n,), device=dev, dtype=torch.int32, generator=g)
+    rew = torch.tensor([1.0, 0.0] * (G // 2) + [1.0] * G + [0.0, 1.0, 1.0, 0.0] * 2, device=dev)
+    gid = torch.arange(3, dtype=torch.int32, device=dev).repeat_interleave(G)
+    off = torch.arange(R + 1, device=dev, dtype=torch.int64) * L
+    old = torch.full((n,), -8.0, device=dev)
+    out = []
+    for dyn in (0, 1):
+        ctx = Espo(V, logits_dtype=torch.bfloat16, device=dev.index)
+        ctx.set_option(OPT_LMHEAD_RASTER, dyn << 29)
+        ctx.prepare(rew, gid, off, n_tokens=n)
+        ctx.lmhead_fwd(h, W, tok, old)
+        loss, stats = ctx.loss_finalize()
+        dh = torch.empty((n, d), dtype=torch.float32, device=dev)
+        dW = torch.zeros((V, d), dtype=torch.float32, device=dev)
+        ctx.lmhead_bwd(h, W, dh, dW)
+        ctx.get_error()
+        tk = ctx.export_token_stats()
+        out.append((loss.clone(), stats.clone(), tk["lp"].clone(), tk["H"].clone(), dh, dW))
+        ctx.close()
+    assert stats_to_dict(out[0][1])["n_zv_groups"] == 1
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(torch.nan_to_num(a, nan=7.0), torch.nan_to_num(b, nan=7.0))
+    assert float(out[0][4].abs().max()) > 0

@@ -67,6 +67,11 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
                 "mc_both": (5, 0, -1, 1, -1, 0, 0), "mc_dh": (6, 0, -1, 1, -1, 0, 0),
                 "mc_dh_nosplit": (6, 0, -1, 1, -1, 0, 1 << 26),
                 "dw256_g1": (0, G(0, 1), -1, 1, -1, 0, 0)}
+    if which == "dyn":           # tile scheduler: dynamic (default) vs static round robin (bit 29)
+        ST, NL = 1 << 29, 1 << 27  # (r2bm measured this set while bit 29 meant "dynamic")
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "static": (0, 0, -1, 1, -1, 0, ST), "static_nolock_dz": (0, 0, -1, 1, -1, 0, ST | NL),
+                "dyn_nolock_all": (0, 0, -1, 1, 0, 0, NL), "dyn_dw_n16": (0, G(0, 16), -1, 1, -1, 0, 0)}
     if which == "dwel":          # dW: A (dz panels) evict_last, B evict_last, C evict_first
         Hd = lambda a, b, c: (a | (b << 2) | (c << 4)) << 8
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
