@@ -17,9 +17,11 @@
 //                 likewise): 256 × 256 tiles (two accumulators) or 256 × 512 (one 512-column
 //                 accumulator = all of TMEM, a quarter less L2 → SM traffic per FLOP, released
 //                 in two column halves so the next tile's first K-steps overlap the epilogue),
-//                 8 epilogue warps; grouped tile raster, L2 cache-policy hints, device-side row
-//                 counts (compacted operands), split-K over 2 (deterministic), soft lockstep
-//                 between the clusters of a wave;
+//                 8 epilogue warps; grouped tile raster taken in order by a dynamic scheduler
+//                 (atomic counter, work items handed to the pair's roles through a
+//                 shared-memory queue), L2 cache-policy hints, device-side row counts
+//                 (compacted operands), split-K over 2 (deterministic), soft lockstep between
+//                 the clusters of a wave;
 //   k_umma_gemm4  two pairs per cluster sharing A through TMA multicast (an option: only 33
 //                 four-CTA clusters are resident on a B200, 132 of 148 SMs).
 // Grids are sized from the resident cluster count (host side). Every barrier wait is bounded by
