@@ -47,6 +47,9 @@ def main(d=4096, rounds=3, burst=4, which="default", n=32768, V=151936):
     if which == "dyn":           # (measured while bit 29 selected the dynamic scheduler, r2bm)
         cfgs = {"default": (0, 0, 0), "static": (0, 0, 1 << 13), "nolock": (0, 0, 0, 0),
                 "static_nolock": (0, 0, 1 << 13, 0), "cublas": None}
+    if which == "groups":        # raster group under the dynamic scheduler (lockstep on)
+        cfgs = {"g16": (0, 16, 0), "g8": (0, 8, 0), "g32": (0, 32, 0), "g64": (0, 64, 0),
+                "g24": (0, 24, 0), "cublas": None}
     if which == "sync2":
         cfgs = {"g16_s8_2": (0, 16, 0, 8 | 2 << 16), "g16_s16_2": (0, 16, 0, 16 | 2 << 16),
                 "g16_s8_4": (0, 16, 0, 8 | 4 << 16), "g16_s4_2": (0, 16, 0, 4 | 2 << 16),
