@@ -72,6 +72,20 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
                 "static": (0, 0, -1, 1, -1, 0, ST), "static_nolock_dz": (0, 0, -1, 1, -1, 0, ST | NL),
                 "dyn_nolock_all": (0, 0, -1, 1, 0, 0, NL), "dyn_dw_n16": (0, G(0, 16), -1, 1, -1, 0, 0)}
+    if which == "wide":          # d > 4096 under the dynamic scheduler: dW tiles / groups, dh groups
+        L = lambda ch, sl: ch | (sl << 16)
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "dw256_n8": (3, G(16, 8), -1, 1, -1, 0, 0),
+                "dw512_n4": (4, G(16, 4), -1, 1, -1, 0, 0), "dw512_n8": (4, G(16, 8), -1, 1, -1, 0, 0),
+                "dh8": (0, G(8, 0), -1, 1, -1, 0, 0), "dh32": (0, G(32, 0), -1, 1, -1, 0, 0),
+                "sync8": (0, 0, -1, 1, L(8, 2), 0, 0)}
+    if which == "wide2":         # d > 4096: lockstep on dh only / dW only / dW with more slack
+        L = lambda ch, sl: ch | (sl << 16)
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "dh_lock_dw_off": (0, 0, -1, 1, L(16, 2) | (L(0, 1) << 32), 0, 0),
+                "dh_off_dw_lock": (0, 0, -1, 1, L(0, 2) | (L(16, 2) << 32), 0, 0),
+                "dw_slack8": (0, 0, -1, 1, L(16, 2) | (L(16, 8) << 32), 0, 0),
+                "dw_chunk32": (0, 0, -1, 1, L(16, 2) | (L(32, 2) << 32), 0, 0)}
     if which == "dwel":          # dW: A (dz panels) evict_last, B evict_last, C evict_first
         Hd = lambda a, b, c: (a | (b << 2) | (c << 4)) << 8
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
