@@ -527,6 +527,7 @@ typedef enum {
                                   3 = pairs 256 × 256 for both; 4 = pairs 256 × 512 for both;
                                   5 = 4-CTA clusters (two pairs sharing A by TMA multicast,
                                   256 × 512 each) for both; 6 = those for dh, default dW;
+                                  7 = default dh, 256 × 256 dW in N-groups of 8 at any d;
                                   1 = cuBLAS (A/B measurement only) */
   ESPO_OPT_GEMM_GROUP_M = 9,   /* backward GEMM tile order: bits 0-15 = dh M-blocks per raster
                                   group (0 = auto: 8, 16 above d = 4096); bits 16-31 = dW N-blocks per group (0 = all

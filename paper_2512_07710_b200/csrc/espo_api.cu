@@ -512,7 +512,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->factored_impl = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_BWD_GEMM:
-      if (value < 0 || value > 6) return ESPO_ERR_INVALID_ARGUMENT;
+      if (value < 0 || value > 7) return ESPO_ERR_INVALID_ARGUMENT;
       c->lmh_bwd_gemm = static_cast<int>(value);
       return ESPO_OK;
     case ESPO_OPT_GEMM_HINTS:     // low 8 bits: dh, next 8 bits: dW (each A | B<<2 | C<<4); −1 auto
@@ -1392,7 +1392,8 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       const int g = c->lmh_bwd_gemm;
       const bool wide_dw = d > 4096;
       const int kind_dh = g == 2 ? 0 : g == 3 ? 1 : (g == 5 || g == 6) ? 3 : 2;
-      const int kind_dw = g == 2 ? 0 : g == 3 ? 1 : g == 4 ? 2 : g == 5 ? 3 : (wide_dw ? 2 : 1);
+      const int kind_dw = g == 2 ? 0 : g == 3 ? 1 : g == 4 ? 2 : g == 5 ? 3 : g == 7 ? 1 :
+                          (wide_dw ? 2 : 1);
       // tile order: dh has a long K (the vocabulary) and few tiles: groups of 8 M-blocks keep
       // the resident tiles' A and B panels small; dW (K = rows): N fastest, so every M-block
       // of dz is read once while h stays in L2
@@ -1403,7 +1404,8 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
       const int sync_dh = sync_auto;
       const int sync_dw = c->gemm_sync_dw >= 0 ? c->gemm_sync_dw : sync_auto;
       // dW: groups of gemm_group_n_dw N-blocks (0 = N fastest over all of d)
-      const int g_dw = c->gemm_group_n_dw > 0 ? -c->gemm_group_n_dw : (g == 0 ? (wide_dw ? -2 : -8) : 1);
+      const int g_dw = c->gemm_group_n_dw > 0 ? -c->gemm_group_n_dw
+                                              : (g == 0 ? (wide_dw ? -2 : -8) : g == 7 ? -8 : 1);
       // L2 policies (2 bits each: A | B << 2 | C << 4; 1 = evict_first, 2 = evict_last):
       // dh streams both panels once per wave; dW streams dz and the dW read-add-write while
       // every tile re-reads h (64 MB at n = 8192, d = 4096), which should stay in L2

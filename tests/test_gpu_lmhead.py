@@ -256,8 +256,9 @@ def test_lmhead_errors_and_state():
     sh.close()
 
 
-@pytest.mark.parametrize("native", [0, 2, 3, 4, 5, 6],
-                         ids=["pair_default", "1cta", "pair256", "pair512", "mcast", "mcast_dh"])
+@pytest.mark.parametrize("native", [0, 2, 3, 4, 5, 6, 7],
+                         ids=["pair_default", "1cta", "pair256", "pair512", "mcast", "mcast_dh",
+                              "dw256"])
 @pytest.mark.parametrize("shape", [(3, 4, 50, 20000, 1000), (2, 4, 130, 5000, 2048)],
                          ids=["V20000_d1000_ntail", "V5000_d2048"])
 def test_lmhead_bwd_native_gemm_equals_cublas(shape, native):

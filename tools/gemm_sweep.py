@@ -86,6 +86,10 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
                 "dh_off_dw_lock": (0, 0, -1, 1, L(0, 2) | (L(16, 2) << 32), 0, 0),
                 "dw_slack8": (0, 0, -1, 1, L(16, 2) | (L(16, 8) << 32), 0, 0),
                 "dw_chunk32": (0, 0, -1, 1, L(16, 2) | (L(32, 2) << 32), 0, 0)}
+    if which == "wide3":         # d > 4096: 256-wide dW tiles with the default 512-wide dh
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "dw256": (7, 0, -1, 1, -1, 0, 0), "dw256_n16": (7, G(0, 16), -1, 1, -1, 0, 0),
+                "dw256_n4": (7, G(0, 4), -1, 1, -1, 0, 0)}
     if which == "dwel":          # dW: A (dz panels) evict_last, B evict_last, C evict_first
         Hd = lambda a, b, c: (a | (b << 2) | (c << 4)) << 8
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
