@@ -565,7 +565,10 @@ typedef enum {
                                   every CTA-pair GEMM (default: a dynamic scheduler — each pair
                                   takes the next tile from an atomic counter, so the tiles in
                                   flight stay a contiguous window of the raster; the backward's
-                                  dz recompute then runs without the lockstep) */
+                                  dz recompute then runs without the lockstep), bit 30 = the dW
+                                  GEMM's epilogue reads, adds and writes dW on the SMs (default:
+                                  it stages 32 × 32 fp32 blocks in shared memory and adds them
+                                  into dW with a TMA reduce, cp.reduce.async.bulk.tensor .add) */
 } espo_option;
 espo_status espo_set_option(espo_ctx_t ctx, int32_t option, int64_t value);
 

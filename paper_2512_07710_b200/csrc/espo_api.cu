@@ -179,6 +179,7 @@ struct espo_ctx_s {
   int lmh_sync = 8 | (2 << 16);  // their soft lockstep (chunk of K-steps | slack << 16; 0 = off)
   int gemm_half_release = 1;     // CTA-pair 256 × 512 GEMMs: accumulator released in halves
   int gemm_dyn = 1;              // CTA-pair GEMMs: dynamic tile scheduler (atomic counter)
+  int gemm_tma_red = 1;          // dW GEMM: epilogue adds into dW with a TMA reduce
   int* gemm_tctr = nullptr;      // its counter
   int gemm_sync_dw = -1;         // dW GEMM's own lockstep (chunk | slack << 16; −1 = as dh)
   int gemm_sync_set = 0;         // ESPO_OPT_GEMM_SYNC given (else: auto, on at d > 4096)
@@ -549,6 +550,7 @@ espo_status espo_set_option(espo_ctx_t c, int32_t option, int64_t value) {
       c->lmh_sync = ((value >> 27) & 1) ? 0 : 8 | (2 << 16);   // bit 27: no lockstep
       c->gemm_half_release = int(((value >> 28) & 1) ^ 1);    // bit 28: whole-accumulator release
       c->gemm_dyn = int(((value >> 29) & 1) ^ 1);             // bit 29: static round robin
+      c->gemm_tma_red = int(((value >> 30) & 1) ^ 1);         // bit 30: dW read-add-write on the SMs
       return ESPO_OK;
     case ESPO_OPT_LMHEAD_IMPL:
       if (value < 0 || value > 1) return ESPO_ERR_INVALID_ARGUMENT;
@@ -948,6 +950,26 @@ bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
                  (unsigned long long)pitch_bytes, box_rows);
   return r == CUDA_SUCCESS;
 }
+// fp32 [rows, cols] (row pitch in bytes) as 32 × 32 boxes with 128-byte swizzle: the target of
+// the dW GEMM's TMA-reduce epilogue
+bool make_map_f32_box32(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
+                        uint64_t pitch_bytes) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_encode),
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_bytes};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
 // vocabulary parts per row block: enough CTAs for ≥ 2 waves; beyond that the best split
 // measured on B200 (tools/bench_lmhead.py, n = 32,768, V = 151,936) is 4 parts for d ≤ 4096
 // and 2 for d = 8192 (fewer parts keep fewer W tiles live in L2, more parts keep fewer A row
@@ -1011,7 +1033,8 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
                              int N, int64_t K, void* C, int64_t ldc, int kind, int group_m,
                              int hints, cudaStream_t s, const GemmDyn& dyn = GemmDyn(),
                              const LmEpi* lm = nullptr, float* split_out = nullptr,
-                             int64_t split_ld = 0, int sync_opt = -1) {
+                             int64_t split_ld = 0, int sync_opt = -1,
+                             const CUtensorMap* mc = nullptr) {
   // kind: 0 = one CTA per 128 × 256 tile, 1 = CTA pair 256 × 256, 2 = CTA pair 256 × 512,
   // 3 = two CTA pairs per cluster sharing A by multicast, 256 × 512 tiles each
   static unsigned long long attr = 0, attr2 = 0, attr3 = 0, attr4 = 0;
@@ -1024,6 +1047,11 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
   p.split_ld = split_ld;
   p.half_release = c->gemm_half_release;
   p.tile_ctr = nullptr;
+  // C through TMA reduce-add (kOutAddF32 on pairs, when the caller passed C's tensor map)
+  p.tma_red = (kOut == kOutAddF32 && mc != nullptr && c->gemm_tma_red) ? 1 : 0;
+  const CUtensorMap& mcc = mc ? *mc : ma;      // unused unless tma_red
+  const size_t smem512 = kOut == kOutAddF32 ? G2<512>::kSmemRed : G2<512>::kSmem;
+  const size_t smem256 = kOut == kOutAddF32 ? G2<256>::kSmemRed : G2<256>::kSmem;
   if (split_out && (kOut != kOutF32 || kind == 0)) return ESPO_ERR_INVALID_ARGUMENT;
   if ((kOut == kOutLmFwd || kOut == kOutLmDz) && kind == 0) return ESPO_ERR_INVALID_ARGUMENT;
   p.dyn_count = dyn.count;
@@ -1055,20 +1083,20 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
   p.sync_timeout_ns = 200000;
   static int res2 = 0, res3 = 0, res4 = 0;   // resident clusters per kernel (this process's GPU)
   if (kind == 3) {
-    ESPO_CUDA(ensure_smem_attr(k_umma_gemm4<kAMN, kBMN, kOut, 512>, int(G2<512>::kSmem), attr4));
+    ESPO_CUDA(ensure_smem_attr(k_umma_gemm4<kAMN, kBMN, kOut, 512>, int(smem512), attr4));
     const int64_t super = int64_t(p.mblk) * ((p.nblk + 1) / 2);
     const int clusters = int(std::min<int64_t>(
         super, max_resident_clusters(k_umma_gemm4<kAMN, kBMN, kOut, 512>, 4, kG2Threads,
-                                     G2<512>::kSmem, c->num_sms, res4)));
-    k_umma_gemm4<kAMN, kBMN, kOut, 512><<<4 * clusters, kG2Threads, G2<512>::kSmem, s>>>(ma, mb, p);
+                                     smem512, c->num_sms, res4)));
+    k_umma_gemm4<kAMN, kBMN, kOut, 512><<<4 * clusters, kG2Threads, smem512, s>>>(ma, mb, mcc, p);
   } else if (pair) {
-    if (kind == 2) ESPO_CUDA(ensure_smem_attr(k_umma_gemm2<kAMN, kBMN, kOut, 512>, int(G2<512>::kSmem), attr3));
-    else ESPO_CUDA(ensure_smem_attr(k_umma_gemm2<kAMN, kBMN, kOut, 256>, int(G2<256>::kSmem), attr2));
+    if (kind == 2) ESPO_CUDA(ensure_smem_attr(k_umma_gemm2<kAMN, kBMN, kOut, 512>, int(smem512), attr3));
+    else ESPO_CUDA(ensure_smem_attr(k_umma_gemm2<kAMN, kBMN, kOut, 256>, int(smem256), attr2));
     const int clusters = int(std::min<int64_t>(
         tiles, kind == 2 ? max_resident_clusters(k_umma_gemm2<kAMN, kBMN, kOut, 512>, 2, kG2Threads,
-                                                 G2<512>::kSmem, c->num_sms, res3)
+                                                 smem512, c->num_sms, res3)
                          : max_resident_clusters(k_umma_gemm2<kAMN, kBMN, kOut, 256>, 2, kG2Threads,
-                                                 G2<256>::kSmem, c->num_sms, res2)));
+                                                 smem256, c->num_sms, res2)));
     if (c->gemm_dyn) {                         // dynamic tile scheduler: a zeroed counter
       if (!c->gemm_tctr) ESPO_CUDA(cudaMalloc(&c->gemm_tctr, sizeof(int)));
       ESPO_CUDA(cudaMemsetAsync(c->gemm_tctr, 0, sizeof(int), s));
@@ -1087,9 +1115,9 @@ espo_status launch_umma_gemm(espo_ctx_t c, const CUtensorMap& ma, const CUtensor
       p.sync = static_cast<unsigned*>(c->gemm_sync);
     }
     if (kind == 2)
-      k_umma_gemm2<kAMN, kBMN, kOut, 512><<<2 * clusters, kG2Threads, G2<512>::kSmem, s>>>(ma, mb, p);
+      k_umma_gemm2<kAMN, kBMN, kOut, 512><<<2 * clusters, kG2Threads, smem512, s>>>(ma, mb, mcc, p);
     else
-      k_umma_gemm2<kAMN, kBMN, kOut, 256><<<2 * clusters, kG2Threads, G2<256>::kSmem, s>>>(ma, mb, p);
+      k_umma_gemm2<kAMN, kBMN, kOut, 256><<<2 * clusters, kG2Threads, smem256, s>>>(ma, mb, mcc, p);
   } else {
     ESPO_CUDA(ensure_smem_attr(k_umma_gemm<kAMN, kBMN, kOut>, int(kGmSmem), attr));
     const int grid = int(std::min<int64_t>(tiles, c->num_sms));
@@ -1453,8 +1481,11 @@ espo_status espo_lmhead_bwd(espo_ctx_t c, const void* hidden, int64_t ldh, const
         }
       }
       if (dweight) {   // dW[V, d] += dzᵀ[V, n] · h[n, d]: A = dz MN-major, B = h MN-major
+        CUtensorMap mdw;
+        const bool red = c->gemm_tma_red && kind_dw != 0 &&
+                         make_map_f32_box32(&mdw, dweight, uint64_t(V), uint64_t(d), uint64_t(lddw) * 4);
         st = launch_umma_gemm<true, true, kOutAddF32>(c, mdz_mn, mh_mn, V, d, n, dweight, lddw, kind_dw, g_dw, hint_dw, s, dyn_k,
-                                                      nullptr, nullptr, 0, sync_dw);
+                                                      nullptr, nullptr, 0, sync_dw, red ? &mdw : nullptr);
         if (st != ESPO_OK) return st;
       }
       continue;

@@ -21,7 +21,7 @@
 //                 (atomic counter, work items handed to the pair's roles through a
 //                 shared-memory queue), L2 cache-policy hints, device-side row counts
 //                 (compacted operands), split-K over 2 (deterministic), soft lockstep between
-//                 the clusters of a wave;
+//                 the clusters of a wave, fp32 accumulation into C by TMA reduce-add;
 //   k_umma_gemm4  two pairs per cluster sharing A through TMA multicast (an option: only 33
 //                 four-CTA clusters are resident on a B200, 132 of 148 SMs).
 // Grids are sized from the resident cluster count (host side). Every barrier wait is bounded by
@@ -111,6 +111,10 @@ struct GemmParams {
   // the pair's other roles through a small shared-memory queue, so the items in flight stay a
   // contiguous window of the raster (a static round robin spreads them as clusters drift)
   int* tile_ctr;
+  // kOutAddF32 on CTA pairs: 1 = the epilogue stages each 32 × 32 fp32 block in shared memory
+  // and adds it into C with a TMA reduce (cp.reduce.async.bulk.tensor .add) instead of an
+  // SM-side read-add-write (the third tensor map of the launch describes C)
+  int tma_red;
 };
 
 // wait until *ctr ≥ target or the timeout expired (acquire; a soft barrier: never deadlocks)
@@ -475,7 +479,43 @@ struct G2 {
   static constexpr int kStages = kNP == 256 ? 6 : 4;
   static constexpr int kAcc = kNP == 256 ? 2 : 1;               // TMEM accumulator buffers
   static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024 + 256;
+  // + the TMA-reduce epilogue's staging: one 32 × 32 fp32 box (4 KB) per epilogue warp,
+  // 1024-B aligned after the barrier region
+  static constexpr size_t kSmemRed = size_t(kStages) * kStageBytes + 1024 + 1024 + 8 * 4096;
 };
+
+// TMA-reduce epilogue (kOutAddF32, CTA pairs): this warp's 32 rows × nchunk·32 columns of the
+// accumulator, 32 columns at a time: TMEM → registers → the warp's staging box (row = lane,
+// 128-byte swizzle: 16-byte chunk j at j ^ (lane & 7)) → one elected lane adds the box into C at
+// (row0, n0 + 32·c) with cp.reduce.async.bulk.tensor (rows / columns past C are dropped by the
+// TMA unit). The box is rewritten only after the previous reduce has read it.
+__device__ __forceinline__ void gemm_red_tile(const CUtensorMap* tmap_c, uint32_t base, int row0,
+                                              int n0, int nchunk, uint32_t stage, int lane) {
+#pragma unroll 1
+  for (int c = 0; c < nchunk; ++c) {
+    float x[32];
+    __syncwarp();
+    tmem_ld32(base + uint32_t(c * 32), x);
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t a = stage + uint32_t(lane) * 128u + (uint32_t(j ^ (lane & 7)) << 4);
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x[4 * j]),
+                   "f"(x[4 * j + 1]), "f"(x[4 * j + 2]), "f"(x[4 * j + 3])
+                   : "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile(
+          "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];"
+          ::"l"(reinterpret_cast<uint64_t>(tmap_c)), "r"(stage), "r"(n0 + c * 32), "r"(row0)
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+}
 
 template <bool kAMN, bool kBMN>
 __host__ __device__ constexpr uint32_t gemm2_idesc() {
@@ -554,7 +594,7 @@ __device__ __forceinline__ void tc_commit_mask(uint32_t bar, uint16_t mask) {
 // pairs move in lockstep: a stage is refilled only when both consumed it).
 template <bool kAMN, bool kBMN, int kOut, int kNP, int kPairs>
 __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUtensorMap& tmap_b,
-                                           const GemmParams& p0) {
+                                           const CUtensorMap& tmap_c, const GemmParams& p0) {
   using C = G2<kNP>;
   constexpr int kG2Stages = C::kStages, kG2ABytes = C::kABytes, kG2BBytes = C::kBBytes;
   constexpr int kG2StageBytes = C::kStageBytes;
@@ -835,6 +875,8 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
     const uint64_t pol_c = l2_policy(p.hint_c);
     const uint32_t leader_tempty0 = mapa_rank(smem_u32(&tempty[0]), leader);
     const uint32_t leader_tempty1 = mapa_rank(smem_u32(&tempty[1]), leader);
+    const uint32_t stage_w = smem_u32(smem + kG2Stages * kG2StageBytes + 1024) +
+                             uint32_t(warp - 2) * 4096u;   // TMA-reduce staging box of this warp
     int i = 0;
     GemmParams p1 = p;                                  // K-half 1 of a split: the scratch
     p1.C = p.split_out;
@@ -897,7 +939,10 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
         } else {
 #pragma unroll 1
           for (int hh = 0; hh < 2; ++hh) {
-            gemm_store_tile<kOut>(second ? p1 : p, lb + uint32_t(hh * 256), r, cb + hh * 256, pol_c, 4);
+            if (kOut == kOutAddF32 && p.tma_red)
+              gemm_red_tile(&tmap_c, lb + uint32_t(hh * 256), r - lane, cb + hh * 256, 4, stage_w, lane);
+            else
+              gemm_store_tile<kOut>(second ? p1 : p, lb + uint32_t(hh * 256), r, cb + hh * 256, pol_c, 4);
             __syncwarp();
             tc_fence_before();
             arrive_remote(hh ? leader_tempty1 : leader_tempty0);
@@ -921,6 +966,8 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
         rc.y = -1;
         if (r < p.M) rc = p.lm.rec[r];
         lm_dz_cols(p, base, r, c0, rc, kChunks);
+      } else if (kOut == kOutAddF32 && p.tma_red) {
+        gemm_red_tile(&tmap_c, base, r - lane, c0, kChunks, stage_w, lane);
       } else {
         gemm_store_tile<kOut>(second ? p1 : p, base, r, c0, pol_c, kChunks);
       }
@@ -929,6 +976,8 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
       arrive_remote(acc ? leader_tempty1 : leader_tempty0);
     }
   }
+  if (kOut == kOutAddF32 && p.tma_red && warp >= 2 && lane == 0)
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // every reduce performed
   tc_fence_before();
   cluster_sync_all();     // all CTAs done with TMEM and with remote barriers
   if (warp == 1) {
@@ -941,15 +990,15 @@ __device__ __forceinline__ void gemm2_body(const CUtensorMap& tmap_a, const CUte
 template <bool kAMN, bool kBMN, int kOut, int kNP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kG2Threads, 1)
     k_umma_gemm2(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                 const GemmParams p0) {
-  gemm2_body<kAMN, kBMN, kOut, kNP, 1>(tmap_a, tmap_b, p0);
+                 const __grid_constant__ CUtensorMap tmap_c, const GemmParams p0) {
+  gemm2_body<kAMN, kBMN, kOut, kNP, 1>(tmap_a, tmap_b, tmap_c, p0);
 }
 
 template <bool kAMN, bool kBMN, int kOut, int kNP>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kG2Threads, 1)
     k_umma_gemm4(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                 const GemmParams p0) {
-  gemm2_body<kAMN, kBMN, kOut, kNP, 2>(tmap_a, tmap_b, p0);
+                 const __grid_constant__ CUtensorMap tmap_c, const GemmParams p0) {
+  gemm2_body<kAMN, kBMN, kOut, kNP, 2>(tmap_a, tmap_b, tmap_c, p0);
 }
 
 // C[row_map ? row_map[r] : r][0, N) += split[r][0, N) for r < the (device) row count.

@@ -498,3 +498,42 @@ def test_dynamic_tile_scheduler_is_bitwise_the_static_one(d):
     for a, b in zip(out[0], out[1]):
         assert torch.equal(torch.nan_to_num(a, nan=7.0), torch.nan_to_num(b, nan=7.0))
     assert float(out[0][4].abs().max()) > 0
+
+
+@pytest.mark.parametrize("d", [1000, 4160])
+def test_tma_reduce_dw_epilogue_is_bitwise(d):
+    """The dW GEMM's epilogue adds each 32 × 32 fp32 block into dW with a TMA reduce
+    (cp.reduce.async.bulk.tensor .add; the default) or an SM-side read-add-write
+    (ESPO_OPT_LMHEAD_RASTER bit 30) — one fp32 add per element either way, so dW (accumulated
+    over several sub-chunks onto a non-zero start, ragged vocabulary rows and d columns) is
+    bitwise the same."""
+    from paper_2512_07710_b200.espo import OPT_LMHEAD_BWD_ROWS, OPT_LMHEAD_RASTER, Espo
+    dev = require_cuda()
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    G, L, V = 4, 96, 5003
+    n = G * L
+    h = (torch.randn(n, d, device=dev, generator=g) / d ** 0.5 * 3).to(torch.bfloat16)
+    W = torch.randn(V, d, device=dev, generator=g).to(torch.bfloat16)
+    tok = torch.randint(0, V, (n,), device=dev, dtype=torch.int32, generator=g)
+    rew = torch.tensor([1.0, 0.0, 1.0, 0.0], device=dev)
+    gid = torch.zeros(G, dtype=torch.int32, device=dev)
+    off = torch.arange(G + 1, device=dev, dtype=torch.int64) * L
+    dW0 = torch.randn(V, d, device=dev, generator=g)
+    out = []
+    for red in (0, 1):
+        ctx = Espo(V, logits_dtype=torch.bfloat16, device=dev.index)
+        ctx.set_option(OPT_LMHEAD_RASTER, red << 30)
+        ctx.set_option(OPT_LMHEAD_BWD_ROWS, 128)          # three sub-chunks accumulate into dW
+        ctx.prepare(rew, gid, off, n_tokens=n)
+        ctx.lmhead_fwd(h, W, tok, torch.full((n,), -8.0, device=dev))
+        ctx.loss_finalize()
+        dh = torch.empty((n, d), dtype=torch.float32, device=dev)
+        dW = dW0.clone()
+        ctx.lmhead_bwd(h, W, dh, dW)
+        ctx.get_error()
+        out.append((dh, dW))
+        ctx.close()
+    assert torch.equal(out[0][0], out[1][0])
+    assert torch.equal(out[0][1], out[1][1])
+    assert not torch.equal(out[0][1], dW0)

@@ -90,6 +90,10 @@ def main(d=4096, n=8192, V=151936, rounds=5, burst=1, which="default"):
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
                 "dw256": (7, 0, -1, 1, -1, 0, 0), "dw256_n16": (7, G(0, 16), -1, 1, -1, 0, 0),
                 "dw256_n4": (7, G(0, 4), -1, 1, -1, 0, 0)}
+    if which == "red":           # dW epilogue: TMA reduce-add (default) vs SM read-add-write (bit 30)
+        RMW = 1 << 30             # (r2bs measured this set while bit 30 meant "TMA reduce")
+        cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
+                "sm_rmw": (0, 0, -1, 1, -1, 0, RMW), "dw256": (7, 0, -1, 1, -1, 0, 0)}
     if which == "dwel":          # dW: A (dz panels) evict_last, B evict_last, C evict_first
         Hd = lambda a, b, c: (a | (b << 2) | (c << 4)) << 8
         cfgs = {"cublas": cfgs["cublas"], "default": cfgs["default"],
